@@ -1,0 +1,78 @@
+"""Layerwise TTFT and stall accounting (oracle; test infrastructure only).
+
+Eq. 3 (Sec. 3.5), one-layer prefetch:
+    T_TTFT ~= X_0 + sum_{l=0}^{L-2} max(X_{l+1}, C_l) + C_{L-1}
+X_l is the transfer time of layer l, C_l the compute exposed at layer l.
+"When X_l > C_l, the transfer time that exceeds the compute window appears as
+additional waiting time."
+
+Reading c14: on B200 the copy stream is free-running (every layer issued back
+to back), so the device pipeline is
+    ready_l = sum_{k<=l} X_k,  start_l = max(ready_l, end_{l-1}),  end_l = start_l + C_l
+with added TTFT = end_{L-1} - sum_l C_l and stall_l = start_l - end_{l-1}.
+Both models coincide when X and C are uniform across layers (the paper's
+footnote); otherwise Eq. 3 is an upper bound.
+"""
+
+
+def eq3_ttft(X, C):
+    """Eq. 3 verbatim."""
+    L = len(X)
+    if L != len(C) or L == 0:
+        raise ValueError("X and C must have the same length L >= 1")
+    t = X[0]
+    for l in range(L - 1):
+        t += max(X[l + 1], C[l])
+    return t + C[L - 1]
+
+
+def free_running(ready, C):
+    """Pipeline from measured layer-ready times; returns (ttft, start, end, stall)."""
+    L = len(ready)
+    if L != len(C) or L == 0:
+        raise ValueError("ready and C must have the same length L >= 1")
+    start, end, stall = [], [], []
+    prev_end = 0.0
+    for l in range(L):
+        s = max(ready[l], prev_end)
+        stall.append(s - prev_end)
+        start.append(s)
+        prev_end = s + C[l]
+        end.append(prev_end)
+    return end[-1], start, end, stall
+
+
+def free_running_ttft(X, C):
+    """Free-running copy stream: ready_l is the prefix sum of X."""
+    ready, acc = [], 0.0
+    for x in X:
+        acc += x
+        ready.append(acc)
+    return free_running(ready, C)[0]
+
+
+def added_ttft(ttft, C):
+    return ttft - sum(C)
+
+
+def simulate(X, C, prefetch_depth):
+    """Discrete-event simulation of one copy engine and one compute engine.
+
+    The transfer of layer l may begin once the transfer of l-1 is done and,
+    with finite ``prefetch_depth`` k, once compute of layer l-k has *started*
+    (its buffer slot is being consumed).  Compute of layer l begins once its
+    transfer is done and compute of l-1 is done.  k = 1 is Eq. 3's
+    "one-layer prefetch"; k = None is the free-running stream.
+    """
+    L = len(X)
+    x_end = [0.0] * L
+    c_start = [0.0] * L
+    c_end = [0.0] * L
+    for l in range(L):
+        begin = x_end[l - 1] if l > 0 else 0.0
+        if prefetch_depth is not None and l - prefetch_depth >= 0:
+            begin = max(begin, c_start[l - prefetch_depth])
+        x_end[l] = begin + X[l]
+        c_start[l] = max(x_end[l], c_end[l - 1] if l > 0 else 0.0)
+        c_end[l] = c_start[l] + C[l]
+    return c_end[-1]
