@@ -1,0 +1,264 @@
+/*
+ * objcache.h -- C ABI of the B200-native ObjectCache hot path (arxiv 2605.22850).
+ *
+ * The library assembles a prefix-cache hit the way ObjectCache's storage server
+ * does (Sec. 3.3; Alg. A1): a request names
+ * N hash-addressed KV chunks, each stored chunk-major (KV_L2TD), and
+ * for every layer l the library moves byte range [lS, (l+1)S) of every chunk,
+ * in prefix order, into the caller's GPU KV memory, announcing each layer as
+ * soon as it is complete so prefill of layer l overlaps the transfer of l+1
+ * (Sec. 3.5, Eq. 3).  On B200 the "storage server" is a CUDA kernel
+ * reading an HBM, pinned-host or peer-GPU chunk store; the "RDMA target" is the
+ * serving engine's paged KV cache (or the paper's flat client buffer); the
+ * layer-ready notification is a device counter / CUDA event per layer.
+ *
+ * Conventions for every entry point:
+ *  - Return value: OC_OK (0) or a negative OC_E* code; the thread-local text of
+ *    the last failure is in oc_last_error().  No entry point aborts the process.
+ *  - "device address" = a CUDA UVA address the store's GPU can dereference: its
+ *    own HBM, mapped pinned host memory, or a peer GPU's memory with peer access.
+ *  - Streams are cudaStream_t passed as void* (NULL = the legacy default stream).
+ *  - Host arrays passed in are read during the call only (copied if kept).
+ *  - Objects (oc_store, oc_desc) are owned by the library and freed by the
+ *    matching *_destroy / *_free call.  KV destination memory and streams are
+ *    owned by the caller.
+ *
+ * No CPU fallback exists: every byte of the data path is moved by the library's
+ * sm_100a kernels; without a usable GPU the data-path calls return OC_ECUDA.
+ */
+#ifndef OBJCACHE_H
+#define OBJCACHE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define OC_API __attribute__((visibility("default")))
+#else
+#define OC_API
+#endif
+
+#define OC_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------- */
+#define OC_OK 0
+#define OC_EINVAL (-1)      /* bad argument or inconsistent layout               */
+#define OC_ENOMEM (-2)      /* host or device allocation failed                  */
+#define OC_ENOTFOUND (-3)   /* a chunk key is not in the store (see bad_index)   */
+#define OC_EIMMUTABLE (-4)  /* put of an existing key with different bytes       */
+#define OC_ERANGE (-5)      /* index/size out of range (layer >= L, small target)*/
+#define OC_EALIGN (-6)      /* address or stride not a multiple of 16 bytes      */
+#define OC_ECUDA (-7)       /* CUDA runtime/driver error (text in oc_last_error) */
+#define OC_EFULL (-8)       /* store capacity exhausted                          */
+#define OC_ENOTSUP (-9)     /* option not supported in this configuration        */
+
+/* ---- geometry ----------------------------------------------------------- */
+/* A rolling-hash chunk key H_i = SHA-256(H_{i-1} || LE-u32 tokens_i), root = 32
+ * zero bytes (the paper names only "Hash", reading c1). */
+typedef struct { uint8_t b[32]; } oc_key;
+
+/* Eq. 1 symbols: L layers, n_kv KV heads, head dim d, element width
+ * p bytes, G tokens per chunk.  Derived: row = n_kv*d*p (one token of K or V at
+ * one layer), S = 2*G*row (one layer of one chunk), chunk object = L*S bytes,
+ * laid out [L][2 (K,V)][G][n_kv][d] (KV_L2TD, reading c2). */
+typedef struct {
+    uint32_t num_layers;
+    uint32_t kv_heads;
+    uint32_t head_dim;
+    uint32_t elem_bytes;
+    uint32_t chunk_tokens;
+} oc_layout;
+
+/* Fills row bytes, S and L*S.  EINVAL if a field is 0 or L*S overflows. */
+OC_API int oc_geometry(const oc_layout* layout, uint64_t* row_bytes, uint64_t* layer_chunk_bytes,
+                       uint64_t* chunk_bytes);
+
+/* Eq. 2: returns OC_DELIVER_CHUNK_MAJOR if W < theta, else
+ * OC_DELIVER_LAYER_MAJOR (theta = 0 always selects layer-major). */
+OC_API int oc_select_mode(uint64_t payload_W, uint64_t theta);
+
+/* ---- keys (host) -------------------------------------------------------- */
+/* SHA-256 (FIPS 180-4) of n bytes. */
+OC_API int oc_sha256(const void* data, uint64_t n, uint8_t out[32]);
+
+/* Keys of the floor(n_tokens/G) complete G-token blocks of `tokens`, chained
+ * from `parent` (NULL = root).  Writes min(count, cap) keys, sets *n_out = count.
+ * A trailing partial block is ignored.  ERANGE if cap < count. */
+OC_API int oc_chunk_keys(const uint32_t* tokens, uint64_t n_tokens, uint32_t chunk_tokens,
+                         const oc_key* parent, oc_key* out, uint64_t cap, uint64_t* n_out);
+
+/* ---- chunk store -------------------------------------------------------- */
+typedef enum { OC_TIER_HBM = 0, OC_TIER_PINNED_HOST = 1 } oc_tier;
+typedef struct oc_store oc_store;
+
+/* Create a store of `capacity_chunks` slots of L*S bytes on GPU `device`:
+ * HBM (cudaMalloc) or pinned, mapped host memory (cudaHostAlloc; the GPU reads
+ * it over PCIe -- the stand-in for the paper's RDMA landing zone). */
+OC_API int oc_store_create(const oc_layout* layout, int tier, int device, uint64_t capacity_chunks,
+                           oc_store** out);
+OC_API int oc_store_destroy(oc_store* store);
+OC_API int oc_store_count(const oc_store* store, uint64_t* n_chunks);
+/* Slab base device address and size in bytes (for IPC export and tests). */
+OC_API int oc_store_slab(const oc_store* store, uint64_t* base, uint64_t* bytes);
+
+/* put_chunks (P:224 offload; P:36-40 immutable, content-addressed writes):
+ * store n chunk objects; payloads = n*L*S contiguous bytes, host or device
+ * memory.  An existing key with identical bytes is deduplicated; with
+ * different bytes the call fails with EIMMUTABLE and *bad_index = its index
+ * (chunks before it are stored).  *n_new = number of keys that were new.
+ * EFULL when capacity is exhausted.  Thread-safe. */
+OC_API int oc_put_chunks(oc_store* store, const oc_key* keys, const void* payloads, uint64_t n,
+                         uint64_t* n_new, uint64_t* bad_index);
+
+/* match_prefix: hash the complete G-blocks of `tokens`
+ * from `parent` (NULL = root) and return the longest leading run of keys
+ * present in the store, in prefix order (reading c17).  Writes up to `cap`
+ * keys; *n_matched = run length (ERANGE if it exceeds cap). */
+OC_API int oc_match_prefix(oc_store* store, const uint32_t* tokens, uint64_t n_tokens,
+                           const oc_key* parent, oc_key* out, uint64_t cap, uint64_t* n_matched);
+
+/* Resolve keys to the device addresses of their slots.  ENOTFOUND with
+ * *bad_index = first missing key. */
+OC_API int oc_store_lookup(oc_store* store, const oc_key* keys, uint64_t n, uint64_t* addrs,
+                           uint64_t* bad_index);
+
+/* Make `peer`'s chunks resolvable through `store` (peer keys are looked up
+ * after local ones).  `peer` must outlive `store`'s descriptors, and its slab
+ * must be readable from `store`'s GPU (same GPU, peer access, or host tier). */
+OC_API int oc_store_attach_peer(oc_store* store, oc_store* peer);
+
+/* Multi-process sharing of an HBM store (config 5, NVLink P2P):
+ * export writes an opaque blob (CUDA IPC handle + key table) of *size bytes
+ * (call with buf = NULL to query the size); import opens it in another process
+ * as a read-only peer store bound to GPU `device`, usable with attach_peer. */
+OC_API int oc_store_export(oc_store* store, void* buf, uint64_t* size);
+OC_API int oc_store_import(const void* buf, uint64_t size, int device, oc_store** out);
+
+/* ---- descriptor (Table 1) ------------------------------------ */
+typedef enum { OC_DELIVER_LAYER_MAJOR = 0, OC_DELIVER_CHUNK_MAJOR = 1 } oc_delivery;
+typedef enum { OC_TARGET_PAGED = 0, OC_TARGET_FLAT = 1 } oc_target_kind;
+
+/* The descriptor's rdma_target, made GPU-native (reading c4).
+ * PAGED: request token u (u = first_token + j*G + t for token t of chunk j),
+ *   matrix K or V, head h, at layer l is written to
+ *     {k,v}_base[l] + block_table[u / block_size]*block_stride
+ *                   + (u % block_size)*token_stride + h*head_stride
+ *   as d*p bytes.  NHD (vLLM FlashAttention): token_stride = row,
+ *   head_stride = d*p.  HND: token_stride = d*p, head_stride = block_size*d*p.
+ *   block_table[0 .. num_blocks) covers tokens [0, num_blocks*block_size);
+ *   the blocks used must be distinct and >= 0.  Slots outside the prefix are
+ *   not touched (reading c5).
+ * FLAT: the paper's client_buffer (Alg. A1 line 6): layer l's payload B_l of
+ *   N*S bytes at flat_base + l*N*S, chunk j at offset j*S; needs
+ *   flat_capacity >= N*L*S.
+ * Every base address, stride and d*p must be a multiple of 16 (EALIGN). */
+typedef struct {
+    uint32_t kind;
+    uint32_t block_size;
+    uint32_t first_token;
+    uint32_t reserved;
+    const uint64_t* k_base;      /* host array [L] of device addresses */
+    const uint64_t* v_base;      /* host array [L] of device addresses */
+    uint64_t block_stride;
+    uint64_t token_stride;
+    uint64_t head_stride;
+    const int32_t* block_table;  /* host array [num_blocks] */
+    uint64_t num_blocks;
+    uint64_t flat_base;          /* device address */
+    uint64_t flat_capacity;      /* bytes */
+} oc_target;
+
+typedef struct oc_desc oc_desc;
+
+/* build_descriptor: validate the request and resolve every key to its chunk
+ * slot (local store first, then attached peers), then upload the packed
+ * device descriptor {src[N], block table, K/V bases} with one H2D copy.
+ * Errors: EINVAL (n = 0, layout != store layout, duplicate/negative block ids,
+ * unknown kind), ENOTFOUND (*bad_index = first missing key in prefix order),
+ * ERANGE (target too small), EALIGN. */
+OC_API int oc_build_descriptor(oc_store* store, const oc_key* keys, uint64_t n, const oc_layout* layout,
+                               int delivery, const oc_target* target, oc_desc** out,
+                               uint64_t* bad_index);
+OC_API int oc_desc_free(oc_desc* desc);
+/* N, W = N*L*S, and the number of copy units per layer. */
+OC_API int oc_desc_info(const oc_desc* desc, uint64_t* n_chunks, uint64_t* payload_W,
+                        uint64_t* units_per_layer);
+
+/* ---- fetch (Alg. A1 on the GPU) ------------------------------------------ */
+typedef enum {
+    OC_FETCH_PERSISTENT = 0, /* one launch covers all layers; per-layer device
+                                counters; wait_layer = stream wait-value      */
+    OC_FETCH_PER_LAYER = 1,  /* one launch + one CUDA event per layer         */
+} oc_fetch_mode;
+
+typedef enum {
+    OC_COPY_LDST = 0,        /* 16-byte vector loads/stores through registers */
+    OC_COPY_BULK = 1,        /* TMA bulk copies through a shared-memory ring  */
+} oc_copy_engine;
+
+typedef struct {
+    uint32_t mode;           /* oc_fetch_mode                                   */
+    uint32_t engine;         /* oc_copy_engine                                  */
+    uint32_t max_ctas;       /* grid cap (SM budget when co-running); 0 = auto  */
+    uint32_t unit_bytes;     /* bytes per work unit; 0 = auto (32 KiB)          */
+    double pace_Bps;         /* minimal pacer: layer l is released no
+                                earlier than t0 + l*(N*S)/pace_Bps; 0 = off.
+                                PERSISTENT mode only.                           */
+} oc_fetch_opts;
+
+/* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and
+ * return at once.  One fetch may be in flight per descriptor at a time; a
+ * second fetch must be ordered after the first (same stream or an event).
+ * opts = NULL selects the defaults (persistent, LD/ST, auto grid, unpaced). */
+OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* copy_stream);
+
+/* wait_layer (NotifyLayerReady, Alg. A1 line 7): make `consumer_stream` wait,
+ * without blocking the host, until layer `layer` of the most recent fetch is
+ * in place.  Layers become ready in increasing order.  For CHUNK_MAJOR
+ * delivery every layer waits for the whole prefix (Eq. 2 chunkwise). */
+OC_API int oc_wait_layer(oc_desc* desc, uint32_t layer, void* consumer_stream);
+
+/* Host-blocking variant of wait_layer. */
+OC_API int oc_sync_layer(oc_desc* desc, uint32_t layer);
+
+/* Per-layer ready times of the most recent fetch, in ns of the GPU global
+ * timer: out[0] = kernel start, out[1 + l] = layer l ready.  Blocks until the
+ * fetch is complete.  `out` holds L + 1 values. */
+OC_API int oc_layer_times(oc_desc* desc, uint64_t* out);
+
+/* ---- bandwidth scheduling (Sec. 3.6) --------------------------- */
+typedef enum {
+    OC_POL_EQUAL = 0,         /* B / n                                    */
+    OC_POL_KV_PROP = 1,       /* proportional to s_i                      */
+    OC_POL_BW_PROP = 2,       /* proportional to r_i* = s_i / c_i         */
+    OC_POL_STALL_OPT = 3,     /* Eq. 6, caps r_i*                         */
+    OC_POL_CAL_STALL_OPT = 4, /* Eq. 7 + Alg. A2, caps r_i* + delta       */
+} oc_policy;
+
+typedef struct {
+    double bytes_per_layer;      /* s_i (bytes)   */
+    double compute_per_layer_s;  /* c_i (seconds) */
+} oc_profile;
+
+/* schedule_bandwidth: per-request rates (bytes/s) under the shared cap B.
+ * Stall-opt solves min sum s_i/r_i s.t. sum r_i = B, 0 < r_i <= cap_i by
+ * capped water-filling (r_i = min(cap_i, lambda*sqrt(s_i)), reading c8); if
+ * the caps fit in B each request gets its cap and the rest stays unused
+ * (reading c10).  EINVAL if B <= 0, delta < 0, or some s_i/c_i <= 0; n = 0 is
+ * OK.  Pure and thread-safe. */
+OC_API int oc_schedule_bandwidth(int policy, const oc_profile* profiles, uint64_t n, double cap_Bps,
+                                 double delta_Bps, double* rates_out);
+
+/* ---- errors ---------------------------------------------------------------- */
+OC_API const char* oc_last_error(void);
+OC_API const char* oc_status_str(int status);
+OC_API int oc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OBJCACHE_H */

@@ -1,0 +1,410 @@
+"""Python binding of libobjcache -- the B200-native ObjectCache hot path (arxiv 2605.22850).
+
+Argument marshalling only: every step of the path (hashing, matching, descriptor resolution,
+the layer-major gather + paged scatter kernels, layer-ready signalling, scheduling) runs inside
+``libobjcache.so`` (C ABI in ``include/objcache.h``).  There is no Python or CPU fallback: if the
+library is missing this import fails, and data-path calls on a machine without a GPU raise
+``ObjcacheError(OC_ECUDA)``.
+
+The boundary calls carry the names the paper's serving path uses (match -> descriptor
+-> layer-ready waits): ``put_chunks``, ``match_prefix``, ``build_descriptor``,
+``fetch_layerwise``, ``wait_layer``, ``schedule_bandwidth``.
+"""
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libobjcache.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2605_22850_b200.build` "
+                      "(there is no fallback implementation)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ---- constants (include/objcache.h) ------------------------------------------------------------
+OC_OK, OC_EINVAL, OC_ENOMEM, OC_ENOTFOUND, OC_EIMMUTABLE = 0, -1, -2, -3, -4
+OC_ERANGE, OC_EALIGN, OC_ECUDA, OC_EFULL, OC_ENOTSUP = -5, -6, -7, -8, -9
+TIER_HBM, TIER_PINNED_HOST = 0, 1
+DELIVER_LAYER_MAJOR, DELIVER_CHUNK_MAJOR = 0, 1
+TARGET_PAGED, TARGET_FLAT = 0, 1
+FETCH_PERSISTENT, FETCH_PER_LAYER = 0, 1
+COPY_LDST, COPY_BULK = 0, 1
+POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
+
+c_u8p = ctypes.POINTER(ctypes.c_uint8)
+c_u32p = ctypes.POINTER(ctypes.c_uint32)
+c_u64p = ctypes.POINTER(ctypes.c_uint64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+
+
+class CLayout(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_uint32), ("kv_heads", ctypes.c_uint32), ("head_dim", ctypes.c_uint32),
+                ("elem_bytes", ctypes.c_uint32), ("chunk_tokens", ctypes.c_uint32)]
+
+
+class CTarget(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_uint32), ("block_size", ctypes.c_uint32), ("first_token", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32), ("k_base", c_u64p), ("v_base", c_u64p),
+                ("block_stride", ctypes.c_uint64), ("token_stride", ctypes.c_uint64),
+                ("head_stride", ctypes.c_uint64), ("block_table", c_i32p), ("num_blocks", ctypes.c_uint64),
+                ("flat_base", ctypes.c_uint64), ("flat_capacity", ctypes.c_uint64)]
+
+
+class CFetchOpts(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_uint32), ("engine", ctypes.c_uint32), ("max_ctas", ctypes.c_uint32),
+                ("unit_bytes", ctypes.c_uint32), ("pace_Bps", ctypes.c_double)]
+
+
+class CProfile(ctypes.Structure):
+    _fields_ = [("bytes_per_layer", ctypes.c_double), ("compute_per_layer_s", ctypes.c_double)]
+
+
+_vp = ctypes.c_void_p
+_SIGS = {
+    "oc_geometry": [ctypes.POINTER(CLayout), c_u64p, c_u64p, c_u64p],
+    "oc_select_mode": [ctypes.c_uint64, ctypes.c_uint64],
+    "oc_sha256": [_vp, ctypes.c_uint64, c_u8p],
+    "oc_chunk_keys": [c_u32p, ctypes.c_uint64, ctypes.c_uint32, _vp, _vp, ctypes.c_uint64, c_u64p],
+    "oc_store_create": [ctypes.POINTER(CLayout), ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(_vp)],
+    "oc_store_destroy": [_vp],
+    "oc_store_count": [_vp, c_u64p],
+    "oc_store_slab": [_vp, c_u64p, c_u64p],
+    "oc_put_chunks": [_vp, _vp, _vp, ctypes.c_uint64, c_u64p, c_u64p],
+    "oc_match_prefix": [_vp, c_u32p, ctypes.c_uint64, _vp, _vp, ctypes.c_uint64, c_u64p],
+    "oc_store_lookup": [_vp, _vp, ctypes.c_uint64, c_u64p, c_u64p],
+    "oc_store_attach_peer": [_vp, _vp],
+    "oc_store_export": [_vp, _vp, c_u64p],
+    "oc_store_import": [_vp, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(_vp)],
+    "oc_build_descriptor": [_vp, _vp, ctypes.c_uint64, ctypes.POINTER(CLayout), ctypes.c_int,
+                            ctypes.POINTER(CTarget), ctypes.POINTER(_vp), c_u64p],
+    "oc_desc_free": [_vp],
+    "oc_desc_info": [_vp, c_u64p, c_u64p, c_u64p],
+    "oc_fetch_layerwise": [_vp, ctypes.POINTER(CFetchOpts), _vp],
+    "oc_wait_layer": [_vp, ctypes.c_uint32, _vp],
+    "oc_sync_layer": [_vp, ctypes.c_uint32],
+    "oc_layer_times": [_vp, c_u64p],
+    "oc_schedule_bandwidth": [ctypes.c_int, ctypes.POINTER(CProfile), ctypes.c_uint64, ctypes.c_double,
+                              ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
+    "oc_last_error": [],
+    "oc_status_str": [ctypes.c_int],
+    "oc_abi_version": [],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = ctypes.c_int
+_lib.oc_last_error.restype = ctypes.c_char_p
+_lib.oc_status_str.restype = ctypes.c_char_p
+
+EXPORTED = tuple(_SIGS)
+
+
+class ObjcacheError(RuntimeError):
+    def __init__(self, code, message, bad_index=None):
+        self.code = code
+        self.bad_index = bad_index
+        name = _lib.oc_status_str(code).decode()
+        super().__init__(f"{name}: {message}" + (f" (index {bad_index})" if bad_index is not None else ""))
+
+
+def _check(rc, bad_index=None):
+    if rc != OC_OK:
+        raise ObjcacheError(rc, _lib.oc_last_error().decode(errors="replace"),
+                            bad_index if rc in (OC_ENOTFOUND, OC_EIMMUTABLE, OC_EFULL) else None)
+
+
+# ---- helpers ------------------------------------------------------------------------------------
+def _layout(lay) -> CLayout:
+    if isinstance(lay, CLayout):
+        return lay
+    if hasattr(lay, "as_tuple"):
+        lay = lay.as_tuple()
+    elif hasattr(lay, "num_layers"):
+        lay = (lay.num_layers, lay.kv_heads, lay.head_dim, lay.elem_bytes, lay.chunk_tokens)
+    return CLayout(*[int(x) for x in lay])
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return int(stream.cuda_stream) or None
+    return int(stream) or None
+
+
+def _ptr(buf):
+    """(address, nbytes, keepalive) of a contiguous numpy array, torch tensor or bytes."""
+    if isinstance(buf, (bytes, bytearray)):
+        arr = np.frombuffer(buf, dtype=np.uint8)
+        return arr.ctypes.data, arr.nbytes, arr
+    if isinstance(buf, np.ndarray):
+        if not buf.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return buf.ctypes.data, buf.nbytes, buf
+    if hasattr(buf, "data_ptr"):  # torch.Tensor
+        if not buf.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return int(buf.data_ptr()), buf.numel() * buf.element_size(), buf
+    raise TypeError(f"unsupported buffer type {type(buf)}")
+
+
+def _keys_array(keys) -> np.ndarray:
+    if isinstance(keys, (list, tuple)) and keys and isinstance(keys[0], (bytes, bytearray)):
+        keys = np.frombuffer(b"".join(keys), dtype=np.uint8)
+    return np.ascontiguousarray(np.asarray(keys, dtype=np.uint8)).reshape(-1, 32)
+
+
+def geometry(layout):
+    """(row_bytes, S, chunk_bytes) of a layout (Eq. 1)."""
+    row, S, ch = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    lay = _layout(layout)
+    _check(_lib.oc_geometry(ctypes.byref(lay), ctypes.byref(row), ctypes.byref(S), ctypes.byref(ch)))
+    return row.value, S.value, ch.value
+
+
+def select_mode(payload_W: int, theta: int) -> int:
+    """Eq. 2 delivery mode (DELIVER_CHUNK_MAJOR if W < theta else DELIVER_LAYER_MAJOR)."""
+    return _lib.oc_select_mode(int(payload_W), int(theta))
+
+
+def sha256(data: bytes) -> bytes:
+    out = (ctypes.c_uint8 * 32)()
+    arr = np.frombuffer(bytes(data), dtype=np.uint8)
+    _check(_lib.oc_sha256(arr.ctypes.data if arr.size else None, arr.size, out))
+    return bytes(out)
+
+
+def chunk_keys(tokens, chunk_tokens: int, parent: Optional[bytes] = None) -> np.ndarray:
+    """[n, 32] uint8 keys of the complete chunk_tokens-blocks of ``tokens``."""
+    t = np.ascontiguousarray(np.asarray(tokens, dtype=np.uint32))
+    n = t.size // int(chunk_tokens) if chunk_tokens else 0
+    out = np.zeros((max(n, 1), 32), dtype=np.uint8)
+    par = np.frombuffer(bytes(parent), dtype=np.uint8) if parent is not None else None
+    cnt = ctypes.c_uint64()
+    _check(_lib.oc_chunk_keys(t.ctypes.data_as(c_u32p), t.size, int(chunk_tokens),
+                              par.ctypes.data if par is not None else None, out.ctypes.data, n, ctypes.byref(cnt)))
+    return out[:cnt.value]
+
+
+def schedule_bandwidth(policy, s: Sequence[float], c: Sequence[float], cap_Bps: float,
+                       delta_Bps: float = 0.0) -> np.ndarray:
+    """Per-request rates in bytes/s (Sec. 3.6).  ``policy``: name in POLICIES or its code."""
+    code = POLICIES[policy] if isinstance(policy, str) else int(policy)
+    n = len(s)
+    prof = (CProfile * max(n, 1))()
+    for i in range(n):
+        prof[i] = CProfile(float(s[i]), float(c[i]))
+    out = (ctypes.c_double * max(n, 1))()
+    _check(_lib.oc_schedule_bandwidth(code, prof, n, float(cap_Bps), float(delta_Bps), out))
+    return np.array(out[:n], dtype=np.float64)
+
+
+# ---- store ---------------------------------------------------------------------------------------
+class Store:
+    """Hash-addressed chunk store on one GPU (HBM slab or pinned, mapped host slab)."""
+
+    def __init__(self, layout, capacity: int, tier: int = TIER_HBM, device: int = 0, _handle=None):
+        self.layout = _layout(layout)
+        self._peers = []
+        if _handle is not None:
+            self._h = _handle
+        else:
+            h = _vp()
+            _check(_lib.oc_store_create(ctypes.byref(self.layout), int(tier), int(device), int(capacity),
+                                        ctypes.byref(h)))
+            self._h = h
+        self.tier, self.device = tier, device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.oc_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def count(self) -> int:
+        n = ctypes.c_uint64()
+        _check(_lib.oc_store_count(self._h, ctypes.byref(n)))
+        return n.value
+
+    @property
+    def slab(self):
+        b, n = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_lib.oc_store_slab(self._h, ctypes.byref(b), ctypes.byref(n)))
+        return b.value, n.value
+
+    def put_chunks(self, keys, payloads) -> int:
+        k = _keys_array(keys)
+        addr, nbytes, keep = _ptr(payloads)
+        if nbytes != k.shape[0] * geometry(self.layout)[2]:
+            raise ValueError("payloads must hold n * L * S bytes")
+        n_new, bad = ctypes.c_uint64(), ctypes.c_uint64()
+        rc = _lib.oc_put_chunks(self._h, k.ctypes.data, addr, k.shape[0], ctypes.byref(n_new), ctypes.byref(bad))
+        del keep
+        _check(rc, bad.value)
+        return n_new.value
+
+    def match_prefix(self, tokens, parent: Optional[bytes] = None) -> np.ndarray:
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.uint32))
+        G = self.layout.chunk_tokens
+        cap = t.size // G
+        out = np.zeros((max(cap, 1), 32), dtype=np.uint8)
+        par = np.frombuffer(bytes(parent), dtype=np.uint8) if parent is not None else None
+        m = ctypes.c_uint64()
+        _check(_lib.oc_match_prefix(self._h, t.ctypes.data_as(c_u32p), t.size,
+                                    par.ctypes.data if par is not None else None, out.ctypes.data, cap,
+                                    ctypes.byref(m)))
+        return out[:m.value]
+
+    def lookup(self, keys) -> np.ndarray:
+        k = _keys_array(keys)
+        out = np.zeros(max(k.shape[0], 1), dtype=np.uint64)
+        bad = ctypes.c_uint64()
+        _check(_lib.oc_store_lookup(self._h, k.ctypes.data, k.shape[0], out.ctypes.data_as(c_u64p),
+                                    ctypes.byref(bad)), bad.value)
+        return out[:k.shape[0]]
+
+    def attach_peer(self, peer: "Store"):
+        _check(_lib.oc_store_attach_peer(self._h, peer._h))
+        self._peers.append(peer)
+
+    def export(self) -> bytes:
+        n = ctypes.c_uint64()
+        _check(_lib.oc_store_export(self._h, None, ctypes.byref(n)))
+        buf = (ctypes.c_uint8 * n.value)()
+        _check(_lib.oc_store_export(self._h, buf, ctypes.byref(n)))
+        return bytes(buf[:n.value])
+
+    @classmethod
+    def import_(cls, blob: bytes, device: int = 0) -> "Store":
+        arr = np.frombuffer(blob, dtype=np.uint8)
+        h = _vp()
+        _check(_lib.oc_store_import(arr.ctypes.data, arr.size, int(device), ctypes.byref(h)))
+        lay = CLayout(*np.frombuffer(blob[8:28], dtype=np.uint32).tolist())
+        return cls(lay, 0, device=device, _handle=h)
+
+
+# ---- targets and descriptors ----------------------------------------------------------------------
+@dataclass
+class PagedTarget:
+    """Paged KV cache: see oc_target in include/objcache.h.  Addresses are device addresses."""
+    k_base: Sequence[int]
+    v_base: Sequence[int]
+    block_stride: int
+    token_stride: int
+    head_stride: int
+    block_size: int
+    block_table: Sequence[int]
+    first_token: int = 0
+
+
+@dataclass
+class FlatTarget:
+    """The paper's flat client buffer: layer l's payload at base + l*N*S."""
+    base: int
+    capacity: int
+
+
+class Descriptor:
+    def __init__(self, handle, store, layout, keepalive):
+        self._h = handle
+        self.store = store
+        self.layout = layout
+        self._keep = keepalive
+        self.num_layers = layout.num_layers
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.oc_desc_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def info(self):
+        n, W, u = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_lib.oc_desc_info(self._h, ctypes.byref(n), ctypes.byref(W), ctypes.byref(u)))
+        return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
+
+    def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_LDST, max_ctas=0, unit_bytes=0,
+                        pace_Bps=0.0):
+        o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps))
+        _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))
+
+    def wait_layer(self, layer: int, stream=None):
+        _check(_lib.oc_wait_layer(self._h, int(layer), _stream(stream)))
+
+    def sync_layer(self, layer: int):
+        _check(_lib.oc_sync_layer(self._h, int(layer)))
+
+    def layer_times(self) -> np.ndarray:
+        out = np.zeros(self.num_layers + 1, dtype=np.uint64)
+        _check(_lib.oc_layer_times(self._h, out.ctypes.data_as(c_u64p)))
+        return out
+
+
+def build_descriptor(store: Store, keys, layout, target, delivery: int = DELIVER_LAYER_MAJOR) -> Descriptor:
+    k = _keys_array(keys)
+    lay = _layout(layout)
+    t = CTarget()
+    keep = [k]
+    if isinstance(target, FlatTarget):
+        t.kind = TARGET_FLAT
+        t.flat_base = int(target.base)
+        t.flat_capacity = int(target.capacity)
+    elif isinstance(target, PagedTarget):
+        kb = np.ascontiguousarray(np.asarray(target.k_base, dtype=np.uint64))
+        vb = np.ascontiguousarray(np.asarray(target.v_base, dtype=np.uint64))
+        bt = np.ascontiguousarray(np.asarray(target.block_table, dtype=np.int32))
+        keep += [kb, vb, bt]
+        t.kind = TARGET_PAGED
+        t.block_size = int(target.block_size)
+        t.first_token = int(target.first_token)
+        t.k_base = kb.ctypes.data_as(c_u64p)
+        t.v_base = vb.ctypes.data_as(c_u64p)
+        t.block_stride, t.token_stride, t.head_stride = (int(target.block_stride), int(target.token_stride),
+                                                         int(target.head_stride))
+        t.block_table = bt.ctypes.data_as(c_i32p)
+        t.num_blocks = bt.size
+        if kb.size != lay.num_layers or vb.size != lay.num_layers:
+            raise ValueError("need one K and one V base per layer")
+    else:
+        raise TypeError("target must be PagedTarget or FlatTarget")
+    h, bad = _vp(), ctypes.c_uint64()
+    rc = _lib.oc_build_descriptor(store._h, k.ctypes.data, k.shape[0], ctypes.byref(lay), int(delivery),
+                                  ctypes.byref(t), ctypes.byref(h), ctypes.byref(bad))
+    _check(rc, bad.value)
+    return Descriptor(h, store, lay, store)
+
+
+# ---- the boundary calls, by the names the method uses ---------------------------------------------
+def put_chunks(store: Store, keys, payloads) -> int:
+    return store.put_chunks(keys, payloads)
+
+
+def match_prefix(store: Store, tokens, parent: Optional[bytes] = None) -> np.ndarray:
+    return store.match_prefix(tokens, parent)
+
+
+def fetch_layerwise(desc: Descriptor, stream=None, **opts):
+    desc.fetch_layerwise(stream, **opts)
+
+
+def wait_layer(desc: Descriptor, layer: int, stream=None):
+    desc.wait_layer(layer, stream)
+
+
+def abi_version() -> int:
+    return _lib.oc_abi_version()

@@ -1,0 +1,130 @@
+// Errors, geometry (Eq. 1), the Eq. 2 mode rule, fast division and driver entry points.
+#include <cuda.h>
+
+#include "oc_internal.h"
+
+namespace oc {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    cudaGetLastError();  // clear the sticky-free error state
+    return OC_ECUDA;
+}
+
+// Eq. 1: row = n_kv*d*p, S = 2*G*row, chunk = L*S.
+int make_geometry(const oc_layout* lay, Geometry* g) {
+    if (!lay) return fail(OC_EINVAL, "null layout");
+    if (!lay->num_layers || !lay->kv_heads || !lay->head_dim || !lay->elem_bytes || !lay->chunk_tokens)
+        return fail(OC_EINVAL, "layout fields must all be >= 1");
+    g->L = lay->num_layers; g->n_kv = lay->kv_heads; g->d = lay->head_dim;
+    g->p = lay->elem_bytes; g->G = lay->chunk_tokens;
+    unsigned __int128 row = (unsigned __int128)g->n_kv * g->d * g->p;
+    unsigned __int128 S = row * 2 * g->G;
+    unsigned __int128 chunk = S * g->L;
+    if (chunk >> 62) return fail(OC_EINVAL, "layout too large (L*S overflows)");
+    g->row = (uint64_t)row;
+    g->hd = (uint64_t)g->d * g->p;
+    g->S = (uint64_t)S;
+    g->chunk = (uint64_t)chunk;
+    return OC_OK;
+}
+
+bool same_layout(const oc_layout& a, const oc_layout& b) {
+    return a.num_layers == b.num_layers && a.kv_heads == b.kv_heads && a.head_dim == b.head_dim &&
+           a.elem_bytes == b.elem_bytes && a.chunk_tokens == b.chunk_tokens;
+}
+
+FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d ? d : 1;
+    uint32_t s = 0;
+    while ((1ull << s) < f.d) s++;
+    f.s = s;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << s) - f.d)) / f.d) + 1);
+    return f;
+}
+
+int device_sm_count(int device) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+namespace {
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+std::once_flag g_wait_once;
+PFN_wait32 g_wait32 = nullptr;
+}  // namespace
+
+// cuStreamWaitValue32(stream, addr, value, GEQ): the consumer stream stalls in the GPU front end
+// until (int32_t)(*addr - value) >= 0.  Resolved through the runtime so the library needs no
+// link-time libcuda (it must load on a machine without a driver).
+int stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t value) {
+    std::call_once(g_wait_once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &fn, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_wait32 = (PFN_wait32)fn;
+        cudaGetLastError();
+    });
+    if (!g_wait32) return fail(OC_ECUDA, "cuStreamWaitValue32 entry point unavailable");
+    CUresult r = g_wait32((CUstream)s, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(OC_ECUDA, "cuStreamWaitValue32 failed: CUresult " + std::to_string((int)r));
+    return OC_OK;
+}
+
+}  // namespace oc
+
+extern "C" {
+
+OC_API const char* oc_last_error(void) { return oc::g_last_error.c_str(); }
+
+OC_API const char* oc_status_str(int st) {
+    switch (st) {
+        case OC_OK: return "OC_OK";
+        case OC_EINVAL: return "OC_EINVAL";
+        case OC_ENOMEM: return "OC_ENOMEM";
+        case OC_ENOTFOUND: return "OC_ENOTFOUND";
+        case OC_EIMMUTABLE: return "OC_EIMMUTABLE";
+        case OC_ERANGE: return "OC_ERANGE";
+        case OC_EALIGN: return "OC_EALIGN";
+        case OC_ECUDA: return "OC_ECUDA";
+        case OC_EFULL: return "OC_EFULL";
+        case OC_ENOTSUP: return "OC_ENOTSUP";
+        default: return "OC_E?";
+    }
+}
+
+OC_API int oc_abi_version(void) { return OC_ABI_VERSION; }
+
+OC_API int oc_geometry(const oc_layout* layout, uint64_t* row_bytes, uint64_t* layer_chunk_bytes,
+                       uint64_t* chunk_bytes) {
+    oc::Geometry g;
+    int rc = oc::make_geometry(layout, &g);
+    if (rc) return rc;
+    if (row_bytes) *row_bytes = g.row;
+    if (layer_chunk_bytes) *layer_chunk_bytes = g.S;
+    if (chunk_bytes) *chunk_bytes = g.chunk;
+    return OC_OK;
+}
+
+// Eq. 2: chunkwise if W < Theta, else layerwise + aggregation.
+OC_API int oc_select_mode(uint64_t payload_W, uint64_t theta) {
+    return payload_W < theta ? OC_DELIVER_CHUNK_MAJOR : OC_DELIVER_LAYER_MAJOR;
+}
+
+}  // extern "C"

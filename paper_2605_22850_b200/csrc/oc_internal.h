@@ -1,0 +1,168 @@
+// Internal definitions shared by the host C++ and the CUDA kernels of libobjcache.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <shared_mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/objcache.h"
+
+namespace oc {
+
+// ---- errors ----------------------------------------------------------------
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define OC_CUDA(call)                                               \
+    do {                                                            \
+        cudaError_t oc_e_ = (call);                                 \
+        if (oc_e_ != cudaSuccess) return ::oc::cuda_fail(oc_e_, #call); \
+    } while (0)
+
+// Switch the calling thread's current device for the scope of a call.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; cudaGetLastError(); }
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ---- geometry ----------------------------------------------------------------
+struct Geometry {
+    uint32_t L, n_kv, d, p, G;
+    uint64_t row;    // n_kv*d*p
+    uint64_t hd;     // d*p
+    uint64_t S;      // 2*G*row
+    uint64_t chunk;  // L*S
+};
+int make_geometry(const oc_layout* lay, Geometry* g);
+bool same_layout(const oc_layout& a, const oc_layout& b);
+
+// ---- keys --------------------------------------------------------------------
+void sha256(const void* data, size_t n, uint8_t out[32]);
+void chunk_key(const uint8_t prev[32], const uint32_t* tokens, uint32_t G, uint8_t out[32]);
+
+struct KeyHash {
+    size_t operator()(const oc_key& k) const {
+        uint64_t h;
+        std::memcpy(&h, k.b, 8);  // SHA-256 output bits are uniform
+        return (size_t)h;
+    }
+};
+struct KeyEq {
+    bool operator()(const oc_key& a, const oc_key& b) const { return std::memcmp(a.b, b.b, 32) == 0; }
+};
+
+// ---- fast division for 32-bit numerators (Granlund-Montgomery round-up) -----
+struct FastDiv {
+    uint32_t d, m, s;
+};
+FastDiv make_fastdiv(uint32_t d);
+
+__host__ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+#ifdef __CUDA_ARCH__
+    uint64_t t = (uint64_t)__umulhi(n, f.m) + n;
+#else
+    uint64_t t = (((uint64_t)n * f.m) >> 32) + n;
+#endif
+    return (uint32_t)(t >> f.s);
+}
+
+// ---- store -------------------------------------------------------------------
+struct Store {
+    oc_layout layout;
+    Geometry geo;
+    int tier;
+    int device;
+    uint64_t capacity;
+    uint8_t* slab = nullptr;  // device address (HBM, mapped host, or IPC-mapped peer)
+    bool owns_slab = true;
+    bool ipc_mapped = false;
+    bool read_only = false;
+    uint64_t count = 0;
+    std::unordered_map<oc_key, uint64_t, KeyHash, KeyEq> index;  // key -> slot
+    std::vector<Store*> peers;
+    mutable std::shared_mutex mu;
+    cudaStream_t put_stream = nullptr;
+};
+// Resolve a key to a device address: local slots first, then peers.  Caller holds no lock.
+bool store_resolve(Store* s, const oc_key& k, uint64_t* addr);
+
+// ---- device descriptor -----------------------------------------------------------
+// Everything the copy kernel needs, passed by value as a kernel parameter.
+struct DevDesc {
+    const uint64_t* src;      // [N] chunk slot device addresses
+    const int32_t* bt;        // block table (first entry = block of token 0)
+    const uint64_t* k_base;   // [L]
+    const uint64_t* v_base;   // [L]
+    uint32_t* unit_cnt;       // [L] units completed (monotone across fetches)
+    uint32_t* done_epoch;     // [L] epoch in which layer l completed
+    uint32_t* ready;          // [1] leading complete layers, monotone: (epoch-1)*L + r
+    uint64_t* ts;             // [L+1] globaltimer: [0] kernel start, [1+l] layer ready
+    uint32_t* host_ready;     // [L] mapped pinned host: epoch once layers 0..l are ready
+    uint64_t S;               // bytes of one layer of one chunk
+    uint64_t row;             // bytes of one token row (n_kv*d*p)
+    uint64_t block_stride, token_stride, head_stride;
+    uint32_t N, L, G, Bs, first_token;
+    uint32_t rows_per_unit;   // R
+    uint32_t tiles;           // ceil(G / R) tiles per K or V half of a chunk-layer
+    uint32_t units_per_layer; // N * 2 * tiles
+    uint32_t vpr;             // 16-byte vectors per row
+    uint32_t nhd;             // 1: a row is contiguous in the destination
+    uint32_t epoch;           // fetch sequence number (>= 1)
+    uint32_t chunk_major;     // 1: only the completion of the whole prefix is announced
+    uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
+    FastDiv div_units_per_chunk;  // 2*tiles
+    FastDiv div_tiles;
+    FastDiv div_vpr;
+    FastDiv div_Bs;
+    FastDiv div_hdv;          // (d*p)/16
+};
+
+struct Desc {
+    Store* store;
+    Geometry geo;
+    oc_layout layout;
+    int device;
+    int delivery;
+    uint64_t N;
+    uint64_t nb;               // block table entries uploaded
+    void* dev_mem = nullptr;   // one allocation: src, k/v base, ts, counters, block table
+    uint32_t* host_ready = nullptr;  // [L] from the pinned host pool
+    DevDesc dd;                // geometry part filled at build; epoch/units/pace at fetch
+    uint32_t epoch = 0;
+    uint32_t last_mode = OC_FETCH_PERSISTENT;
+    bool fetched = false;
+    std::vector<cudaEvent_t> events;  // per-layer (PER_LAYER mode), created lazily
+    cudaEvent_t done_ev = nullptr;    // recorded after every fetch launch
+    cudaStream_t last_stream = nullptr;
+};
+
+// Plan work units of about `unit_bytes` bytes and fill the unit fields of d->dd.
+void plan_units(Desc* d, uint32_t unit_bytes);
+
+// kernel launchers (fetch.cu)
+int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s);
+
+// small pinned, mapped host words (layer-ready mirrors)
+uint32_t* host_words_alloc(uint32_t n);
+void host_words_free(uint32_t* p, uint32_t n);
+
+// driver entry point for cuStreamWaitValue32 (resolved lazily)
+int stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t value);
+
+int device_sm_count(int device);
+
+}  // namespace oc

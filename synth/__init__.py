@@ -75,8 +75,9 @@ def family_streams(seed: int, G: int, shared_blocks: int, own_blocks, tail_token
 def chunk_payload(seed: int, payload_id, nbytes: int) -> np.ndarray:
     """nbytes of PCG64 output for one chunk (uint8)."""
     owner, block = payload_id
-    rng = np.random.Generator(np.random.PCG64([seed, 0xC4C4, int(owner), int(block)]))
-    return np.frombuffer(rng.bytes(nbytes), dtype=np.uint8)
+    bg = np.random.PCG64([seed, 0xC4C4, int(owner), int(block)])
+    words = bg.random_raw(-(-nbytes // 8)).astype(np.uint64, copy=False)
+    return words.view(np.uint8)[:nbytes]
 
 
 def payloads(seed: int, payload_ids, nbytes: int) -> np.ndarray:
