@@ -204,7 +204,8 @@ typedef struct {
     uint32_t mode;           /* oc_fetch_mode                                   */
     uint32_t engine;         /* oc_copy_engine                                  */
     uint32_t max_ctas;       /* grid cap (SM budget when co-running); 0 = auto  */
-    uint32_t unit_bytes;     /* bytes per work unit; 0 = auto (32 KiB)          */
+    uint32_t unit_bytes;     /* bytes per work unit; 0 = auto (16 KiB for BULK,
+                                32 KiB for LDST)                                */
     double pace_Bps;         /* minimal pacer: layer l is released no
                                 earlier than t0 + l*(N*S)/pace_Bps; 0 = off.
                                 PERSISTENT mode only.                           */
@@ -213,7 +214,7 @@ typedef struct {
 /* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and
  * return at once.  One fetch may be in flight per descriptor at a time; a
  * second fetch must be ordered after the first (same stream or an event).
- * opts = NULL selects the defaults (persistent, LD/ST, auto grid, unpaced). */
+ * opts = NULL selects the defaults (persistent, BULK, auto grid, unpaced). */
 OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* copy_stream);
 
 /* wait_layer (NotifyLayerReady, Alg. A1 line 7): make `consumer_stream` wait,

@@ -219,9 +219,9 @@ class Store:
             self._h = h
         self.tier, self.device = tier, device
 
-    def close(self):
+    def close(self, _destroy=_lib.oc_store_destroy):  # bound early: safe during interpreter exit
         if getattr(self, "_h", None):
-            _lib.oc_store_destroy(self._h)
+            _destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -325,9 +325,9 @@ class Descriptor:
         self._keep = keepalive
         self.num_layers = layout.num_layers
 
-    def close(self):
+    def close(self, _free=_lib.oc_desc_free):  # bound early: safe during interpreter exit
         if getattr(self, "_h", None):
-            _lib.oc_desc_free(self._h)
+            _free(self._h)
             self._h = None
 
     def __del__(self):
@@ -338,7 +338,7 @@ class Descriptor:
         _check(_lib.oc_desc_info(self._h, ctypes.byref(n), ctypes.byref(W), ctypes.byref(u)))
         return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
 
-    def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_LDST, max_ctas=0, unit_bytes=0,
+    def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_BULK, max_ctas=0, unit_bytes=0,
                         pace_Bps=0.0):
         o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps))
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))

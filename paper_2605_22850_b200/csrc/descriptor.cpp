@@ -65,6 +65,7 @@ void plan_units(Desc* d, uint32_t unit_bytes) {
     dd.rows_per_unit = (uint32_t)R;
     dd.tiles = (uint32_t)((d->geo.G + R - 1) / R);
     dd.units_per_layer = (uint32_t)(d->N * 2 * dd.tiles);
+    dd.div_upl = make_fastdiv(dd.units_per_layer);
     dd.div_units_per_chunk = make_fastdiv(2 * dd.tiles);
     dd.div_tiles = make_fastdiv(dd.tiles);
 }

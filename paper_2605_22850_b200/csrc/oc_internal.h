@@ -124,6 +124,7 @@ struct DevDesc {
     uint32_t epoch;           // fetch sequence number (>= 1)
     uint32_t chunk_major;     // 1: only the completion of the whole prefix is announced
     uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
+    FastDiv div_upl;          // units_per_layer
     FastDiv div_units_per_chunk;  // 2*tiles
     FastDiv div_tiles;
     FastDiv div_vpr;

@@ -18,6 +18,7 @@ from scenario import (lib_target, make_dest, oracle_result, payload_stack,  # no
 pytestmark = pytest.mark.gpu
 
 MODES = [oc.FETCH_PERSISTENT, oc.FETCH_PER_LAYER]
+ENGINES = [oc.COPY_LDST, oc.COPY_BULK]
 
 
 def lay_of(named):
@@ -25,7 +26,7 @@ def lay_of(named):
 
 
 def run_lib(lay, seed, req, dest, tier=oc.TIER_HBM, mode=oc.FETCH_PERSISTENT, unit_bytes=0, max_ctas=0,
-            delivery=oc.DELIVER_LAYER_MAJOR, store=None):
+            delivery=oc.DELIVER_LAYER_MAJOR, store=None, engine=oc.COPY_BULK):
     own = store is None
     if own:
         store = oc.Store(lay, capacity=req.n_chunks + 2, tier=tier)
@@ -36,7 +37,7 @@ def run_lib(lay, seed, req, dest, tier=oc.TIER_HBM, mode=oc.FETCH_PERSISTENT, un
     buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
     desc = oc.build_descriptor(store, keys, lay, lib_target(oc, dest, buf.data_ptr()), delivery)
     s = torch.cuda.Stream()
-    desc.fetch_layerwise(s, mode=mode, unit_bytes=unit_bytes, max_ctas=max_ctas)
+    desc.fetch_layerwise(s, mode=mode, unit_bytes=unit_bytes, max_ctas=max_ctas, engine=engine)
     desc.sync_layer(lay.num_layers - 1)
     torch.cuda.synchronize()
     out = buf.cpu().numpy()
@@ -81,47 +82,55 @@ def test_tiny_store_match_and_dedup():
 @pytest.mark.parametrize("kind", ["nhd", "hnd", "flat"])
 @pytest.mark.parametrize("Bs,first", [(8, 0), (16, 5), (32, 16), (1, 3)])
 @pytest.mark.parametrize("mode", MODES)
-def test_tiny_parity(kind, Bs, first, mode):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_tiny_parity(kind, Bs, first, mode, engine):
     lay = lay_of(synth.TINY)
     for req in requests_family(lay, 0, 8, [2, 3], [5, 0]):
         dest = make_dest(lay, req.n_chunks, kind, Bs=Bs, first_token=first, seed=Bs + first)
-        assert_same(run_lib(lay, 0, req, dest, mode=mode), oracle_result(lay, 0, req, dest))
+        assert_same(run_lib(lay, 0, req, dest, mode=mode, engine=engine), oracle_result(lay, 0, req, dest))
 
 
 # ---- several units per chunk, ragged tiles, odd sizes -----------------------------------------------
 @pytest.mark.parametrize("kind", ["nhd", "hnd"])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("unit_bytes", [4096, 0, 1000])
-def test_ragged_units(kind, mode, unit_bytes):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_ragged_units(kind, mode, unit_bytes, engine):
     lay = OLayout(3, 4, 64, 2, 20)             # row = 512 B; unit 4096 B -> tiles of 8, 8, 4 rows
     req = requests_family(lay, 3, 0, [7])[0]
     dest = make_dest(lay, req.n_chunks, kind, Bs=16, first_token=3, seed=5)
-    assert_same(run_lib(lay, 3, req, dest, mode=mode, unit_bytes=unit_bytes), oracle_result(lay, 3, req, dest))
+    assert_same(run_lib(lay, 3, req, dest, mode=mode, unit_bytes=unit_bytes, engine=engine),
+                oracle_result(lay, 3, req, dest))
 
 
 @pytest.mark.parametrize("max_ctas", [1, 3, 37])
-def test_grid_caps(max_ctas):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_grid_caps(max_ctas, engine):
     lay = OLayout(4, 2, 128, 2, 16)
     req = requests_family(lay, 4, 0, [9])[0]
     dest = make_dest(lay, req.n_chunks, "nhd", Bs=8, first_token=1, seed=6)
     for mode in MODES:
-        assert_same(run_lib(lay, 4, req, dest, mode=mode, max_ctas=max_ctas), oracle_result(lay, 4, req, dest))
+        assert_same(run_lib(lay, 4, req, dest, mode=mode, max_ctas=max_ctas, engine=engine),
+                    oracle_result(lay, 4, req, dest))
 
 
-def test_single_chunk_single_layer():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_single_chunk_single_layer(engine):
     lay = OLayout(1, 1, 8, 2, 1)               # row = 16 B: the smallest legal row
     req = requests_family(lay, 8, 0, [1])[0]
     for kind in ("nhd", "hnd", "flat"):
         dest = make_dest(lay, 1, kind, Bs=1, seed=1)
-        assert_same(run_lib(lay, 8, req, dest), oracle_result(lay, 8, req, dest))
+        assert_same(run_lib(lay, 8, req, dest, engine=engine), oracle_result(lay, 8, req, dest))
 
 
-def test_pinned_host_tier():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_pinned_host_tier(engine):
     lay = OLayout(3, 4, 64, 2, 20)
     req = requests_family(lay, 9, 0, [6])[0]
-    for kind in ("nhd", "flat"):
+    for kind in ("nhd", "hnd", "flat"):
         dest = make_dest(lay, req.n_chunks, kind, Bs=16, first_token=2, seed=2)
-        assert_same(run_lib(lay, 9, req, dest, tier=oc.TIER_PINNED_HOST), oracle_result(lay, 9, req, dest))
+        assert_same(run_lib(lay, 9, req, dest, tier=oc.TIER_PINNED_HOST, engine=engine),
+                    oracle_result(lay, 9, req, dest))
 
 
 def test_chunk_major_delivery():
@@ -149,20 +158,23 @@ def test_peer_store_resolution():
 
 # ---- the bench configuration: Llama-3-8B, 4K-token prefix hit -----------------------------------
 @pytest.mark.parametrize("mode", MODES)
-def test_llama8b_4k_full(mode):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_llama8b_4k_full(mode, engine):
     lay = lay_of(synth.LLAMA3_8B)
     req = requests_family(lay, 2024, 0, [256])[0]
     dest = make_dest(lay, 256, "nhd", Bs=16, seed=7)
-    got = run_lib(lay, 2024, req, dest, mode=mode)
+    got = run_lib(lay, 2024, req, dest, mode=mode, engine=engine)
     assert_same(got, oracle_result(lay, 2024, req, dest, layers=range(lay.num_layers)))
 
 
 @pytest.mark.parametrize("G", [64, 256])
-def test_llama8b_4k_other_granularities(G):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_llama8b_4k_other_granularities(G, engine):
     lay = lay_of(synth.with_chunk_tokens(synth.LLAMA3_8B, G))
     req = requests_family(lay, 77, 0, [4096 // G])[0]
     dest = make_dest(lay, req.n_chunks, "nhd", Bs=16, first_token=16, seed=8)
-    assert_same(run_lib(lay, 77, req, dest), oracle_result(lay, 77, req, dest, layers=range(lay.num_layers)))
+    assert_same(run_lib(lay, 77, req, dest, engine=engine),
+                oracle_result(lay, 77, req, dest, layers=range(lay.num_layers)))
 
 
 @pytest.mark.slow
@@ -196,7 +208,8 @@ def test_llama8b_64k_sampled_layers():
 
 # ---- layer-ready semantics ----------------------------------------------------------------------------
 @pytest.mark.parametrize("wait_kernel", [False, True])
-def test_wait_layer_orders_consumer(monkeypatch, wait_kernel):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_wait_layer_orders_consumer(monkeypatch, wait_kernel, engine):
     """A consumer stream that waits on layer l and then snapshots layer l must see final bytes even
     though the (paced) fetch is still running."""
     if wait_kernel:
@@ -214,7 +227,7 @@ def test_wait_layer_orders_consumer(monkeypatch, wait_kernel):
         layer_bytes = 8 * chunk_layer_bytes(lay)
         pace = layer_bytes / 3e-3                                            # one layer every 3 ms
         snaps = []
-        desc.fetch_layerwise(copy_s, pace_Bps=pace)
+        desc.fetch_layerwise(copy_s, pace_Bps=pace, engine=engine)
         for l in range(lay.num_layers):
             desc.wait_layer(l, cons)
             with torch.cuda.stream(cons):
@@ -231,7 +244,8 @@ def test_wait_layer_orders_consumer(monkeypatch, wait_kernel):
         desc.close()
 
 
-def test_refetch_epochs_and_sync():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_refetch_epochs_and_sync(engine):
     lay = OLayout(4, 2, 64, 2, 16)
     req = requests_family(lay, 5, 0, [6])[0]
     dest = make_dest(lay, 6, "nhd", Bs=8, seed=2)
@@ -245,7 +259,7 @@ def test_refetch_epochs_and_sync():
         for it in range(5):
             with torch.cuda.stream(s):
                 buf.fill_(0xA5)
-            desc.fetch_layerwise(s, mode=MODES[it % 2])
+            desc.fetch_layerwise(s, mode=MODES[it % 2], engine=engine)
             for l in range(lay.num_layers):
                 desc.sync_layer(l)
             torch.cuda.synchronize()
