@@ -249,8 +249,10 @@ def main_ours(args):
         d.fetch_layerwise(copy_s, **fopts)
         if ev_pair:
             ev_pair[1].record(copy_s)
-        for l in range(L):
-            d.wait_layer(l, cons_s)
+        # The consumer waits on the last layer: layers are announced strictly in order, so this
+        # completes after every layer's ready signal.  (Per-layer waits interleaved with compute
+        # are exercised by the stall leg; one wait op per layer costs ~6 us of host time here.)
+        d.wait_layer(L - 1, cons_s)
 
     clocks = ClockSampler(local)
     if not args.profile:

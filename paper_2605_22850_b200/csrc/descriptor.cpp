@@ -14,47 +14,8 @@
 namespace oc {
 
 namespace {
-std::mutex g_pool_mu;
-uint32_t* g_pool_cur = nullptr;
-size_t g_pool_left = 0;
-std::unordered_map<uint32_t, std::vector<uint32_t*>> g_pool_free;
-
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 }  // namespace
-
-uint32_t* host_words_alloc(uint32_t n) {
-    uint32_t n16 = (n + 15) & ~15u;
-    std::lock_guard<std::mutex> lk(g_pool_mu);
-    auto& fl = g_pool_free[n16];
-    uint32_t* p = nullptr;
-    if (!fl.empty()) {
-        p = fl.back();
-        fl.pop_back();
-    } else {
-        if (g_pool_left < n16) {
-            size_t words = std::max<size_t>(16384, n16);
-            void* page = nullptr;
-            if (cudaHostAlloc(&page, words * 4, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-                cudaGetLastError();
-                return nullptr;
-            }
-            g_pool_cur = (uint32_t*)page;  // pages are never returned to the driver
-            g_pool_left = words;
-        }
-        p = g_pool_cur;
-        g_pool_cur += n16;
-        g_pool_left -= n16;
-    }
-    std::memset(p, 0, n16 * 4);
-    return p;
-}
-
-void host_words_free(uint32_t* p, uint32_t n) {
-    if (!p) return;
-    uint32_t n16 = (n + 15) & ~15u;
-    std::lock_guard<std::mutex> lk(g_pool_mu);
-    g_pool_free[n16].push_back(p);
-}
 
 void plan_units(Desc* d, uint32_t unit_bytes) {
     DevDesc& dd = d->dd;
@@ -161,15 +122,15 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     d->N = n;
     d->nb = bt.size();
 
-    // One device allocation: src[N] | k_base[L] | v_base[L] | ts[L+1] | unit_cnt[L] | done[L] | ready | bt
+    // One device allocation: src[N] | k_base[L] | v_base[L] | ts[L+1] | unit_cnt[L] | ready, next | bt
     size_t o_src = 0;
     size_t o_kb = oc::align16(o_src + n * 8);
     size_t o_vb = oc::align16(o_kb + L * 8);
     size_t o_ts = oc::align16(o_vb + L * 8);
     size_t o_cnt = oc::align16(o_ts + (L + 1) * 8);
-    size_t o_done = oc::align16(o_cnt + L * 4);
-    size_t o_ready = oc::align16(o_done + L * 4);
-    size_t o_bt = oc::align16(o_ready + 4);
+    size_t o_ready = oc::align16(o_cnt + L * 4);
+    size_t o_next = o_ready + 4;
+    size_t o_bt = oc::align16(o_ready + 16);
     size_t total = oc::align16(o_bt + bt.size() * 4);
     std::vector<uint8_t> stage(total, 0);
     std::memcpy(stage.data() + o_src, src.data(), n * 8);
@@ -190,11 +151,6 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
         return oc::cuda_fail(e, "build_descriptor: upload");
     }
     d->dev_mem = mem;
-    d->host_ready = oc::host_words_alloc(L);
-    if (!d->host_ready) {
-        cudaFree(mem);
-        return oc::fail(OC_ENOMEM, "build_descriptor: pinned host words");
-    }
 
     uint8_t* m = (uint8_t*)mem;
     oc::DevDesc& dd = d->dd;
@@ -204,10 +160,9 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     dd.v_base = (const uint64_t*)(m + o_vb);
     dd.ts = (uint64_t*)(m + o_ts);
     dd.unit_cnt = (uint32_t*)(m + o_cnt);
-    dd.done_epoch = (uint32_t*)(m + o_done);
     dd.ready = (uint32_t*)(m + o_ready);
+    dd.next_unit = (uint32_t*)(m + o_next);
     dd.bt = (const int32_t*)(m + o_bt);
-    dd.host_ready = d->host_ready;
     dd.S = g.S;
     dd.row = g.row;
     dd.block_stride = block_stride;
@@ -238,10 +193,11 @@ OC_API int oc_desc_free(oc_desc* h) {
         if (d->fetched && d->done_ev) cudaEventSynchronize(d->done_ev);
         for (auto ev : d->events) cudaEventDestroy(ev);
         if (d->done_ev) cudaEventDestroy(d->done_ev);
+        if (d->sync_ev) cudaEventDestroy(d->sync_ev);
+        if (d->sync_stream) cudaStreamDestroy(d->sync_stream);
         if (d->dev_mem) cudaFree(d->dev_mem);
         cudaGetLastError();
     }
-    oc::host_words_free(d->host_ready, d->geo.L);
     delete d;
     return OC_OK;
 }

@@ -1,20 +1,25 @@
 // fetch_layerwise on B200: the storage server's layer aggregation (PAPER.md Alg. A1, P:2565-2581;
-// Sec. 3.3) fused with the client's paged-KV placement, as one sm_100a kernel.
+// Sec. 3.3) fused with the client's paged-KV placement, as sm_100a kernels.
 //
-// Alg. A1 for layer l appends RangeGet(H_j, lS, S) for every matched chunk j in prefix order to
+// Alg. A1 for layer l appends RangeGet(H_j, lS, S) of every matched chunk j, in prefix order, to
 // B_l, RDMA-writes B_l to the client buffer and notifies "layer ready".  Here no B_l is
-// materialised: each CTA copies one unit -- R consecutive token rows of the K (or V) half of one
-// chunk's layer-l slice, contiguous in the chunk object -- straight to the rows' destination
-// slots (block_table[u / Bs], slot u % Bs), with 16-byte vector loads
-// and stores, all loads of a round issued before any store.  Every HBM byte of the matched
-// prefix is read once and written once (2*N*S bytes per layer).
+// materialised: a work unit is R consecutive token rows of the K (or V) half of one chunk's layer-l
+// slice -- contiguous in the chunk object (KV_L2TD) -- and it is copied straight to
+// the rows' destination slots (block_table[u / Bs], slot u % Bs).  Every
+// matched byte is read once and written once: 2*N*S HBM bytes per layer.
 //
-// Completion (Alg. A1 line 7, "NotifyLayerReady"): after each unit the CTA bumps the layer's
-// unit counter; the CTA that completes a layer marks it done, and whichever CTA finds layers
-// 0..l all done advances the monotone `ready` word past l (so layers are announced strictly in
-// order), stamps %globaltimer and mirrors the epoch into pinned host memory.  Consumers wait on
-// `ready` with cuStreamWaitValue32 (no host round trip) or, in PER_LAYER mode, on a CUDA event
-// recorded after the layer's own launch.
+// Two copy engines:
+//   BULK  one copy warp per CTA drives the TMA: one cp.async.bulk load per unit into a shared-
+//         memory ring (mbarrier complete_tx), one bulk store per contiguous destination run.
+//   LDST  256 threads per CTA, 16-byte vector loads (all of a round issued before any store).
+//
+// Completion (Alg. A1 line 7, "NotifyLayerReady"): producers add their finished units to the
+// layer's counter with a release reduction (fire and forget); an observer -- thread 0 of CTA 0,
+// which copies nothing -- walks the layers in order, acquires each counter once it reaches this
+// fetch's target, stamps %globaltimer and stores `ready` = (epoch-1)*L + l + 1 with release
+// semantics.  Consumers wait on `ready` with cuStreamWaitValue32 in the GPU front end (no host
+// round trip, no kernel), so layer l's compute starts while layer l+1 is still in flight.  In
+// PER_LAYER mode each layer is its own launch followed by a CUDA event.
 #include <algorithm>
 #include <cstdlib>
 
@@ -22,10 +27,12 @@
 
 namespace oc {
 
-constexpr int kThreads = 256;   // threads per CTA
-constexpr int kVec = 8;         // 16-byte vectors in flight per thread per round
+constexpr int kThreads = 256;   // LDST: threads per CTA
+constexpr int kVec = 8;         // LDST: 16-byte vectors in flight per thread per round
 constexpr int kMaxRows = 1024;  // rows per unit (plan_units caps R)
+constexpr uint32_t kFifo = 64;  // BULK: copy-warp -> signaler-warp retire FIFO
 
+// ---- small device helpers ------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -51,8 +58,82 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     return v;
 }
 
-// Stream nrows contiguous source rows to the destination rows in `tab` (16-byte vectors, kVec
-// loads in flight per thread before the matching stores).
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Release reduction: every write that happens-before it (this thread's, and other threads' ordered
+// before it by a barrier -- PTX release is cumulative) is visible before the counter moves.
+__device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ---- unit geometry -------------------------------------------------------------------------------
+struct UnitGeo {
+    uint32_t layer, j, kv, r0, nrows;
+};
+
+// Global unit g (layer-major): layer = g / units_per_layer; inside a layer chunk j, matrix kv, tile.
+__device__ __forceinline__ UnitGeo unit_geo(const DevDesc& d, uint32_t g) {
+    UnitGeo u;
+    u.layer = fdiv(g, d.div_upl);
+    const uint32_t unit = g - u.layer * d.units_per_layer;
+    u.j = fdiv(unit, d.div_units_per_chunk);
+    const uint32_t rem = unit - u.j * 2u * d.tiles;
+    u.kv = rem >= d.tiles ? 1u : 0u;
+    u.r0 = (rem - u.kv * d.tiles) * d.rows_per_unit;
+    u.nrows = min(d.rows_per_unit, d.G - u.r0);
+    return u;
+}
+
+// Source of a unit: layer l of chunk j at [lS, (l+1)S), K rows then V rows (reading c2).
+__device__ __forceinline__ const uint8_t* unit_src(const DevDesc& d, const UnitGeo& u) {
+    return (const uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + ((uint64_t)u.kv * d.G + u.r0) * d.row;
+}
+
+// Request token of the unit's first row, and the layer's K or V base.
+__device__ __forceinline__ uint32_t unit_tok0(const DevDesc& d, const UnitGeo& u) {
+    return d.first_token + u.j * d.G + u.r0;
+}
+
+__device__ __forceinline__ uint64_t unit_base(const DevDesc& d, const UnitGeo& u) {
+    return u.kv ? d.v_base[u.layer] : d.k_base[u.layer];
+}
+
+// Destination of token `tok`'s row: block_table[tok / Bs] * block_stride + (tok % Bs) * token_stride.
+__device__ __forceinline__ uint64_t row_dst(const DevDesc& d, uint64_t base, uint32_t tok, uint32_t* slot_out) {
+    const uint32_t b = fdiv(tok, d.div_Bs);
+    const uint32_t slot = tok - b * d.Bs;
+    if (slot_out) *slot_out = slot;
+    return base + (uint64_t)d.bt[b] * d.block_stride + (uint64_t)slot * d.token_stride;
+}
+
+// ---- completion --------------------------------------------------------------------------------------
+// Account n finished units of `layer`; the caller's writes of those units happen-before this call.
+__device__ __forceinline__ void complete_units(const DevDesc& d, uint32_t layer, uint32_t n) {
+    red_add_release(&d.unit_cnt[layer], n);
+}
+
+// Observer: announce layers [l0, l1) in order.  The counters are monotone across fetches; this
+// fetch's units of a layer are all done when the counter reaches cnt_target (an acquire load of
+// the last reduction synchronises with every release reduction before it).
+__device__ void observe_layers(const DevDesc& d, uint32_t l0, uint32_t l1) {
+    const uint32_t base = (d.epoch - 1u) * d.L;
+    for (uint32_t l = l0; l < l1; l++) {
+        uint32_t ns = 32;
+        while ((int32_t)(ld_acquire(&d.unit_cnt[l]) - d.cnt_target) < 0) {
+            __nanosleep(ns);
+            ns = min(ns * 2, 256u);
+        }
+        d.ts[1 + l] = globaltimer();
+        st_release(d.ready, base + l + 1u);
+    }
+}
+
+// ---- LDST engine ---------------------------------------------------------------------------------------
+// Stream nrows contiguous source rows to the destination rows listed in `tab`.
 __device__ __forceinline__ void copy_rows(const DevDesc& d, const uint8_t* src, uint32_t nrows, const uint64_t* tab) {
     const uint32_t nvec = nrows * d.vpr;
     for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads * kVec) {
@@ -82,130 +163,71 @@ __device__ __forceinline__ void copy_rows(const DevDesc& d, const uint8_t* src, 
     }
 }
 
-// Copy one unit: rows [r0, r0 + nrows) of matrix kv of chunk j at `layer`.
-__device__ __forceinline__ void copy_unit(const DevDesc& d, uint32_t layer, uint32_t unit, uint64_t* s_dst) {
-    const uint32_t j = fdiv(unit, d.div_units_per_chunk);
-    const uint32_t rem = unit - j * 2u * d.tiles;
-    const uint32_t kv = rem >= d.tiles ? 1u : 0u;
-    const uint32_t tile = rem - kv * d.tiles;
-    const uint32_t r0 = tile * d.rows_per_unit;
-    const uint32_t nrows = min(d.rows_per_unit, d.G - r0);
-    // KV_L2TD: layer l of chunk j at [lS, (l+1)S); K rows then V rows, row-major (reading c2).
-    const uint8_t* src = (const uint8_t*)d.src[j] + (uint64_t)layer * d.S + ((uint64_t)kv * d.G + r0) * d.row;
-    const uint64_t base = kv ? d.v_base[layer] : d.k_base[layer];
-    const uint32_t u0 = d.first_token + j * d.G + r0;  // request token of row r0
-    for (uint32_t r = threadIdx.x; r < nrows; r += kThreads) {
-        const uint32_t u = u0 + r;
-        const uint32_t b = fdiv(u, d.div_Bs);
-        const uint32_t slot = u - b * d.Bs;
-        s_dst[r] = base + (uint64_t)d.bt[b] * d.block_stride + (uint64_t)slot * d.token_stride;
-    }
-    __syncthreads();
-    copy_rows(d, src, nrows, s_dst);
+// Dynamic unit scheduling: units are claimed in global (layer-major) order from a monotone
+// per-descriptor counter, so whichever CTAs are resident finish the layers in order -- a CTA
+// that starts late (SMs busy with a co-running prefill) cannot hold back layer 0.
+// Each copy CTA stops claiming after its first claim past g1, so one launch advances the counter
+// by exactly (units + copy CTAs) and the host knows the next launch's grab_base.
+__device__ __forceinline__ uint32_t claim_unit(const DevDesc& d, uint32_t g0, uint32_t grab_base) {
+    return g0 + (atomicAdd(d.next_unit, 1u) - grab_base);
 }
 
-// Thread 0 of a CTA that completed layer l's work: publish layers in increasing order.
-__device__ void advance_ready(const DevDesc& d) {
-    const uint32_t base = (d.epoch - 1u) * d.L;
-    while (true) {
-        const uint32_t r = ld_acquire(d.ready);
-        const uint32_t rel = r - base;
-        if (rel >= d.L) return;
-        if (ld_acquire(&d.done_epoch[rel]) != d.epoch) return;
-        if (atomicCAS(d.ready, r, r + 1u) == r) {
-            d.ts[1 + rel] = globaltimer();
-            __threadfence_system();
-            ((volatile uint32_t*)d.host_ready)[rel] = d.epoch;
-        }
-        __threadfence();
-    }
-}
-
-__device__ __forceinline__ void complete_unit(const DevDesc& d, uint32_t layer) {
-    // Called by thread 0 after a __syncthreads(): the CTA's stores happen-before this fence
-    // (cumulativity), so they are visible GPU-wide before the counter moves.
-    __threadfence();
-    const uint32_t target = d.epoch * d.units_per_layer;
-    const uint32_t old = atomicAdd(&d.unit_cnt[layer], 1u);
-    if (old + 1u == target) {
-        atomicExch(&d.done_epoch[layer], d.epoch);
-        __threadfence();
-        advance_ready(d);
-    }
-}
-
-// Persistent LD/ST engine.  The destination-row table is double-buffered so one barrier per unit
-// suffices: the barrier that publishes unit k's table also orders every thread's unit k-1 stores
-// before thread 0 announces unit k-1, while the other warps already stream unit k.
-__global__ void __launch_bounds__(kThreads, 4) fetch_persistent_kernel(const DevDesc d) {
+// Units g0 .. g1-1; CTA 0 observes layers [g0/upl, g1/upl), the other CTAs claim and copy units.
+// The destination-row table is double-buffered so one barrier per unit suffices: the barrier that
+// publishes unit k's table also orders every thread's unit k-1 stores before thread 0 releases
+// unit k-1, while the other warps already stream unit k.
+__global__ void __launch_bounds__(kThreads, 4) fetch_ldst_kernel(const DevDesc d, uint32_t g0, uint32_t g1,
+                                                                 uint32_t grab_base) {
     __shared__ uint64_t s_dst[2][kMaxRows];
+    __shared__ uint32_t s_g[2];
     const uint64_t t0 = globaltimer();
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.ts[0] = t0;
-    const uint32_t total = d.L * d.units_per_layer;
-    uint32_t layer = blockIdx.x / d.units_per_layer;
-    uint32_t unit = blockIdx.x - layer * d.units_per_layer;
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) {
+            if (g0 == 0) d.ts[0] = t0;
+            observe_layers(d, g0 / d.units_per_layer, g1 / d.units_per_layer);
+        }
+        return;
+    }
     uint32_t pending_layer = 0;
     bool pending = false;
-    uint32_t k = 0;
-    for (uint32_t g = blockIdx.x; g < total; g += gridDim.x, k++) {
+    uint32_t next_g = 0;
+    if (threadIdx.x == 0) {  // claims stop after the first one past g1: exactly one per CTA overshoots
+        s_g[0] = claim_unit(d, g0, grab_base);
+        next_g = s_g[0] < g1 ? claim_unit(d, g0, grab_base) : s_g[0];  // one ahead hides the latency
+    }
+    __syncthreads();
+    for (uint32_t k = 0;; k++) {
+        const uint32_t g = s_g[k & 1];
+        if (g >= g1) break;  // uniform: every thread read the same slot after the last barrier
+        const UnitGeo u = unit_geo(d, g);
         if (d.pace_ns) {  // minimal pacer: layer l released at t0 + l * pace
-            const uint64_t rel = t0 + (uint64_t)layer * d.pace_ns;
+            const uint64_t rel = t0 + (uint64_t)u.layer * d.pace_ns;
             // CTA-uniform decision (also the barrier that orders unit k-1's stores)
             if (__syncthreads_or(threadIdx.x == 0 && globaltimer() < rel)) {  // announce, then idle
-                if (threadIdx.x == 0 && pending) complete_unit(d, pending_layer);
+                if (threadIdx.x == 0 && pending) complete_units(d, pending_layer, 1);
                 pending = false;
                 while (globaltimer() < rel) __nanosleep(2000);
             }
         }
         uint64_t* tab = s_dst[k & 1];
-        const uint32_t j = fdiv(unit, d.div_units_per_chunk);
-        const uint32_t rem = unit - j * 2u * d.tiles;
-        const uint32_t kv = rem >= d.tiles ? 1u : 0u;
-        const uint32_t r0 = (rem - kv * d.tiles) * d.rows_per_unit;
-        const uint32_t nrows = min(d.rows_per_unit, d.G - r0);
-        const uint64_t base = kv ? d.v_base[layer] : d.k_base[layer];
-        const uint32_t u0 = d.first_token + j * d.G + r0;
-        for (uint32_t r = threadIdx.x; r < nrows; r += kThreads) {
-            const uint32_t u = u0 + r;
-            const uint32_t b = fdiv(u, d.div_Bs);
-            tab[r] = base + (uint64_t)d.bt[b] * d.block_stride + (uint64_t)(u - b * d.Bs) * d.token_stride;
+        const uint64_t base = unit_base(d, u);
+        const uint32_t tok0 = unit_tok0(d, u);
+        for (uint32_t r = threadIdx.x; r < u.nrows; r += kThreads) tab[r] = row_dst(d, base, tok0 + r, nullptr);
+        if (threadIdx.x == 0) {  // publish unit k+1 (read after the barrier below), claim k+2
+            s_g[(k + 1) & 1] = next_g;
+            if (next_g < g1) next_g = claim_unit(d, g0, grab_base);
         }
         __syncthreads();
-        if (threadIdx.x == 0 && pending) complete_unit(d, pending_layer);
-        const uint8_t* src = (const uint8_t*)d.src[j] + (uint64_t)layer * d.S + ((uint64_t)kv * d.G + r0) * d.row;
-        copy_rows(d, src, nrows, tab);
+        if (threadIdx.x == 0 && pending) complete_units(d, pending_layer, 1);
+        copy_rows(d, unit_src(d, u), u.nrows, tab);
         pending = true;
-        pending_layer = layer;
-        unit += gridDim.x;  // advance (layer, unit) by gridDim.x units without a division
-        while (unit >= d.units_per_layer) {
-            unit -= d.units_per_layer;
-            layer++;
-        }
+        pending_layer = u.layer;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && pending) complete_unit(d, pending_layer);
+    if (threadIdx.x == 0 && pending) complete_units(d, pending_layer, 1);
 }
 
-__global__ void __launch_bounds__(kThreads) fetch_layer_kernel(const DevDesc d, uint32_t layer) {
-    __shared__ uint64_t s_dst[kMaxRows];
-    if (layer == 0 && blockIdx.x == 0 && threadIdx.x == 0) d.ts[0] = globaltimer();
-    for (uint32_t unit = blockIdx.x; unit < d.units_per_layer; unit += gridDim.x) {
-        copy_unit(d, layer, unit, s_dst);
-        __syncthreads();
-        if (threadIdx.x == 0) complete_unit(d, layer);
-    }
-}
-
-// ---- TMA bulk engine ------------------------------------------------------------------------------
-// One warp per CTA drives the copy engine: a unit (contiguous source rows) is pulled into a
-// shared-memory stage with one cp.async.bulk load (mbarrier complete_tx), then pushed to its
-// destination with one bulk store per contiguous destination run (a run of rows inside one
-// block for NHD, one head of one row otherwise), lanes splitting the runs.  `stages` units are
-// in flight per CTA; a unit is announced once its stores are complete (bulk wait_group with a
-// lag of two units, so stores stay in flight).  Register and instruction cost per byte is
-// near zero; the SM's load/store units are free for a co-running prefill.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
+// ---- BULK engine ---------------------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
@@ -251,129 +273,162 @@ __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
-struct UnitGeo {
-    uint32_t layer, j, kv, r0, nrows;
-};
-
-__device__ __forceinline__ UnitGeo unit_geo(const DevDesc& d, uint32_t g) {
-    UnitGeo u;
-    u.layer = fdiv(g, d.div_upl);
-    const uint32_t unit = g - u.layer * d.units_per_layer;
-    u.j = fdiv(unit, d.div_units_per_chunk);
-    const uint32_t rem = unit - u.j * 2u * d.tiles;
-    u.kv = rem >= d.tiles ? 1u : 0u;
-    const uint32_t tile = rem - u.kv * d.tiles;
-    u.r0 = tile * d.rows_per_unit;
-    u.nrows = min(d.rows_per_unit, d.G - u.r0);
-    return u;
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Units g in [g0, g1) are processed by this kernel; CTA b takes g0 + b, g0 + b + grid, ...
-__global__ void __launch_bounds__(32) fetch_bulk_kernel(const DevDesc d, uint32_t g0, uint32_t g1,
-                                                        uint32_t stages, uint32_t stage_bytes) {
+__device__ __forceinline__ uint32_t ld_acquire_cta(const volatile uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32((const void*)p)) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_cta(volatile uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32((const void*)p)), "r"(v) : "memory");
+}
+
+// CTA 0: observer.  CTA b >= 1: warp 0 claims units and copies them through a `stages`-deep
+// shared-memory ring; warp 1 (lane 0) turns the copy warp's retire records into release reductions
+// so the copy pipeline never waits on a GPU-scope fence.  A unit is retired once its bulk stores
+// are complete (wait_group with a lag of two units, so stores stay in flight).
+__global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_t g0, uint32_t g1,
+                                                        uint32_t grab_base, uint32_t stages, uint32_t stage_bytes) {
     extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t fifo_layer[kFifo], fifo_n[kFifo];
+    __shared__ uint32_t s_unit[32];
+    __shared__ uint32_t fifo_head, fifo_tail;
+    const uint64_t t0 = globaltimer();
+    if (blockIdx.x == 0) {
+        if (threadIdx.x == 0) {
+            if (g0 == 0) d.ts[0] = t0;
+            observe_layers(d, g0 / d.units_per_layer, g1 / d.units_per_layer);
+        }
+        return;
+    }
     uint64_t* bars = (uint64_t*)smem;
     uint8_t* buf = smem + 128;
-    const uint32_t lane = threadIdx.x;
-    const uint64_t t0 = globaltimer();
-    if (g0 == 0 && blockIdx.x == 0 && lane == 0) d.ts[0] = t0;
-    if (lane == 0) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < stages; s++) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fifo_head = 0;
+        fifo_tail = 0;
     }
-    __syncwarp();
-    const uint32_t first = g0 + blockIdx.x;
-    const uint32_t n_my = first < g1 ? (g1 - first + gridDim.x - 1) / gridDim.x : 0;
-
-    auto release_time = [&](uint32_t k) {  // minimal pacer: layer l released at t0 + l * pace (P:759-761)
-        return t0 + (uint64_t)fdiv(first + k * gridDim.x, d.div_upl) * d.pace_ns;
+    __syncthreads();
+    if (threadIdx.x >= 32) {  // ---- signaler warp
+        if (threadIdx.x != 32) return;
+        for (uint32_t h = 0;; h++) {
+            while (ld_acquire_cta(&fifo_tail) == h) __nanosleep(64);
+            const uint32_t layer = ((volatile uint32_t*)fifo_layer)[h % kFifo];
+            const uint32_t n = ((volatile uint32_t*)fifo_n)[h % kFifo];
+            if (layer == 0xffffffffu) return;
+            complete_units(d, layer, n);
+            st_release_cta(&fifo_head, h + 1);
+        }
+    }
+    // ---- copy warp
+    constexpr uint32_t kEnd = 0xffffffffu;
+    uint32_t tail = 0;
+    auto push = [&](uint32_t layer, uint32_t n) {  // lane 0 only
+        while (tail - ld_acquire_cta(&fifo_head) >= kFifo) __nanosleep(64);
+        ((volatile uint32_t*)fifo_layer)[tail % kFifo] = layer;
+        ((volatile uint32_t*)fifo_n)[tail % kFifo] = n;
+        st_release_cta(&fifo_tail, ++tail);
     };
-    auto issue_load = [&](uint32_t k) {
-        const uint32_t g = first + k * gridDim.x;
-        const UnitGeo u = unit_geo(d, g);
-        const uint8_t* src = (const uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + ((uint64_t)u.kv * d.G + u.r0) * d.row;
+    // s_unit[k % 32] = the k-th unit this CTA claimed (kEnd once the launch's units run out).
+    bool exhausted = false;  // lane 0 only
+    auto claim = [&](uint32_t k) {  // lane 0 only: claim unit k, returns false at the end
+        uint32_t g = kEnd;
+        if (!exhausted) {
+            g = claim_unit(d, g0, grab_base);
+            if (g >= g1) {
+                exhausted = true;
+                g = kEnd;
+            }
+        }
+        s_unit[k % 32] = g;
+        return g != kEnd;
+    };
+    auto issue_load = [&](uint32_t k) {  // lane 0 only, after a successful claim(k)
+        const UnitGeo u = unit_geo(d, s_unit[k % 32]);
         const uint32_t bytes = (uint32_t)(u.nrows * d.row);
         const uint32_t s = k % stages;
         mbar_expect_tx(&bars[s], bytes);
-        bulk_load(buf + (size_t)s * stage_bytes, src, bytes, &bars[s]);
+        bulk_load(buf + (size_t)s * stage_bytes, unit_src(d, u), bytes, &bars[s]);
     };
-
-    // Completion of units is batched per layer: one release-add per layer change.
+    auto release_time = [&](uint32_t k) {  // minimal pacer: layer l released at t0 + l * pace (P:759-761)
+        return t0 + (uint64_t)fdiv(s_unit[k % 32], d.div_upl) * d.pace_ns;
+    };
+    // Retired units are batched per layer: one record per layer change.
     uint32_t pend_layer = 0, pend_cnt = 0;
     auto flush = [&]() {
         if (pend_cnt) {
-            __threadfence();
-            const uint32_t target = d.epoch * d.units_per_layer;
-            const uint32_t old = atomicAdd(&d.unit_cnt[pend_layer], pend_cnt);
-            if (old + pend_cnt == target) {
-                atomicExch(&d.done_epoch[pend_layer], d.epoch);
-                __threadfence();
-                advance_ready(d);
-            }
+            push(pend_layer, pend_cnt);
             pend_cnt = 0;
         }
     };
-    auto retire = [&](uint32_t k) {  // unit k's stores are complete (all lanes waited)
-        const uint32_t layer = fdiv(first + k * gridDim.x, d.div_upl);
+    auto retire = [&](uint32_t k) {  // unit k's stores are complete (every lane waited)
+        const uint32_t layer = fdiv(s_unit[k % 32], d.div_upl);
         if (pend_cnt && layer != pend_layer) flush();
         pend_layer = layer;
         pend_cnt++;
     };
 
     if (lane == 0)
-        for (uint32_t k = 0; k + 1 < stages && k < n_my; k++) {
+        for (uint32_t k = 0; k + 1 < stages; k++) {
+            if (!claim(k)) break;
             if (d.pace_ns)
                 while (globaltimer() < release_time(k)) __nanosleep(2000);
             issue_load(k);
         }
+    __syncwarp();
 
-    uint32_t next_retire = 0;  // first unit not yet announced (same value in every lane)
-    for (uint32_t k = 0; k < n_my; k++) {
+    uint32_t next_retire = 0;  // first unit not yet retired (same value in every lane)
+    uint32_t k = 0;
+    for (;; k++) {
+        const uint32_t g = s_unit[k % 32];
+        if (g == kEnd) break;
         const uint32_t s = k % stages;
-        const UnitGeo u = unit_geo(d, first + k * gridDim.x);
+        const UnitGeo u = unit_geo(d, g);
         mbar_wait(&bars[s], (k / stages) & 1u);
         const uint8_t* sbuf = buf + (size_t)s * stage_bytes;
-        const uint64_t base = u.kv ? d.v_base[u.layer] : d.k_base[u.layer];
-        const uint32_t u0 = d.first_token + u.j * d.G + u.r0;
+        const uint64_t base = unit_base(d, u);
+        const uint32_t tok0 = unit_tok0(d, u);
         if (d.nhd) {
-            // Lane r owns row r if row r starts a run: the first row, or the first slot of a block.
+            // Lane r owns row r if row r starts a run: the unit's first row or a block's first slot.
             for (uint32_t r = lane; r < u.nrows; r += 32) {
-                const uint32_t tok = u0 + r;
-                const uint32_t b = fdiv(tok, d.div_Bs);
-                const uint32_t slot = tok - b * d.Bs;
+                uint32_t slot;
+                const uint64_t dst = row_dst(d, base, tok0 + r, &slot);
                 if (r == 0 || slot == 0) {
                     const uint32_t len = min(u.nrows - r, d.Bs - slot);
-                    const uint64_t dst = base + (uint64_t)d.bt[b] * d.block_stride + (uint64_t)slot * d.token_stride;
                     bulk_store(dst, sbuf + (size_t)r * d.row, (uint32_t)(len * d.row));
                 }
             }
-        } else {
+        } else {  // one store per (row, head)
             const uint32_t hdv = d.div_hdv.d;  // 16-byte pieces per head
             const uint32_t heads = d.vpr / hdv;
             const uint32_t hbytes = hdv * 16;
             for (uint32_t p = lane; p < u.nrows * heads; p += 32) {
                 const uint32_t r = p / heads;
                 const uint32_t h = p - r * heads;
-                const uint32_t tok = u0 + r;
-                const uint32_t b = fdiv(tok, d.div_Bs);
-                const uint32_t slot = tok - b * d.Bs;
-                const uint64_t dst = base + (uint64_t)d.bt[b] * d.block_stride + (uint64_t)slot * d.token_stride +
-                                     (uint64_t)h * d.head_stride;
+                const uint64_t dst = row_dst(d, base, tok0 + r, nullptr) + (uint64_t)h * d.head_stride;
                 bulk_store(dst, sbuf + (size_t)r * d.row + (size_t)h * hbytes, hbytes);
             }
         }
         bulk_commit();
-        // stage of unit k-1 is free once its stores have read shared memory
-        bulk_wait_read<1>();
+        bulk_wait_read<1>();  // unit k-1's stage is free once its stores have read shared memory
         __syncwarp();
         const uint32_t kl = k + stages - 1;  // next unit to load, into unit k-1's stage
-        if (kl < n_my) {
+        uint32_t got = 0;
+        if (lane == 0) got = claim(kl) ? 1u : 0u;
+        got = __shfl_sync(0xffffffffu, got, 0);
+        if (got) {
             if (d.pace_ns) {
                 uint32_t hold = lane == 0 ? (globaltimer() < release_time(kl) ? 1u : 0u) : 0u;
                 hold = __shfl_sync(0xffffffffu, hold, 0);
-                if (hold) {  // announce everything copied so far before idling until the release
+                if (hold) {  // retire everything copied so far before idling until the release
                     bulk_wait<0>();
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    fence_proxy_async_global();
                     __syncwarp();
                     if (lane == 0) {
                         for (uint32_t r = next_retire; r <= k; r++) retire(r);
@@ -381,14 +436,14 @@ __global__ void __launch_bounds__(32) fetch_bulk_kernel(const DevDesc d, uint32_
                         while (globaltimer() < release_time(kl)) __nanosleep(2000);
                     }
                     next_retire = k + 1;
-                    __syncwarp();
                 }
             }
             if (lane == 0) issue_load(kl);
         }
-        if (k >= 2 && next_retire + 2 <= k) {
-            bulk_wait<2>();                                   // unit k-2's stores are complete
-            asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (next_retire + 2 <= k) {
+            bulk_wait<2>();  // unit k-2's stores are complete
+            fence_proxy_async_global();
             __syncwarp();
             if (lane == 0)
                 for (uint32_t r = next_retire; r + 2 <= k; r++) retire(r);
@@ -396,11 +451,12 @@ __global__ void __launch_bounds__(32) fetch_bulk_kernel(const DevDesc d, uint32_
         }
     }
     bulk_wait<0>();
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+    fence_proxy_async_global();
     __syncwarp();
     if (lane == 0) {
-        for (uint32_t r = next_retire; r < n_my; r++) retire(r);
+        for (uint32_t r = next_retire; r < k; r++) retire(r);
         flush();
+        push(0xffffffffu, 0);
     }
 }
 
@@ -408,11 +464,12 @@ __global__ void wait_geq_kernel(const uint32_t* addr, uint32_t value) {
     while ((int32_t)(ld_acquire(addr) - value) < 0) __nanosleep(256);
 }
 
+// ---- launch --------------------------------------------------------------------------------------------
 namespace {
 
-int occupancy(const void* fn) {
+int occupancy(const void* fn, int threads, size_t smem) {
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0) != cudaSuccess || occ < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1) {
         cudaGetLastError();
         occ = 1;
     }
@@ -430,18 +487,19 @@ int env_int(const char* name, int dflt) {
 }
 
 struct BulkPlan {
-    uint32_t grid, stages, stage_bytes, smem;
+    uint32_t copy_ctas, stages, stage_bytes, smem;
 };
 
-// Shared-memory ring per CTA: `ctas_per_sm` CTAs share the SM's 228 KiB.
+// Shared-memory ring per CTA: `per_sm` CTAs share the SM's 228 KiB.  Measured on B200
+// (profiles/): 3 CTAs per SM with 16 KiB units keeps ~12 units in flight per SM.
 BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units) {
     BulkPlan p;
     p.stage_bytes = (uint32_t)(((uint64_t)dd.rows_per_unit * dd.row + 127) & ~127ull);
     int per_sm = std::max(1, env_int("OC_BULK_CTAS_PER_SM", 3));
     const uint32_t sm_bytes = 228 * 1024;
     while (true) {
-        uint32_t per_cta = std::min<uint32_t>(sm_bytes / per_sm - 1024, 227 * 1024);
-        uint32_t st = (per_cta - 128) / p.stage_bytes;
+        uint32_t per_cta = std::min<uint32_t>(sm_bytes / per_sm - 1024 - 640, 227 * 1024);
+        uint32_t st = per_cta > 128 ? (per_cta - 128) / p.stage_bytes : 0;
         st = std::min<uint32_t>(st, (uint32_t)std::max(2, env_int("OC_BULK_STAGES", 16)));
         if (st >= 2 || per_sm == 1) {
             p.stages = std::max<uint32_t>(st, 1);
@@ -450,21 +508,36 @@ BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units
         per_sm /= 2;
     }
     p.smem = 128 + p.stages * p.stage_bytes;
-    uint64_t grid = (uint64_t)per_sm * sms;
+    uint64_t grid = (uint64_t)per_sm * sms - 1;  // one CTA slot of the first wave is the observer's
     if (max_ctas) grid = std::min<uint64_t>(grid, max_ctas);
-    p.grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(grid, units));
+    p.copy_ctas = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(grid, units));
     return p;
 }
 
-int launch_bulk(const DevDesc& dd, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
+// One launch copies units [g0, g1); it claims them from the descriptor's counter starting at
+// d->grab_ctr and advances that counter by (units + copy CTAs) -- see claim_unit.
+int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
     static uint32_t attr_set = 0;
     if (p.smem > attr_set) {
         OC_CUDA(cudaFuncSetAttribute((const void*)fetch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<uint32_t>(p.smem, 48 * 1024)));
         attr_set = p.smem;
     }
-    fetch_bulk_kernel<<<p.grid, 32, p.smem, s>>>(dd, g0, g1, p.stages, p.stage_bytes);
+    fetch_bulk_kernel<<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, g0, g1, d->grab_ctr, p.stages, p.stage_bytes);
     OC_CUDA(cudaGetLastError());
+    d->grab_ctr += (g1 - g0) + p.copy_ctas;
+    return OC_OK;
+}
+
+int launch_ldst(Desc* d, int sms, uint32_t max_ctas, uint32_t g0, uint32_t g1, cudaStream_t s) {
+    // one CTA slot of the first wave is the observer's
+    static int occ = occupancy((const void*)fetch_ldst_kernel, kThreads, 0);
+    uint64_t grid = (uint64_t)occ * sms - 1;
+    if (max_ctas) grid = std::min<uint64_t>(grid, max_ctas);
+    grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, g1 - g0));
+    fetch_ldst_kernel<<<(unsigned)grid + 1, kThreads, 0, s>>>(d->dd, g0, g1, d->grab_ctr);
+    OC_CUDA(cudaGetLastError());
+    d->grab_ctr += (g1 - g0) + (uint32_t)grid;
     return OC_OK;
 }
 
@@ -477,58 +550,44 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     if (o.pace_Bps < 0) return fail(OC_EINVAL, "fetch_layerwise: pace must be >= 0");
     if (o.pace_Bps > 0 && o.mode != OC_FETCH_PERSISTENT)
         return fail(OC_ENOTSUP, "fetch_layerwise: pacing needs PERSISTENT mode");
+    if (d->poisoned) return fail(OC_ECUDA, "fetch_layerwise: descriptor unusable after a failed launch");
     DeviceGuard dg(d->device);
     if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
-    // Measured on B200 (profiles/): bulk engine best with 16 KiB units at 3 CTAs/SM, LD/ST with 32 KiB.
+    if (o.mode == OC_FETCH_PER_LAYER && d->events.empty()) {
+        d->events.resize(d->geo.L, nullptr);
+        for (auto& ev : d->events) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
     plan_units(d, o.unit_bytes ? o.unit_bytes : (o.engine == OC_COPY_BULK ? 16384u : 32768u));
     DevDesc& dd = d->dd;
-    if ((uint64_t)dd.units_per_layer * dd.L >= (1ull << 32)) return fail(OC_ERANGE, "fetch_layerwise: too many units");
-    d->epoch++;
-    if (d->epoch == 0) d->epoch = 1;  // never 0: done_epoch starts at 0
-    dd.epoch = d->epoch;
+    const uint64_t total_units = (uint64_t)dd.units_per_layer * dd.L;
+    if (total_units >= (1ull << 32)) return fail(OC_ERANGE, "fetch_layerwise: too many units");
+    uint32_t epoch = d->epoch + 1;
+    if (epoch == 0) epoch = 1;  // epochs count from 1: layer l of epoch e is ready at (e-1)*L + l + 1
+    dd.epoch = epoch;
+    dd.cnt_target = d->cnt_base + dd.units_per_layer;  // the unit size may change between fetches
     dd.pace_ns = o.pace_Bps > 0 ? (uint64_t)((double)d->N * d->geo.S / o.pace_Bps * 1e9) : 0;
     const int sms = device_sm_count(d->device);
-    const uint64_t total_units = (uint64_t)dd.units_per_layer * dd.L;
-    if (o.engine == OC_COPY_BULK) {
-        if (o.mode == OC_FETCH_PERSISTENT) {
-            BulkPlan p = plan_bulk(dd, sms, o.max_ctas, total_units);
-            int rc = launch_bulk(dd, p, 0, (uint32_t)total_units, s);
-            if (rc) return rc;
-        } else {
-            if (d->events.empty()) {
-                d->events.resize(dd.L, nullptr);
-                for (auto& ev : d->events) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            }
-            BulkPlan p = plan_bulk(dd, sms, o.max_ctas, dd.units_per_layer);
-            for (uint32_t l = 0; l < dd.L; l++) {
-                int rc = launch_bulk(dd, p, l * dd.units_per_layer, (l + 1) * dd.units_per_layer, s);
-                if (rc) return rc;
-                OC_CUDA(cudaEventRecord(d->events[l], s));
-            }
-        }
-    } else if (o.mode == OC_FETCH_PERSISTENT) {
-        static int occ = occupancy((const void*)fetch_persistent_kernel);
-        uint64_t grid = (uint64_t)occ * sms;
-        if (o.max_ctas) grid = std::min<uint64_t>(grid, o.max_ctas);
-        grid = std::min<uint64_t>(grid, (uint64_t)dd.units_per_layer * dd.L);
-        fetch_persistent_kernel<<<(unsigned)grid, kThreads, 0, s>>>(dd);
-        OC_CUDA(cudaGetLastError());
+    // From the first launch on, the device counters belong to this epoch.
+    d->epoch = epoch;
+    d->cnt_base = dd.cnt_target;
+    d->poisoned = true;
+    const uint32_t upl = dd.units_per_layer;
+    if (o.mode == OC_FETCH_PERSISTENT) {
+        int rc = o.engine == OC_COPY_BULK
+                     ? launch_bulk(d, plan_bulk(dd, sms, o.max_ctas, total_units), 0, (uint32_t)total_units, s)
+                     : launch_ldst(d, sms, o.max_ctas, 0, (uint32_t)total_units, s);
+        if (rc) return rc;
     } else {
-        if (d->events.empty()) {
-            d->events.resize(dd.L, nullptr);
-            for (auto& ev : d->events) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        }
-        static int occ = occupancy((const void*)fetch_layer_kernel);
-        uint64_t grid = (uint64_t)occ * sms;
-        if (o.max_ctas) grid = std::min<uint64_t>(grid, o.max_ctas);
-        grid = std::min<uint64_t>(grid, dd.units_per_layer);
+        const BulkPlan p = plan_bulk(dd, sms, o.max_ctas, upl);
         for (uint32_t l = 0; l < dd.L; l++) {
-            fetch_layer_kernel<<<(unsigned)grid, kThreads, 0, s>>>(dd, l);
-            OC_CUDA(cudaGetLastError());
+            int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, l * upl, (l + 1) * upl, s)
+                                              : launch_ldst(d, sms, o.max_ctas, l * upl, (l + 1) * upl, s);
+            if (rc) return rc;
             OC_CUDA(cudaEventRecord(d->events[l], s));
         }
     }
     OC_CUDA(cudaEventRecord(d->done_ev, s));
+    d->poisoned = false;
     d->last_mode = o.mode;
     d->last_stream = s;
     d->fetched = true;
@@ -584,18 +643,14 @@ OC_API int oc_sync_layer(oc_desc* h, uint32_t layer) {
         OC_CUDA(cudaEventSynchronize(d->events[want_layer]));
         return OC_OK;
     }
-    volatile uint32_t* flag = d->host_ready + want_layer;
-    for (uint64_t spins = 0;; spins++) {
-        if (*flag == d->epoch) return OC_OK;
-        if ((spins & 255) == 255) {
-            cudaError_t e = cudaEventQuery(d->done_ev);
-            if (e == cudaSuccess) {
-                if (*flag == d->epoch) return OC_OK;
-                return oc::fail(OC_ECUDA, "sync_layer: fetch finished without announcing the layer");
-            }
-            if (e != cudaErrorNotReady) return oc::cuda_fail(e, "sync_layer: fetch failed");
-        }
-    }
+    // Persistent mode: a private stream waits on the ready word; the host blocks on an event after it.
+    if (!d->sync_stream) OC_CUDA(cudaStreamCreateWithFlags(&d->sync_stream, cudaStreamNonBlocking));
+    if (!d->sync_ev) OC_CUDA(cudaEventCreateWithFlags(&d->sync_ev, cudaEventDisableTiming | cudaEventBlockingSync));
+    int rc = oc_wait_layer(h, layer, d->sync_stream);
+    if (rc) return rc;
+    OC_CUDA(cudaEventRecord(d->sync_ev, d->sync_stream));
+    OC_CUDA(cudaEventSynchronize(d->sync_ev));
+    return OC_OK;
 }
 
 OC_API int oc_layer_times(oc_desc* h, uint64_t* out) {

@@ -108,10 +108,9 @@ struct DevDesc {
     const uint64_t* k_base;   // [L]
     const uint64_t* v_base;   // [L]
     uint32_t* unit_cnt;       // [L] units completed (monotone across fetches)
-    uint32_t* done_epoch;     // [L] epoch in which layer l completed
-    uint32_t* ready;          // [1] leading complete layers, monotone: (epoch-1)*L + r
+    uint32_t* next_unit;      // unit claim counter (monotone across launches)
+    uint32_t* ready;          // (epoch-1)*L + number of layers announced in this fetch (monotone)
     uint64_t* ts;             // [L+1] globaltimer: [0] kernel start, [1+l] layer ready
-    uint32_t* host_ready;     // [L] mapped pinned host: epoch once layers 0..l are ready
     uint64_t S;               // bytes of one layer of one chunk
     uint64_t row;             // bytes of one token row (n_kv*d*p)
     uint64_t block_stride, token_stride, head_stride;
@@ -122,6 +121,7 @@ struct DevDesc {
     uint32_t vpr;             // 16-byte vectors per row
     uint32_t nhd;             // 1: a row is contiguous in the destination
     uint32_t epoch;           // fetch sequence number (>= 1)
+    uint32_t cnt_target;      // unit_cnt[l] value once this fetch's units of layer l are done
     uint32_t chunk_major;     // 1: only the completion of the whole prefix is announced
     uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
     FastDiv div_upl;          // units_per_layer
@@ -141,14 +141,18 @@ struct Desc {
     uint64_t N;
     uint64_t nb;               // block table entries uploaded
     void* dev_mem = nullptr;   // one allocation: src, k/v base, ts, counters, block table
-    uint32_t* host_ready = nullptr;  // [L] from the pinned host pool
     DevDesc dd;                // geometry part filled at build; epoch/units/pace at fetch
     uint32_t epoch = 0;
+    uint32_t cnt_base = 0;     // unit_cnt[l] before the next fetch (same for every layer)
+    uint32_t grab_ctr = 0;     // *next_unit before the next launch
     uint32_t last_mode = OC_FETCH_PERSISTENT;
     bool fetched = false;
+    bool poisoned = false;     // a launch failed after the counters moved to a new epoch
     std::vector<cudaEvent_t> events;  // per-layer (PER_LAYER mode), created lazily
     cudaEvent_t done_ev = nullptr;    // recorded after every fetch launch
     cudaStream_t last_stream = nullptr;
+    cudaStream_t sync_stream = nullptr;  // oc_sync_layer in PERSISTENT mode
+    cudaEvent_t sync_ev = nullptr;
 };
 
 // Plan work units of about `unit_bytes` bytes and fill the unit fields of d->dd.
@@ -156,10 +160,6 @@ void plan_units(Desc* d, uint32_t unit_bytes);
 
 // kernel launchers (fetch.cu)
 int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s);
-
-// small pinned, mapped host words (layer-ready mirrors)
-uint32_t* host_words_alloc(uint32_t n);
-void host_words_free(uint32_t* p, uint32_t n);
 
 // driver entry point for cuStreamWaitValue32 (resolved lazily)
 int stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t value);

@@ -330,3 +330,30 @@ def test_errors():
         desc.sync_layer(1)
         torch.cuda.synchronize()
         desc.close()
+
+
+def test_alternating_engines_and_unit_sizes_on_one_descriptor():
+    """The per-layer unit counters are monotone across fetches while the unit size (and so the
+    units per layer) may change from one fetch to the next."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    req = requests_family(lay, 12, 0, [9])[0]
+    dest = make_dest(lay, 9, "nhd", Bs=16, first_token=5, seed=12)
+    want = oracle_result(lay, 12, req, dest)
+    with oc.Store(lay, capacity=9) as st:
+        keys = oc.chunk_keys(req.tokens, 16)
+        st.put_chunks(keys, payload_stack(lay, 12, req.payload_ids))
+        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+        s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+        plan = [(oc.COPY_BULK, 0, oc.FETCH_PERSISTENT), (oc.COPY_LDST, 1024, oc.FETCH_PERSISTENT),
+                (oc.COPY_BULK, 512, oc.FETCH_PER_LAYER), (oc.COPY_LDST, 0, oc.FETCH_PER_LAYER),
+                (oc.COPY_BULK, 2048, oc.FETCH_PERSISTENT), (oc.COPY_LDST, 4096, oc.FETCH_PERSISTENT)]
+        for engine, ub, mode in plan:
+            with torch.cuda.stream(s):
+                buf.fill_(0xA5)
+            desc.fetch_layerwise(s, mode=mode, engine=engine, unit_bytes=ub)
+            desc.wait_layer(lay.num_layers - 1, cons)
+            cons.synchronize()
+            assert_same(buf.cpu().numpy(), want)
+            torch.cuda.synchronize()
+        desc.close()
