@@ -203,9 +203,10 @@ typedef enum {
 typedef struct {
     uint32_t mode;           /* oc_fetch_mode                                   */
     uint32_t engine;         /* oc_copy_engine                                  */
-    uint32_t max_ctas;       /* grid cap (SM budget when co-running); 0 = auto  */
-    uint32_t unit_bytes;     /* bytes per work unit; 0 = auto (16 KiB for BULK,
-                                32 KiB for LDST)                                */
+    uint32_t max_ctas;       /* copy-CTA cap (SM budget when co-running); 0 = auto:
+                                the whole GPU for HBM sources, 16 CTAs when most
+                                chunks live in pinned host memory (PCIe-bound)   */
+    uint32_t unit_bytes;     /* bytes per work unit; 0 = auto (32 KiB)          */
     double pace_Bps;         /* minimal pacer: layer l is released no
                                 earlier than t0 + l*(N*S)/pace_Bps; 0 = off.
                                 PERSISTENT mode only.                           */

@@ -53,8 +53,12 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
 
     // Resolve every key (first missing key reported by index, in prefix order).
     std::vector<uint64_t> src(n);
+    uint64_t host_chunks = 0;
     for (uint64_t i = 0; i < n; i++) {
-        if (!oc::store_resolve(s, keys[i], &src[i])) {
+        int tier = OC_TIER_HBM;
+        const bool found = oc::store_resolve(s, keys[i], &src[i], &tier);
+        host_chunks += tier == OC_TIER_PINNED_HOST;
+        if (!found) {
             if (bad_index) *bad_index = i;
             return oc::fail(OC_ENOTFOUND, "build_descriptor: chunk key " + std::to_string(i) + " not found");
         }
@@ -121,6 +125,7 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     d->delivery = delivery;
     d->N = n;
     d->nb = bt.size();
+    d->host_chunks = host_chunks;
 
     // One device allocation: src[N] | k_base[L] | v_base[L] | ts[L+1] | unit_cnt[L] | ready, next | bt
     size_t o_src = 0;

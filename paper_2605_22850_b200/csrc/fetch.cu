@@ -491,7 +491,7 @@ struct BulkPlan {
 };
 
 // Shared-memory ring per CTA: `per_sm` CTAs share the SM's 228 KiB.  Measured on B200
-// (profiles/): 3 CTAs per SM with 16 KiB units keeps ~12 units in flight per SM.
+// (profiles/): 3 CTAs per SM with 32 KiB units (2 stages each) reach the copy roofline.
 BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units) {
     BulkPlan p;
     p.stage_bytes = (uint32_t)(((uint64_t)dd.rows_per_unit * dd.row + 127) & ~127ull);
@@ -557,7 +557,12 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
         d->events.resize(d->geo.L, nullptr);
         for (auto& ev : d->events) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
-    plan_units(d, o.unit_bytes ? o.unit_bytes : (o.engine == OC_COPY_BULK ? 16384u : 32768u));
+    plan_units(d, o.unit_bytes ? o.unit_bytes : 32768u);
+    // PCIe-bound sources (pinned host tier) saturate the link from a handful of CTAs; more only
+    // spreads the link over more layers in flight and delays layer 0 (profiles/: 16 CTAs give
+    // 51.4 GB/s and X0 = one layer's transfer time at 4K).  The rest of the GPU stays free.
+    uint32_t max_ctas = o.max_ctas;
+    if (!max_ctas && d->host_chunks * 2 > d->N) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 16));
     DevDesc& dd = d->dd;
     const uint64_t total_units = (uint64_t)dd.units_per_layer * dd.L;
     if (total_units >= (1ull << 32)) return fail(OC_ERANGE, "fetch_layerwise: too many units");
@@ -574,14 +579,14 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     const uint32_t upl = dd.units_per_layer;
     if (o.mode == OC_FETCH_PERSISTENT) {
         int rc = o.engine == OC_COPY_BULK
-                     ? launch_bulk(d, plan_bulk(dd, sms, o.max_ctas, total_units), 0, (uint32_t)total_units, s)
-                     : launch_ldst(d, sms, o.max_ctas, 0, (uint32_t)total_units, s);
+                     ? launch_bulk(d, plan_bulk(dd, sms, max_ctas, total_units), 0, (uint32_t)total_units, s)
+                     : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
         if (rc) return rc;
     } else {
-        const BulkPlan p = plan_bulk(dd, sms, o.max_ctas, upl);
+        const BulkPlan p = plan_bulk(dd, sms, max_ctas, upl);
         for (uint32_t l = 0; l < dd.L; l++) {
             int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, l * upl, (l + 1) * upl, s)
-                                              : launch_ldst(d, sms, o.max_ctas, l * upl, (l + 1) * upl, s);
+                                              : launch_ldst(d, sms, max_ctas, l * upl, (l + 1) * upl, s);
             if (rc) return rc;
             OC_CUDA(cudaEventRecord(d->events[l], s));
         }

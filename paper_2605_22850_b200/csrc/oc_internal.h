@@ -97,8 +97,8 @@ struct Store {
     mutable std::shared_mutex mu;
     cudaStream_t put_stream = nullptr;
 };
-// Resolve a key to a device address: local slots first, then peers.  Caller holds no lock.
-bool store_resolve(Store* s, const oc_key& k, uint64_t* addr);
+// Resolve a key to a device address (and the tier holding it): local slots first, then peers.
+bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier = nullptr);
 
 // ---- device descriptor -----------------------------------------------------------
 // Everything the copy kernel needs, passed by value as a kernel parameter.
@@ -140,6 +140,7 @@ struct Desc {
     int delivery;
     uint64_t N;
     uint64_t nb;               // block table entries uploaded
+    uint64_t host_chunks = 0;  // chunks whose source lives in pinned host memory (PCIe reads)
     void* dev_mem = nullptr;   // one allocation: src, k/v base, ts, counters, block table
     DevDesc dd;                // geometry part filled at build; epoch/units/pace at fetch
     uint32_t epoch = 0;

@@ -26,17 +26,18 @@ struct ExportHeader {
 
 }  // namespace
 
-bool store_resolve(Store* s, const oc_key& k, uint64_t* addr) {
+bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier) {
     {
         std::shared_lock<std::shared_mutex> lk(s->mu);
         auto it = s->index.find(k);
         if (it != s->index.end()) {
             *addr = (uint64_t)(uintptr_t)s->slab + it->second * s->geo.chunk;
+            if (tier) *tier = s->tier;
             return true;
         }
     }
     for (Store* p : s->peers)
-        if (store_resolve(p, k, addr)) return true;
+        if (store_resolve(p, k, addr, tier)) return true;
     return false;
 }
 
