@@ -141,7 +141,8 @@ struct Desc {
     uint64_t N;
     uint64_t nb;               // block table entries uploaded
     uint64_t host_chunks = 0;  // chunks whose source lives in pinned host memory (PCIe reads)
-    void* dev_mem = nullptr;   // one allocation: src, k/v base, ts, counters, block table
+    void* dev_mem = nullptr;   // one pooled block: src, k/v base, ts, counters, block table
+    uint64_t dev_mem_class = 0;
     DevDesc dd;                // geometry part filled at build; epoch/units/pace at fetch
     uint32_t epoch = 0;
     uint32_t cnt_base = 0;     // unit_cnt[l] before the next fetch (same for every layer)
