@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--stall64k", type=int, default=1)
     p.add_argument("--profile", action="store_true", help="no soak / clock sampling (for ncu runs)")
+    p.add_argument("--sched", default="", help="comma list of paper scheduler workloads to run (A,B,C): "
+                   "concurrent paced fetches under a shared cap, per policy (adds a 'sched' object)")
     return p.parse_args()
 
 
@@ -323,6 +325,8 @@ def main_ours(args):
 
     if rank == 0 and not args.no_e2e:
         out["e2e"] = e2e_leg(args, oc, torch, dev, lay_t, fopts)
+    if rank == 0 and args.sched:
+        out["sched"] = sched_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_stall:
         out["stall"] = stall_leg(args, oc, torch, dev, lay_t, fopts)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -461,6 +465,111 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts):
     res["windows"] = ("Table A5 A100 per-layer compute (P:2706-2713), 87.5% hit; spin-kernel emulation; "
                       "baseline = same chain with KV resident (opt-local-LW analog)")
     return res
+
+
+# The paper's scheduler workloads (Sec. 5.7; Table A6): requests named
+# by (context, hit rate); per-layer bytes s_i = cached tokens * 4096 B and per-layer compute
+# c_i = T_total / 32 from Table A5 (A100); caps 80 / 50 / 50 Gbps; delta = 5 Gbps.
+TABLE_A5_T_TOTAL_MS = {(16384, 0.5): 955.89, (16384, 0.875): 281.76, (32768, 0.5): 2589.25,
+                       (32768, 0.875): 763.19, (65536, 0.5): 8672.79, (65536, 0.875): 2423.90}
+SCHED_WORKLOADS = {
+    "A": (80.0, [(16384, 0.5), (16384, 0.875), (65536, 0.5), (65536, 0.875)]),
+    "B": (50.0, [(16384, 0.5), (16384, 0.875), (65536, 0.5), (65536, 0.875)]),
+    "C": (50.0, [(16384, 0.5), (16384, 0.875), (32768, 0.5), (32768, 0.875), (65536, 0.5), (65536, 0.875)]),
+}
+
+
+def sched_leg(args, oc, torch, dev, lay_t):
+    """Concurrent layerwise fetches under a shared cap: Equal / KV-prop / BW-prop / Stall-opt /
+    Calibrated Stall-opt rates from oc.schedule_bandwidth, enforced by the fetch's pacer (layer l
+    released at t0 + l*s/r), chunks in the pinned host tier (the shared PCIe link plays the
+    paper's shared NIC).  Each request's consumer waits on every layer and then spins for c_i.
+    dTTFT_i = TTFT_i - TTFT_i(no limit); the paper's Table A8 reports the sum per policy."""
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    n_max = 65536 * 7 // 8 // G
+    store = oc.Store(lay_t, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
+    import synth
+    (tok,), _ = synth.family_streams(4242, G, 0, [n_max])
+    keys = oc.chunk_keys(tok, G)                           # one shared-prefix corpus
+    gen = torch.Generator(device=dev).manual_seed(4242)
+    for b0 in range(0, n_max, 256):
+        b1 = min(n_max, b0 + 256)
+        pl = torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
+        store.put_chunks(keys[b0:b1], pl)
+        del pl
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(1000)
+    e0.record()
+    torch.cuda._sleep(20_000_000)
+    e1.record()
+    torch.cuda.synchronize()
+    cyc_per_ms = 20_000_000 / e0.elapsed_time(e1)
+    GB = 1e9 / 8                                            # bytes/s per Gbps (decimal)
+    out = {}
+    for wl in [w.strip().upper() for w in args.sched.split(",") if w.strip()]:
+        cap_gbps, cells = SCHED_WORKLOADS[wl]
+        reqs = []
+        for ctx, hit in cells:
+            N = int(ctx * hit) // G
+            need = N * G // Bs
+            cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
+            per_kv = need * Bs * row
+            kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+            tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+                                 synth.block_table(N, need, need), 0)
+            d = oc.build_descriptor(store, keys[:N], lay_t, tgt)
+            reqs.append({"cell": f"{ctx // 1024}K,{hit:g}", "N": N, "s": N * S,
+                         "c": TABLE_A5_T_TOTAL_MS[(ctx, hit)] / L / 1e3, "d": d, "cache": cache,
+                         "copy": torch.cuda.Stream(device=dev), "cons": torch.cuda.Stream(device=dev)})
+
+        def run(rates):
+            """All requests concurrently; rates None = unpaced.  Returns TTFT per request (ms)."""
+            torch.cuda.synchronize()
+            start = torch.cuda.Event(enable_timing=True)
+            start.record(torch.cuda.current_stream())
+            ends = []
+            for r in reqs:
+                r["copy"].wait_event(start)
+                r["cons"].wait_event(start)
+            for i, r in enumerate(reqs):
+                r["d"].fetch_layerwise(r["copy"], pace_Bps=0.0 if rates is None else float(rates[i]))
+            for l in range(L):                              # enqueue layer by layer across requests
+                for r in reqs:
+                    r["d"].wait_layer(l, r["cons"])
+                    with torch.cuda.stream(r["cons"]):
+                        torch.cuda._sleep(int(r["c"] * 1e3 * cyc_per_ms))
+            for r in reqs:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(r["cons"])
+                ends.append(e)
+            torch.cuda.synchronize()
+            return [start.elapsed_time(e) for e in ends]
+
+        s_i = [r["s"] for r in reqs]
+        c_i = [r["c"] for r in reqs]
+        base = run(None)                                    # "no-limit base" (Table A8)
+        res = {"cap_gbps": cap_gbps, "requests": [r["cell"] for r in reqs],
+               "zero_stall_gbps": [round(s / c / GB, 3) for s, c in zip(s_i, c_i)],
+               "no_limit_ttft_ms": [round(x, 1) for x in base], "policies": {}}
+        for pol in ("equal", "kv_prop", "bw_prop", "stall_opt", "cal_stall_opt"):
+            rates = oc.schedule_bandwidth(pol, s_i, c_i, cap_gbps * GB, 5 * GB)
+            ttft = run(rates)
+            # Eq. 3 with uniform X = s/r and C = c: added = X + (L-1) max(0, X - C)
+            model = [s / r + (L - 1) * max(0.0, s / r - c) for s, c, r in zip(s_i, c_i, rates)]
+            res["policies"][pol] = {"rates_gbps": [round(r / GB, 2) for r in rates],
+                                    "ttft_ms": [round(x, 1) for x in ttft],
+                                    "dttft_ms": round(sum(t - b for t, b in zip(ttft, base)), 1),
+                                    "model_dttft_ms": round(sum(model) * 1e3, 1)}
+        res["equal_over_cal"] = round(res["policies"]["equal"]["dttft_ms"] /
+                                      max(1e-9, res["policies"]["cal_stall_opt"]["dttft_ms"]), 3)
+        out[wl] = res
+        for r in reqs:
+            r["d"].close()
+        del reqs
+        torch.cuda.empty_cache()
+    store.close()
+    return out
 
 
 def cpu_baseline_leg():
