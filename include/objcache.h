@@ -218,6 +218,18 @@ typedef struct {
  * opts = NULL selects the defaults (persistent, BULK, auto grid, unpaced). */
 OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* copy_stream);
 
+/* Batches: concurrent requests (P:467-598 treats them as tenants sharing one link) fetched by
+ * ONE persistent launch.  Units are claimed in a single global order -- layer l of every request,
+ * then layer l+1 -- so every request's layers arrive in order and all requests' early layers go
+ * first.  Descriptors must share layout and device, and stay alive (not freed) until the batch
+ * is freed.  Each member keeps its own layer-ready state: wait_layer / sync_layer / layer_times
+ * work per descriptor as after fetch_layerwise.  PERSISTENT mode, BULK engine, unpaced only
+ * (ENOTSUP otherwise); a batch may be fetched repeatedly, one fetch in flight at a time. */
+typedef struct oc_batch oc_batch;
+OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out);
+OC_API int oc_fetch_batch(oc_batch* batch, const oc_fetch_opts* opts, void* copy_stream);
+OC_API int oc_batch_free(oc_batch* batch);
+
 /* wait_layer (NotifyLayerReady, Alg. A1 line 7): make `consumer_stream` wait,
  * without blocking the host, until layer `layer` of the most recent fetch is
  * in place.  Layers become ready in increasing order.  For CHUNK_MAJOR

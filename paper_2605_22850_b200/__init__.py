@@ -84,6 +84,9 @@ _SIGS = {
     "oc_desc_free": [_vp],
     "oc_desc_info": [_vp, c_u64p, c_u64p, c_u64p],
     "oc_fetch_layerwise": [_vp, ctypes.POINTER(CFetchOpts), _vp],
+    "oc_batch_create": [ctypes.POINTER(_vp), ctypes.c_uint32, ctypes.POINTER(_vp)],
+    "oc_fetch_batch": [_vp, ctypes.POINTER(CFetchOpts), _vp],
+    "oc_batch_free": [_vp],
     "oc_wait_layer": [_vp, ctypes.c_uint32, _vp],
     "oc_sync_layer": [_vp, ctypes.c_uint32],
     "oc_layer_times": [_vp, c_u64p],
@@ -387,6 +390,36 @@ def build_descriptor(store: Store, keys, layout, target, delivery: int = DELIVER
                                   ctypes.byref(t), ctypes.byref(h), ctypes.byref(bad))
     _check(rc, bad.value)
     return Descriptor(h, store, lay, store)
+
+
+class Batch:
+    """Several descriptors fetched by one launch (layer-major across the batch)."""
+
+    def __init__(self, descs: Sequence[Descriptor]):
+        self.descs = list(descs)
+        arr = (_vp * len(self.descs))(*[d._h for d in self.descs])
+        h = _vp()
+        _check(_lib.oc_batch_create(arr, len(self.descs), ctypes.byref(h)))
+        self._h = h
+
+    def fetch(self, stream=None, max_ctas=0, unit_bytes=0):
+        o = CFetchOpts(FETCH_PERSISTENT, COPY_BULK, int(max_ctas), int(unit_bytes), 0.0)
+        _check(_lib.oc_fetch_batch(self._h, ctypes.byref(o), _stream(stream)))
+
+    def close(self, _free=_lib.oc_batch_free):  # bound early: safe during interpreter exit
+        if getattr(self, "_h", None):
+            _free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def fetch_batch(descs: Sequence[Descriptor], stream=None, **opts) -> Batch:
+    """Create a batch of descriptors and fetch it once; returns the (reusable) batch."""
+    b = Batch(descs)
+    b.fetch(stream, **opts)
+    return b
 
 
 # ---- the boundary calls, by the names the method uses ---------------------------------------------

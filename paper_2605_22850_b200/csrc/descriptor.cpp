@@ -16,47 +16,6 @@ namespace oc {
 namespace {
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Descriptor memory comes from a per-device pool of power-of-two blocks that are never returned
-// to the driver: cudaMalloc/cudaFree per request cost 0.3-8 ms on B200 (cudaFree synchronises the
-// device), which would dominate the control plane of a 4K-token fetch.  The pinned staging
-// buffer makes the one H2D upload a DMA from page-locked memory.
-struct DevPool {
-    std::mutex mu;
-    std::unordered_map<uint64_t, std::vector<void*>> free_by_class;  // key: (device << 48) | class
-};
-DevPool g_pool;
-
-uint64_t size_class(size_t n) {
-    uint64_t c = 4096;
-    while (c < n) c <<= 1;
-    return c;
-}
-
-void* pool_alloc(int device, size_t n, uint64_t* cls_out) {
-    const uint64_t cls = size_class(n);
-    *cls_out = cls;
-    {
-        std::lock_guard<std::mutex> lk(g_pool.mu);
-        auto& fl = g_pool.free_by_class[((uint64_t)device << 48) | cls];
-        if (!fl.empty()) {
-            void* p = fl.back();
-            fl.pop_back();
-            return p;
-        }
-    }
-    void* p = nullptr;
-    if (cudaMalloc(&p, cls) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    return p;
-}
-
-void pool_free(int device, void* p, uint64_t cls) {
-    if (!p) return;
-    std::lock_guard<std::mutex> lk(g_pool.mu);
-    g_pool.free_by_class[((uint64_t)device << 48) | cls].push_back(p);
-}
 }  // namespace
 
 void plan_units(Desc* d, uint32_t unit_bytes) {
@@ -187,11 +146,11 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
 
     oc::DeviceGuard dg(d->device);
     uint64_t cls = 0;
-    void* mem = oc::pool_alloc(d->device, total, &cls);
+    void* mem = oc::dev_pool_alloc(d->device, total, &cls);
     if (!mem) return oc::fail(OC_ENOMEM, "build_descriptor: device allocation failed");
     cudaError_t e = cudaMemcpy(mem, stage.data(), total, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-        oc::pool_free(d->device, mem, cls);
+        oc::dev_pool_free(d->device, mem, cls);
         return oc::cuda_fail(e, "build_descriptor: upload");
     }
     d->dev_mem = mem;
@@ -240,7 +199,7 @@ OC_API int oc_desc_free(oc_desc* h) {
         if (d->done_ev) cudaEventDestroy(d->done_ev);
         if (d->sync_ev) cudaEventDestroy(d->sync_ev);
         if (d->sync_stream) cudaStreamDestroy(d->sync_stream);
-        oc::pool_free(d->device, d->dev_mem, d->dev_mem_class);
+        oc::dev_pool_free(d->device, d->dev_mem, d->dev_mem_class);
         cudaGetLastError();
     }
     delete d;

@@ -31,6 +31,7 @@ constexpr int kThreads = 256;   // LDST: threads per CTA
 constexpr int kVec = 8;         // LDST: 16-byte vectors in flight per thread per round
 constexpr int kMaxRows = 1024;  // rows per unit (plan_units caps R)
 constexpr uint32_t kFifo = 64;  // BULK: copy-warp -> signaler-warp retire FIFO
+constexpr uint32_t kBulkStaticSmem = 1280;  // BULK: FIFO + claim ring (static shared memory, rounded up)
 
 // ---- small device helpers ------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -287,21 +288,78 @@ __device__ __forceinline__ void st_release_cta(volatile uint32_t* p, uint32_t v)
     asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32((const void*)p)), "r"(v) : "memory");
 }
 
+// A batch: several descriptors (same L) fetched by one launch.  Units are claimed in one global
+// order -- layer-major across the batch: layer l of request 0, of request 1, ..., then layer l+1 --
+// so every request sees its layers delivered in order and all requests' early layers go first.
+struct BatchArgs {
+    const DevDesc* descs;  // [n] device copies of the requests' descriptors
+    const uint32_t* cum;   // [n + 1] prefix sums of units_per_layer
+    uint32_t* claim;       // batch claim counter (monotone across launches)
+    uint32_t n;
+    uint32_t upl_total;    // cum[n]
+    FastDiv div_upl_total;
+};
+
+struct Resolved {
+    const DevDesc* d;
+    uint32_t g;    // unit index within the request
+    uint32_t req;  // request index within the batch (0 without a batch)
+};
+
+template <bool BATCH>
+__device__ __forceinline__ Resolved resolve(const DevDesc& d0, const BatchArgs& ba, uint32_t g) {
+    if (!BATCH) return {&d0, g, 0u};
+    const uint32_t layer = fdiv(g, ba.div_upl_total);
+    const uint32_t rem = g - layer * ba.upl_total;
+    uint32_t lo = 0, hi = ba.n;  // largest r with cum[r] <= rem
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&ba.cum[mid]) <= rem) lo = mid;
+        else hi = mid;
+    }
+    const DevDesc* d = &ba.descs[lo];
+    return {d, layer * d->units_per_layer + (rem - __ldg(&ba.cum[lo])), lo};
+}
+
+// Batch observer: lane i announces the layers of requests i, i+32, ...; each request's layers go
+// out in order (same protocol as observe_layers).
+__device__ void observe_batch(const BatchArgs& ba, uint64_t t0) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t r = lane; r < ba.n; r += 32) ba.descs[r].ts[0] = t0;
+    const uint32_t L = ba.descs[0].L;
+    for (uint32_t l = 0; l < L; l++)
+        for (uint32_t r = lane; r < ba.n; r += 32) {
+            const DevDesc& d = ba.descs[r];
+            uint32_t ns = 32;
+            while ((int32_t)(ld_acquire(&d.unit_cnt[l]) - d.cnt_target) < 0) {
+                __nanosleep(ns);
+                ns = min(ns * 2, 256u);
+            }
+            d.ts[1 + l] = globaltimer();
+            st_release(d.ready, (d.epoch - 1u) * d.L + l + 1u);
+        }
+}
+
 // CTA 0: observer.  CTA b >= 1: warp 0 claims units and copies them through a `stages`-deep
 // shared-memory ring; warp 1 (lane 0) turns the copy warp's retire records into release reductions
 // so the copy pipeline never waits on a GPU-scope fence.  A unit is retired once its bulk stores
 // are complete (wait_group with a lag of two units, so stores stay in flight).
-__global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_t g0, uint32_t g1,
-                                                        uint32_t grab_base, uint32_t stages, uint32_t stage_bytes) {
+template <bool BATCH>
+__global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ DevDesc d0,
+                                                        const __grid_constant__ BatchArgs ba, uint32_t g0,
+                                                        uint32_t g1, uint32_t grab_base, uint32_t stages,
+                                                        uint32_t stage_bytes) {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint32_t fifo_layer[kFifo], fifo_n[kFifo];
-    __shared__ uint32_t s_unit[32];
+    __shared__ uint32_t fifo_req[kFifo], fifo_layer[kFifo], fifo_n[kFifo];
+    __shared__ uint32_t s_unit[32], s_req[32];
     __shared__ uint32_t fifo_head, fifo_tail;
     const uint64_t t0 = globaltimer();
     if (blockIdx.x == 0) {
-        if (threadIdx.x == 0) {
-            if (g0 == 0) d.ts[0] = t0;
-            observe_layers(d, g0 / d.units_per_layer, g1 / d.units_per_layer);
+        if (BATCH) {
+            if (threadIdx.x < 32) observe_batch(ba, t0);
+        } else if (threadIdx.x == 0) {
+            if (g0 == 0) d0.ts[0] = t0;
+            observe_layers(d0, g0 / d0.units_per_layer, g1 / d0.units_per_layer);
         }
         return;
     }
@@ -319,37 +377,48 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_
         if (threadIdx.x != 32) return;
         for (uint32_t h = 0;; h++) {
             while (ld_acquire_cta(&fifo_tail) == h) __nanosleep(64);
+            const uint32_t req = ((volatile uint32_t*)fifo_req)[h % kFifo];
             const uint32_t layer = ((volatile uint32_t*)fifo_layer)[h % kFifo];
             const uint32_t n = ((volatile uint32_t*)fifo_n)[h % kFifo];
             if (layer == 0xffffffffu) return;
-            complete_units(d, layer, n);
+            complete_units(BATCH ? ba.descs[req] : d0, layer, n);
             st_release_cta(&fifo_head, h + 1);
         }
     }
     // ---- copy warp
     constexpr uint32_t kEnd = 0xffffffffu;
+    uint32_t* claim_ctr = BATCH ? ba.claim : d0.next_unit;
     uint32_t tail = 0;
-    auto push = [&](uint32_t layer, uint32_t n) {  // lane 0 only
+    auto push = [&](uint32_t req, uint32_t layer, uint32_t n) {  // lane 0 only
         while (tail - ld_acquire_cta(&fifo_head) >= kFifo) __nanosleep(64);
+        ((volatile uint32_t*)fifo_req)[tail % kFifo] = req;
         ((volatile uint32_t*)fifo_layer)[tail % kFifo] = layer;
         ((volatile uint32_t*)fifo_n)[tail % kFifo] = n;
         st_release_cta(&fifo_tail, ++tail);
     };
-    // s_unit[k % 32] = the k-th unit this CTA claimed (kEnd once the launch's units run out).
+    // s_unit/s_req[k % 32] = the k-th unit this CTA claimed (kEnd once the launch's units run out).
     bool exhausted = false;  // lane 0 only
     auto claim = [&](uint32_t k) {  // lane 0 only: claim unit k, returns false at the end
-        uint32_t g = kEnd;
+        uint32_t g = kEnd, req = 0;
         if (!exhausted) {
-            g = claim_unit(d, g0, grab_base);
-            if (g >= g1) {
+            // Each copy CTA stops after its first claim past g1: a launch advances the counter by
+            // exactly (units + copy CTAs), so the host knows the next launch's grab_base.
+            const uint32_t gg = g0 + (atomicAdd(claim_ctr, 1u) - grab_base);
+            if (gg >= g1) {
                 exhausted = true;
-                g = kEnd;
+            } else {
+                const Resolved rs = resolve<BATCH>(d0, ba, gg);
+                g = rs.g;
+                req = rs.req;
             }
         }
         s_unit[k % 32] = g;
+        s_req[k % 32] = req;
         return g != kEnd;
     };
+    auto desc_of = [&](uint32_t k) -> const DevDesc& { return BATCH ? ba.descs[s_req[k % 32]] : d0; };
     auto issue_load = [&](uint32_t k) {  // lane 0 only, after a successful claim(k)
+        const DevDesc& d = desc_of(k);
         const UnitGeo u = unit_geo(d, s_unit[k % 32]);
         const uint32_t bytes = (uint32_t)(u.nrows * d.row);
         const uint32_t s = k % stages;
@@ -357,19 +426,22 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_
         bulk_load(buf + (size_t)s * stage_bytes, unit_src(d, u), bytes, &bars[s]);
     };
     auto release_time = [&](uint32_t k) {  // minimal pacer: layer l released at t0 + l * pace
+        const DevDesc& d = desc_of(k);
         return t0 + (uint64_t)fdiv(s_unit[k % 32], d.div_upl) * d.pace_ns;
     };
-    // Retired units are batched per layer: one record per layer change.
-    uint32_t pend_layer = 0, pend_cnt = 0;
+    // Retired units are batched per (request, layer): one record per change.
+    uint32_t pend_req = 0, pend_layer = 0, pend_cnt = 0;
     auto flush = [&]() {
         if (pend_cnt) {
-            push(pend_layer, pend_cnt);
+            push(pend_req, pend_layer, pend_cnt);
             pend_cnt = 0;
         }
     };
     auto retire = [&](uint32_t k) {  // unit k's stores are complete (every lane waited)
-        const uint32_t layer = fdiv(s_unit[k % 32], d.div_upl);
-        if (pend_cnt && layer != pend_layer) flush();
+        const uint32_t req = s_req[k % 32];
+        const uint32_t layer = fdiv(s_unit[k % 32], desc_of(k).div_upl);
+        if (pend_cnt && (layer != pend_layer || req != pend_req)) flush();
+        pend_req = req;
         pend_layer = layer;
         pend_cnt++;
     };
@@ -377,7 +449,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_
     if (lane == 0)
         for (uint32_t k = 0; k + 1 < stages; k++) {
             if (!claim(k)) break;
-            if (d.pace_ns)
+            if (!BATCH && d0.pace_ns)
                 while (globaltimer() < release_time(k)) __nanosleep(2000);
             issue_load(k);
         }
@@ -388,6 +460,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_
     for (;; k++) {
         const uint32_t g = s_unit[k % 32];
         if (g == kEnd) break;
+        const DevDesc& d = desc_of(k);
         const uint32_t s = k % stages;
         const UnitGeo u = unit_geo(d, g);
         mbar_wait(&bars[s], (k / stages) & 1u);
@@ -423,7 +496,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_
         if (lane == 0) got = claim(kl) ? 1u : 0u;
         got = __shfl_sync(0xffffffffu, got, 0);
         if (got) {
-            if (d.pace_ns) {
+            if (!BATCH && d0.pace_ns) {
                 uint32_t hold = lane == 0 ? (globaltimer() < release_time(kl) ? 1u : 0u) : 0u;
                 hold = __shfl_sync(0xffffffffu, hold, 0);
                 if (hold) {  // retire everything copied so far before idling until the release
@@ -456,7 +529,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const DevDesc d, uint32_
     if (lane == 0) {
         for (uint32_t r = next_retire; r < k; r++) retire(r);
         flush();
-        push(0xffffffffu, 0);
+        push(0, 0xffffffffu, 0);
     }
 }
 
@@ -498,7 +571,7 @@ BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units
     int per_sm = std::max(1, env_int("OC_BULK_CTAS_PER_SM", 3));
     const uint32_t sm_bytes = 228 * 1024;
     while (true) {
-        uint32_t per_cta = std::min<uint32_t>(sm_bytes / per_sm - 1024 - 640, 227 * 1024);
+        uint32_t per_cta = std::min<uint32_t>(sm_bytes / per_sm - 1024 - kBulkStaticSmem, 227 * 1024);
         uint32_t st = per_cta > 128 ? (per_cta - 128) / p.stage_bytes : 0;
         st = std::min<uint32_t>(st, (uint32_t)std::max(2, env_int("OC_BULK_STAGES", 16)));
         if (st >= 2 || per_sm == 1) {
@@ -514,16 +587,23 @@ BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units
     return p;
 }
 
+template <bool BATCH>
+cudaError_t set_bulk_smem(uint32_t smem) {
+    static uint32_t attr_set = 0;
+    if (smem <= attr_set) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute((const void*)fetch_bulk_kernel<BATCH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<uint32_t>(smem, 48 * 1024));
+    if (e == cudaSuccess) attr_set = smem;
+    return e;
+}
+
 // One launch copies units [g0, g1); it claims them from the descriptor's counter starting at
 // d->grab_ctr and advances that counter by (units + copy CTAs) -- see claim_unit.
 int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
-    static uint32_t attr_set = 0;
-    if (p.smem > attr_set) {
-        OC_CUDA(cudaFuncSetAttribute((const void*)fetch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::max<uint32_t>(p.smem, 48 * 1024)));
-        attr_set = p.smem;
-    }
-    fetch_bulk_kernel<<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, g0, g1, d->grab_ctr, p.stages, p.stage_bytes);
+    OC_CUDA(set_bulk_smem<false>(p.smem));
+    fetch_bulk_kernel<false><<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
+                                                                 p.stage_bytes);
     OC_CUDA(cudaGetLastError());
     d->grab_ctr += (g1 - g0) + p.copy_ctas;
     return OC_OK;
@@ -599,6 +679,84 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     return OC_OK;
 }
 
+// ---- batches --------------------------------------------------------------------------------------
+struct Batch {
+    std::vector<Desc*> descs;
+    int device = 0;
+    uint32_t n = 0;
+    size_t upload_bytes = 0;   // DevDesc[n] | cum[n+1]
+    void* dev = nullptr;       // upload area + claim counter
+    uint64_t dev_class = 0;
+    void* stage = nullptr;     // pinned staging of the upload area
+    uint64_t stage_class = 0;
+    cudaEvent_t staged = nullptr;  // the last upload has finished reading `stage`
+    uint32_t grab_ctr = 0;
+    uint32_t* claim = nullptr;
+};
+
+int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
+    if (o.mode != OC_FETCH_PERSISTENT) return fail(OC_ENOTSUP, "fetch_batch: batches use PERSISTENT mode");
+    if (o.engine != OC_COPY_BULK) return fail(OC_ENOTSUP, "fetch_batch: batches use the BULK engine");
+    if (o.pace_Bps != 0) return fail(OC_ENOTSUP, "fetch_batch: pacing is per request (fetch_layerwise)");
+    for (Desc* d : b->descs)
+        if (d->poisoned) return fail(OC_ECUDA, "fetch_batch: a descriptor is unusable after a failed launch");
+    DeviceGuard dg(b->device);
+    OC_CUDA(cudaEventSynchronize(b->staged));  // previous upload done with the staging buffer
+    DevDesc* st = (DevDesc*)b->stage;
+    uint32_t* cum = (uint32_t*)((uint8_t*)b->stage + sizeof(DevDesc) * b->n);
+    uint64_t host_chunks = 0, chunks = 0, total = 0;
+    cum[0] = 0;
+    for (uint32_t i = 0; i < b->n; i++) {
+        Desc* d = b->descs[i];
+        if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
+        plan_units(d, o.unit_bytes ? o.unit_bytes : 32768u);
+        DevDesc& dd = d->dd;
+        uint32_t epoch = d->epoch + 1;
+        if (epoch == 0) epoch = 1;
+        dd.epoch = epoch;
+        dd.cnt_target = d->cnt_base + dd.units_per_layer;
+        dd.pace_ns = 0;
+        st[i] = dd;
+        total += dd.units_per_layer;
+        cum[i + 1] = (uint32_t)total;
+        host_chunks += d->host_chunks;
+        chunks += d->N;
+    }
+    const uint32_t L = b->descs[0]->geo.L;
+    if (total * L >= (1ull << 32)) return fail(OC_ERANGE, "fetch_batch: too many units in one batch");
+    uint32_t max_ctas = o.max_ctas;
+    if (!max_ctas && host_chunks * 2 > chunks) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 16));
+    const int sms = device_sm_count(b->device);
+    const BulkPlan p = plan_bulk(b->descs[0]->dd, sms, max_ctas, total * L);
+    OC_CUDA(cudaMemcpyAsync(b->dev, b->stage, b->upload_bytes, cudaMemcpyHostToDevice, s));
+    OC_CUDA(cudaEventRecord(b->staged, s));
+    for (Desc* d : b->descs) {  // from the launch on, the device counters belong to the new epoch
+        d->epoch = d->dd.epoch;
+        d->cnt_base = d->dd.cnt_target;
+        d->poisoned = true;
+    }
+    BatchArgs ba;
+    ba.descs = (const DevDesc*)b->dev;
+    ba.cum = (const uint32_t*)((uint8_t*)b->dev + sizeof(DevDesc) * b->n);
+    ba.claim = b->claim;
+    ba.n = b->n;
+    ba.upl_total = (uint32_t)total;
+    ba.div_upl_total = make_fastdiv((uint32_t)total);
+    OC_CUDA(set_bulk_smem<true>(p.smem));
+    fetch_bulk_kernel<true><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)(total * L), b->grab_ctr,
+                                                                p.stages, p.stage_bytes);
+    OC_CUDA(cudaGetLastError());
+    b->grab_ctr += (uint32_t)(total * L) + p.copy_ctas;
+    for (Desc* d : b->descs) {
+        OC_CUDA(cudaEventRecord(d->done_ev, s));
+        d->poisoned = false;
+        d->last_mode = OC_FETCH_PERSISTENT;
+        d->last_stream = s;
+        d->fetched = true;
+    }
+    return OC_OK;
+}
+
 }  // namespace oc
 
 using oc::Desc;
@@ -612,6 +770,66 @@ OC_API int oc_fetch_layerwise(oc_desc* h, const oc_fetch_opts* opts, void* strea
     o.engine = OC_COPY_BULK;
     if (opts) o = *opts;
     return oc::launch_fetch((Desc*)h, o, (cudaStream_t)stream);
+}
+
+OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out) {
+    if (!out || !descs || n == 0) return oc::fail(OC_EINVAL, "batch_create: need n >= 1 descriptors");
+    *out = nullptr;
+    auto b = std::make_unique<oc::Batch>();
+    for (uint32_t i = 0; i < n; i++) {
+        Desc* d = (Desc*)descs[i];
+        if (!d) return oc::fail(OC_EINVAL, "batch_create: null descriptor");
+        if (!oc::same_layout(d->layout, ((Desc*)descs[0])->layout) || d->device != ((Desc*)descs[0])->device)
+            return oc::fail(OC_EINVAL, "batch_create: descriptors must share layout and device");
+        for (uint32_t k = 0; k < i; k++)
+            if (descs[k] == descs[i]) return oc::fail(OC_EINVAL, "batch_create: duplicate descriptor");
+        b->descs.push_back(d);
+    }
+    b->n = n;
+    b->device = b->descs[0]->device;
+    b->upload_bytes = sizeof(oc::DevDesc) * n + 4 * (n + 1);
+    const size_t dev_bytes = ((b->upload_bytes + 15) & ~size_t(15)) + 16;
+    oc::DeviceGuard dg(b->device);
+    b->dev = oc::dev_pool_alloc(b->device, dev_bytes, &b->dev_class);
+    b->stage = oc::dev_pool_alloc(-1, b->upload_bytes, &b->stage_class);
+    if (!b->dev || !b->stage) {
+        oc::dev_pool_free(b->device, b->dev, b->dev_class);
+        oc::dev_pool_free(-1, b->stage, b->stage_class);
+        return oc::fail(OC_ENOMEM, "batch_create: allocation failed");
+    }
+    b->claim = (uint32_t*)((uint8_t*)b->dev + ((b->upload_bytes + 15) & ~size_t(15)));
+    OC_CUDA(cudaMemset(b->claim, 0, 16));
+    OC_CUDA(cudaEventCreateWithFlags(&b->staged, cudaEventDisableTiming));
+    *out = (oc_batch*)b.release();
+    return OC_OK;
+}
+
+OC_API int oc_fetch_batch(oc_batch* h, const oc_fetch_opts* opts, void* stream) {
+    if (!h) return oc::fail(OC_EINVAL, "fetch_batch: null batch");
+    oc_fetch_opts o{};
+    o.mode = OC_FETCH_PERSISTENT;
+    o.engine = OC_COPY_BULK;
+    if (opts) o = *opts;
+    return oc::fetch_batch((oc::Batch*)h, o, (cudaStream_t)stream);
+}
+
+OC_API int oc_batch_free(oc_batch* h) {
+    if (!h) return OC_OK;
+    oc::Batch* b = (oc::Batch*)h;
+    {
+        oc::DeviceGuard dg(b->device);
+        for (Desc* d : b->descs)  // the batch's device copy is read until its launches finish
+            if (d->fetched && d->done_ev) cudaEventSynchronize(d->done_ev);
+        if (b->staged) {
+            cudaEventSynchronize(b->staged);
+            cudaEventDestroy(b->staged);
+        }
+        oc::dev_pool_free(b->device, b->dev, b->dev_class);
+        oc::dev_pool_free(-1, b->stage, b->stage_class);
+        cudaGetLastError();
+    }
+    delete b;
+    return OC_OK;
 }
 
 OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {

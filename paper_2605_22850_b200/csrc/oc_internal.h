@@ -157,6 +157,11 @@ struct Desc {
     cudaEvent_t sync_ev = nullptr;
 };
 
+// Pooled memory (pool.cpp): power-of-two blocks of device memory on `device`, or of pinned host
+// memory (device = -1), recycled instead of returned to the driver.
+void* dev_pool_alloc(int device, size_t n, uint64_t* cls_out);
+void dev_pool_free(int device, void* p, uint64_t cls);
+
 // Plan work units of about `unit_bytes` bytes and fill the unit fields of d->dd.
 void plan_units(Desc* d, uint32_t unit_bytes);
 
