@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--stall64k", type=int, default=1)
     p.add_argument("--profile", action="store_true", help="no soak / clock sampling (for ncu runs)")
+    p.add_argument("--sweep", action="store_true", help="rate sweep (Fig. 15 analog): added TTFT of one "
+                   "paced request vs rate / r*, against Eq. 3 (adds a 'sweep' object)")
     p.add_argument("--batch", default="", help="NxM: N 4K-token + M 64K-token concurrent requests (config 5, "
                    "one GPU): one batched launch vs per-request launches (adds a 'batch' object)")
     p.add_argument("--sched", default="", help="comma list of paper scheduler workloads to run (A,B,C): "
@@ -209,10 +211,17 @@ def main_ours(args):
     import synth
 
     ws, rank, local = dist_env()
+    # OC_BENCH_DIST_BACKEND=gloo lets several ranks share one GPU to exercise the N>1 code path
+    # (NCCL refuses duplicate GPUs); real multi-GPU runs use NCCL with one GPU per rank.
+    backend = os.environ.get("OC_BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     mode = oc.FETCH_PERSISTENT if args.mode == "persistent" else oc.FETCH_PER_LAYER
     engine = oc.COPY_BULK if args.engine == "bulk" else oc.COPY_LDST
     fopts = {"mode": mode, "engine": engine}
@@ -288,8 +297,8 @@ def main_ours(args):
     elapsed_ms = t_start.elapsed_time(t_end)
     launch_ms = [a.elapsed_time(b) for a, b in evs]
     if ws > 1:
-        t = torch.tensor([elapsed_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([elapsed_ms], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)                # max over ranks
         elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
     value = ws * bytes_per_step * args.steps / (elapsed_ms / 1e3) / 1e9
@@ -331,6 +340,8 @@ def main_ours(args):
         out["sched"] = sched_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.batch:
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and args.sweep:
+        out["sweep"] = sweep_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_stall:
         out["stall"] = stall_leg(args, oc, torch, dev, lay_t, fopts)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -458,9 +469,14 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts):
                 t = d.layer_times().astype(np.int64)
                 runs.append((ttft - base, (t[1] - t[0]) / 1e6, (t[L] - t[0]) / 1e6, ttft))
             best = min(runs)
+            # Eq. 2's other side: chunkwise delivery (every wait_layer waits for the whole prefix)
+            d_cw = oc.build_descriptor(store, keys, lay_t, tgt, oc.DELIVER_CHUNK_MAJOR)
+            cw = min(chain(copy_s, cons_s, d_cw, C_ms) for _ in range(2)) - base
+            d_cw.close()
             res[f"{name}_{tier_name}"] = {"N": N, "C_ms_per_layer": round(C_ms, 4), "added_ms": round(best[0], 4),
                                           "X0_ms": round(best[1], 4), "transfer_ms": round(best[2], 4),
                                           "ttft_ms": round(best[3], 3), "baseline_ttft_ms": round(base, 3),
+                                          "added_ms_chunkwise": round(cw, 4),
                                           "payload_MiB": N * S * L / 2**20}
             d.close()
             store.close()
@@ -469,6 +485,76 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts):
     res["windows"] = ("Table A5 A100 per-layer compute (P:2706-2713), 87.5% hit; spin-kernel emulation; "
                       "baseline = same chain with KV resident (opt-local-LW analog)")
     return res
+
+
+def sweep_leg(args, oc, torch, dev, lay_t):
+    """Fig. 15 analog: one request from the pinned host tier, paced at f * r*, with
+    the Table A5 A100 compute windows; added TTFT against the resident-KV chain and against Eq. 3
+    with uniform X = s/r, C = c (added = X + (L-1) max(0, X - C)).  The knee sits at f = 1."""
+    import synth
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(1000)
+    e0.record()
+    torch.cuda._sleep(20_000_000)
+    e1.record()
+    torch.cuda.synchronize()
+    cyc_per_ms = 20_000_000 / e0.elapsed_time(e1)
+    out = {}
+    for ctx, hit in ((16384, 0.875), (65536, 0.875)):
+        N = int(ctx * hit) // G
+        c = TABLE_A5_T_TOTAL_MS[(ctx, hit)] / L / 1e3
+        s = N * S
+        rstar = s / c
+        store = oc.Store(lay_t, capacity=N, tier=oc.TIER_PINNED_HOST, device=dev.index)
+        (tok,), _ = synth.family_streams(31 + N, G, 0, [N])
+        keys = oc.chunk_keys(tok, G)
+        gen = torch.Generator(device=dev).manual_seed(N)
+        for b0 in range(0, N, 512):
+            pl = torch.randint(0, 256, (min(N, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
+            store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
+            del pl
+        need = N * G // Bs
+        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
+        per_kv = need * Bs * row
+        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+                             synth.block_table(3, need, need), 0)
+        d = oc.build_descriptor(store, keys, lay_t, tgt)
+        copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+        def chain(pace):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(copy_s)
+            cons_s.wait_event(a)
+            if pace is not None:
+                d.fetch_layerwise(copy_s, pace_Bps=pace)
+            for l in range(L):
+                if pace is not None:
+                    d.wait_layer(l, cons_s)
+                with torch.cuda.stream(cons_s):
+                    torch.cuda._sleep(int(c * 1e3 * cyc_per_ms))
+            b.record(cons_s)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b)
+
+        base = min(chain(None) for _ in range(2))
+        pts = []
+        for f in (0.25, 0.5, 0.75, 0.9, 1.0, 1.1, 1.25, 1.5, 2.0, 4.0):
+            r = f * rstar
+            added = chain(r) - base
+            X = s / r
+            pts.append({"f": f, "rate_GBps": round(r / 1e9, 3), "added_ms": round(added, 3),
+                        "eq3_added_ms": round((X + (L - 1) * max(0.0, X - c)) * 1e3, 3)})
+        out[f"{ctx // 1024}K,{hit:g}"] = {"r_star_GBps": round(rstar / 1e9, 3), "C_ms": round(c * 1e3, 3),
+                                          "payload_per_layer_MiB": s / 2**20, "points": pts}
+        d.close()
+        store.close()
+        del cache
+        torch.cuda.empty_cache()
+    return out
 
 
 def batch_leg(args, oc, torch, dev, lay_t):
