@@ -188,6 +188,17 @@ OC_API int oc_desc_free(oc_desc* desc);
 OC_API int oc_desc_info(const oc_desc* desc, uint64_t* n_chunks, uint64_t* payload_W,
                         uint64_t* units_per_layer);
 
+/* put_from_paged -- the offload path ("newly produced KV blocks are offloaded back to
+ * object storage for future reuse"): chunk j of a request (its tokens first_token + j*G ..
+ * + G-1) is gathered from the paged KV cache described by `target` (OC_TARGET_PAGED, same address
+ * rule as build_descriptor) into a new slot in KV_L2TD order, on `stream` (asynchronous: later
+ * fetches of these keys must be ordered after `stream`).  Keys already in the store are
+ * deduplicated without reading their bytes (identity is the prefix-chain key, reading c18).
+ * *n_new = new keys.  Errors as build_descriptor, plus EFULL (*bad_index = first key that did
+ * not fit; earlier new keys are stored). */
+OC_API int oc_put_from_paged(oc_store* store, const oc_key* keys, uint64_t n, const oc_layout* layout,
+                             const oc_target* target, void* stream, uint64_t* n_new, uint64_t* bad_index);
+
 /* ---- fetch (Alg. A1 on the GPU) ------------------------------------------ */
 typedef enum {
     OC_FETCH_PERSISTENT = 0, /* one launch covers all layers; per-layer device

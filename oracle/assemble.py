@@ -114,3 +114,31 @@ def scatter_paged_advanced_index(B: bytes, layer: int, desc, dst: np.ndarray):
         n_rows = (int(slots.max()) + 1)
         cache = dst[base:base + n_rows * row].reshape(n_rows, row)
         cache[slots] = payload[:, kv].reshape(N * G, row)
+
+
+def offload_paged(store, keys, layout, target, mem: np.ndarray) -> int:
+    """The offload path (Sec. 3: "newly produced KV blocks are offloaded back to object
+    storage for future reuse"): chunk j of the request -- tokens first_token + j*G .. +G-1 --
+    is read out of the paged cache ``mem`` in KV_L2TD order (layer, then K/V, then token, then
+    head; reading c2) and put under key j.  Keys already stored are left as they are (identity is
+    the chain key, reading c18).  Returns the number of new keys."""
+    G = layout.chunk_tokens
+    hd = head_bytes(layout)
+    parts_new = 0
+    for j, key in enumerate(keys):
+        if bytes(key) in store:
+            continue
+        parts = []
+        for layer in range(layout.num_layers):
+            for kv in (0, 1):
+                base = (target.k_base if kv == 0 else target.v_base)[layer]
+                for tok in range(G):
+                    u = target.first_token + j * G + tok
+                    blk = target.block_table[u // target.block_size]
+                    slot = u % target.block_size
+                    for h in range(layout.kv_heads):
+                        a = base + blk * target.block_stride + slot * target.token_stride + h * target.head_stride
+                        parts.append(mem[a:a + hd].tobytes())
+        store.put([key], [b"".join(parts)])
+        parts_new += 1
+    return parts_new

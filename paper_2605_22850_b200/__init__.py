@@ -81,6 +81,8 @@ _SIGS = {
     "oc_store_import": [_vp, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(_vp)],
     "oc_build_descriptor": [_vp, _vp, ctypes.c_uint64, ctypes.POINTER(CLayout), ctypes.c_int,
                             ctypes.POINTER(CTarget), ctypes.POINTER(_vp), c_u64p],
+    "oc_put_from_paged": [_vp, _vp, ctypes.c_uint64, ctypes.POINTER(CLayout), ctypes.POINTER(CTarget), _vp,
+                          c_u64p, c_u64p],
     "oc_desc_free": [_vp],
     "oc_desc_info": [_vp, c_u64p, c_u64p, c_u64p],
     "oc_fetch_layerwise": [_vp, ctypes.POINTER(CFetchOpts), _vp],
@@ -358,11 +360,10 @@ class Descriptor:
         return out
 
 
-def build_descriptor(store: Store, keys, layout, target, delivery: int = DELIVER_LAYER_MAJOR) -> Descriptor:
-    k = _keys_array(keys)
-    lay = _layout(layout)
+def _ctarget(target, lay):
+    """(CTarget, keepalive list) for a PagedTarget / FlatTarget."""
     t = CTarget()
-    keep = [k]
+    keep = []
     if isinstance(target, FlatTarget):
         t.kind = TARGET_FLAT
         t.flat_base = int(target.base)
@@ -385,6 +386,14 @@ def build_descriptor(store: Store, keys, layout, target, delivery: int = DELIVER
             raise ValueError("need one K and one V base per layer")
     else:
         raise TypeError("target must be PagedTarget or FlatTarget")
+    return t, keep
+
+
+def build_descriptor(store: Store, keys, layout, target, delivery: int = DELIVER_LAYER_MAJOR) -> Descriptor:
+    k = _keys_array(keys)
+    lay = _layout(layout)
+    t, keep = _ctarget(target, lay)
+    keep.append(k)
     h, bad = _vp(), ctypes.c_uint64()
     rc = _lib.oc_build_descriptor(store._h, k.ctypes.data, k.shape[0], ctypes.byref(lay), int(delivery),
                                   ctypes.byref(t), ctypes.byref(h), ctypes.byref(bad))
@@ -425,6 +434,20 @@ def fetch_batch(descs: Sequence[Descriptor], stream=None, **opts) -> Batch:
 # ---- the boundary calls, by the names the method uses ---------------------------------------------
 def put_chunks(store: Store, keys, payloads) -> int:
     return store.put_chunks(keys, payloads)
+
+
+def put_from_paged(store: Store, keys, layout, target: "PagedTarget", stream=None) -> int:
+    """Offload: gather chunk j of a request from a paged cache into new store slots
+    (asynchronous on `stream`); existing keys are deduplicated.  Returns the number of new keys."""
+    k = _keys_array(keys)
+    lay = _layout(layout)
+    t, keep = _ctarget(target, lay)
+    n_new, bad = ctypes.c_uint64(), ctypes.c_uint64()
+    rc = _lib.oc_put_from_paged(store._h, k.ctypes.data, k.shape[0], ctypes.byref(lay), ctypes.byref(t),
+                                _stream(stream), ctypes.byref(n_new), ctypes.byref(bad))
+    del keep
+    _check(rc, bad.value)
+    return n_new.value
 
 
 def match_prefix(store: Store, tokens, parent: Optional[bytes] = None) -> np.ndarray:

@@ -1,11 +1,15 @@
-// The ObjectCache descriptor (Table 1) made GPU-native.
+// The ObjectCache descriptor (Table 1) made GPU-native, and the offload path.
 //
 // Table 1 names the matched chunk keys [H_0..H_{N-1}], L, G, S, the delivery order and the RDMA
-// target.  Here build_descriptor validates the request, resolves every key to its chunk slot
-// (the gateway's key validation and the storage server's object resolution), and
-// uploads one packed device descriptor: src[N] slot addresses, the K/V base of every layer, the
-// block table and the per-layer completion words.  The descriptor is "arithmetic rather than
+// target.  build_descriptor validates the request, resolves every key to its chunk slot (the
+// gateway's key validation and the storage server's object resolution), and uploads
+// one packed device descriptor: src[N] slot addresses, the K/V base of every layer, the block
+// table and the per-layer completion words.  The descriptor is "arithmetic rather than
 // manifest-heavy": every layer range is [lS, (l+1)S) of a slot.
+//
+// put_from_paged is the inverse direction (newly produced KV blocks are offloaded back for
+// future reuse): the same target normalisation, then a gather kernel from the paged cache into
+// freshly reserved slots.
 #include <algorithm>
 #include <unordered_set>
 
@@ -16,21 +20,167 @@ namespace oc {
 namespace {
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-}  // namespace
+// A target in the paged form: the flat client buffer is a paged cache with one G-token block per
+// chunk, identity block table, block_stride = S and V after K in each block.
+struct PagedView {
+    std::vector<uint64_t> kb, vb;
+    std::vector<int32_t> bt;
+    uint64_t block_stride = 0, token_stride = 0, head_stride = 0;
+    uint32_t Bs = 0, first_token = 0;
+};
 
-void plan_units(Desc* d, uint32_t unit_bytes) {
-    DevDesc& dd = d->dd;
+int normalize_target(const Geometry& g, uint64_t n, const oc_target* t, const char* who, PagedView* v) {
+    const uint32_t L = g.L;
+    v->kb.resize(L);
+    v->vb.resize(L);
+    if (t->kind == OC_TARGET_FLAT) {
+        uint64_t W = n * L * g.S;
+        if (t->flat_capacity < W) return fail(OC_ERANGE, std::string(who) + ": flat target smaller than W = N*L*S");
+        if (t->flat_base % 16) return fail(OC_EALIGN, std::string(who) + ": flat_base not 16-byte aligned");
+        for (uint32_t l = 0; l < L; l++) {
+            v->kb[l] = t->flat_base + (uint64_t)l * n * g.S;
+            v->vb[l] = v->kb[l] + (uint64_t)g.G * g.row;
+        }
+        v->bt.resize(n);
+        for (uint64_t i = 0; i < n; i++) v->bt[i] = (int32_t)i;
+        v->block_stride = g.S;
+        v->token_stride = g.row;
+        v->head_stride = g.hd;
+        v->Bs = g.G;
+        v->first_token = 0;
+        return OC_OK;
+    }
+    if (t->kind != OC_TARGET_PAGED) return fail(OC_EINVAL, std::string(who) + ": unknown target kind");
+    if (!t->k_base || !t->v_base || !t->block_table)
+        return fail(OC_EINVAL, std::string(who) + ": null paged arrays");
+    if (t->block_size == 0) return fail(OC_EINVAL, std::string(who) + ": block_size must be >= 1");
+    v->Bs = t->block_size;
+    v->first_token = t->first_token;
+    const uint64_t last = (uint64_t)v->first_token + n * g.G - 1;
+    if (last >= (1ull << 31)) return fail(OC_ERANGE, std::string(who) + ": token index exceeds 2^31");
+    const uint64_t need = last / v->Bs + 1;
+    if (t->num_blocks < need) return fail(OC_ERANGE, std::string(who) + ": block table does not cover the prefix");
+    v->block_stride = t->block_stride;
+    v->token_stride = t->token_stride;
+    v->head_stride = t->head_stride;
+    if (v->block_stride % 16 || v->token_stride % 16 || v->head_stride % 16)
+        return fail(OC_EALIGN, std::string(who) + ": strides must be multiples of 16 bytes");
+    for (uint32_t l = 0; l < L; l++) {
+        v->kb[l] = t->k_base[l];
+        v->vb[l] = t->v_base[l];
+        if (v->kb[l] % 16 || v->vb[l] % 16) return fail(OC_EALIGN, std::string(who) + ": K/V base not 16-byte aligned");
+    }
+    v->bt.assign(t->block_table, t->block_table + need);
+    std::unordered_set<int32_t> seen;
+    seen.reserve(need * 2);
+    for (uint64_t b = v->first_token / v->Bs; b < need; b++) {
+        if (v->bt[b] < 0) return fail(OC_EINVAL, std::string(who) + ": negative block id");
+        if (!seen.insert(v->bt[b]).second)
+            return fail(OC_EINVAL, std::string(who) + ": duplicate block id in the prefix (reading c4)");
+    }
+    return OC_OK;
+}
+
+// Device block layout shared by descriptors and offload jobs:
+//   src[N] | k_base[L] | v_base[L] | ts[L+1] | unit_cnt[L] | ready, next | bt[nb] | pos[N]
+struct BlockLayout {
+    size_t o_src, o_kb, o_vb, o_ts, o_cnt, o_ready, o_next, o_bt, o_pos, total;
+};
+
+BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos) {
+    BlockLayout b;
+    b.o_src = 0;
+    b.o_kb = align16(b.o_src + n * 8);
+    b.o_vb = align16(b.o_kb + L * 8);
+    b.o_ts = align16(b.o_vb + L * 8);
+    b.o_cnt = align16(b.o_ts + (L + 1) * 8);
+    b.o_ready = align16(b.o_cnt + L * 4);
+    b.o_next = b.o_ready + 4;
+    b.o_bt = align16(b.o_ready + 16);
+    b.o_pos = align16(b.o_bt + nb * 4);
+    b.total = align16(b.o_pos + (with_pos ? n * 4 : 0));
+    return b;
+}
+
+// Upload src/bases/bt(/pos) into a pooled device block and fill the static DevDesc fields.
+int upload_block(int device, const Geometry& g, const std::vector<uint64_t>& src, const PagedView& v,
+                 const std::vector<uint32_t>* pos, const char* who, void** mem_out, uint64_t* cls_out, DevDesc* dd,
+                 const uint32_t** pos_dev) {
+    const uint64_t n = src.size();
+    const uint32_t L = g.L;
+    const BlockLayout b = block_layout(n, L, v.bt.size(), pos != nullptr);
+    std::vector<uint8_t> stage(b.total, 0);
+    std::memcpy(stage.data() + b.o_src, src.data(), n * 8);
+    std::memcpy(stage.data() + b.o_kb, v.kb.data(), L * 8);
+    std::memcpy(stage.data() + b.o_vb, v.vb.data(), L * 8);
+    std::memcpy(stage.data() + b.o_bt, v.bt.data(), v.bt.size() * 4);
+    if (pos) std::memcpy(stage.data() + b.o_pos, pos->data(), n * 4);
+    uint64_t cls = 0;
+    void* mem = dev_pool_alloc(device, b.total, &cls);
+    if (!mem) return fail(OC_ENOMEM, std::string(who) + ": device allocation failed");
+    cudaError_t e = cudaMemcpy(mem, stage.data(), b.total, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        dev_pool_free(device, mem, cls);
+        return cuda_fail(e, who);
+    }
+    *mem_out = mem;
+    *cls_out = cls;
+    uint8_t* m = (uint8_t*)mem;
+    std::memset(dd, 0, sizeof *dd);
+    dd->src = (const uint64_t*)(m + b.o_src);
+    dd->k_base = (const uint64_t*)(m + b.o_kb);
+    dd->v_base = (const uint64_t*)(m + b.o_vb);
+    dd->ts = (uint64_t*)(m + b.o_ts);
+    dd->unit_cnt = (uint32_t*)(m + b.o_cnt);
+    dd->ready = (uint32_t*)(m + b.o_ready);
+    dd->next_unit = (uint32_t*)(m + b.o_next);
+    dd->bt = (const int32_t*)(m + b.o_bt);
+    if (pos_dev) *pos_dev = pos ? (const uint32_t*)(m + b.o_pos) : nullptr;
+    dd->S = g.S;
+    dd->row = g.row;
+    dd->block_stride = v.block_stride;
+    dd->token_stride = v.token_stride;
+    dd->head_stride = v.head_stride;
+    dd->N = (uint32_t)n;
+    dd->L = L;
+    dd->G = g.G;
+    dd->Bs = v.Bs;
+    dd->first_token = v.first_token;
+    dd->vpr = (uint32_t)(g.row / 16);
+    dd->nhd = (v.token_stride == g.row && v.head_stride == g.hd) ? 1u : 0u;
+    dd->div_vpr = make_fastdiv(dd->vpr);
+    dd->div_Bs = make_fastdiv(v.Bs);
+    dd->div_hdv = make_fastdiv((uint32_t)(g.hd / 16));
+    return OC_OK;
+}
+
+void plan_into(DevDesc& dd, const Geometry& g, uint64_t n, uint32_t unit_bytes) {
     if (unit_bytes == 0) unit_bytes = 32768;
-    uint64_t R = std::max<uint64_t>(1, unit_bytes / d->geo.row);
-    R = std::min<uint64_t>(R, d->geo.G);
+    uint64_t R = std::max<uint64_t>(1, unit_bytes / g.row);
+    R = std::min<uint64_t>(R, g.G);
     R = std::min<uint64_t>(R, 1024);  // rows per unit are staged in a 1024-entry shared table
     dd.rows_per_unit = (uint32_t)R;
-    dd.tiles = (uint32_t)((d->geo.G + R - 1) / R);
-    dd.units_per_layer = (uint32_t)(d->N * 2 * dd.tiles);
+    dd.tiles = (uint32_t)((g.G + R - 1) / R);
+    dd.units_per_layer = (uint32_t)(n * 2 * dd.tiles);
     dd.div_upl = make_fastdiv(dd.units_per_layer);
     dd.div_units_per_chunk = make_fastdiv(2 * dd.tiles);
     dd.div_tiles = make_fastdiv(dd.tiles);
 }
+
+struct OffloadJob {
+    int device;
+    void* mem;
+    uint64_t cls;
+};
+
+void CUDART_CB offload_done(void* p) {  // host callback after the gather kernel: recycle the block
+    OffloadJob* j = (OffloadJob*)p;
+    dev_pool_free(j->device, j->mem, j->cls);
+    delete j;
+}
+}  // namespace
+
+void plan_units(Desc* d, uint32_t unit_bytes) { plan_into(d->dd, d->geo, d->N, unit_bytes); }
 
 }  // namespace oc
 
@@ -64,59 +214,9 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
             return oc::fail(OC_ENOTFOUND, "build_descriptor: chunk key " + std::to_string(i) + " not found");
         }
     }
-
-    // Normalise the target to the paged form: the flat client buffer is a paged cache with one
-    // G-token block per chunk, identity block table, block_stride = S and V after K in each block.
-    const uint32_t L = g.L;
-    std::vector<uint64_t> kb(L), vb(L);
-    std::vector<int32_t> bt;
-    uint64_t block_stride, token_stride, head_stride;
-    uint32_t Bs, first_token;
-    if (t->kind == OC_TARGET_FLAT) {
-        uint64_t W = n * L * g.S;
-        if (t->flat_capacity < W) return oc::fail(OC_ERANGE, "build_descriptor: flat target smaller than W = N*L*S");
-        if (t->flat_base % 16) return oc::fail(OC_EALIGN, "build_descriptor: flat_base not 16-byte aligned");
-        for (uint32_t l = 0; l < L; l++) {
-            kb[l] = t->flat_base + (uint64_t)l * n * g.S;
-            vb[l] = kb[l] + (uint64_t)g.G * g.row;
-        }
-        bt.resize(n);
-        for (uint64_t i = 0; i < n; i++) bt[i] = (int32_t)i;
-        block_stride = g.S;
-        token_stride = g.row;
-        head_stride = g.hd;
-        Bs = g.G;
-        first_token = 0;
-    } else if (t->kind == OC_TARGET_PAGED) {
-        if (!t->k_base || !t->v_base || !t->block_table) return oc::fail(OC_EINVAL, "build_descriptor: null paged arrays");
-        if (t->block_size == 0) return oc::fail(OC_EINVAL, "build_descriptor: block_size must be >= 1");
-        Bs = t->block_size;
-        first_token = t->first_token;
-        uint64_t last = (uint64_t)first_token + n * g.G - 1;
-        if (last >= (1ull << 31)) return oc::fail(OC_ERANGE, "build_descriptor: token index exceeds 2^31");
-        uint64_t need = last / Bs + 1;
-        if (t->num_blocks < need) return oc::fail(OC_ERANGE, "build_descriptor: block table does not cover the prefix");
-        block_stride = t->block_stride;
-        token_stride = t->token_stride;
-        head_stride = t->head_stride;
-        if (block_stride % 16 || token_stride % 16 || head_stride % 16)
-            return oc::fail(OC_EALIGN, "build_descriptor: strides must be multiples of 16 bytes");
-        for (uint32_t l = 0; l < L; l++) {
-            kb[l] = t->k_base[l];
-            vb[l] = t->v_base[l];
-            if (kb[l] % 16 || vb[l] % 16) return oc::fail(OC_EALIGN, "build_descriptor: K/V base not 16-byte aligned");
-        }
-        bt.assign(t->block_table, t->block_table + need);
-        std::unordered_set<int32_t> seen;
-        seen.reserve(need * 2);
-        for (uint64_t b = first_token / Bs; b < need; b++) {
-            if (bt[b] < 0) return oc::fail(OC_EINVAL, "build_descriptor: negative block id");
-            if (!seen.insert(bt[b]).second)
-                return oc::fail(OC_EINVAL, "build_descriptor: duplicate block id in the prefix (reading c4)");
-        }
-    } else {
-        return oc::fail(OC_EINVAL, "build_descriptor: unknown target kind");
-    }
+    oc::PagedView v;
+    int rc = oc::normalize_target(g, n, t, "build_descriptor", &v);
+    if (rc) return rc;
 
     auto d = std::make_unique<Desc>();
     d->store = s;
@@ -125,67 +225,88 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     d->device = s->device;
     d->delivery = delivery;
     d->N = n;
-    d->nb = bt.size();
+    d->nb = v.bt.size();
     d->host_chunks = host_chunks;
-
-    // One device allocation: src[N] | k_base[L] | v_base[L] | ts[L+1] | unit_cnt[L] | ready, next | bt
-    size_t o_src = 0;
-    size_t o_kb = oc::align16(o_src + n * 8);
-    size_t o_vb = oc::align16(o_kb + L * 8);
-    size_t o_ts = oc::align16(o_vb + L * 8);
-    size_t o_cnt = oc::align16(o_ts + (L + 1) * 8);
-    size_t o_ready = oc::align16(o_cnt + L * 4);
-    size_t o_next = o_ready + 4;
-    size_t o_bt = oc::align16(o_ready + 16);
-    size_t total = oc::align16(o_bt + bt.size() * 4);
-    std::vector<uint8_t> stage(total, 0);
-    std::memcpy(stage.data() + o_src, src.data(), n * 8);
-    std::memcpy(stage.data() + o_kb, kb.data(), L * 8);
-    std::memcpy(stage.data() + o_vb, vb.data(), L * 8);
-    std::memcpy(stage.data() + o_bt, bt.data(), bt.size() * 4);
-
     oc::DeviceGuard dg(d->device);
-    uint64_t cls = 0;
-    void* mem = oc::dev_pool_alloc(d->device, total, &cls);
-    if (!mem) return oc::fail(OC_ENOMEM, "build_descriptor: device allocation failed");
-    cudaError_t e = cudaMemcpy(mem, stage.data(), total, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-        oc::dev_pool_free(d->device, mem, cls);
-        return oc::cuda_fail(e, "build_descriptor: upload");
-    }
-    d->dev_mem = mem;
-    d->dev_mem_class = cls;
-
-    uint8_t* m = (uint8_t*)mem;
-    oc::DevDesc& dd = d->dd;
-    std::memset(&dd, 0, sizeof dd);
-    dd.src = (const uint64_t*)(m + o_src);
-    dd.k_base = (const uint64_t*)(m + o_kb);
-    dd.v_base = (const uint64_t*)(m + o_vb);
-    dd.ts = (uint64_t*)(m + o_ts);
-    dd.unit_cnt = (uint32_t*)(m + o_cnt);
-    dd.ready = (uint32_t*)(m + o_ready);
-    dd.next_unit = (uint32_t*)(m + o_next);
-    dd.bt = (const int32_t*)(m + o_bt);
-    dd.S = g.S;
-    dd.row = g.row;
-    dd.block_stride = block_stride;
-    dd.token_stride = token_stride;
-    dd.head_stride = head_stride;
-    dd.N = (uint32_t)n;
-    dd.L = L;
-    dd.G = g.G;
-    dd.Bs = Bs;
-    dd.first_token = first_token;
-    dd.vpr = (uint32_t)(g.row / 16);
-    dd.nhd = (token_stride == g.row && head_stride == g.hd) ? 1u : 0u;
-    dd.chunk_major = delivery == OC_DELIVER_CHUNK_MAJOR;
-    dd.div_vpr = oc::make_fastdiv(dd.vpr);
-    dd.div_Bs = oc::make_fastdiv(Bs);
-    dd.div_hdv = oc::make_fastdiv((uint32_t)(g.hd / 16));
+    rc = oc::upload_block(d->device, g, src, v, nullptr, "build_descriptor", &d->dev_mem, &d->dev_mem_class, &d->dd,
+                          nullptr);
+    if (rc) return rc;
+    d->dd.chunk_major = delivery == OC_DELIVER_CHUNK_MAJOR;
     oc::plan_units(d.get(), 0);
     *out = (oc_desc*)d.release();
     return OC_OK;
+}
+
+OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const oc_layout* layout,
+                             const oc_target* t, void* stream, uint64_t* n_new, uint64_t* bad_index) {
+    if (!sh || !layout || !t) return oc::fail(OC_EINVAL, "put_from_paged: null pointer");
+    oc::Store* s = (oc::Store*)sh;
+    if (n_new) *n_new = 0;
+    if (n == 0) return OC_OK;
+    if (!keys) return oc::fail(OC_EINVAL, "put_from_paged: null keys");
+    if (s->read_only) return oc::fail(OC_EINVAL, "put_from_paged: store is a read-only imported peer");
+    if (t->kind != OC_TARGET_PAGED) return oc::fail(OC_EINVAL, "put_from_paged: source must be a paged cache");
+    if (!oc::same_layout(*layout, s->layout)) return oc::fail(OC_EINVAL, "put_from_paged: layout differs from the store's");
+    const oc::Geometry& g = s->geo;
+    if ((unsigned __int128)n * g.G >= ((unsigned __int128)1 << 31))
+        return oc::fail(OC_ERANGE, "put_from_paged: prefix longer than 2^31 tokens");
+    oc::PagedView v;
+    int rc = oc::normalize_target(g, n, t, "put_from_paged", &v);
+    if (rc) return rc;
+
+    // Reserve slots for the new keys (dedup by key), in prefix order.
+    std::vector<uint64_t> dst;
+    std::vector<uint32_t> pos;
+    int status = OC_OK;
+    {
+        std::unique_lock<std::shared_mutex> lk(s->mu);
+        for (uint64_t i = 0; i < n; i++) {
+            if (s->index.count(keys[i])) continue;
+            if (s->count >= s->capacity) {
+                if (bad_index) *bad_index = i;
+                status = oc::fail(OC_EFULL, "put_from_paged: store capacity exhausted");
+                break;
+            }
+            const uint64_t slot = s->count++;
+            s->index.emplace(keys[i], slot);
+            dst.push_back((uint64_t)(uintptr_t)s->slab + slot * g.chunk);
+            pos.push_back((uint32_t)i);
+        }
+    }
+    if (n_new) *n_new = dst.size();
+    if (dst.empty()) return status;
+    auto rollback = [&]() {  // the reserved slots never received their bytes: forget the keys
+        std::unique_lock<std::shared_mutex> lk(s->mu);
+        for (uint32_t p : pos) s->index.erase(keys[p]);
+        if (n_new) *n_new = 0;
+    };
+    oc::DeviceGuard dg(s->device);
+    oc::DevDesc dd;
+    void* mem = nullptr;
+    uint64_t cls = 0;
+    const uint32_t* pos_dev = nullptr;
+    rc = oc::upload_block(s->device, g, dst, v, &pos, "put_from_paged", &mem, &cls, &dd, &pos_dev);
+    if (rc) {
+        rollback();
+        return rc;
+    }
+    oc::plan_into(dd, g, dst.size(), 0);
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = oc::launch_offload(dd, pos_dev, s->device, st);
+    if (rc) {
+        cudaStreamSynchronize(st);
+        oc::dev_pool_free(s->device, mem, cls);
+        rollback();
+        return rc;
+    }
+    oc::OffloadJob* job = new oc::OffloadJob{s->device, mem, cls};
+    cudaError_t e = cudaLaunchHostFunc(st, oc::offload_done, job);
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(st);
+        oc::offload_done(job);
+        return oc::cuda_fail(e, "put_from_paged: completion callback");
+    }
+    return status;
 }
 
 OC_API int oc_desc_free(oc_desc* h) {

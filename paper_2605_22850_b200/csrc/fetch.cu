@@ -228,6 +228,52 @@ __global__ void __launch_bounds__(kThreads, 4) fetch_ldst_kernel(const DevDesc d
     if (threadIdx.x == 0 && pending) complete_units(d, pending_layer, 1);
 }
 
+// ---- offload (paged cache -> chunk slots) ----------------------------------------------------------
+// The inverse of copy_rows: nrows scattered source rows (listed in `tab`) to contiguous `dst`.
+__device__ __forceinline__ void gather_rows(const DevDesc& d, uint8_t* dst, uint32_t nrows, const uint64_t* tab) {
+    const uint32_t nvec = nrows * d.vpr;
+    for (uint32_t v0 = 0; v0 < nvec; v0 += kThreads * kVec) {
+        uint4 buf[kVec];
+#pragma unroll
+        for (int k = 0; k < kVec; k++) {
+            const uint32_t v = v0 + threadIdx.x + k * kThreads;
+            if (v < nvec) {
+                const uint32_t r = fdiv(v, d.div_vpr);
+                const uint32_t c = v - r * d.vpr;
+                uint64_t off;
+                if (d.nhd) {
+                    off = (uint64_t)c * 16;
+                } else {
+                    const uint32_t h = fdiv(c, d.div_hdv);
+                    off = (uint64_t)h * d.head_stride + (uint64_t)(c - h * d.div_hdv.d) * 16;
+                }
+                buf[k] = ld_stream((const void*)(tab[r] + off));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kVec; k++) {
+            const uint32_t v = v0 + threadIdx.x + k * kThreads;
+            if (v < nvec) st_global((uint64_t)(dst + (uint64_t)v * 16), buf[k]);
+        }
+    }
+}
+
+// Unit g of the offload job: chunk j (new slot d.src[j], request chunk pos[j]), matrix, row tile.
+__global__ void __launch_bounds__(kThreads, 4) offload_kernel(const DevDesc d, const uint32_t* __restrict__ pos,
+                                                              uint32_t total) {
+    __shared__ uint64_t tab[kMaxRows];
+    for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
+        const UnitGeo u = unit_geo(d, g);
+        const uint64_t base = unit_base(d, u);
+        const uint32_t tok0 = d.first_token + pos[u.j] * d.G + u.r0;
+        __syncthreads();  // the previous unit is done with tab
+        for (uint32_t r = threadIdx.x; r < u.nrows; r += kThreads) tab[r] = row_dst(d, base, tok0 + r, nullptr);
+        __syncthreads();
+        uint8_t* dst = (uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + ((uint64_t)u.kv * d.G + u.r0) * d.row;
+        gather_rows(d, dst, u.nrows, tab);
+    }
+}
+
 // ---- BULK engine ---------------------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
@@ -622,6 +668,16 @@ int launch_ldst(Desc* d, int sms, uint32_t max_ctas, uint32_t g0, uint32_t g1, c
 }
 
 }  // namespace
+
+int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s) {
+    static int occ = occupancy((const void*)offload_kernel, kThreads, 0);
+    const uint64_t total = (uint64_t)dd.units_per_layer * dd.L;
+    if (total >= (1ull << 32)) return fail(OC_ERANGE, "put_from_paged: too many units");
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)occ * device_sm_count(device), total));
+    offload_kernel<<<(unsigned)grid, kThreads, 0, s>>>(dd, pos, (uint32_t)total);
+    OC_CUDA(cudaGetLastError());
+    return OC_OK;
+}
 
 int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     if (o.mode != OC_FETCH_PERSISTENT && o.mode != OC_FETCH_PER_LAYER)

@@ -167,6 +167,8 @@ void plan_units(Desc* d, uint32_t unit_bytes);
 
 // kernel launchers (fetch.cu)
 int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s);
+// Offload gather: new chunk j (slot dd.src[j]) <- the paged rows of request chunk pos[j].
+int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s);
 
 // driver entry point for cuStreamWaitValue32 (resolved lazily)
 int stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t value);
