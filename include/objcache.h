@@ -278,6 +278,25 @@ typedef struct {
 OC_API int oc_schedule_bandwidth(int policy, const oc_profile* profiles, uint64_t n, double cap_Bps,
                                  double delta_Bps, double* rates_out);
 
+/* ---- multi-tenant pool: epoch admission (Sec. 3.4; Sec. 3.6; Alg. A2) -----
+ * submit: a request (its descriptor, per-layer compute window c_i and copy stream) joins the
+ *   pool.  If W = N*L*S < theta (Eq. 2) it is served chunkwise at once, unpaced and outside the
+ *   pool (state CHUNKWISE); otherwise it waits for the next epoch (state WAITING).
+ * epoch: requests whose fetch has finished leave (their bandwidth returns now, not earlier);
+ *   every waiting request is admitted with a rate from schedule_bandwidth(policy, s_i = N*S,
+ *   c_i, cap - rates still in use, delta) and its fetch is launched paced at that rate for the
+ *   whole load (state RUNNING).  No admission when nothing is left of the cap.
+ * The descriptors must outlive the pool's use of them.  Not thread-safe across pools sharing a
+ * descriptor. */
+typedef struct oc_tenant_pool oc_tenant_pool;
+enum { OC_TENANT_WAITING = 0, OC_TENANT_RUNNING = 1, OC_TENANT_DONE = 2, OC_TENANT_CHUNKWISE = 3 };
+OC_API int oc_pool_create(int policy, double cap_Bps, double delta_Bps, uint64_t theta_bytes, oc_tenant_pool** out);
+OC_API int oc_pool_submit(oc_tenant_pool* pool, oc_desc* desc, double compute_per_layer_s, void* copy_stream,
+                          uint64_t* ticket);
+OC_API int oc_pool_epoch(oc_tenant_pool* pool, uint64_t* n_admitted);
+OC_API int oc_pool_status(oc_tenant_pool* pool, uint64_t ticket, int* state, double* rate_Bps);
+OC_API int oc_pool_destroy(oc_tenant_pool* pool);
+
 /* ---- errors ---------------------------------------------------------------- */
 OC_API const char* oc_last_error(void);
 OC_API const char* oc_status_str(int status);

@@ -149,3 +149,15 @@ def schedule(policy: str, s, c, B, delta=0.0):
             raise ValueError("bandwidth cap B must be > 0")
         return []
     return POLICIES[policy](s, c, B, delta)
+
+
+def epoch_admission(policy: str, running_rates, s, c, B, delta=0.0):
+    """One scheduling epoch (Sec. 3.6; Alg. A2 lines 1-6): the waiting requests
+    (s_i, c_i) are admitted under the budget the still-running requests leave, B - sum(running),
+    with the policy's allocation; rates then stay fixed for the whole load, and bandwidth of a
+    request that finishes returns only at the next epoch.  Returns None when nothing is admitted
+    (no waiting request, or no budget left)."""
+    budget = B - sum(running_rates)
+    if len(s) == 0 or budget <= 0:
+        return None
+    return schedule(policy, s, c, budget, delta)

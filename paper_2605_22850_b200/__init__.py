@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libobjcache.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2605_22850_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2605_22850_b200/build.py` "
                       "(there is no fallback implementation)")
 _lib = ctypes.CDLL(LIB_PATH)
 
@@ -32,6 +32,7 @@ TIER_HBM, TIER_PINNED_HOST = 0, 1
 DELIVER_LAYER_MAJOR, DELIVER_CHUNK_MAJOR = 0, 1
 TARGET_PAGED, TARGET_FLAT = 0, 1
 FETCH_PERSISTENT, FETCH_PER_LAYER = 0, 1
+TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 COPY_LDST, COPY_BULK = 0, 1
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
@@ -94,12 +95,21 @@ _SIGS = {
     "oc_layer_times": [_vp, c_u64p],
     "oc_schedule_bandwidth": [ctypes.c_int, ctypes.POINTER(CProfile), ctypes.c_uint64, ctypes.c_double,
                               ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
+    "oc_pool_create": [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, ctypes.POINTER(_vp)],
+    "oc_pool_submit": [_vp, _vp, ctypes.c_double, _vp, c_u64p],
+    "oc_pool_epoch": [_vp, c_u64p],
+    "oc_pool_status": [_vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)],
+    "oc_pool_destroy": [_vp],
     "oc_last_error": [],
     "oc_status_str": [ctypes.c_int],
     "oc_abi_version": [],
 }
 for _name, _args in _SIGS.items():
-    _f = getattr(_lib, _name)
+    try:
+        _f = getattr(_lib, _name)
+    except AttributeError as _e:
+        raise ImportError(f"{LIB_PATH} is stale (no {_name}): rebuild with "
+                          "`python paper_2605_22850_b200/build.py`") from _e
     _f.argtypes = _args
     _f.restype = ctypes.c_int
 _lib.oc_last_error.restype = ctypes.c_char_p
@@ -429,6 +439,41 @@ def fetch_batch(descs: Sequence[Descriptor], stream=None, **opts) -> Batch:
     b = Batch(descs)
     b.fetch(stream, **opts)
     return b
+
+
+class TenantPool:
+    """Epoch admission of concurrent layerwise requests under a shared cap (Sec. 3.6, Alg. A2)."""
+
+    def __init__(self, policy, cap_Bps: float, delta_Bps: float = 0.0, theta_bytes: int = 0):
+        code = POLICIES[policy] if isinstance(policy, str) else int(policy)
+        h = _vp()
+        _check(_lib.oc_pool_create(code, float(cap_Bps), float(delta_Bps), int(theta_bytes), ctypes.byref(h)))
+        self._h = h
+        self._descs = []
+
+    def submit(self, desc: Descriptor, compute_per_layer_s: float, stream=None) -> int:
+        t = ctypes.c_uint64()
+        _check(_lib.oc_pool_submit(self._h, desc._h, float(compute_per_layer_s), _stream(stream), ctypes.byref(t)))
+        self._descs.append(desc)
+        return t.value
+
+    def epoch(self) -> int:
+        n = ctypes.c_uint64()
+        _check(_lib.oc_pool_epoch(self._h, ctypes.byref(n)))
+        return n.value
+
+    def status(self, ticket: int):
+        st, r = ctypes.c_int(), ctypes.c_double()
+        _check(_lib.oc_pool_status(self._h, int(ticket), ctypes.byref(st), ctypes.byref(r)))
+        return st.value, r.value
+
+    def close(self, _free=_lib.oc_pool_destroy):
+        if getattr(self, "_h", None):
+            _free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 # ---- the boundary calls, by the names the method uses ---------------------------------------------

@@ -2,7 +2,7 @@
 
 All sources go through nvcc; the CUDA runtime is linked statically and the driver is reached via
 cudaGetDriverEntryPoint, so the library loads (and its host-only entry points work) on a machine
-without a GPU driver.  Usage: python -m paper_2605_22850_b200.build [--force]
+without a GPU driver.  Usage: python paper_2605_22850_b200/build.py [--force]
 """
 import os
 import subprocess
@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden,-Wall",
           "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["common.cpp", "sha256.cpp", "scheduler.cpp", "pool.cpp", "store.cpp", "descriptor.cpp", "fetch.cu"]
+SOURCES = ["common.cpp", "sha256.cpp", "scheduler.cpp", "pool.cpp", "store.cpp", "descriptor.cpp", "tenants.cpp", "fetch.cu"]
 
 
 def _newer(target, deps):

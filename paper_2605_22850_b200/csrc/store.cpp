@@ -269,7 +269,9 @@ OC_API int oc_store_import(const void* buf, uint64_t size, int device, oc_store*
     std::memcpy(&hd, buf, sizeof hd);
     if (hd.magic != oc::kExportMagic || hd.version != OC_ABI_VERSION)
         return oc::fail(OC_EINVAL, "store_import: not an objcache export blob");
-    if (size < sizeof hd + hd.count * 40) return oc::fail(OC_EINVAL, "store_import: truncated blob");
+    if (hd.count > (size - sizeof hd) / 40 || hd.count > hd.capacity)
+        return oc::fail(OC_EINVAL, "store_import: truncated or corrupt blob");
+    if (hd.tier != OC_TIER_HBM) return oc::fail(OC_EINVAL, "store_import: only HBM stores are exported");
     auto s = std::make_unique<Store>();
     int rc = oc::make_geometry(&hd.layout, &s->geo);
     if (rc) return rc;
@@ -280,13 +282,7 @@ OC_API int oc_store_import(const void* buf, uint64_t size, int device, oc_store*
     s->count = hd.count;
     s->owns_slab = false;
     s->read_only = true;
-    {
-        oc::DeviceGuard dg(device);
-        void* p = nullptr;
-        OC_CUDA(cudaIpcOpenMemHandle(&p, hd.handle, cudaIpcMemLazyEnablePeerAccess));
-        s->slab = (uint8_t*)p;
-        s->ipc_mapped = true;
-    }
+    // Parse and validate the key table before mapping anything.
     const uint8_t* in = (const uint8_t*)buf + sizeof hd;
     s->index.reserve(hd.count * 2);
     for (uint64_t i = 0; i < hd.count; i++, in += 40) {
@@ -296,6 +292,13 @@ OC_API int oc_store_import(const void* buf, uint64_t size, int device, oc_store*
         std::memcpy(&slot, in + 32, 8);
         if (slot >= hd.capacity) return oc::fail(OC_EINVAL, "store_import: corrupt slot index");
         s->index.emplace(k, slot);
+    }
+    {
+        oc::DeviceGuard dg(device);
+        void* p = nullptr;
+        OC_CUDA(cudaIpcOpenMemHandle(&p, hd.handle, cudaIpcMemLazyEnablePeerAccess));
+        s->slab = (uint8_t*)p;
+        s->ipc_mapped = true;
     }
     *out = (oc_store*)s.release();
     return OC_OK;

@@ -160,3 +160,17 @@ def test_errors_and_empty():
     assert sch.stall_opt([4.0], [2.0], 100.0) == [2.0]           # caps fit: r = r*, leftover unused
     assert sch.calibrated_stall_opt([4.0], [2.0], 100.0, 1.0) == [3.0]
     assert sch.stall_opt([4.0, 9.0], [1.0, 1.0], 5.0) == pytest.approx([2.0, 3.0])   # sqrt-proportional
+
+
+def test_epoch_admission():
+    s = [4e9, 9e9]
+    c = [1.0, 1.0]
+    # nothing running: one epoch is plain scheduling
+    assert sch.epoch_admission("stall_opt", [], s, c, 5e9) == pytest.approx(sch.stall_opt(s, c, 5e9))
+    # running requests hold their rates: the new ones share what is left, never more than B in total
+    r = sch.epoch_admission("equal", [1e9, 1.5e9], s, c, 5e9)
+    assert r == pytest.approx([1.25e9, 1.25e9]) and sum(r) + 2.5e9 == pytest.approx(5e9)
+    r = sch.epoch_admission("cal_stall_opt", [3e9], s, c, 5e9, 0.5e9)
+    assert sum(r) <= 2e9 * (1 + 1e-12)
+    assert sch.epoch_admission("equal", [5e9], s, c, 5e9) is None        # budget exhausted: wait
+    assert sch.epoch_admission("equal", [1e9], [], [], 5e9) is None       # nobody waiting
