@@ -30,7 +30,7 @@ namespace oc {
 constexpr int kThreads = 256;   // LDST: threads per CTA
 constexpr int kVec = 8;         // LDST: 16-byte vectors in flight per thread per round
 constexpr int kMaxRows = 1024;  // rows per unit (plan_units caps R)
-constexpr uint32_t kFifo = 64;  // BULK: copy-warp -> signaler-warp retire FIFO
+constexpr uint32_t kFifo = 16;  // BULK: copy-warp -> signaler-warp retire FIFO (mbarrier slots)
 constexpr uint32_t kBulkStaticSmem = 1280;  // BULK: FIFO + claim ring (static shared memory, rounded up)
 
 // ---- small device helpers ------------------------------------------------------------------------
@@ -283,6 +283,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -322,16 +326,6 @@ __device__ __forceinline__ void bulk_wait_read() {
 
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-__device__ __forceinline__ uint32_t ld_acquire_cta(const volatile uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32((const void*)p)) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release_cta(volatile uint32_t* p, uint32_t v) {
-    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32((const void*)p)), "r"(v) : "memory");
 }
 
 // A batch: several descriptors (same L) fetched by one launch.  Units are claimed in one global
@@ -387,8 +381,9 @@ __device__ void observe_batch(const BatchArgs& ba, uint64_t t0) {
 }
 
 // CTA 0: observer.  CTA b >= 1: warp 0 claims units and copies them through a `stages`-deep
-// shared-memory ring; warp 1 (lane 0) turns the copy warp's retire records into release reductions
-// so the copy pipeline never waits on a GPU-scope fence.  A unit is retired once its bulk stores
+// shared-memory ring; warp 1 (lane 0) turns the copy warp's retire records -- handed over through
+// an mbarrier-guarded shared-memory FIFO -- into release reductions, so the copy pipeline never
+// waits on a GPU-scope fence.  A unit is retired once its bulk stores
 // are complete (wait_group with a lag of two units, so stores stay in flight).
 template <bool BATCH>
 __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ DevDesc d0,
@@ -398,7 +393,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t fifo_req[kFifo], fifo_layer[kFifo], fifo_n[kFifo];
     __shared__ uint32_t s_unit[32], s_req[32];
-    __shared__ uint32_t fifo_head, fifo_tail;
+    __shared__ __align__(8) uint64_t fifo_full[kFifo], fifo_empty[kFifo];
     const uint64_t t0 = globaltimer();
     if (blockIdx.x == 0) {
         if (BATCH) {
@@ -414,21 +409,22 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     const uint32_t lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < stages; s++) mbar_init(&bars[s], 1);
+        for (uint32_t f = 0; f < kFifo; f++) {
+            mbar_init(&fifo_full[f], 1);
+            mbar_init(&fifo_empty[f], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        fifo_head = 0;
-        fifo_tail = 0;
     }
     __syncthreads();
     if (threadIdx.x >= 32) {  // ---- signaler warp
         if (threadIdx.x != 32) return;
-        for (uint32_t h = 0;; h++) {
-            while (ld_acquire_cta(&fifo_tail) == h) __nanosleep(64);
-            const uint32_t req = ((volatile uint32_t*)fifo_req)[h % kFifo];
-            const uint32_t layer = ((volatile uint32_t*)fifo_layer)[h % kFifo];
-            const uint32_t n = ((volatile uint32_t*)fifo_n)[h % kFifo];
+        for (uint32_t h = 0;; h++) {  // slot h % kFifo, round h / kFifo
+            const uint32_t f = h % kFifo;
+            mbar_wait(&fifo_full[f], (h / kFifo) & 1u);  // acquire: the record is visible
+            const uint32_t req = fifo_req[f], layer = fifo_layer[f], n = fifo_n[f];
+            mbar_arrive(&fifo_empty[f]);                 // release: the slot may be reused
             if (layer == 0xffffffffu) return;
             complete_units(BATCH ? ba.descs[req] : d0, layer, n);
-            st_release_cta(&fifo_head, h + 1);
         }
     }
     // ---- copy warp
@@ -436,11 +432,13 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     uint32_t* claim_ctr = BATCH ? ba.claim : d0.next_unit;
     uint32_t tail = 0;
     auto push = [&](uint32_t req, uint32_t layer, uint32_t n) {  // lane 0 only
-        while (tail - ld_acquire_cta(&fifo_head) >= kFifo) __nanosleep(64);
-        ((volatile uint32_t*)fifo_req)[tail % kFifo] = req;
-        ((volatile uint32_t*)fifo_layer)[tail % kFifo] = layer;
-        ((volatile uint32_t*)fifo_n)[tail % kFifo] = n;
-        st_release_cta(&fifo_tail, ++tail);
+        const uint32_t f = tail % kFifo;
+        mbar_wait(&fifo_empty[f], ((tail / kFifo) & 1u) ^ 1u);  // round 0 passes on the fresh barrier
+        fifo_req[f] = req;
+        fifo_layer[f] = layer;
+        fifo_n[f] = n;
+        mbar_arrive(&fifo_full[f]);
+        tail++;
     };
     // s_unit/s_req[k % 32] = the k-th unit this CTA claimed (kEnd once the launch's units run out).
     bool exhausted = false;  // lane 0 only

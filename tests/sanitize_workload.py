@@ -1,0 +1,40 @@
+"""Small fetches of every engine/mode/target under compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import numpy as np
+import torch
+import paper_2605_22850_b200 as oc
+from oracle.geometry import Layout
+from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family
+
+lay = Layout(2, 2, 64, 2, 16)
+ok = 0
+for kind in ("nhd", "hnd"):
+    for engine in (oc.COPY_BULK, oc.COPY_LDST):
+        for mode in (oc.FETCH_PERSISTENT, oc.FETCH_PER_LAYER):
+            req = requests_family(lay, 3, 0, [5])[0]
+            with oc.Store(lay, capacity=8) as st:
+                keys = oc.chunk_keys(req.tokens, 16)
+                st.put_chunks(keys, payload_stack(lay, 3, req.payload_ids))
+                dest = make_dest(lay, 5, kind, Bs=8, first_token=3, seed=1)
+                buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+                d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+                s = torch.cuda.Stream()
+                d.fetch_layerwise(s, engine=engine, mode=mode, unit_bytes=1024)
+                d.wait_layer(1, torch.cuda.current_stream())
+                assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 3, req, dest))
+                if engine == oc.COPY_BULK and mode == oc.FETCH_PERSISTENT:
+                    b = oc.Batch([d])
+                    b.fetch(s)
+                    d.sync_layer(1)
+                    b.close()
+                    src = make_dest(lay, 5, kind, Bs=8, first_token=3, seed=1)
+                    st2 = oc.Store(lay, capacity=8)
+                    oc.put_from_paged(st2, keys, lay, lib_target(oc, src, buf.data_ptr()), s)
+                    s.synchronize()
+                    st2.close()
+                d.close()
+                ok += 1
+torch.cuda.synchronize()
+print("sanitize workload ok", ok)
