@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--stall64k", type=int, default=1)
     p.add_argument("--profile", action="store_true", help="no soak / clock sampling (for ncu runs)")
+    p.add_argument("--corun", action="store_true", help="fetches co-running with a bf16 GEMM stream: both "
+                   "throughputs vs the copy-CTA budget (adds a 'corun' object)")
     p.add_argument("--sweep", action="store_true", help="rate sweep (Fig. 15 analog): added TTFT of one "
                    "paced request vs rate / r*, against Eq. 3 (adds a 'sweep' object)")
     p.add_argument("--batch", default="", help="NxM: N 4K-token + M 64K-token concurrent requests (config 5, "
@@ -342,6 +344,8 @@ def main_ours(args):
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.sweep:
         out["sweep"] = sweep_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and args.corun:
+        out["corun"] = corun_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_stall:
         out["stall"] = stall_leg(args, oc, torch, dev, lay_t, fopts)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -485,6 +489,74 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts):
     res["windows"] = ("Table A5 A100 per-layer compute (P:2706-2713), 87.5% hit; spin-kernel emulation; "
                       "baseline = same chain with KV resident (opt-local-LW analog)")
     return res
+
+
+def corun_leg(args, oc, torch, dev, lay_t):
+    """Prefill compute and KV delivery share the GPU (hard part 2): a stream of bf16
+    8192^3 GEMMs (torch.matmul, the compute stand-in) runs concurrently with back-to-back 4K fetches
+    on another stream.  Reported per copy-CTA budget: fetch GB/s and GEMM TFLOP/s alone and together."""
+    import synth
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    N = N_CHUNKS_4K
+    store = oc.Store(lay_t, capacity=2 * N, tier=oc.TIER_HBM, device=dev.index)
+    descs = []
+    for r in range(2):
+        (tok,), _ = synth.family_streams(600 + r, G, 0, [N])
+        keys = oc.chunk_keys(tok, G)
+        store.put_chunks(keys, torch.randint(0, 256, (N, chunk), dtype=torch.uint8, device=dev))
+        need = N * G // Bs
+        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
+        per_kv = need * Bs * row
+        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+                             synth.block_table(r, need, need), 0)
+        descs.append((oc.build_descriptor(store, keys, lay_t, tgt), cache))
+    a = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev)
+    b = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev)
+    cbuf = torch.empty(8192, 8192, dtype=torch.bfloat16, device=dev)
+    gs, fs = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    n_gemm, n_fetch = 40, 200
+    flops = 2 * 8192 ** 3
+
+    def run(do_gemm, do_fetch, fopts):
+        torch.cuda.synchronize()
+        e = {k: torch.cuda.Event(enable_timing=True) for k in ("g0", "g1", "f0", "f1")}
+        if do_gemm:
+            e["g0"].record(gs)
+            with torch.cuda.stream(gs):
+                for _ in range(n_gemm):
+                    torch.matmul(a, b, out=cbuf)
+            e["g1"].record(gs)
+        if do_fetch:
+            e["f0"].record(fs)
+            for i in range(n_fetch):
+                descs[i % 2][0].fetch_layerwise(fs, **fopts)
+            e["f1"].record(fs)
+        torch.cuda.synchronize()
+        res = {}
+        if do_gemm:
+            res["gemm_tflops"] = round(n_gemm * flops / e["g0"].elapsed_time(e["g1"]) / 1e9, 1)
+        if do_fetch:
+            res["fetch_GBps"] = round(n_fetch * 2 * N * S * L / e["f0"].elapsed_time(e["f1"]) / 1e6, 1)
+        return res
+
+    run(True, True, {})                                     # warm up cuBLAS and the fetch path
+    out = {"gemm_alone": run(True, False, {})}
+    for engine, name in ((oc.COPY_BULK, "bulk"), (oc.COPY_LDST, "ldst")):
+        for mc in (0, 148, 64, 32, 16):
+            fo = {"engine": engine, "max_ctas": mc}
+            alone = run(False, True, fo)
+            both = run(True, True, fo)
+            out[f"{name}_ctas{mc or 'auto'}"] = {"fetch_alone_GBps": alone["fetch_GBps"],
+                                                 "fetch_corun_GBps": both["fetch_GBps"],
+                                                 "gemm_corun_tflops": both["gemm_tflops"]}
+    for d, _ in descs:
+        d.close()
+    store.close()
+    del a, b, cbuf, descs
+    torch.cuda.empty_cache()
+    return out
 
 
 def sweep_leg(args, oc, torch, dev, lay_t):

@@ -442,15 +442,20 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     };
     // s_unit/s_req[k % 32] = the k-th unit this CTA claimed (kEnd once the launch's units run out).
     bool exhausted = false;  // lane 0 only
+    // The claim for the next unit is issued one claim ahead, so the atomic's round trip (~1 us)
+    // overlaps a unit's copy instead of stalling the issue loop -- with a small copy-CTA budget
+    // that latency would otherwise cap each CTA at one unit per round trip.
+    uint32_t next_raw = lane == 0 ? atomicAdd(claim_ctr, 1u) : 0u;
     auto claim = [&](uint32_t k) {  // lane 0 only: claim unit k, returns false at the end
         uint32_t g = kEnd, req = 0;
         if (!exhausted) {
             // Each copy CTA stops after its first claim past g1: a launch advances the counter by
             // exactly (units + copy CTAs), so the host knows the next launch's grab_base.
-            const uint32_t gg = g0 + (atomicAdd(claim_ctr, 1u) - grab_base);
+            const uint32_t gg = g0 + (next_raw - grab_base);
             if (gg >= g1) {
                 exhausted = true;
             } else {
+                next_raw = atomicAdd(claim_ctr, 1u);
                 const Resolved rs = resolve<BATCH>(d0, ba, gg);
                 g = rs.g;
                 req = rs.req;
@@ -558,13 +563,31 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
             if (lane == 0) issue_load(kl);
         }
         __syncwarp();
-        if (next_retire + 2 <= k) {
-            bulk_wait<2>();  // unit k-2's stores are complete
+        // Retire policy.  Units of one (request, layer) keep their stores in flight together; when
+        // the next unit starts another layer (or the CTA's work ends) every outstanding unit is
+        // retired as soon as its stores complete, so the layer is announced promptly.  Inside a
+        // layer at most 8 units stay unretired -- a small copy-CTA budget (a CTA owning many
+        // units per layer) keeps 4-8 units of stores in flight instead of waiting on each.
+        const uint32_t gn = s_unit[(k + 1) % 32];  // claimed already: claims run stages-1 ahead
+        bool boundary = gn == kEnd || s_req[(k + 1) % 32] != s_req[k % 32];
+        if (!boundary)
+            boundary = fdiv(gn, desc_of(k + 1).div_upl) != fdiv(g, d.div_upl);
+        if (boundary) {
+            bulk_wait<0>();
+            fence_proxy_async_global();
+            __syncwarp();
+            if (lane == 0) {
+                for (uint32_t r = next_retire; r <= k; r++) retire(r);
+                flush();
+            }
+            next_retire = k + 1;
+        } else if (k + 1 - next_retire >= 8) {
+            bulk_wait<4>();  // units up to k-4 have completed stores
             fence_proxy_async_global();
             __syncwarp();
             if (lane == 0)
-                for (uint32_t r = next_retire; r + 2 <= k; r++) retire(r);
-            next_retire = k - 1;
+                for (uint32_t r = next_retire; r + 4 <= k; r++) retire(r);
+            next_retire = k - 3;
         }
     }
     bulk_wait<0>();
@@ -619,7 +642,7 @@ BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units
         uint32_t st = per_cta > 128 ? (per_cta - 128) / p.stage_bytes : 0;
         st = std::min<uint32_t>(st, (uint32_t)std::max(2, env_int("OC_BULK_STAGES", 16)));
         if (st >= 2 || per_sm == 1) {
-            p.stages = std::max<uint32_t>(st, 1);
+            p.stages = st >= 2 ? st : 0;  // 0: a unit does not fit twice in shared memory
             break;
         }
         per_sm /= 2;
@@ -645,6 +668,7 @@ cudaError_t set_bulk_smem(uint32_t smem) {
 // One launch copies units [g0, g1); it claims them from the descriptor's counter starting at
 // d->grab_ctr and advances that counter by (units + copy CTAs) -- see claim_unit.
 int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
+    if (p.stages < 2) return fail(OC_ENOTSUP, "bulk engine: two units do not fit in shared memory (use LDST)");
     OC_CUDA(set_bulk_smem<false>(p.smem));
     fetch_bulk_kernel<false><<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
                                                                  p.stage_bytes);
@@ -796,6 +820,7 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
     ba.n = b->n;
     ba.upl_total = (uint32_t)total;
     ba.div_upl_total = make_fastdiv((uint32_t)total);
+    if (p.stages < 2) return fail(OC_ENOTSUP, "fetch_batch: two units do not fit in shared memory");
     OC_CUDA(set_bulk_smem<true>(p.smem));
     fetch_bulk_kernel<true><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)(total * L), b->grab_ctr,
                                                                 p.stages, p.stage_bytes);
