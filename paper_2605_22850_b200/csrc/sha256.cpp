@@ -1,5 +1,8 @@
 // SHA-256 (FIPS 180-4) and the rolling chunk key H_i = SHA-256(H_{i-1} || LE-u32 tokens_i)
 // (Sec. 2.1; the paper names only "Hash", reading c1 in DESIGN.md).
+#include <cpuid.h>
+#include <immintrin.h>
+
 #include "oc_internal.h"
 
 namespace oc {
@@ -17,6 +20,51 @@ const uint32_t K256[64] = {
 
 inline uint32_t rotr(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
 
+// x86 SHA extensions (SHA-NI): the same FIPS 180-4 compression, 4 rounds per sha256rnds2 pair.
+// The chain keys of a 64K-token prefix are 4096 sequential hashes on the match_prefix critical
+// path; SHA-NI makes them ~5x cheaper than the portable rounds.
+bool cpu_has_sha_ni() {
+    unsigned a, b, c, d;
+    if (!__get_cpuid_count(7, 0, &a, &b, &c, &d)) return false;
+    return (b >> 29) & 1u;  // CPUID.(EAX=7,ECX=0):EBX.SHA[bit 29]
+}
+const bool g_sha_ni = cpu_has_sha_ni();
+
+__attribute__((target("sha,sse4.1,ssse3"))) void blocks_sha_ni(uint32_t h[8], const uint8_t* p, size_t nblocks) {
+    const __m128i bswap = _mm_set_epi64x(0x0c0d0e0f08090a0bULL, 0x0405060700010203ULL);
+    __m128i tmp = _mm_loadu_si128((const __m128i*)&h[0]);
+    __m128i st1 = _mm_loadu_si128((const __m128i*)&h[4]);
+    tmp = _mm_shuffle_epi32(tmp, 0xB1);      // CDAB
+    st1 = _mm_shuffle_epi32(st1, 0x1B);      // EFGH
+    __m128i st0 = _mm_alignr_epi8(tmp, st1, 8);  // ABEF
+    st1 = _mm_blend_epi16(st1, tmp, 0xF0);       // CDGH
+    for (; nblocks; nblocks--, p += 64) {
+        const __m128i abef = st0, cdgh = st1;
+        __m128i w[16];
+        for (int g = 0; g < 16; g++) {
+            if (g < 4) {
+                w[g] = _mm_shuffle_epi8(_mm_loadu_si128((const __m128i*)(p + 16 * g)), bswap);
+            } else {
+                __m128i x = _mm_sha256msg1_epu32(w[g - 4], w[g - 3]);
+                x = _mm_add_epi32(x, _mm_alignr_epi8(w[g - 1], w[g - 2], 4));
+                w[g] = _mm_sha256msg2_epu32(x, w[g - 1]);
+            }
+            __m128i m = _mm_add_epi32(w[g], _mm_loadu_si128((const __m128i*)&K256[4 * g]));
+            st1 = _mm_sha256rnds2_epu32(st1, st0, m);
+            m = _mm_shuffle_epi32(m, 0x0E);
+            st0 = _mm_sha256rnds2_epu32(st0, st1, m);
+        }
+        st0 = _mm_add_epi32(st0, abef);
+        st1 = _mm_add_epi32(st1, cdgh);
+    }
+    tmp = _mm_shuffle_epi32(st0, 0x1B);      // FEBA
+    st1 = _mm_shuffle_epi32(st1, 0xB1);      // DCHG
+    st0 = _mm_blend_epi16(tmp, st1, 0xF0);   // DCBA
+    st1 = _mm_alignr_epi8(st1, tmp, 8);      // HGFE
+    _mm_storeu_si128((__m128i*)&h[0], st0);
+    _mm_storeu_si128((__m128i*)&h[4], st1);
+}
+
 struct Sha {
     uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
                      0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
@@ -25,6 +73,10 @@ struct Sha {
     uint64_t total = 0;
 
     void block(const uint8_t* p) {
+        if (g_sha_ni) {
+            blocks_sha_ni(h, p, 1);
+            return;
+        }
         uint32_t w[64];
         for (int i = 0; i < 16; i++)
             w[i] = (uint32_t)p[4 * i] << 24 | (uint32_t)p[4 * i + 1] << 16 | (uint32_t)p[4 * i + 2] << 8 |
@@ -54,18 +106,21 @@ struct Sha {
             fill += take; p += take; n -= take;
             if (fill == 64) { block(buf); fill = 0; }
         }
+        if (n >= 64 && g_sha_ni) {
+            blocks_sha_ni(h, p, n / 64);
+            p += n & ~size_t(63);
+            n &= 63;
+        }
         while (n >= 64) { block(p); p += 64; n -= 64; }
         if (n) { std::memcpy(buf, p, n); fill = n; }
     }
     void finish(uint8_t out[32]) {
-        uint64_t bits = total * 8;
-        uint8_t pad = 0x80;
-        update(&pad, 1);
-        uint8_t z = 0;
-        while (fill != 56) update(&z, 1);
-        uint8_t len[8];
-        for (int i = 0; i < 8; i++) len[i] = (uint8_t)(bits >> (56 - 8 * i));
-        update(len, 8);
+        // padding: 0x80, zeros up to 56 mod 64, then the 64-bit big-endian bit length
+        const uint64_t bits = total * 8;
+        uint8_t pad[72] = {0x80};
+        const size_t zeros = (fill < 56 ? 56 - fill : 120 - fill) - 1;
+        for (int i = 0; i < 8; i++) pad[1 + zeros + i] = (uint8_t)(bits >> (56 - 8 * i));
+        update(pad, 1 + zeros + 8);
         for (int i = 0; i < 8; i++) {
             out[4 * i] = (uint8_t)(h[i] >> 24); out[4 * i + 1] = (uint8_t)(h[i] >> 16);
             out[4 * i + 2] = (uint8_t)(h[i] >> 8); out[4 * i + 3] = (uint8_t)h[i];

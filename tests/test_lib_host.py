@@ -143,3 +143,10 @@ def test_data_path_fails_loudly_without_gpu():
 
 def test_abi_version():
     assert oc.abi_version() == 1
+
+
+def test_sha256_padding_boundaries_vs_hashlib():
+    import hashlib
+    data = bytes(range(256)) * 8
+    for n in (0, 1, 55, 56, 57, 63, 64, 65, 96, 119, 120, 127, 128, 129, 1000, 2048):
+        assert oc.sha256(data[:n]) == hashlib.sha256(data[:n]).digest(), n
