@@ -415,7 +415,7 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts):
     The consumer stream waits on layer l (wait_layer), then emulates layer-l compute with a spin
     kernel of C_l; TTFT runs from the fetch launch to the end of the last layer's compute (Eq. 3
     with the free-running copy stream, reading c14).  The baseline is the same consumer chain
-    with the KV already resident (no fetch, no waits): the analog of the paper's opt-local-LW.
+    with the KV already delivered (same waits, no transfer): the analog of the paper's opt-local-LW.
     added = TTFT - TTFT_baseline; X0 = layer 0's ready time after the fetch launch.
     """
     import synth
@@ -429,27 +429,38 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts):
     torch.cuda.synchronize()
     cyc_per_ms = 20_000_000 / e0.elapsed_time(e1)          # torch.cuda._sleep calibration
 
-    def chain(copy_s, cons_s, d, C_ms):
+    def chain(copy_s, cons_s, d, C_ms, timeline=None, fetch=True):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(L)] if timeline is not None else None
         torch.cuda.synchronize()
         a.record(copy_s)
         cons_s.wait_event(a)
-        if d is not None:
+        if d is not None and fetch:
             d.fetch_layerwise(copy_s, **fopts)
         for l in range(L):
             if d is not None:
                 d.wait_layer(l, cons_s)
+            if ev:
+                ev[l][0].record(cons_s)
             with torch.cuda.stream(cons_s):
                 torch.cuda._sleep(int(C_ms * cyc_per_ms))
+            if ev:
+                ev[l][1].record(cons_s)
         b.record(cons_s)
         torch.cuda.synchronize()
+        if ev:  # device timeline: compute start/end per layer (ms after the fetch launch)
+            timeline["compute_start_ms"] = [round(a.elapsed_time(x), 4) for x, _ in ev]
+            timeline["compute_end_ms"] = [round(a.elapsed_time(y), 4) for _, y in ev]
         return a.elapsed_time(b)
 
-    res = {}
-    cells = [("4k", 3584, 63.47), ("64k", 57344, 2423.90)] if args.stall64k else [("4k", 3584, 63.47)]
-    for name, cached, t_total_ms in cells:
+    res = {"timelines": {}}
+    cells = [("4k", 4096, 3584, 63.47), ("64k", 65536, 57344, 2423.90)] if args.stall64k else \
+        [("4k", 4096, 3584, 63.47)]
+    for name, ctx, cached, t_total_ms in cells:
         N = cached // G
-        C_ms = t_total_ms / L
+        windows = {"a100": t_total_ms / L,                                    # Table A5 (A100)
+                   "b200": prefill_window_s("llama3-8b", ctx, cached / ctx) * 1e3}  # FLOP model
         for tier_name, tier in (("hbm", oc.TIER_HBM), ("pinned_host", oc.TIER_PINNED_HOST)):
             store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
             (tok,), _ = synth.family_streams(9000 + N, G, 0, [N])
@@ -466,28 +477,36 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts):
             tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs, bt, 0)
             d = oc.build_descriptor(store, keys, lay_t, tgt)
             copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-            base = min(chain(copy_s, cons_s, None, C_ms) for _ in range(2))
-            runs = []
-            for it in range(3):
-                ttft = chain(copy_s, cons_s, d, C_ms)
-                t = d.layer_times().astype(np.int64)
-                runs.append((ttft - base, (t[1] - t[0]) / 1e6, (t[L] - t[0]) / 1e6, ttft))
-            best = min(runs)
-            # Eq. 2's other side: chunkwise delivery (every wait_layer waits for the whole prefix)
             d_cw = oc.build_descriptor(store, keys, lay_t, tgt, oc.DELIVER_CHUNK_MAJOR)
-            cw = min(chain(copy_s, cons_s, d_cw, C_ms) for _ in range(2)) - base
+            for wname, C_ms in windows.items():
+                # baseline: the same consumer chain, waits included, on KV already delivered
+                d.fetch_layerwise(copy_s, **fopts)
+                base = min(chain(copy_s, cons_s, d, C_ms, fetch=False) for _ in range(2))
+                runs = []
+                for it in range(3):
+                    tl = {}
+                    ttft = chain(copy_s, cons_s, d, C_ms, timeline=tl)
+                    t = d.layer_times().astype(np.int64)
+                    tl["layer_ready_ms"] = [round((x - t[0]) / 1e6, 4) for x in t[1:]]
+                    runs.append((ttft - base, (t[1] - t[0]) / 1e6, (t[L] - t[0]) / 1e6, ttft, tl))
+                best = min(runs, key=lambda r: r[0])
+                # Eq. 2's other side: chunkwise delivery (every wait_layer waits for the whole prefix)
+                cw = min(chain(copy_s, cons_s, d_cw, C_ms) for _ in range(2)) - base
+                key = f"{name}_{tier_name}" + ("" if wname == "a100" else "_b200win")
+                res[key] = {"N": N, "window": wname, "C_ms_per_layer": round(C_ms, 4), "added_ms": round(best[0], 4),
+                            "X0_ms": round(best[1], 4), "transfer_ms": round(best[2], 4),
+                            "ttft_ms": round(best[3], 3), "baseline_ttft_ms": round(base, 3),
+                            "added_ms_chunkwise": round(cw, 4), "payload_MiB": N * S * L / 2**20}
+                if name == "4k":  # per-layer device timeline (the overlap evidence), 4K cells only
+                    res["timelines"][key] = best[4]
             d_cw.close()
-            res[f"{name}_{tier_name}"] = {"N": N, "C_ms_per_layer": round(C_ms, 4), "added_ms": round(best[0], 4),
-                                          "X0_ms": round(best[1], 4), "transfer_ms": round(best[2], 4),
-                                          "ttft_ms": round(best[3], 3), "baseline_ttft_ms": round(base, 3),
-                                          "added_ms_chunkwise": round(cw, 4),
-                                          "payload_MiB": N * S * L / 2**20}
             d.close()
             store.close()
             del cache
             torch.cuda.empty_cache()
-    res["windows"] = ("Table A5 A100 per-layer compute (P:2706-2713), 87.5% hit; spin-kernel emulation; "
-                      "baseline = same chain with KV resident (opt-local-LW analog)")
+    res["windows"] = ("a100: Table A5 per-layer compute (P:2706-2713), 87.5% hit; b200: FLOP model at half the "
+                      "measured sustained bf16 rate; spin-kernel emulation; baseline = same chain (waits included) with "
+                      "the KV already delivered (opt-local-LW analog)")
     return res
 
 
@@ -709,11 +728,35 @@ def batch_leg(args, oc, torch, dev, lay_t):
 # c_i = T_total / 32 from Table A5 (A100); caps 80 / 50 / 50 Gbps; delta = 5 Gbps.
 TABLE_A5_T_TOTAL_MS = {(16384, 0.5): 955.89, (16384, 0.875): 281.76, (32768, 0.5): 2589.25,
                        (32768, 0.875): 763.19, (65536, 0.5): 8672.79, (65536, 0.875): 2423.90}
-SCHED_WORKLOADS = {
-    "A": (80.0, [(16384, 0.5), (16384, 0.875), (65536, 0.5), (65536, 0.875)]),
-    "B": (50.0, [(16384, 0.5), (16384, 0.875), (65536, 0.5), (65536, 0.875)]),
-    "C": (50.0, [(16384, 0.5), (16384, 0.875), (32768, 0.5), (32768, 0.875), (65536, 0.5), (65536, 0.875)]),
-}
+def prefill_window_s(lay_name, ctx, hit, flops_per_s=0.5 * 1399.5e12):
+    """Per-layer prefill compute exposed by the miss tokens (SURVEY 8(d) sanity model): with m
+    miss tokens after h hit tokens a layer costs 2*m*P_layer + 4*n_heads*d*m*(h + m/2) FLOPs;
+    executed at half of the measured sustained bf16 rate (MEASURED_PEAKS.json)."""
+    h_d, n_heads, d, n_kv, inter = {"llama3-70b": (8192, 64, 128, 8, 28672),
+                                   "llama3-8b": (4096, 32, 128, 8, 14336)}[lay_name]
+    p_layer = 2 * h_d * h_d + 2 * h_d * n_kv * d + 3 * h_d * inter
+    h = ctx * hit
+    m = ctx - h
+    return (2 * m * p_layer + 4 * n_heads * d * m * (h + m / 2)) / flops_per_s
+
+
+def sched_workloads():
+    """name -> (layout, cap Gbps, [(label, context, hit, c seconds per layer)], window source)."""
+    import synth
+    a5 = lambda ctx, hit: TABLE_A5_T_TOTAL_MS[(ctx, hit)] / 32 / 1e3
+    cells = lambda lst: [(f"{c // 1024}K,{h:g}", c, h, a5(c, h)) for c, h in lst]
+    ab = [(16384, 0.5), (16384, 0.875), (65536, 0.5), (65536, 0.875)]
+    w = {"A": (synth.LLAMA3_8B, 80.0, cells(ab), "Table A5 (A100)"),
+         "B": (synth.LLAMA3_8B, 50.0, cells(ab), "Table A5 (A100)"),
+         "C": (synth.LLAMA3_8B, 50.0, cells(ab[:2] + [(32768, 0.5), (32768, 0.875)] + ab[2:]), "Table A5 (A100)")}
+    # BASELINE.json configs[3]: Llama-3-70B layout, 16 concurrent 32K requests (hit 50% / 87.5%
+    # alternating), cap at half the aggregate zero-stall rate (Workload B/C regime).
+    c70 = [(f"32K,{h:g}#{i}", 32768, h, prefill_window_s("llama3-70b", 32768, h))
+           for i, h in enumerate([0.5, 0.875] * 8)]
+    sum_rstar = sum(int(ctx * h) * 4096 / c for _, ctx, h, c in c70)
+    w["70B"] = (synth.LLAMA3_70B, round(sum_rstar / 2 * 8 / 1e9, 3), c70,
+                "FLOP model at 50% of the measured sustained bf16 rate (B200)")
+    return w
 
 
 def sched_leg(args, oc, torch, dev, lay_t):
@@ -722,19 +765,7 @@ def sched_leg(args, oc, torch, dev, lay_t):
     released at t0 + l*s/r), chunks in the pinned host tier (the shared PCIe link plays the
     paper's shared NIC).  Each request's consumer waits on every layer and then spins for c_i.
     dTTFT_i = TTFT_i - TTFT_i(no limit); the paper's Table A8 reports the sum per policy."""
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    n_max = 65536 * 7 // 8 // G
-    store = oc.Store(lay_t, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
     import synth
-    (tok,), _ = synth.family_streams(4242, G, 0, [n_max])
-    keys = oc.chunk_keys(tok, G)                           # one shared-prefix corpus
-    gen = torch.Generator(device=dev).manual_seed(4242)
-    for b0 in range(0, n_max, 256):
-        b1 = min(n_max, b0 + 256)
-        pl = torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
-        store.put_chunks(keys[b0:b1], pl)
-        del pl
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda._sleep(1000)
     e0.record()
@@ -744,20 +775,33 @@ def sched_leg(args, oc, torch, dev, lay_t):
     cyc_per_ms = 20_000_000 / e0.elapsed_time(e1)
     GB = 1e9 / 8                                            # bytes/s per Gbps (decimal)
     out = {}
+    table = sched_workloads()
     for wl in [w.strip().upper() for w in args.sched.split(",") if w.strip()]:
-        cap_gbps, cells = SCHED_WORKLOADS[wl]
+        named, cap_gbps, cells, window_src = table[wl]
+        lay = named.as_tuple()
+        L, G, Bs = lay[0], lay[4], 16
+        row, S, chunk = oc.geometry(lay)
+        n_max = max(int(ctx * hit) // G for _, ctx, hit, _ in cells)
+        store = oc.Store(lay, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
+        (tok,), _ = synth.family_streams(4242, G, 0, [n_max])
+        keys = oc.chunk_keys(tok, G)                       # one shared-prefix corpus
+        gen = torch.Generator(device=dev).manual_seed(4242)
+        for b0 in range(0, n_max, 128):
+            b1 = min(n_max, b0 + 128)
+            pl = torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
+            store.put_chunks(keys[b0:b1], pl)
+            del pl
         reqs = []
-        for ctx, hit in cells:
+        for label, ctx, hit, c in cells:
             N = int(ctx * hit) // G
             need = N * G // Bs
             cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
             per_kv = need * Bs * row
             kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-            tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+            tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay[2] * lay[3], Bs,
                                  synth.block_table(N, need, need), 0)
-            d = oc.build_descriptor(store, keys[:N], lay_t, tgt)
-            reqs.append({"cell": f"{ctx // 1024}K,{hit:g}", "N": N, "s": N * S,
-                         "c": TABLE_A5_T_TOTAL_MS[(ctx, hit)] / L / 1e3, "d": d, "cache": cache,
+            d = oc.build_descriptor(store, keys[:N], lay, tgt)
+            reqs.append({"cell": label, "N": N, "s": N * S, "c": c, "d": d, "cache": cache,
                          "copy": torch.cuda.Stream(device=dev), "cons": torch.cuda.Stream(device=dev)})
 
         def run(rates):
@@ -786,7 +830,8 @@ def sched_leg(args, oc, torch, dev, lay_t):
         s_i = [r["s"] for r in reqs]
         c_i = [r["c"] for r in reqs]
         base = run(None)                                    # "no-limit base" (Table A8)
-        res = {"cap_gbps": cap_gbps, "requests": [r["cell"] for r in reqs],
+        res = {"layout": named.name, "cap_gbps": cap_gbps, "windows": window_src,
+               "requests": [r["cell"] for r in reqs], "c_ms": [round(c * 1e3, 3) for c in c_i],
                "zero_stall_gbps": [round(s / c / GB, 3) for s, c in zip(s_i, c_i)],
                "no_limit_ttft_ms": [round(x, 1) for x in base], "policies": {}}
         for pol in ("equal", "kv_prop", "bw_prop", "stall_opt", "cal_stall_opt"):
@@ -800,12 +845,14 @@ def sched_leg(args, oc, torch, dev, lay_t):
                                     "model_dttft_ms": round(sum(model) * 1e3, 1)}
         res["equal_over_cal"] = round(res["policies"]["equal"]["dttft_ms"] /
                                       max(1e-9, res["policies"]["cal_stall_opt"]["dttft_ms"]), 3)
+        res["equal_over_stall_opt"] = round(res["policies"]["equal"]["dttft_ms"] /
+                                            max(1e-9, res["policies"]["stall_opt"]["dttft_ms"]), 3)
         out[wl] = res
         for r in reqs:
             r["d"].close()
         del reqs
+        store.close()
         torch.cuda.empty_cache()
-    store.close()
     return out
 
 
