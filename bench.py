@@ -564,7 +564,7 @@ def corun_leg(args, oc, torch, dev, lay_t):
     out = {"gemm_alone": run(True, False, {})}
     for engine, name in ((oc.COPY_BULK, "bulk"), (oc.COPY_LDST, "ldst")):
         for mc in (0, 148, 64, 32, 16):
-            fo = {"engine": engine, "max_ctas": mc}
+            fo = {"engine": engine, "max_ctas": mc, "unit_bytes": int(os.environ.get("OC_CORUN_UNIT", "0"))}
             alone = run(False, True, fo)
             both = run(True, True, fo)
             out[f"{name}_ctas{mc or 'auto'}"] = {"fetch_alone_GBps": alone["fetch_GBps"],

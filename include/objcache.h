@@ -217,7 +217,9 @@ typedef struct {
     uint32_t max_ctas;       /* copy-CTA cap (SM budget when co-running); 0 = auto:
                                 the whole GPU for HBM sources, 16 CTAs when most
                                 chunks live in pinned host memory (PCIe-bound)   */
-    uint32_t unit_bytes;     /* bytes per work unit; 0 = auto (32 KiB)          */
+    uint32_t unit_bytes;     /* bytes per work unit (a run of rows of one chunk's
+                                layer slice); 0 = auto: 32 KiB, or 64 KiB when an
+                                HBM-sourced fetch has a budget of <= 1 CTA/SM    */
     double pace_Bps;         /* minimal pacer: layer l is released no
                                 earlier than t0 + l*(N*S)/pace_Bps; 0 = off.
                                 PERSISTENT mode only.                           */

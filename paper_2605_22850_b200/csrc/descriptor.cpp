@@ -156,14 +156,14 @@ int upload_block(int device, const Geometry& g, const std::vector<uint64_t>& src
 
 void plan_into(DevDesc& dd, const Geometry& g, uint64_t n, uint32_t unit_bytes) {
     if (unit_bytes == 0) unit_bytes = 32768;
+    // A unit is R consecutive rows of a chunk's 2G-row layer slice (K rows, then V rows).
     uint64_t R = std::max<uint64_t>(1, unit_bytes / g.row);
-    R = std::min<uint64_t>(R, g.G);
+    R = std::min<uint64_t>(R, 2ull * g.G);
     R = std::min<uint64_t>(R, 1024);  // rows per unit are staged in a 1024-entry shared table
     dd.rows_per_unit = (uint32_t)R;
-    dd.tiles = (uint32_t)((g.G + R - 1) / R);
-    dd.units_per_layer = (uint32_t)(n * 2 * dd.tiles);
+    dd.tiles = (uint32_t)((2ull * g.G + R - 1) / R);
+    dd.units_per_layer = (uint32_t)(n * dd.tiles);
     dd.div_upl = make_fastdiv(dd.units_per_layer);
-    dd.div_units_per_chunk = make_fastdiv(2 * dd.tiles);
     dd.div_tiles = make_fastdiv(dd.tiles);
 }
 

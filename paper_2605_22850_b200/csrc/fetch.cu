@@ -72,42 +72,39 @@ __device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // ---- unit geometry -------------------------------------------------------------------------------
+// Layer l of chunk j is 2G rows at [lS, (l+1)S) of the slot: K rows 0..G-1, then V rows G..2G-1
+// (KV_L2TD, reading c2).  A unit is R consecutive rows q0 .. q0+R-1 of that slice -- contiguous
+// in the source; it may cover part of K, part of V, or both.
 struct UnitGeo {
-    uint32_t layer, j, kv, r0, nrows;
+    uint32_t layer, j, q0, nrows;
 };
 
-// Global unit g (layer-major): layer = g / units_per_layer; inside a layer chunk j, matrix kv, tile.
+// Global unit g (layer-major): layer = g / units_per_layer; inside a layer chunk j, then tile.
 __device__ __forceinline__ UnitGeo unit_geo(const DevDesc& d, uint32_t g) {
     UnitGeo u;
     u.layer = fdiv(g, d.div_upl);
     const uint32_t unit = g - u.layer * d.units_per_layer;
-    u.j = fdiv(unit, d.div_units_per_chunk);
-    const uint32_t rem = unit - u.j * 2u * d.tiles;
-    u.kv = rem >= d.tiles ? 1u : 0u;
-    u.r0 = (rem - u.kv * d.tiles) * d.rows_per_unit;
-    u.nrows = min(d.rows_per_unit, d.G - u.r0);
+    u.j = fdiv(unit, d.div_tiles);
+    u.q0 = (unit - u.j * d.tiles) * d.rows_per_unit;
+    u.nrows = min(d.rows_per_unit, 2u * d.G - u.q0);
     return u;
 }
 
-// Source of a unit: layer l of chunk j at [lS, (l+1)S), K rows then V rows (reading c2).
 __device__ __forceinline__ const uint8_t* unit_src(const DevDesc& d, const UnitGeo& u) {
-    return (const uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + ((uint64_t)u.kv * d.G + u.r0) * d.row;
+    return (const uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + (uint64_t)u.q0 * d.row;
 }
 
-// Request token of the unit's first row, and the layer's K or V base.
-__device__ __forceinline__ uint32_t unit_tok0(const DevDesc& d, const UnitGeo& u) {
-    return d.first_token + u.j * d.G + u.r0;
-}
-
-__device__ __forceinline__ uint64_t unit_base(const DevDesc& d, const UnitGeo& u) {
-    return u.kv ? d.v_base[u.layer] : d.k_base[u.layer];
-}
-
-// Destination of token `tok`'s row: block_table[tok / Bs] * block_stride + (tok % Bs) * token_stride.
-__device__ __forceinline__ uint64_t row_dst(const DevDesc& d, uint64_t base, uint32_t tok, uint32_t* slot_out) {
+// Destination of row q of chunk `pos`'s layer-l slice: matrix kv = q >= G, token t = q - kv*G,
+// request token u = first_token + pos*G + t, at {k,v}_base[l] + block_table[u / Bs]*block_stride
+// + (u % Bs)*token_stride.
+__device__ __forceinline__ uint64_t row_addr(const DevDesc& d, uint32_t layer, uint32_t pos, uint32_t q,
+                                             uint32_t* slot_out) {
+    const uint32_t kv = q >= d.G ? 1u : 0u;
+    const uint32_t tok = d.first_token + pos * d.G + (q - kv * d.G);
     const uint32_t b = fdiv(tok, d.div_Bs);
     const uint32_t slot = tok - b * d.Bs;
     if (slot_out) *slot_out = slot;
+    const uint64_t base = kv ? d.v_base[layer] : d.k_base[layer];
     return base + (uint64_t)d.bt[b] * d.block_stride + (uint64_t)slot * d.token_stride;
 }
 
@@ -211,9 +208,7 @@ __global__ void __launch_bounds__(kThreads, 4) fetch_ldst_kernel(const DevDesc d
             }
         }
         uint64_t* tab = s_dst[k & 1];
-        const uint64_t base = unit_base(d, u);
-        const uint32_t tok0 = unit_tok0(d, u);
-        for (uint32_t r = threadIdx.x; r < u.nrows; r += kThreads) tab[r] = row_dst(d, base, tok0 + r, nullptr);
+        for (uint32_t r = threadIdx.x; r < u.nrows; r += kThreads) tab[r] = row_addr(d, u.layer, u.j, u.q0 + r, nullptr);
         if (threadIdx.x == 0) {  // publish unit k+1 (read after the barrier below), claim k+2
             s_g[(k + 1) & 1] = next_g;
             if (next_g < g1) next_g = claim_unit(d, g0, grab_base);
@@ -264,13 +259,11 @@ __global__ void __launch_bounds__(kThreads, 4) offload_kernel(const DevDesc d, c
     __shared__ uint64_t tab[kMaxRows];
     for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
         const UnitGeo u = unit_geo(d, g);
-        const uint64_t base = unit_base(d, u);
-        const uint32_t tok0 = d.first_token + pos[u.j] * d.G + u.r0;
+        const uint32_t p = pos[u.j];
         __syncthreads();  // the previous unit is done with tab
-        for (uint32_t r = threadIdx.x; r < u.nrows; r += kThreads) tab[r] = row_dst(d, base, tok0 + r, nullptr);
+        for (uint32_t r = threadIdx.x; r < u.nrows; r += kThreads) tab[r] = row_addr(d, u.layer, p, u.q0 + r, nullptr);
         __syncthreads();
-        uint8_t* dst = (uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + ((uint64_t)u.kv * d.G + u.r0) * d.row;
-        gather_rows(d, dst, u.nrows, tab);
+        gather_rows(d, (uint8_t*)unit_src(d, u), u.nrows, tab);
     }
 }
 
@@ -514,15 +507,16 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         const UnitGeo u = unit_geo(d, g);
         mbar_wait(&bars[s], (k / stages) & 1u);
         const uint8_t* sbuf = buf + (size_t)s * stage_bytes;
-        const uint64_t base = unit_base(d, u);
-        const uint32_t tok0 = unit_tok0(d, u);
         if (d.nhd) {
-            // Lane r owns row r if row r starts a run: the unit's first row or a block's first slot.
+            // Lane r owns row r if row r starts a run: the unit's first row, a block's first slot,
+            // or the first V row.  A run ends at the next such row.
             for (uint32_t r = lane; r < u.nrows; r += 32) {
+                const uint32_t q = u.q0 + r;
                 uint32_t slot;
-                const uint64_t dst = row_dst(d, base, tok0 + r, &slot);
-                if (r == 0 || slot == 0) {
-                    const uint32_t len = min(u.nrows - r, d.Bs - slot);
+                const uint64_t dst = row_addr(d, u.layer, u.j, q, &slot);
+                if (r == 0 || slot == 0 || q == d.G) {
+                    uint32_t len = min(u.nrows - r, d.Bs - slot);
+                    if (q < d.G) len = min(len, d.G - q);
                     bulk_store(dst, sbuf + (size_t)r * d.row, (uint32_t)(len * d.row));
                 }
             }
@@ -533,7 +527,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
             for (uint32_t p = lane; p < u.nrows * heads; p += 32) {
                 const uint32_t r = p / heads;
                 const uint32_t h = p - r * heads;
-                const uint64_t dst = row_dst(d, base, tok0 + r, nullptr) + (uint64_t)h * d.head_stride;
+                const uint64_t dst = row_addr(d, u.layer, u.j, u.q0 + r, nullptr) + (uint64_t)h * d.head_stride;
                 bulk_store(dst, sbuf + (size_t)r * d.row + (size_t)h * hbytes, hbytes);
             }
         }
@@ -626,6 +620,14 @@ int env_int(const char* name, int dflt) {
     return e && *e ? std::atoi(e) : dflt;
 }
 
+// Default unit size (profiles/r01_engine_sweep.txt, r01_corun.json): with the whole GPU, 32 KiB
+// units at 3 CTAs per SM reach the copy roofline; with a copy-CTA budget of at most one CTA per
+// SM (co-running with prefill) 64 KiB units -- a whole chunk-layer slice at Llama layouts --
+// halve the per-unit latency a single copy warp pays (0.85 vs 0.54 TB/s at 16 CTAs).
+uint32_t default_unit_bytes(uint32_t max_ctas, int sms) {
+    return (max_ctas && max_ctas <= (uint32_t)sms) ? 65536u : 32768u;
+}
+
 struct BulkPlan {
     uint32_t copy_ctas, stages, stage_bytes, smem;
 };
@@ -715,12 +717,14 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
         d->events.resize(d->geo.L, nullptr);
         for (auto& ev : d->events) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
-    plan_units(d, o.unit_bytes ? o.unit_bytes : 32768u);
     // PCIe-bound sources (pinned host tier) saturate the link from a handful of CTAs; more only
     // spreads the link over more layers in flight and delays layer 0 (profiles/: 16 CTAs give
     // 51.4 GB/s and X0 = one layer's transfer time at 4K).  The rest of the GPU stays free.
+    const bool host_src = d->host_chunks * 2 > d->N;
     uint32_t max_ctas = o.max_ctas;
-    if (!max_ctas && d->host_chunks * 2 > d->N) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 16));
+    if (!max_ctas && host_src) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 16));
+    // PCIe-bound fetches keep 32 KiB units: finer units finish layer 0 sooner on a slow link.
+    plan_units(d, o.unit_bytes ? o.unit_bytes : default_unit_bytes(host_src ? 0 : max_ctas, device_sm_count(d->device)));
     DevDesc& dd = d->dd;
     const uint64_t total_units = (uint64_t)dd.units_per_layer * dd.L;
     if (total_units >= (1ull << 32)) return fail(OC_ERANGE, "fetch_layerwise: too many units");
@@ -787,7 +791,7 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
     for (uint32_t i = 0; i < b->n; i++) {
         Desc* d = b->descs[i];
         if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
-        plan_units(d, o.unit_bytes ? o.unit_bytes : 32768u);
+        plan_units(d, o.unit_bytes ? o.unit_bytes : default_unit_bytes(o.max_ctas, device_sm_count(b->device)));
         DevDesc& dd = d->dd;
         uint32_t epoch = d->epoch + 1;
         if (epoch == 0) epoch = 1;

@@ -116,8 +116,8 @@ struct DevDesc {
     uint64_t block_stride, token_stride, head_stride;
     uint32_t N, L, G, Bs, first_token;
     uint32_t rows_per_unit;   // R
-    uint32_t tiles;           // ceil(G / R) tiles per K or V half of a chunk-layer
-    uint32_t units_per_layer; // N * 2 * tiles
+    uint32_t tiles;           // ceil(2G / R) units per chunk-layer slice (K and V rows)
+    uint32_t units_per_layer; // N * tiles
     uint32_t vpr;             // 16-byte vectors per row
     uint32_t nhd;             // 1: a row is contiguous in the destination
     uint32_t epoch;           // fetch sequence number (>= 1)
@@ -125,8 +125,7 @@ struct DevDesc {
     uint32_t chunk_major;     // 1: only the completion of the whole prefix is announced
     uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
     FastDiv div_upl;          // units_per_layer
-    FastDiv div_units_per_chunk;  // 2*tiles
-    FastDiv div_tiles;
+    FastDiv div_tiles;        // tiles per chunk-layer slice
     FastDiv div_vpr;
     FastDiv div_Bs;
     FastDiv div_hdv;          // (d*p)/16
