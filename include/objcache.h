@@ -215,8 +215,9 @@ typedef struct {
     uint32_t mode;           /* oc_fetch_mode                                   */
     uint32_t engine;         /* oc_copy_engine                                  */
     uint32_t max_ctas;       /* copy-CTA cap (SM budget when co-running); 0 = auto:
-                                the whole GPU for HBM sources, 16 CTAs when most
-                                chunks live in pinned host memory (PCIe-bound)   */
+                                the whole GPU for HBM sources, 8 CTAs when most
+                                chunks live in pinned host memory (PCIe-bound:
+                                enough for the link, a short read queue)         */
     uint32_t unit_bytes;     /* bytes per work unit (a run of rows of one chunk's
                                 layer slice); 0 = auto: 32 KiB, or 64 KiB when an
                                 HBM-sourced fetch has a budget of <= 1 CTA/SM    */
@@ -256,6 +257,15 @@ OC_API int oc_sync_layer(oc_desc* desc, uint32_t layer);
  * timer: out[0] = kernel start, out[1 + l] = layer l ready.  Blocks until the
  * fetch is complete.  `out` holds L + 1 values. */
 OC_API int oc_layer_times(oc_desc* desc, uint64_t* out);
+
+/* Measurement support (not a step of the method): the compute window C_l of
+ * the stall accounting (Eq. 3; a8).  Enqueues on `stream` (the
+ * current device's) one single-CTA kernel that spins on the GPU global timer
+ * for `ns` nanoseconds, leaving the other SMs to the fetch.  If `stamps` (a
+ * device address, 8-byte aligned) is not NULL the kernel writes its start and
+ * end time there (2 values, same clock as oc_layer_times).  ns > 60 s ->
+ * OC_ERANGE. */
+OC_API int oc_emulate_compute(uint64_t ns, uint64_t* stamps, void* stream);
 
 /* ---- bandwidth scheduling (Sec. 3.6) --------------------------- */
 typedef enum {

@@ -93,6 +93,7 @@ _SIGS = {
     "oc_wait_layer": [_vp, ctypes.c_uint32, _vp],
     "oc_sync_layer": [_vp, ctypes.c_uint32],
     "oc_layer_times": [_vp, c_u64p],
+    "oc_emulate_compute": [ctypes.c_uint64, _vp, _vp],
     "oc_schedule_bandwidth": [ctypes.c_int, ctypes.POINTER(CProfile), ctypes.c_uint64, ctypes.c_double,
                               ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
     "oc_pool_create": [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, ctypes.POINTER(_vp)],
@@ -505,6 +506,13 @@ def fetch_layerwise(desc: Descriptor, stream=None, **opts):
 
 def wait_layer(desc: Descriptor, layer: int, stream=None):
     desc.wait_layer(layer, stream)
+
+
+def emulate_compute(ns: int, stream=None, stamps=None):
+    """Measurement support: a single-CTA %globaltimer spin of `ns` on `stream` standing in for a
+    layer's compute window C_l; `stamps` (device tensor/address, 2 x u64) receives start and end."""
+    addr = None if stamps is None else (int(stamps.data_ptr()) if hasattr(stamps, "data_ptr") else int(stamps))
+    _check(_lib.oc_emulate_compute(int(ns), addr, _stream(stream)))
 
 
 def abi_version() -> int:

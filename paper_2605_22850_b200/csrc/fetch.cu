@@ -598,6 +598,18 @@ __global__ void wait_geq_kernel(const uint32_t* addr, uint32_t value) {
     while ((int32_t)(ld_acquire(addr) - value) < 0) __nanosleep(256);
 }
 
+// Compute window C_l of the stall measurement: one thread spins on %globaltimer for
+// `ns` and stamps its start and end on the same clock as the fetch's layer-ready stamps.
+__global__ void emulate_kernel(uint64_t ns, uint64_t* stamps) {
+    const uint64_t t0 = globaltimer();
+    uint64_t t = t0;
+    while (t - t0 < ns) t = globaltimer();
+    if (stamps) {
+        stamps[0] = t0;
+        stamps[1] = t;
+    }
+}
+
 // ---- launch --------------------------------------------------------------------------------------------
 namespace {
 
@@ -717,12 +729,14 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
         d->events.resize(d->geo.L, nullptr);
         for (auto& ev : d->events) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
-    // PCIe-bound sources (pinned host tier) saturate the link from a handful of CTAs; more only
-    // spreads the link over more layers in flight and delays layer 0 (profiles/: 16 CTAs give
-    // 51.4 GB/s and X0 = one layer's transfer time at 4K).  The rest of the GPU stays free.
+    // PCIe-bound sources (pinned host tier) saturate the link from a handful of CTAs.  More CTAs
+    // only lengthen the PCIe read queue, and every other GPU read of host memory -- the command
+    // fetches of the consumer's stream -- waits behind it: 16 CTAs add ~30 us to each consumer
+    // launch, 8 CTAs x 32 KiB units ~4 us at the same 51.4 GB/s; 6 CTAs lose bandwidth on large
+    // slabs (profiles/r01_pcie_latency*.txt).
     const bool host_src = d->host_chunks * 2 > d->N;
     uint32_t max_ctas = o.max_ctas;
-    if (!max_ctas && host_src) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 16));
+    if (!max_ctas && host_src) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8));
     // PCIe-bound fetches keep 32 KiB units: finer units finish layer 0 sooner on a slow link.
     plan_units(d, o.unit_bytes ? o.unit_bytes : default_unit_bytes(host_src ? 0 : max_ctas, device_sm_count(d->device)));
     DevDesc& dd = d->dd;
@@ -807,7 +821,7 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
     const uint32_t L = b->descs[0]->geo.L;
     if (total * L >= (1ull << 32)) return fail(OC_ERANGE, "fetch_batch: too many units in one batch");
     uint32_t max_ctas = o.max_ctas;
-    if (!max_ctas && host_chunks * 2 > chunks) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 16));
+    if (!max_ctas && host_chunks * 2 > chunks) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8));
     const int sms = device_sm_count(b->device);
     const BulkPlan p = plan_bulk(b->descs[0]->dd, sms, max_ctas, total * L);
     OC_CUDA(cudaMemcpyAsync(b->dev, b->stage, b->upload_bytes, cudaMemcpyHostToDevice, s));
@@ -966,6 +980,14 @@ OC_API int oc_layer_times(oc_desc* h, uint64_t* out) {
     oc::DeviceGuard dg(d->device);
     OC_CUDA(cudaEventSynchronize(d->done_ev));
     OC_CUDA(cudaMemcpy(out, d->dd.ts, (d->geo.L + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return OC_OK;
+}
+
+OC_API int oc_emulate_compute(uint64_t ns, uint64_t* stamps, void* stream) {
+    if (ns > 60ull * 1000000000ull) return oc::fail(OC_ERANGE, "emulate_compute: window > 60 s");
+    if (stamps && ((uintptr_t)stamps & 7)) return oc::fail(OC_EALIGN, "emulate_compute: stamps not 8-byte aligned");
+    oc::emulate_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ns, stamps);
+    OC_CUDA(cudaGetLastError());
     return OC_OK;
 }
 
