@@ -55,6 +55,8 @@ def parse():
                    "throughputs vs the copy-CTA budget (adds a 'corun' object)")
     p.add_argument("--no-granularity", action="store_true", help="skip the G = 16/64/256 sweep and the "
                    "unfused gather->flat->scatter comparison")
+    p.add_argument("--sensitivity", action="store_true", help="Fig. 14 analog: TTFT increase at a 10 Gbps vs "
+                   "100 Gbps cap, layerwise vs chunkwise, Table A5 cells")
     p.add_argument("--crossover", action="store_true", help="Eq. 2 / Fig. 13 analog: layerwise vs chunkwise "
                    "added TTFT over 1K-64K contexts, HBM and pinned-host tiers")
     p.add_argument("--sweep", action="store_true", help="rate sweep (Fig. 15 analog): added TTFT of one "
@@ -350,6 +352,8 @@ def main_ours(args):
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_granularity and not args.profile:
         out["granularity"] = granularity_leg(args, oc, torch, dev, lay_t, fopts)
+    if rank == 0 and args.sensitivity:
+        out["sensitivity"] = sensitivity_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.crossover:
         out["crossover"] = crossover_leg(args, oc, torch, dev, lay_t, fopts)
     if rank == 0 and args.sweep:
@@ -563,6 +567,76 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
                       "buffer on the same tier, one contiguous copy + event per layer; times relative to the "
                       "fetch kernel's start")
     return res
+
+
+def sensitivity_leg(args, oc, torch, dev, lay_t):
+    """Fig. 14 analog: TTFT increase when the transfer path is capped at 10 Gbps
+    instead of 100 Gbps, layerwise vs chunkwise, for the Table A5 cells (4K/64K x 50%/87.5%, A100
+    windows).  Chunks in the pinned host tier; the cap is the fetch's pacer (layer l released at
+    t0 + l*s/r; chunkwise = the same paced transfer with every wait on the whole prefix).  Model:
+    Eq. 3 with uniform X = s/r (layerwise), L*X + L*C (chunkwise)."""
+    import synth
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    out = {}
+    for ctx, hit in ((4096, 0.5), (4096, 0.875), (65536, 0.5), (65536, 0.875)):
+        N = int(ctx * hit) // G
+        c = TABLE_A5_T_TOTAL_MS[(ctx, hit)] / L / 1e3                 # A100 windows (P:2706-2713)
+        s = N * S
+        store = oc.Store(lay_t, capacity=N, tier=oc.TIER_PINNED_HOST, device=dev.index)
+        (tok,), _ = synth.family_streams(77 + N, G, 0, [N])
+        keys = oc.chunk_keys(tok, G)
+        gen = torch.Generator(device=dev).manual_seed(N)
+        for b0 in range(0, N, 512):
+            pl = torch.randint(0, 256, (min(N, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
+            store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
+            del pl
+        need = N * G // Bs
+        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
+        per_kv = need * Bs * row
+        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+                             synth.block_table(9, need, need), 0)
+        descs = {"layerwise": oc.build_descriptor(store, keys, lay_t, tgt),
+                 "chunkwise": oc.build_descriptor(store, keys, lay_t, tgt, oc.DELIVER_CHUNK_MAJOR)}
+        copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+        def chain(d, rate):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(copy_s)
+            cons_s.wait_event(a)
+            d.fetch_layerwise(copy_s, pace_Bps=rate)
+            for l in range(L):
+                d.wait_layer(l, cons_s)
+                oc.emulate_compute(int(c * 1e9), cons_s)
+            b.record(cons_s)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b)
+
+        for d in descs.values():           # warm-up (module load, wait entry point), untimed
+            d.fetch_layerwise(copy_s)
+            for l in range(L):
+                d.wait_layer(l, cons_s)
+                oc.emulate_compute(0, cons_s)
+            torch.cuda.synchronize()
+        cell = {"N": N, "s_MiB": s / 2**20, "C_ms": round(c * 1e3, 3), "r_star_GBps": round(s / c / 1e9, 3)}
+        for mode, d in descs.items():
+            t = {g: chain(d, g * 1e9 / 8) for g in (100, 10)}
+            model = {}
+            for g in (100, 10):
+                X = s / (g * 1e9 / 8)
+                model[g] = (X + (L - 1) * max(X, c) + c) if mode == "layerwise" else L * X + L * c
+            cell[mode] = {"ttft_100G_ms": round(t[100], 2), "ttft_10G_ms": round(t[10], 2),
+                          "increase_pct": round(100 * (t[10] / t[100] - 1), 2),
+                          "model_increase_pct": round(100 * (model[10] / model[100] - 1), 2)}
+        out[f"{ctx // 1024}K,{hit:g}"] = cell
+        for d in descs.values():
+            d.close()
+        store.close()
+        del cache
+        torch.cuda.empty_cache()
+    return out
 
 
 def granularity_leg(args, oc, torch, dev, lay_t, fopts):
@@ -891,7 +965,7 @@ def batch_leg(args, oc, torch, dev, lay_t):
 # The paper's scheduler workloads (Sec. 5.7; Table A6): requests named
 # by (context, hit rate); per-layer bytes s_i = cached tokens * 4096 B and per-layer compute
 # c_i = T_total / 32 from Table A5 (A100); caps 80 / 50 / 50 Gbps; delta = 5 Gbps.
-TABLE_A5_T_TOTAL_MS = {(16384, 0.5): 955.89, (16384, 0.875): 281.76, (32768, 0.5): 2589.25,
+TABLE_A5_T_TOTAL_MS = {(4096, 0.5): 185.31, (4096, 0.875): 63.47, (16384, 0.5): 955.89, (16384, 0.875): 281.76, (32768, 0.5): 2589.25,
                        (32768, 0.875): 763.19, (65536, 0.5): 8672.79, (65536, 0.875): 2423.90}
 def prefill_window_s(lay_name, ctx, hit, flops_per_s=0.5 * 1399.5e12):
     """Per-layer prefill compute exposed by the miss tokens (SURVEY 8(d) sanity model): with m
