@@ -55,6 +55,8 @@ def parse():
                    "throughputs vs the copy-CTA budget (adds a 'corun' object)")
     p.add_argument("--no-granularity", action="store_true", help="skip the G = 16/64/256 sweep and the "
                    "unfused gather->flat->scatter comparison")
+    p.add_argument("--serve", type=int, default=0, help="config 5 on one GPU: this many mixed 4K/64K requests "
+                   "streaming through a bounded paged pool with FIFO block admission")
     p.add_argument("--sensitivity", action="store_true", help="Fig. 14 analog: TTFT increase at a 10 Gbps vs "
                    "100 Gbps cap, layerwise vs chunkwise, Table A5 cells")
     p.add_argument("--crossover", action="store_true", help="Eq. 2 / Fig. 13 analog: layerwise vs chunkwise "
@@ -352,6 +354,8 @@ def main_ours(args):
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_granularity and not args.profile:
         out["granularity"] = granularity_leg(args, oc, torch, dev, lay_t, fopts)
+    if rank == 0 and args.serve:
+        out["serve"] = serve_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.sensitivity:
         out["sensitivity"] = sensitivity_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.crossover:
@@ -566,6 +570,114 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
                       "(waits included) with the KV already delivered; opt_local_lw = pre-aggregated layer-major "
                       "buffer on the same tier, one contiguous copy + event per layer; times relative to the "
                       "fetch kernel's start")
+    return res
+
+
+def serve_leg(args, oc, torch, dev, lay_t):
+    """Config 5 on one GPU: a stream of concurrent mixed requests through the public
+    API into a bounded paged KV pool.  Corpus: 32 x 4K-token + 4 x 64K-token prefix families in an
+    HBM store (48 GiB); requests pick 4K/64K 50/50, a family by Zipf(1.1), hit 50% or 87.5%.  The
+    pool (48 GiB of [L][2][blocks][Bs][row]) hands out blocks from a free list in FIFO admission
+    order (a fragmented, seeded initial order); a request is admitted when its blocks are free,
+    gets a descriptor over its blocks, is fetched on one of 8 streams, and its blocks return to the
+    free list when its fetch's completion event fires.  GB/s = 2*N*S*L summed over requests /
+    device time from the first launch to the last completion."""
+    import collections
+    import synth
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    R = args.serve
+    fam_short, fam_long = (int(x) for x in os.environ.get("OC_SERVE_FAMILIES", "32,4").split(","))
+    n_short, n_long = 4096 // G, 65536 // G
+    store = oc.Store(lay_t, capacity=fam_short * n_short + fam_long * n_long, tier=oc.TIER_HBM, device=dev.index)
+    gen = torch.Generator(device=dev).manual_seed(5)
+    fam_keys = {}
+    for long, nf, n in ((False, fam_short, n_short), (True, fam_long, n_long)):
+        for f in range(nf):
+            (tok,), _ = synth.family_streams(8000 + 100 * long + f, G, 0, [n])
+            keys = oc.chunk_keys(tok, G)
+            for b0 in range(0, n, 512):
+                pl = torch.randint(0, 256, (min(n, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
+                store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
+                del pl
+            fam_keys[(long, f)] = keys
+    pool_blocks = (int(os.environ.get("OC_SERVE_POOL_GIB", "48")) << 30) // (L * 2 * Bs * row)
+    cache = torch.empty((L, 2, pool_blocks, Bs, row), dtype=torch.uint8, device=dev)
+    per_kv = pool_blocks * Bs * row
+    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+    vb = [x + per_kv for x in kb]
+    reqs = synth.serving_requests(11, R, fam_short, fam_long)
+    streams = [torch.cuda.Stream(device=dev) for _ in range(8)]
+    start = torch.cuda.Event(enable_timing=True)
+
+    def run():
+        free = collections.deque(int(b) for b in synth.block_table(3, pool_blocks, pool_blocks))
+        pending = collections.deque(enumerate(reqs))
+        inflight = []
+        total_bytes, fetch_us, wait_blocks, n_done = 0, [], 0, 0
+        torch.cuda.synchronize()
+        start.record(streams[0])
+        for s in streams[1:]:
+            s.wait_event(start)
+        ends = []
+        t_host = time.perf_counter()
+        while pending or inflight:
+            still = []
+            for ev, d, blocks, nb in inflight:
+                if ev.query():
+                    t = d.layer_times().astype(np.int64)
+                    fetch_us.append((t[L] - t[0]) / 1e3)
+                    d.close()
+                    free.extend(blocks)
+                    n_done += 1
+                else:
+                    still.append((ev, d, blocks, nb))
+            inflight = still
+            admitted = False
+            while pending:
+                i, (long, fam, hit) = pending[0]
+                n = int((65536 if long else 4096) * hit) // G
+                need = n * G // Bs
+                if len(free) < need:
+                    wait_blocks += 1
+                    break
+                pending.popleft()
+                blocks = [free.popleft() for _ in range(need)]
+                tgt = oc.PagedTarget(kb, vb, Bs * row, row, lay_t[2] * lay_t[3], Bs, np.asarray(blocks, np.int32), 0)
+                try:
+                    d = oc.build_descriptor(store, fam_keys[(long, fam)][:n], lay_t, tgt)
+                    s = streams[i % len(streams)]
+                    d.fetch_layerwise(s)
+                except oc.ObjcacheError:
+                    print(f"serve: request {i} (long={long}, family={fam}, hit={hit}, N={n}, "
+                          f"blocks {min(blocks)}..{max(blocks)}, {len(inflight)} in flight) failed",
+                          file=sys.stderr)
+                    raise
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                ends.append(ev)
+                inflight.append((ev, d, blocks, n))
+                total_bytes += 2 * n * S * L
+                admitted = True
+            if not admitted and inflight:
+                inflight[0][0].synchronize()
+        torch.cuda.synchronize()
+        host_s = time.perf_counter() - t_host
+        dev_ms = max(start.elapsed_time(e) for e in ends)
+        return total_bytes, dev_ms, host_s, fetch_us, wait_blocks
+
+    run()                                               # warm-up pass (descriptor pool, modules)
+    total_bytes, dev_ms, host_s, fetch_us, waits = run()
+    res = {"requests": R, "mix": f"4K/64K 50/50, Zipf(1.1) over {fam_short} + {fam_long} families, hit 50%/87.5%",
+           "pool_GiB": pool_blocks * L * 2 * Bs * row / 2**30, "bytes_rw": total_bytes,
+           "GBps_device": round(total_bytes / dev_ms / 1e6, 1), "GBps_host_wall": round(total_bytes / host_s / 1e9, 1),
+           "device_ms": round(dev_ms, 2), "host_s": round(host_s, 3),
+           "fetch_us_p50": round(float(np.percentile(fetch_us, 50)), 1),
+           "fetch_us_p99": round(float(np.percentile(fetch_us, 99)), 1),
+           "admission_stalls": waits}
+    del cache
+    store.close()
+    torch.cuda.empty_cache()
     return res
 
 

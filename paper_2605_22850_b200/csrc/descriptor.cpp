@@ -11,6 +11,8 @@
 // future reuse): the same target normalisation, then a gather kernel from the paged cache into
 // freshly reserved slots.
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <unordered_set>
 
 #include "oc_internal.h"
@@ -102,27 +104,63 @@ BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos) {
     return b;
 }
 
-// Upload src/bases/bt(/pos) into a pooled device block and fill the static DevDesc fields.
+cudaStream_t upload_stream(int device) {
+    static std::mutex mu;
+    static std::unordered_map<int, cudaStream_t> streams;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = streams.find(device);
+    if (it != streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    streams.emplace(device, s);
+    return s;
+}
+
+// Upload src/bases/bt(/pos) into a pooled device block and fill the static DevDesc fields.  The
+// block is staged in pooled pinned memory and copied asynchronously: on `on_stream` itself when
+// `ordered` (the caller launches its kernel on that stream next), else on the device's private
+// upload stream with up->ev marking completion (see Upload in oc_internal.h).
 int upload_block(int device, const Geometry& g, const std::vector<uint64_t>& src, const PagedView& v,
                  const std::vector<uint32_t>* pos, const char* who, void** mem_out, uint64_t* cls_out, DevDesc* dd,
-                 const uint32_t** pos_dev) {
+                 const uint32_t** pos_dev, Upload* up, bool ordered, cudaStream_t on_stream) {
     const uint64_t n = src.size();
     const uint32_t L = g.L;
     const BlockLayout b = block_layout(n, L, v.bt.size(), pos != nullptr);
-    std::vector<uint8_t> stage(b.total, 0);
-    std::memcpy(stage.data() + b.o_src, src.data(), n * 8);
-    std::memcpy(stage.data() + b.o_kb, v.kb.data(), L * 8);
-    std::memcpy(stage.data() + b.o_vb, v.vb.data(), L * 8);
-    std::memcpy(stage.data() + b.o_bt, v.bt.data(), v.bt.size() * 4);
-    if (pos) std::memcpy(stage.data() + b.o_pos, pos->data(), n * 4);
+    uint64_t scls = 0;
+    uint8_t* stage = (uint8_t*)dev_pool_alloc(-1, b.total, &scls);
+    if (!stage) return fail(OC_ENOMEM, std::string(who) + ": pinned staging allocation failed");
+    std::memset(stage, 0, b.total);
+    std::memcpy(stage + b.o_src, src.data(), n * 8);
+    std::memcpy(stage + b.o_kb, v.kb.data(), L * 8);
+    std::memcpy(stage + b.o_vb, v.vb.data(), L * 8);
+    std::memcpy(stage + b.o_bt, v.bt.data(), v.bt.size() * 4);
+    if (pos) std::memcpy(stage + b.o_pos, pos->data(), n * 4);
     uint64_t cls = 0;
     void* mem = dev_pool_alloc(device, b.total, &cls);
-    if (!mem) return fail(OC_ENOMEM, std::string(who) + ": device allocation failed");
-    cudaError_t e = cudaMemcpy(mem, stage.data(), b.total, cudaMemcpyHostToDevice);
+    if (!mem) {
+        dev_pool_free(-1, stage, scls);
+        return fail(OC_ENOMEM, std::string(who) + ": device allocation failed");
+    }
+    cudaStream_t us = ordered ? on_stream : upload_stream(device);
+    cudaEvent_t ev = nullptr;
+    cudaError_t e = !ordered && !us ? cudaErrorInvalidResourceHandle : cudaSuccess;
+    if (e == cudaSuccess && !ordered) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(mem, stage, b.total, cudaMemcpyHostToDevice, us);
+    if (e == cudaSuccess && ev) e = cudaEventRecord(ev, us);
     if (e != cudaSuccess) {
+        if (us) cudaStreamSynchronize(us);
+        if (ev) cudaEventDestroy(ev);
         dev_pool_free(device, mem, cls);
+        dev_pool_free(-1, stage, scls);
         return cuda_fail(e, who);
     }
+    up->ev = ev;
+    up->stage = stage;
+    up->stage_cls = scls;
+    up->done = false;
     *mem_out = mem;
     *cls_out = cls;
     uint8_t* m = (uint8_t*)mem;
@@ -171,16 +209,45 @@ struct OffloadJob {
     int device;
     void* mem;
     uint64_t cls;
+    void* stage;
+    uint64_t stage_cls;
 };
 
-void CUDART_CB offload_done(void* p) {  // host callback after the gather kernel: recycle the block
+void CUDART_CB offload_done(void* p) {  // host callback after the gather kernel: recycle the blocks
     OffloadJob* j = (OffloadJob*)p;
     dev_pool_free(j->device, j->mem, j->cls);
+    dev_pool_free(-1, j->stage, j->stage_cls);
     delete j;
 }
 }  // namespace
 
 void plan_units(Desc* d, uint32_t unit_bytes) { plan_into(d->dd, d->geo, d->N, unit_bytes); }
+
+int upload_order(Upload* u, cudaStream_t s) {
+    if (!u->ev || u->done) return OC_OK;
+    cudaError_t q = cudaEventQuery(u->ev);
+    if (q == cudaSuccess) {  // landed: later launches need no wait; recycle the stage
+        u->done = true;
+        dev_pool_free(-1, u->stage, u->stage_cls);
+        u->stage = nullptr;
+        return OC_OK;
+    }
+    if (q != cudaErrorNotReady) return cuda_fail(q, "descriptor upload");
+    cudaGetLastError();
+    OC_CUDA(cudaStreamWaitEvent(s, u->ev, 0));
+    return OC_OK;
+}
+
+void upload_release(Upload* u) {
+    if (u->ev) {
+        cudaEventSynchronize(u->ev);
+        cudaEventDestroy(u->ev);
+        u->ev = nullptr;
+    }
+    if (u->stage) dev_pool_free(-1, u->stage, u->stage_cls);
+    u->stage = nullptr;
+    u->done = true;
+}
 
 }  // namespace oc
 
@@ -229,7 +296,7 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     d->host_chunks = host_chunks;
     oc::DeviceGuard dg(d->device);
     rc = oc::upload_block(d->device, g, src, v, nullptr, "build_descriptor", &d->dev_mem, &d->dev_mem_class, &d->dd,
-                          nullptr);
+                          nullptr, &d->up, false, nullptr);
     if (rc) return rc;
     d->dd.chunk_major = delivery == OC_DELIVER_CHUNK_MAJOR;
     oc::plan_units(d.get(), 0);
@@ -285,21 +352,23 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
     void* mem = nullptr;
     uint64_t cls = 0;
     const uint32_t* pos_dev = nullptr;
-    rc = oc::upload_block(s->device, g, dst, v, &pos, "put_from_paged", &mem, &cls, &dd, &pos_dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    oc::Upload up;
+    rc = oc::upload_block(s->device, g, dst, v, &pos, "put_from_paged", &mem, &cls, &dd, &pos_dev, &up, true, st);
     if (rc) {
         rollback();
         return rc;
     }
     oc::plan_into(dd, g, dst.size(), 0);
-    cudaStream_t st = (cudaStream_t)stream;
     rc = oc::launch_offload(dd, pos_dev, s->device, st);
     if (rc) {
         cudaStreamSynchronize(st);
         oc::dev_pool_free(s->device, mem, cls);
+        oc::dev_pool_free(-1, up.stage, up.stage_cls);
         rollback();
         return rc;
     }
-    oc::OffloadJob* job = new oc::OffloadJob{s->device, mem, cls};
+    oc::OffloadJob* job = new oc::OffloadJob{s->device, mem, cls, up.stage, up.stage_cls};
     cudaError_t e = cudaLaunchHostFunc(st, oc::offload_done, job);
     if (e != cudaSuccess) {
         cudaStreamSynchronize(st);
@@ -316,6 +385,7 @@ OC_API int oc_desc_free(oc_desc* h) {
         oc::DeviceGuard dg(d->device);
         // Defer until the last fetch has finished with the descriptor's device memory.
         if (d->fetched && d->done_ev) cudaEventSynchronize(d->done_ev);
+        oc::upload_release(&d->up);
         for (auto ev : d->events) cudaEventDestroy(ev);
         if (d->done_ev) cudaEventDestroy(d->done_ev);
         if (d->sync_ev) cudaEventDestroy(d->sync_ev);

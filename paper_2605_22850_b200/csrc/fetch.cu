@@ -724,6 +724,8 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
         return fail(OC_ENOTSUP, "fetch_layerwise: pacing needs PERSISTENT mode");
     if (d->poisoned) return fail(OC_ECUDA, "fetch_layerwise: descriptor unusable after a failed launch");
     DeviceGuard dg(d->device);
+    int urc = upload_order(&d->up, s);  // the kernel reads the descriptor block
+    if (urc) return urc;
     if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
     if (o.mode == OC_FETCH_PER_LAYER && d->events.empty()) {
         d->events.resize(d->geo.L, nullptr);
@@ -804,6 +806,8 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
     cum[0] = 0;
     for (uint32_t i = 0; i < b->n; i++) {
         Desc* d = b->descs[i];
+        int urc = upload_order(&d->up, s);  // the kernel reads every descriptor's block
+        if (urc) return urc;
         if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
         plan_units(d, o.unit_bytes ? o.unit_bytes : default_unit_bytes(o.max_ctas, device_sm_count(b->device)));
         DevDesc& dd = d->dd;
@@ -943,6 +947,8 @@ OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {
         return OC_OK;
     }
     const uint32_t target = (d->epoch - 1u) * L + want_layer + 1u;
+    int urc = oc::upload_order(&d->up, s);  // the ready word lives in the uploaded block
+    if (urc) return urc;
     if (!oc::force_wait_kernel()) {
         int rc = oc::stream_wait_geq(s, d->dd.ready, target);
         if (rc == OC_OK) return OC_OK;

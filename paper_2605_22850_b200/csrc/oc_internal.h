@@ -100,6 +100,20 @@ struct Store {
 // Resolve a key to a device address (and the tier holding it): local slots first, then peers.
 bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier = nullptr);
 
+// Host -> device upload of a descriptor/offload block (descriptor.cpp).  The bytes are staged in
+// pooled pinned memory and copied on a private non-blocking stream of the device; `ev` completes
+// when they have landed.  Every launch that reads the block is ordered after `ev` (upload_order);
+// a plain cudaMemcpy would not do: from pageable memory it may return before the DMA lands, and
+// it runs on the legacy stream, which the caller's non-blocking streams do not wait for.
+struct Upload {
+    cudaEvent_t ev = nullptr;
+    void* stage = nullptr;     // pinned staging block (released once ev is observed complete)
+    uint64_t stage_cls = 0;
+    bool done = false;
+};
+int upload_order(Upload* u, cudaStream_t s);  // make s wait for the upload (no-op once complete)
+void upload_release(Upload* u);               // wait for the upload, free the stage and the event
+
 // ---- device descriptor -----------------------------------------------------------
 // Everything the copy kernel needs, passed by value as a kernel parameter.
 struct DevDesc {
@@ -142,6 +156,7 @@ struct Desc {
     uint64_t host_chunks = 0;  // chunks whose source lives in pinned host memory (PCIe reads)
     void* dev_mem = nullptr;   // one pooled block: src, k/v base, ts, counters, block table
     uint64_t dev_mem_class = 0;
+    Upload up;                 // the block's host -> device upload (launches wait for it)
     DevDesc dd;                // geometry part filled at build; epoch/units/pace at fetch
     uint32_t epoch = 0;
     uint32_t cnt_base = 0;     // unit_cnt[l] before the next fetch (same for every layer)
@@ -161,12 +176,14 @@ struct Desc {
 void* dev_pool_alloc(int device, size_t n, uint64_t* cls_out);
 void dev_pool_free(int device, void* p, uint64_t cls);
 
+
 // Plan work units of about `unit_bytes` bytes and fill the unit fields of d->dd.
 void plan_units(Desc* d, uint32_t unit_bytes);
 
 // kernel launchers (fetch.cu)
 int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s);
 // Offload gather: new chunk j (slot dd.src[j]) <- the paged rows of request chunk pos[j].
+// The caller orders `s` after the block's upload first.
 int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s);
 
 // driver entry point for cuStreamWaitValue32 (resolved lazily)

@@ -98,3 +98,19 @@ def block_table(seed: int, n_needed: int, pool_blocks: int) -> np.ndarray:
 
 def sentinel(nbytes: int, value: int = 0xA5) -> np.ndarray:
     return np.full(nbytes, value, dtype=np.uint8)
+
+
+def serving_requests(seed: int, n_requests: int, n_fam_short: int, n_fam_long: int, zipf_s: float = 1.1,
+                     hits=(0.5, 0.875)):
+    """Config 5's request mix: each request picks a length class (short / long,
+    50/50), a prefix family of that class by a Zipf(s) rank law, and a hit rate from ``hits``.
+    Returns a list of (long: bool, family index within the class, hit rate)."""
+    rng = np.random.Generator(np.random.PCG64([seed, 0x5E7]))
+    out = []
+    for _ in range(n_requests):
+        long = bool(rng.integers(0, 2))
+        n = n_fam_long if long else n_fam_short
+        w = 1.0 / np.arange(1, n + 1) ** zipf_s
+        fam = int(rng.choice(n, p=w / w.sum()))
+        out.append((long, fam, float(hits[int(rng.integers(0, len(hits)))])))
+    return out
