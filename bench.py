@@ -354,8 +354,10 @@ def main_ours(args):
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_granularity and not args.profile:
         out["granularity"] = granularity_leg(args, oc, torch, dev, lay_t, fopts)
-    if rank == 0 and args.serve:
-        out["serve"] = serve_leg(args, oc, torch, dev, lay_t)
+    if args.serve:                                 # every rank serves its share (config 5)
+        res = serve_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
+        if rank == 0:
+            out["serve"] = res
     if rank == 0 and args.sensitivity:
         out["sensitivity"] = sensitivity_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.crossover:
@@ -573,40 +575,62 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
     return res
 
 
-def serve_leg(args, oc, torch, dev, lay_t):
-    """Config 5 on one GPU: a stream of concurrent mixed requests through the public
-    API into a bounded paged KV pool.  Corpus: 32 x 4K-token + 4 x 64K-token prefix families in an
-    HBM store (48 GiB); requests pick 4K/64K 50/50, a family by Zipf(1.1), hit 50% or 87.5%.  The
-    pool (48 GiB of [L][2][blocks][Bs][row]) hands out blocks from a free list in FIFO admission
-    order (a fragmented, seeded initial order); a request is admitted when its blocks are free,
-    gets a descriptor over its blocks, is fetched on one of 8 streams, and its blocks return to the
-    free list when its fetch's completion event fires.  GB/s = 2*N*S*L summed over requests /
-    device time from the first launch to the last completion."""
+def serve_leg(args, oc, torch, dev, lay_t, ws=1, rank=0, backend="nccl"):
+    """Config 5: a stream of concurrent mixed requests through the public API
+    into a bounded paged KV pool.  Corpus: 32 x 4K-token + 4 x 64K-token prefix families (48 GiB
+    in all); requests pick 4K/64K 50/50, a family by Zipf(1.1), hit 50% or 87.5%.  The pool
+    (48 GiB of [L][2][blocks][Bs][row] per GPU) hands out blocks from a free list in FIFO
+    admission order (a fragmented, seeded initial order); a request is admitted when its blocks
+    are free, gets a descriptor over its blocks, is fetched on one of 8 streams, and its blocks
+    return to the free list when its fetch's completion event fires.
+    With N ranks (weak scaling, R requests per rank): family g is homed on rank g mod N, each
+    rank's store holds its home families, the stores are exchanged once at setup (CUDA IPC blobs,
+    all_gather_object) and attached as peers, and a rank's requests pick a local family with
+    probability p_aff = 0.875 -- the rest read their chunks from a peer GPU inside the same fetch
+    kernel (NVLink P2P loads).  No collective on the data path.  GB/s = 2*N*S*L summed over all
+    requests / the max over ranks of the device time from the first launch to the last
+    completion."""
     import collections
     import synth
+    from paper_2605_22850_b200 import dist as odist
     L, G, Bs = lay_t[0], lay_t[4], 16
     row, S, chunk = oc.geometry(lay_t)
     R = args.serve
     fam_short, fam_long = (int(x) for x in os.environ.get("OC_SERVE_FAMILIES", "32,4").split(","))
     n_short, n_long = 4096 // G, 65536 // G
-    store = oc.Store(lay_t, capacity=fam_short * n_short + fam_long * n_long, tier=oc.TIER_HBM, device=dev.index)
-    gen = torch.Generator(device=dev).manual_seed(5)
+    home_of = lambda long, f: (f + fam_short * int(long)) % ws
+    mine = [(lg, f, n) for lg, nf, n in ((False, fam_short, n_short), (True, fam_long, n_long))
+            for f in range(nf) if home_of(lg, f) == rank]
+    store = oc.Store(lay_t, capacity=max(1, sum(n for _, _, n in mine)), tier=oc.TIER_HBM, device=dev.index)
+    gen = torch.Generator(device=dev).manual_seed(5 + rank)
     fam_keys = {}
     for long, nf, n in ((False, fam_short, n_short), (True, fam_long, n_long)):
         for f in range(nf):
             (tok,), _ = synth.family_streams(8000 + 100 * long + f, G, 0, [n])
             keys = oc.chunk_keys(tok, G)
+            fam_keys[(long, f)] = keys
+            if home_of(long, f) != rank:
+                continue
             for b0 in range(0, n, 512):
                 pl = torch.randint(0, 256, (min(n, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
                 store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
                 del pl
-            fam_keys[(long, f)] = keys
+    peers = []
+    if ws > 1:                                     # setup only: exchange store handles, attach peers
+        torch.cuda.synchronize()
+        blobs = odist.exchange_blobs(store.export())
+        for r, blob in enumerate(blobs):
+            if r != rank:
+                p = oc.Store.import_(blob, device=dev.index)
+                store.attach_peer(p)
+                peers.append(p)
     pool_blocks = (int(os.environ.get("OC_SERVE_POOL_GIB", "48")) << 30) // (L * 2 * Bs * row)
     cache = torch.empty((L, 2, pool_blocks, Bs, row), dtype=torch.uint8, device=dev)
     per_kv = pool_blocks * Bs * row
     kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
     vb = [x + per_kv for x in kb]
-    reqs = synth.serving_requests(11, R, fam_short, fam_long)
+    reqs = synth.serving_requests(11 + rank, R, fam_short, fam_long, home_of=home_of if ws > 1 else None, rank=rank)
+    remote_bytes = sum(2 * (int((65536 if lg else 4096) * h) // G) * S * L for lg, f, h in reqs if home_of(lg, f) != rank)
     streams = [torch.cuda.Stream(device=dev) for _ in range(8)]
     start = torch.cuda.Event(enable_timing=True)
 
@@ -616,6 +640,8 @@ def serve_leg(args, oc, torch, dev, lay_t):
         inflight = []
         total_bytes, fetch_us, wait_blocks, n_done = 0, [], 0, 0
         torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
         start.record(streams[0])
         for s in streams[1:]:
             s.wait_event(start)
@@ -668,15 +694,27 @@ def serve_leg(args, oc, torch, dev, lay_t):
 
     run()                                               # warm-up pass (descriptor pool, modules)
     total_bytes, dev_ms, host_s, fetch_us, waits = run()
-    res = {"requests": R, "mix": f"4K/64K 50/50, Zipf(1.1) over {fam_short} + {fam_long} families, hit 50%/87.5%",
-           "pool_GiB": pool_blocks * L * 2 * Bs * row / 2**30, "bytes_rw": total_bytes,
-           "GBps_device": round(total_bytes / dev_ms / 1e6, 1), "GBps_host_wall": round(total_bytes / host_s / 1e9, 1),
-           "device_ms": round(dev_ms, 2), "host_s": round(host_s, 3),
-           "fetch_us_p50": round(float(np.percentile(fetch_us, 50)), 1),
-           "fetch_us_p99": round(float(np.percentile(fetch_us, 99)), 1),
-           "admission_stalls": waits}
+    red_dev = dev if backend == "nccl" else None
+    max_ms = odist.max_over_ranks(dev_ms, device=red_dev)
+    all_bytes = odist.sum_over_ranks(total_bytes, device=red_dev)
+    all_remote = odist.sum_over_ranks(remote_bytes, device=red_dev)
+    res = {"requests_per_rank": R, "ranks": ws,
+           "mix": f"4K/64K 50/50, Zipf(1.1) over {fam_short} + {fam_long} families, hit 50%/87.5%"
+                  + (f", family g homed on rank g mod {ws}, p_aff 0.875" if ws > 1 else ""),
+           "pool_GiB_per_rank": pool_blocks * L * 2 * Bs * row / 2**30, "bytes_rw": all_bytes,
+           "remote_byte_fraction": round(all_remote / all_bytes, 4),
+           "GBps_device": round(all_bytes / max_ms / 1e6, 1),
+           "GBps_rank0_host_wall": round(total_bytes / host_s / 1e9, 1),
+           "device_ms_max_over_ranks": round(max_ms, 2),
+           "fetch_us_p50_rank0": round(float(np.percentile(fetch_us, 50)), 1),
+           "fetch_us_p99_rank0": round(float(np.percentile(fetch_us, 99)), 1),
+           "admission_stalls_rank0": waits}
     del cache
+    if ws > 1:
+        torch.distributed.barrier()                # peers' fetches done before any store goes away
     store.close()
+    for p in peers:
+        p.close()
     torch.cuda.empty_cache()
     return res
 

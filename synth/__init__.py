@@ -101,9 +101,12 @@ def sentinel(nbytes: int, value: int = 0xA5) -> np.ndarray:
 
 
 def serving_requests(seed: int, n_requests: int, n_fam_short: int, n_fam_long: int, zipf_s: float = 1.1,
-                     hits=(0.5, 0.875)):
+                     hits=(0.5, 0.875), home_of=None, rank: int = 0, p_aff: float = 0.875):
     """Config 5's request mix: each request picks a length class (short / long,
     50/50), a prefix family of that class by a Zipf(s) rank law, and a hit rate from ``hits``.
+    With ``home_of(long, family) -> rank`` (multi-GPU), a request served by ``rank`` picks a family
+    homed on it with probability ``p_aff`` and a family homed elsewhere otherwise (Zipf law
+    restricted to that set; unrestricted if the set is empty).
     Returns a list of (long: bool, family index within the class, hit rate)."""
     rng = np.random.Generator(np.random.PCG64([seed, 0x5E7]))
     out = []
@@ -111,6 +114,11 @@ def serving_requests(seed: int, n_requests: int, n_fam_short: int, n_fam_long: i
         long = bool(rng.integers(0, 2))
         n = n_fam_long if long else n_fam_short
         w = 1.0 / np.arange(1, n + 1) ** zipf_s
+        local = rng.random() < p_aff
+        if home_of is not None:
+            keep = np.array([(home_of(long, f) == rank) == local for f in range(n)])
+            if keep.any():
+                w = np.where(keep, w, 0.0)
         fam = int(rng.choice(n, p=w / w.sum()))
         out.append((long, fam, float(hits[int(rng.integers(0, len(hits)))])))
     return out
