@@ -36,5 +36,36 @@ for kind in ("nhd", "hnd"):
                     st2.close()
                 d.close()
                 ok += 1
+# descriptors built and fetched back to back on several streams (pooled blocks recycled), each
+# with a consumer that waits on its last layer and runs a compute-window spin
+req = requests_family(lay, 4, 0, [6])[0]
+with oc.Store(lay, capacity=8) as st:
+    keys = oc.chunk_keys(req.tokens, 16)
+    st.put_chunks(keys, payload_stack(lay, 4, req.payload_ids))
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    cons = torch.cuda.Stream()
+    stamps = torch.zeros(2, dtype=torch.int64, device="cuda")
+    live = []
+    for i in range(12):
+        dest = make_dest(lay, 6, "nhd", Bs=16, seed=10 + i)
+        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+        s = streams[i % 4]
+        s.wait_stream(torch.cuda.current_stream())
+        d.fetch_layerwise(s)
+        d.wait_layer(1, cons)
+        oc.emulate_compute(1000, cons, stamps)
+        live.append((d, buf, dest))
+        if len(live) > 4:
+            d0, b0, de0 = live.pop(0)
+            d0.sync_layer(1)
+            assert np.array_equal(b0.cpu().numpy(), oracle_result(lay, 4, req, de0))
+            d0.close()
+            ok += 1
+    for d0, b0, de0 in live:
+        d0.sync_layer(1)
+        assert np.array_equal(b0.cpu().numpy(), oracle_result(lay, 4, req, de0))
+        d0.close()
+        ok += 1
 torch.cuda.synchronize()
 print("sanitize workload ok", ok)
