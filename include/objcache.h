@@ -110,7 +110,10 @@ OC_API int oc_store_slab(const oc_store* store, uint64_t* base, uint64_t* bytes)
  * memory.  An existing key with identical bytes is deduplicated; with
  * different bytes the call fails with EIMMUTABLE and *bad_index = its index
  * (chunks before it are stored).  *n_new = number of keys that were new.
- * EFULL when capacity is exhausted.  Thread-safe. */
+ * EFULL when capacity is exhausted.  Thread-safe.  Device payloads are read
+ * after all work enqueued so far on the legacy default stream (and on streams
+ * that synchronize with it); a producer on a non-blocking stream must be
+ * synchronized by the caller first.  Returns when the bytes are stored. */
 OC_API int oc_put_chunks(oc_store* store, const oc_key* keys, const void* payloads, uint64_t n,
                          uint64_t* n_new, uint64_t* bad_index);
 

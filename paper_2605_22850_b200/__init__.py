@@ -266,6 +266,9 @@ class Store:
         addr, nbytes, keep = _ptr(payloads)
         if nbytes != k.shape[0] * geometry(self.layout)[2]:
             raise ValueError("payloads must hold n * L * S bytes")
+        if getattr(payloads, "is_cuda", False):  # a torch producer may sit on a side stream
+            import torch
+            torch.cuda.current_stream(payloads.device).synchronize()
         n_new, bad = ctypes.c_uint64(), ctypes.c_uint64()
         rc = _lib.oc_put_chunks(self._h, k.ctypes.data, addr, k.shape[0], ctypes.byref(n_new), ctypes.byref(bad))
         del keep

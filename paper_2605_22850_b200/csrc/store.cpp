@@ -143,6 +143,18 @@ OC_API int oc_put_chunks(oc_store* h, const oc_key* keys, const void* payloads, 
     const uint64_t cb = s->geo.chunk;
     const uint8_t* src = (const uint8_t*)payloads;
     uint64_t fresh = 0;
+    // put_stream is non-blocking: order its copies after the legacy stream's work (the usual
+    // producer of device payloads), which an event recorded there captures.
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, payloads) == cudaSuccess && pa.type == cudaMemoryTypeDevice) {
+        cudaEvent_t ev;
+        OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        cudaError_t e = cudaEventRecord(ev, cudaStreamLegacy);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s->put_stream, ev, 0);
+        cudaEventDestroy(ev);
+        if (e != cudaSuccess) return oc::cuda_fail(e, "put_chunks: ordering after the producer");
+    }
+    cudaGetLastError();
     std::vector<uint8_t> a, b;
     for (uint64_t i = 0; i < n; i++) {
         auto it = s->index.find(keys[i]);
