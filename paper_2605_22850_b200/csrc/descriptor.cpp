@@ -104,20 +104,6 @@ BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos) {
     return b;
 }
 
-cudaStream_t upload_stream(int device) {
-    static std::mutex mu;
-    static std::unordered_map<int, cudaStream_t> streams;
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = streams.find(device);
-    if (it != streams.end()) return it->second;
-    cudaStream_t s = nullptr;
-    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    streams.emplace(device, s);
-    return s;
-}
 
 // Upload src/bases/bt(/pos) into a pooled device block and fill the static DevDesc fields.  The
 // block is staged in pooled pinned memory and copied asynchronously: on `on_stream` itself when
@@ -222,6 +208,21 @@ void CUDART_CB offload_done(void* p) {  // host callback after the gather kernel
 }  // namespace
 
 void plan_units(Desc* d, uint32_t unit_bytes) { plan_into(d->dd, d->geo, d->N, unit_bytes); }
+
+cudaStream_t upload_stream(int device) {
+    static std::mutex mu;
+    static std::unordered_map<int, cudaStream_t> streams;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = streams.find(device);
+    if (it != streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    streams.emplace(device, s);
+    return s;
+}
 
 int upload_order(Upload* u, cudaStream_t s) {
     if (!u->ev || u->done) return OC_OK;

@@ -899,7 +899,12 @@ OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out) {
         return oc::fail(OC_ENOMEM, "batch_create: allocation failed");
     }
     b->claim = (uint32_t*)((uint8_t*)b->dev + ((b->upload_bytes + 15) & ~size_t(15)));
-    OC_CUDA(cudaMemset(b->claim, 0, 16));
+    {  // zero the (possibly recycled) claim counter before any stream can launch on it
+        cudaStream_t us = oc::upload_stream(b->device);
+        if (!us) return oc::fail(OC_ECUDA, "batch_create: no upload stream");
+        OC_CUDA(cudaMemsetAsync(b->claim, 0, 16, us));
+        OC_CUDA(cudaStreamSynchronize(us));
+    }
     OC_CUDA(cudaEventCreateWithFlags(&b->staged, cudaEventDisableTiming));
     *out = (oc_batch*)b.release();
     return OC_OK;

@@ -112,6 +112,7 @@ struct Upload {
     bool done = false;
 };
 int upload_order(Upload* u, cudaStream_t s);  // make s wait for the upload (no-op once complete)
+cudaStream_t upload_stream(int device);        // the device's private non-blocking upload stream
 void upload_release(Upload* u);               // wait for the upload, free the stage and the event
 
 // ---- device descriptor -----------------------------------------------------------
