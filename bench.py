@@ -183,6 +183,19 @@ def cores_used():
         return 1, os.cpu_count()
 
 
+def bench_config(args, lay_t, ws):
+    """The N=1 workload (BASELINE configs[1]) -- shared by both arms so their lines compare."""
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    return {"workload": "llama3-8b KV layout, single request, 4K-token prefix hit (N=256 x G=16), "
+                        "paged NHD cache Bs=16 fragmented",
+            "layout": {"L": L, "n_kv": lay_t[1], "d": lay_t[2], "p": lay_t[3], "G": G, "Bs": Bs},
+            "fetch_mode": args.mode, "engine": args.engine, "tier": "hbm",
+            "l2": f"inputs larger than L2: {ROTATE} rotating request sets, "
+                  f"{ROTATE * 2 * N_CHUNKS_4K * 2 * G * lay_t[1] * lay_t[2] * lay_t[3] * L / 2**30:.1f} GiB "
+                  "touched per rotation",
+            "parallelism": f"replicas x{ws} (independent requests per GPU, no collective)"}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -190,10 +203,10 @@ def run_reference(args):
     import synth
     from oracle.geometry import Layout
     lay = Layout(*synth.LLAMA3_8B.as_tuple())
-    # one step = one layer of a 16-chunk slice of the 4K request (2 MiB read + 2 MiB written)
-    wl = OracleWorkload(1, 16, lay)
-    for _ in range(args.warmup):
-        wl.run([0])
+    # one step = one layer of the full 4K request (N = 256 chunks: 16 MiB read + 16 MiB written)
+    wl = OracleWorkload(1, N_CHUNKS_4K, lay)
+    for i in range(args.warmup):
+        wl.run([i % lay.num_layers])
     tot_b, tot_s = 0, 0.0
     for i in range(args.steps):
         b, s = wl.run([i % lay.num_layers])
@@ -204,10 +217,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "llama3-8b 4K-token prefix hit (sample: 16 chunks x 1 layer per step)",
-                   "parallelism": "replicas (rank 0 only)"},
+        "config": bench_config(args, synth.LLAMA3_8B.as_tuple(), ws),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} steps x (16 chunks x 1 layer of Llama-3-8B, G=16, Bs=16)"},
+                         "sample": f"{args.steps} steps, each one layer of the 4K request (256 chunks, G=16, "
+                                   "Bs=16): Alg. A1 gather + paged scatter, single-threaded numpy"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -320,13 +333,7 @@ def main_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8", "data": "synthetic (seeded PCG64 chunk bytes, Llama-3 vocab tokens)",
-        "config": {"workload": "llama3-8b KV layout, single request, 4K-token prefix hit (N=256 x G=16), "
-                               "paged NHD cache Bs=16 fragmented",
-                   "layout": {"L": L, "n_kv": lay_t[1], "d": lay_t[2], "p": lay_t[3], "G": G, "Bs": Bs},
-                   "fetch_mode": args.mode, "engine": args.engine, "tier": "hbm",
-                   "l2": f"inputs larger than L2: {ROTATE} rotating request sets, "
-                         f"{ROTATE * bytes_per_step / 2**30:.1f} GiB touched per rotation",
-                   "parallelism": f"replicas x{ws} (independent requests per GPU, no collective)"},
+        "config": bench_config(args, lay_t, ws),
         "kv_delivered_GBps": value / 2,
         "frac_of_spec_8TBps": value / 8000.0,
         "launch_us": {q: float(np.percentile(launch_ms, p)) * 1e3 for q, p in (("p10", 10), ("p50", 50), ("p90", 90))},
