@@ -353,8 +353,10 @@ def main_ours(args):
     store.close()
     torch.cuda.empty_cache()
 
-    if rank == 0 and not args.no_e2e:
-        out["e2e"] = e2e_leg(args, oc, torch, dev, lay_t, fopts)
+    if not args.no_e2e:                            # every rank: the whole job's end-to-end rate
+        e2e = e2e_leg(args, oc, torch, dev, lay_t, fopts, ws, backend)
+        if rank == 0:
+            out["e2e"] = e2e
     if rank == 0 and args.sched:
         out["sched"] = sched_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.batch:
@@ -384,7 +386,7 @@ def main_ours(args):
         print(json.dumps(out), flush=True)
 
 
-def e2e_leg(args, oc, torch, dev, lay_t, fopts):
+def e2e_leg(args, oc, torch, dev, lay_t, fopts, ws=1, backend="nccl"):
     """Public API end to end with the chunk store in pinned host memory (wall clock)."""
     import synth
     L, G, Bs = lay_t[0], lay_t[4], 16
@@ -420,20 +422,25 @@ def e2e_leg(args, oc, torch, dev, lay_t, fopts):
     for i in range(min(3, args.warmup) + 1):
         one(i)
     torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for i in range(steps):
         one(i)
     torch.cuda.synchronize()
     secs = time.perf_counter() - t0
+    if ws > 1:                                      # whole job: all ranks' bytes / the slowest rank
+        from paper_2605_22850_b200 import dist as odist
+        secs = odist.max_over_ranks(secs, device=dev if backend == "nccl" else None)
     store.close()
     del reqs
     torch.cuda.empty_cache()
     bytes_per_step = 2 * N * S * L
     desc_bytes = N * 8 + 2 * L * 8 + (N * G // Bs + N * G // Bs // 4) * 4
-    return {"value": bytes_per_step * steps / secs / 1e9, "unit": UNIT,
-            "h2d_bytes_per_step": N * S * L + desc_bytes, "d2h_bytes_per_step": (L + 1) * 8,
+    return {"value": ws * bytes_per_step * steps / secs / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": ws * (N * S * L + desc_bytes), "d2h_bytes_per_step": ws * (L + 1) * 8,
             "steps": steps, "ms_per_step": secs / steps * 1e3, "tier": "pinned_host (PCIe zero-copy reads)",
-            "timing": "host wall clock around match_prefix + build_descriptor + fetch + waits + D2H"}
+            "timing": "host wall clock around match_prefix + build_descriptor + fetch + waits + D2H (max over ranks)"}
 
 
 def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, windows_sel=("a100", "b200"),
