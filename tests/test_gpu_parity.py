@@ -206,6 +206,30 @@ def test_llama8b_64k_sampled_layers():
         del buf
 
 
+def test_llama70b_layout_sampled_layers():
+    """BASELINE config 4's layout (L = 80): a 2K-token prefix (N = 128) into a fragmented paged
+    cache, first_token offset 8, checked against the oracle on sampled layers."""
+    lay = lay_of(synth.LLAMA3_70B)
+    N = 128
+    req = requests_family(lay, 70, 0, [N])[0]
+    dest = make_dest(lay, N, "nhd", Bs=16, first_token=8, seed=70)
+    layers = (0, 1, 39, 78, 79)
+    want = oracle_result(lay, 70, req, dest, layers=layers)
+    with oc.Store(lay, capacity=N) as st:
+        keys = oc.chunk_keys(req.tokens, 16)
+        assert st.put_chunks(keys, payload_stack(lay, 70, req.payload_ids)) == N
+        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+        desc.fetch_layerwise(torch.cuda.current_stream())
+        desc.sync_layer(79)
+        got = buf.cpu().numpy()
+        per_kv = dest.v_off[0] - dest.k_off[0]                 # one layer's K (or V) cache
+        for l in layers:
+            for off in (dest.k_off[l], dest.v_off[l]):
+                assert np.array_equal(got[off:off + per_kv], want[off:off + per_kv]), l
+        desc.close()
+
+
 # ---- layer-ready semantics ----------------------------------------------------------------------------
 @pytest.mark.parametrize("wait_kernel", [False, True])
 @pytest.mark.parametrize("engine", ENGINES)
