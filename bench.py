@@ -57,6 +57,7 @@ def parse():
                    "unfused gather->flat->scatter comparison")
     p.add_argument("--serve", type=int, default=0, help="config 5 on one GPU: this many mixed 4K/64K requests "
                    "streaming through a bounded paged pool with FIFO block admission")
+    p.add_argument("--no-offload", action="store_true", help="skip the offload (put_from_paged) leg")
     p.add_argument("--sensitivity", action="store_true", help="Fig. 14 analog: TTFT increase at a 10 Gbps vs "
                    "100 Gbps cap, layerwise vs chunkwise, Table A5 cells")
     p.add_argument("--crossover", action="store_true", help="Eq. 2 / Fig. 13 analog: layerwise vs chunkwise "
@@ -367,6 +368,8 @@ def main_ours(args):
         res = serve_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
         if rank == 0:
             out["serve"] = res
+    if rank == 0 and not args.no_offload and not args.profile:
+        out["offload"] = offload_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.sensitivity:
         out["sensitivity"] = sensitivity_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.crossover:
@@ -729,6 +732,55 @@ def serve_leg(args, oc, torch, dev, lay_t, ws=1, rank=0, backend="nccl"):
     store.close()
     for p in peers:
         p.close()
+    torch.cuda.empty_cache()
+    return res
+
+
+def offload_leg(args, oc, torch, dev, lay_t):
+    """Offload path: put_from_paged of 4K-token requests (N = 256 chunks)
+    from a fragmented paged cache into fresh slots of an HBM store -- the inverse gather.  Each
+    iteration offloads a new key set (no dedup); 10 offloads are issued back to back on one stream
+    and timed with CUDA events around them.  GB/s = 2*N*S*L per offload / device time per
+    offload; host_us = one call's host time (key reservation + descriptor upload + launch)."""
+    import synth
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    N = N_CHUNKS_4K
+    iters = 12
+    store = oc.Store(lay_t, capacity=iters * N, tier=oc.TIER_HBM, device=dev.index)
+    need = N * G // Bs
+    pool = need + need // 4
+    cache = torch.randint(0, 256, (L, 2, pool, Bs, row), dtype=torch.uint8, device=dev)
+    per_kv = pool * Bs * row
+    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+    tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+                         synth.block_table(21, need, pool), 0)
+    key_sets = []
+    for i in range(iters):
+        (tok,), _ = synth.family_streams(6000 + i, G, 0, [N])
+        key_sets.append(oc.chunk_keys(tok, G))
+    s = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    for i in range(2):                              # warm-up (pools, module load)
+        assert oc.put_from_paged(store, key_sets[i], lay_t, tgt, s) == N
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host_us = []
+    a.record(s)
+    for i in range(2, iters):                       # back to back: the host enqueues ahead of the GPU
+        t0 = time.perf_counter()
+        n_new = oc.put_from_paged(store, key_sets[i], lay_t, tgt, s)
+        host_us.append((time.perf_counter() - t0) * 1e6)
+        assert n_new == N
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / (iters - 2)
+    res = {"N": N, "bytes_rw_per_offload": 2 * N * S * L, "GBps": round(2 * N * S * L / ms / 1e6, 1),
+           "ms_per_offload": round(ms, 4), "offloads_timed": iters - 2,
+           "host_us_median": round(float(np.median(host_us)), 1),
+           "engine": os.environ.get("OC_OFFLOAD_ENGINE", "bulk")}
+    store.close()
+    del cache
     torch.cuda.empty_cache()
     return res
 

@@ -191,19 +191,39 @@ void plan_into(DevDesc& dd, const Geometry& g, uint64_t n, uint32_t unit_bytes) 
     dd.div_tiles = make_fastdiv(dd.tiles);
 }
 
+// Blocks of offload jobs still in flight.  They are recycled once the job's event has completed,
+// polled at the next put_from_paged -- a host callback in the caller's stream would make that
+// stream wait for a host thread's wake-up after every offload.
 struct OffloadJob {
+    cudaEvent_t done;
     int device;
     void* mem;
     uint64_t cls;
     void* stage;
     uint64_t stage_cls;
 };
+std::mutex g_jobs_mu;
+std::vector<OffloadJob> g_jobs;
 
-void CUDART_CB offload_done(void* p) {  // host callback after the gather kernel: recycle the blocks
-    OffloadJob* j = (OffloadJob*)p;
-    dev_pool_free(j->device, j->mem, j->cls);
-    dev_pool_free(-1, j->stage, j->stage_cls);
-    delete j;
+void release_job(const OffloadJob& j) {
+    dev_pool_free(j.device, j.mem, j.cls);
+    dev_pool_free(-1, j.stage, j.stage_cls);
+    if (j.done) cudaEventDestroy(j.done);
+}
+
+void reap_jobs() {
+    std::lock_guard<std::mutex> lk(g_jobs_mu);
+    size_t keep = 0;
+    for (size_t i = 0; i < g_jobs.size(); i++) {
+        cudaError_t q = cudaEventQuery(g_jobs[i].done);
+        if (q == cudaErrorNotReady) {
+            g_jobs[keep++] = g_jobs[i];
+        } else {
+            release_job(g_jobs[i]);
+        }
+    }
+    g_jobs.resize(keep);
+    cudaGetLastError();
 }
 }  // namespace
 
@@ -308,6 +328,7 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
 OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const oc_layout* layout,
                              const oc_target* t, void* stream, uint64_t* n_new, uint64_t* bad_index) {
     if (!sh || !layout || !t) return oc::fail(OC_EINVAL, "put_from_paged: null pointer");
+    oc::reap_jobs();  // recycle the blocks of finished offloads
     oc::Store* s = (oc::Store*)sh;
     if (n_new) *n_new = 0;
     if (n == 0) return OC_OK;
@@ -369,12 +390,17 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
         rollback();
         return rc;
     }
-    oc::OffloadJob* job = new oc::OffloadJob{s->device, mem, cls, up.stage, up.stage_cls};
-    cudaError_t e = cudaLaunchHostFunc(st, oc::offload_done, job);
+    oc::OffloadJob job{nullptr, s->device, mem, cls, up.stage, up.stage_cls};
+    cudaError_t e = cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(job.done, st);
     if (e != cudaSuccess) {
         cudaStreamSynchronize(st);
-        oc::offload_done(job);
-        return oc::cuda_fail(e, "put_from_paged: completion callback");
+        oc::release_job(job);
+        return oc::cuda_fail(e, "put_from_paged: completion event");
+    }
+    {
+        std::lock_guard<std::mutex> lk(oc::g_jobs_mu);
+        oc::g_jobs.push_back(job);
     }
     return status;
 }

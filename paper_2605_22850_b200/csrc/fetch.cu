@@ -22,6 +22,7 @@
 // PER_LAYER mode each layer is its own launch followed by a CUDA event.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "oc_internal.h"
 
@@ -594,6 +595,85 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     }
 }
 
+// Offload on the TMA (put_from_paged): the mirror of fetch_bulk_kernel.  A unit is R rows of
+// one new chunk's layer slice; its rows are gathered from their paged slots (one bulk load per
+// contiguous run, all completing on the stage's mbarrier) into shared memory, then written to the
+// slot with one contiguous bulk store.  One warp per CTA, units claimed from the job's counter.
+__global__ void __launch_bounds__(32) offload_bulk_kernel(const __grid_constant__ DevDesc d,
+                                                          const uint32_t* __restrict__ pos, uint32_t total,
+                                                          uint32_t stages, uint32_t stage_bytes) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t s_unit[32];
+    constexpr uint32_t kEnd = 0xffffffffu;
+    uint64_t* bars = (uint64_t*)smem;
+    uint8_t* buf = smem + 128;
+    const uint32_t lane = threadIdx.x;
+    if (lane == 0) {
+        for (uint32_t s = 0; s < stages; s++) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto claim = [&](uint32_t k) {  // all lanes; returns whether unit k exists
+        uint32_t g = 0;
+        if (lane == 0) {
+            g = atomicAdd(d.next_unit, 1u);
+            s_unit[k % 32] = g < total ? g : kEnd;
+        }
+        __syncwarp();
+        return s_unit[k % 32] != kEnd;
+    };
+    auto issue_loads = [&](uint32_t k) {  // all lanes
+        const UnitGeo u = unit_geo(d, s_unit[k % 32]);
+        const uint32_t p = __ldg(&pos[u.j]);
+        const uint32_t s = k % stages;
+        uint8_t* sb = buf + (size_t)s * stage_bytes;
+        if (lane == 0) mbar_expect_tx(&bars[s], (uint32_t)(u.nrows * d.row));
+        __syncwarp();
+        if (d.nhd) {
+            for (uint32_t r = lane; r < u.nrows; r += 32) {
+                const uint32_t q = u.q0 + r;
+                uint32_t slot;
+                const uint64_t src = row_addr(d, u.layer, p, q, &slot);
+                if (r == 0 || slot == 0 || q == d.G) {
+                    uint32_t len = min(u.nrows - r, d.Bs - slot);
+                    if (q < d.G) len = min(len, d.G - q);
+                    bulk_load(sb + (size_t)r * d.row, (const void*)src, (uint32_t)(len * d.row), &bars[s]);
+                }
+            }
+        } else {
+            const uint32_t hdv = d.div_hdv.d;
+            const uint32_t heads = d.vpr / hdv;
+            const uint32_t hbytes = hdv * 16;
+            for (uint32_t i = lane; i < u.nrows * heads; i += 32) {
+                const uint32_t r = i / heads;
+                const uint32_t h = i - r * heads;
+                const uint64_t src = row_addr(d, u.layer, p, u.q0 + r, nullptr) + (uint64_t)h * d.head_stride;
+                bulk_load(sb + (size_t)r * d.row + (size_t)h * hbytes, (const void*)src, hbytes, &bars[s]);
+            }
+        }
+    };
+    for (uint32_t k = 0; k + 1 < stages; k++) {
+        if (!claim(k)) break;
+        issue_loads(k);
+    }
+    for (uint32_t k = 0;; k++) {
+        __syncwarp();
+        const uint32_t g = s_unit[k % 32];
+        if (g == kEnd) break;
+        const UnitGeo u = unit_geo(d, g);
+        const uint32_t s = k % stages;
+        mbar_wait(&bars[s], (k / stages) & 1u);
+        if (lane == 0) {
+            bulk_store((uint64_t)unit_src(d, u), buf + (size_t)s * stage_bytes, (uint32_t)(u.nrows * d.row));
+            bulk_commit();
+            bulk_wait_read<1>();  // unit k-1's stage has been read by its store
+        }
+        __syncwarp();
+        if (claim(k + stages - 1)) issue_loads(k + stages - 1);
+    }
+    if (lane == 0) bulk_wait<0>();  // the slots are written before the kernel ends
+}
+
 __global__ void wait_geq_kernel(const uint32_t* addr, uint32_t value) {
     while ((int32_t)(ld_acquire(addr) - value) < 0) __nanosleep(256);
 }
@@ -706,9 +786,26 @@ int launch_ldst(Desc* d, int sms, uint32_t max_ctas, uint32_t g0, uint32_t g1, c
 }  // namespace
 
 int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s) {
-    static int occ = occupancy((const void*)offload_kernel, kThreads, 0);
     const uint64_t total = (uint64_t)dd.units_per_layer * dd.L;
     if (total >= (1ull << 32)) return fail(OC_ERANGE, "put_from_paged: too many units");
+    const char* eng = std::getenv("OC_OFFLOAD_ENGINE");
+    if (!(eng && std::strcmp(eng, "ldst") == 0)) {
+        const BulkPlan p = plan_bulk(dd, device_sm_count(device), 0, total);
+        if (p.stages >= 2) {
+            static uint32_t attr_set = 0;
+            if (p.smem > attr_set) {
+                OC_CUDA(cudaFuncSetAttribute((const void*)offload_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)std::max<uint32_t>(p.smem, 48 * 1024)));
+                attr_set = p.smem;
+            }
+            // no observer CTA here: the whole first wave copies
+            const uint32_t grid = (uint32_t)std::min<uint64_t>(p.copy_ctas + 1, total);
+            offload_bulk_kernel<<<grid, 32, p.smem, s>>>(dd, pos, (uint32_t)total, p.stages, p.stage_bytes);
+            OC_CUDA(cudaGetLastError());
+            return OC_OK;
+        }
+    }
+    static int occ = occupancy((const void*)offload_kernel, kThreads, 0);
     const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)occ * device_sm_count(device), total));
     offload_kernel<<<(unsigned)grid, kThreads, 0, s>>>(dd, pos, (uint32_t)total);
     OC_CUDA(cudaGetLastError());

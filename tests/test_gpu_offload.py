@@ -15,8 +15,10 @@ from scenario import lib_target, make_dest, oracle_target, requests_family  # no
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("engine", ["bulk", "ldst"])
 @pytest.mark.parametrize("kind,Bs,first", [("nhd", 16, 0), ("nhd", 8, 5), ("hnd", 8, 3), ("nhd", 32, 17)])
-def test_offload_then_fetch_flat_matches_oracle(kind, Bs, first):
+def test_offload_then_fetch_flat_matches_oracle(monkeypatch, engine, kind, Bs, first):
+    monkeypatch.setenv("OC_OFFLOAD_ENGINE", engine)
     lay = OLayout(3, 2, 64, 2, 16)
     N = 7
     req = requests_family(lay, 40, 0, [N])[0]
@@ -26,6 +28,7 @@ def test_offload_then_fetch_flat_matches_oracle(kind, Bs, first):
     keys = oc.chunk_keys(req.tokens, 16)
     with oc.Store(lay, capacity=N + 1) as st:
         s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())  # the cache bytes were written on the current stream
         assert oc.put_from_paged(st, keys, lay, lib_target(oc, src, cache.data_ptr()), s) == N
         s.synchronize()
         assert st.count == N
@@ -48,7 +51,9 @@ def test_offload_then_fetch_flat_matches_oracle(kind, Bs, first):
     assert np.array_equal(got, want)
 
 
-def test_offload_round_trip_into_another_cache():
+@pytest.mark.parametrize("engine", ["bulk", "ldst"])
+def test_offload_round_trip_into_another_cache(monkeypatch, engine):
+    monkeypatch.setenv("OC_OFFLOAD_ENGINE", engine)
     lay = OLayout(2, 4, 32, 2, 16)
     N = 9
     req = requests_family(lay, 41, 0, [N])[0]
@@ -60,6 +65,7 @@ def test_offload_round_trip_into_another_cache():
     keys = oc.chunk_keys(req.tokens, 16)
     with oc.Store(lay, capacity=N) as st:
         s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
         oc.put_from_paged(st, keys, lay, lib_target(oc, a, cache_a.data_ptr()), s)
         d = oc.build_descriptor(st, keys, lay, lib_target(oc, b, cache_b.data_ptr()))
         d.fetch_layerwise(s)                         # ordered after the offload on the same stream
