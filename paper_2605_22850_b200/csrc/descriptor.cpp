@@ -382,7 +382,7 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
         return rc;
     }
     oc::plan_into(dd, g, dst.size(), 0);
-    rc = oc::launch_offload(dd, pos_dev, s->device, st);
+    rc = oc::launch_offload(dd, pos_dev, s->device, st, s->tier == OC_TIER_PINNED_HOST);
     if (rc) {
         cudaStreamSynchronize(st);
         oc::dev_pool_free(s->device, mem, cls);

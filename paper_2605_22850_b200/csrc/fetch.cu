@@ -785,12 +785,14 @@ int launch_ldst(Desc* d, int sms, uint32_t max_ctas, uint32_t g0, uint32_t g1, c
 
 }  // namespace
 
-int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s) {
+int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s, bool host_dst) {
     const uint64_t total = (uint64_t)dd.units_per_layer * dd.L;
     if (total >= (1ull << 32)) return fail(OC_ERANGE, "put_from_paged: too many units");
     const char* eng = std::getenv("OC_OFFLOAD_ENGINE");
     if (!(eng && std::strcmp(eng, "ldst") == 0)) {
-        const BulkPlan p = plan_bulk(dd, device_sm_count(device), 0, total);
+        // Writes into a pinned-host store cross PCIe: a few CTAs saturate it (as for host-tier fetches).
+        const uint32_t cap = host_dst ? (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8)) : 0;
+        const BulkPlan p = plan_bulk(dd, device_sm_count(device), cap, total);
         if (p.stages >= 2) {
             static uint32_t attr_set = 0;
             if (p.smem > attr_set) {
@@ -799,14 +801,15 @@ int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStrea
                 attr_set = p.smem;
             }
             // no observer CTA here: the whole first wave copies
-            const uint32_t grid = (uint32_t)std::min<uint64_t>(p.copy_ctas + 1, total);
+            const uint32_t grid = (uint32_t)std::min<uint64_t>(host_dst ? p.copy_ctas : p.copy_ctas + 1, total);
             offload_bulk_kernel<<<grid, 32, p.smem, s>>>(dd, pos, (uint32_t)total, p.stages, p.stage_bytes);
             OC_CUDA(cudaGetLastError());
             return OC_OK;
         }
     }
     static int occ = occupancy((const void*)offload_kernel, kThreads, 0);
-    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)occ * device_sm_count(device), total));
+    uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)occ * device_sm_count(device), total));
+    if (host_dst) grid = std::min<uint64_t>(grid, (uint64_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8)));
     offload_kernel<<<(unsigned)grid, kThreads, 0, s>>>(dd, pos, (uint32_t)total);
     OC_CUDA(cudaGetLastError());
     return OC_OK;

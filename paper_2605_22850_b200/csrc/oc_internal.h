@@ -185,7 +185,7 @@ void plan_units(Desc* d, uint32_t unit_bytes);
 int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s);
 // Offload gather: new chunk j (slot dd.src[j]) <- the paged rows of request chunk pos[j].
 // The caller orders `s` after the block's upload first.
-int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s);
+int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s, bool host_dst);
 
 // driver entry point for cuStreamWaitValue32 (resolved lazily)
 int stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t value);

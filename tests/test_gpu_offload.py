@@ -95,3 +95,34 @@ def test_offload_errors():
         with pytest.raises(oc.ObjcacheError) as e:
             oc.put_from_paged(st, keys, lay, oc.FlatTarget(cache.data_ptr(), src.size))
         assert e.value.code == oc.OC_EINVAL
+
+
+@pytest.mark.parametrize("engine", ["bulk", "ldst"])
+def test_offload_into_pinned_host_store(monkeypatch, engine):
+    """Offload whose slots live in the pinned host tier (writes cross PCIe), read back through a
+    fetch from that tier, against the oracle."""
+    monkeypatch.setenv("OC_OFFLOAD_ENGINE", engine)
+    lay = OLayout(3, 2, 64, 2, 16)
+    N = 10
+    req = requests_family(lay, 42, 0, [N])[0]
+    src = make_dest(lay, N, "nhd", Bs=16, first_token=4, seed=42)
+    gen = torch.Generator(device="cuda").manual_seed(42)
+    cache = torch.randint(0, 256, (src.size,), dtype=torch.uint8, device="cuda", generator=gen)
+    keys = oc.chunk_keys(req.tokens, 16)
+    W = N * lay.num_layers * chunk_layer_bytes(lay)
+    with oc.Store(lay, capacity=N, tier=oc.TIER_PINNED_HOST) as st:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        assert oc.put_from_paged(st, keys, lay, lib_target(oc, src, cache.data_ptr()), s) == N
+        flat = torch.full((W,), 0xA5, dtype=torch.uint8, device="cuda")
+        d = oc.build_descriptor(st, keys, lay, oc.FlatTarget(flat.data_ptr(), W))
+        d.fetch_layerwise(s)
+        d.sync_layer(lay.num_layers - 1)
+        got = flat.cpu().numpy()
+        d.close()
+    ost = ChunkStore(lay)
+    ok = okeys.chunk_keys(req.tokens, 16)
+    assert offload_paged(ost, ok, lay, oracle_target(src), cache.cpu().numpy()) == N
+    want = np.full(W, 0xA5, np.uint8)
+    fetch_layerwise(ost, obuild(ost, ok, lay, OFlat(0, W)), want)
+    assert np.array_equal(got, want)
