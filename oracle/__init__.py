@@ -9,7 +9,7 @@ method arithmetic).
 
 Every function is a plain, slow restatement of a passage of PAPER.md, cited as
 ``P:<lines> <section/equation/algorithm>``.  Readings of silent or ambiguous
-passages are numbered c1..c18 after SURVEY.md section 8(c) and listed in
+passages are numbered c1..c22 after SURVEY.md section 8(c) and listed in
 DESIGN.md.  All parts are pinned by ``tests/test_oracle_*.py`` (paper-printed
 values, closed forms, brute force, invariants); no part is "parity unpinned".
 
@@ -24,4 +24,5 @@ assemble    Alg. A1 layer-major gather; paged scatter                    (c2-c5)
 scheduler   Eqs. 4-7, Equal / KV-prop / BW-prop / Stall-opt / Calibrated (c8-c12)
 stall       Eq. 3 TTFT model, free-running pipeline, discrete-event sim  (c14)
 counts      Table A4 element counts, recompute-token delta
+dispatch    Alg. A2 lines 6-7: weighted deficit round robin, held rates   (c21-c22)
 """
