@@ -247,6 +247,36 @@ OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out);
 OC_API int oc_fetch_batch(oc_batch* batch, const oc_fetch_opts* opts, void* copy_stream);
 OC_API int oc_batch_free(oc_batch* batch);
 
+/* Weighted deficit round robin dispatch (Alg. A2 lines 6-7: "Hold per-request
+ * rates stable for this epoch. Dispatch layer payloads with weighted deficit round robin.").
+ * The batch's requests become one claim order: each request's copy units in layer-major order
+ * (its layers still complete in order), interleaved by deficit round robin with quantum
+ * q_i = floor(Q * w_i / min_j w_j) bytes per round (reading c21), cut into claim entries of at
+ * most E units that copy CTAs take in sequence.  With hold_rates, w_i are rates in bytes/s and
+ * request i's entries are released no earlier than t0 + (its bytes in earlier entries) / w_i
+ * (whole microseconds; never before the previous entry; reading c22), t0 = the launch's start. */
+typedef struct {
+    const double* weights;   /* [n] one per batch member, finite and > 0 (e.g. the epoch rates r_i) */
+    uint64_t quantum_bytes;  /* Q: bytes per round of the lightest request; 0 = max(256 KiB,
+                                largest unit); EINVAL if below the largest unit               */
+    uint32_t entry_units;    /* E: units per claim entry; 0 = 8                               */
+    uint32_t hold_rates;     /* 1: pace request i at weights[i] bytes/s                       */
+} oc_wdrr_opts;
+
+/* Fetch a batch in WDRR order (instead of layer-major across requests).  Same contract as
+ * oc_fetch_batch; opts as there (PERSISTENT, BULK; pace_Bps must be 0 -- use hold_rates).
+ * Errors: EINVAL (weights, quantum), ERANGE (a release time beyond 2^32 us, too many units). */
+OC_API int oc_fetch_batch_wdrr(oc_batch* batch, const oc_fetch_opts* opts, const oc_wdrr_opts* wdrr,
+                               void* copy_stream);
+
+/* The claim order itself (host only; what oc_fetch_batch_wdrr uploads): n requests of
+ * n_units[i] units, unit u of every request carrying tile_bytes[u % tiles] bytes.  Writes up to
+ * `cap` entries (request, first unit, unit count, release us; any output pointer may be NULL)
+ * and sets *n_entries (ERANGE if it exceeds cap). */
+OC_API int oc_wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, uint32_t tiles,
+                        const oc_wdrr_opts* wdrr, uint32_t* ent_req, uint32_t* ent_first, uint32_t* ent_count,
+                        uint32_t* ent_release_us, uint64_t cap, uint64_t* n_entries);
+
 /* wait_layer (NotifyLayerReady, Alg. A1 line 7): make `consumer_stream` wait,
  * without blocking the host, until layer `layer` of the most recent fetch is
  * in place.  Layers become ready in increasing order.  For CHUNK_MAJOR
@@ -301,11 +331,16 @@ OC_API int oc_schedule_bandwidth(int policy, const oc_profile* profiles, uint64_
  *   every waiting request is admitted with a rate from schedule_bandwidth(policy, s_i = N*S,
  *   c_i, cap - rates still in use, delta) and its fetch is launched paced at that rate for the
  *   whole load (state RUNNING).  No admission when nothing is left of the cap.
+ * set_dispatch: INDEPENDENT (default) launches each admitted request as its own fetch paced at
+ *   its rate; WDRR launches the epoch's admitted requests as one oc_fetch_batch_wdrr with weights
+ *   = rates and hold_rates = 1 (Alg. A2 lines 6-7) on the first admitted request's stream.
  * The descriptors must outlive the pool's use of them.  Not thread-safe across pools sharing a
  * descriptor. */
 typedef struct oc_tenant_pool oc_tenant_pool;
 enum { OC_TENANT_WAITING = 0, OC_TENANT_RUNNING = 1, OC_TENANT_DONE = 2, OC_TENANT_CHUNKWISE = 3 };
 OC_API int oc_pool_create(int policy, double cap_Bps, double delta_Bps, uint64_t theta_bytes, oc_tenant_pool** out);
+enum { OC_DISPATCH_INDEPENDENT = 0, OC_DISPATCH_WDRR = 1 };
+OC_API int oc_pool_set_dispatch(oc_tenant_pool* pool, int dispatch);
 OC_API int oc_pool_submit(oc_tenant_pool* pool, oc_desc* desc, double compute_per_layer_s, void* copy_stream,
                           uint64_t* ticket);
 OC_API int oc_pool_epoch(oc_tenant_pool* pool, uint64_t* n_admitted);

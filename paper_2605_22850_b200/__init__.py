@@ -33,6 +33,7 @@ DELIVER_LAYER_MAJOR, DELIVER_CHUNK_MAJOR = 0, 1
 TARGET_PAGED, TARGET_FLAT = 0, 1
 FETCH_PERSISTENT, FETCH_PER_LAYER = 0, 1
 TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
+DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
 COPY_LDST, COPY_BULK = 0, 1
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
@@ -58,6 +59,11 @@ class CTarget(ctypes.Structure):
 class CFetchOpts(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_uint32), ("engine", ctypes.c_uint32), ("max_ctas", ctypes.c_uint32),
                 ("unit_bytes", ctypes.c_uint32), ("pace_Bps", ctypes.c_double)]
+
+
+class CWdrrOpts(ctypes.Structure):
+    _fields_ = [("weights", ctypes.POINTER(ctypes.c_double)), ("quantum_bytes", ctypes.c_uint64),
+                ("entry_units", ctypes.c_uint32), ("hold_rates", ctypes.c_uint32)]
 
 
 class CProfile(ctypes.Structure):
@@ -90,6 +96,9 @@ _SIGS = {
     "oc_batch_create": [ctypes.POINTER(_vp), ctypes.c_uint32, ctypes.POINTER(_vp)],
     "oc_fetch_batch": [_vp, ctypes.POINTER(CFetchOpts), _vp],
     "oc_batch_free": [_vp],
+    "oc_fetch_batch_wdrr": [_vp, ctypes.POINTER(CFetchOpts), ctypes.POINTER(CWdrrOpts), _vp],
+    "oc_wdrr_plan": [c_u64p, ctypes.c_uint32, c_u32p, ctypes.c_uint32, ctypes.POINTER(CWdrrOpts), c_u32p, c_u32p,
+                     c_u32p, c_u32p, ctypes.c_uint64, c_u64p],
     "oc_wait_layer": [_vp, ctypes.c_uint32, _vp],
     "oc_sync_layer": [_vp, ctypes.c_uint32],
     "oc_layer_times": [_vp, c_u64p],
@@ -97,6 +106,7 @@ _SIGS = {
     "oc_schedule_bandwidth": [ctypes.c_int, ctypes.POINTER(CProfile), ctypes.c_uint64, ctypes.c_double,
                               ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
     "oc_pool_create": [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, ctypes.POINTER(_vp)],
+    "oc_pool_set_dispatch": [_vp, ctypes.c_int],
     "oc_pool_submit": [_vp, _vp, ctypes.c_double, _vp, c_u64p],
     "oc_pool_epoch": [_vp, c_u64p],
     "oc_pool_status": [_vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)],
@@ -425,9 +435,19 @@ class Batch:
         _check(_lib.oc_batch_create(arr, len(self.descs), ctypes.byref(h)))
         self._h = h
 
-    def fetch(self, stream=None, max_ctas=0, unit_bytes=0):
+    def fetch(self, stream=None, max_ctas=0, unit_bytes=0, wdrr_weights=None, quantum_bytes=0, entry_units=0,
+              hold_rates=False):
+        """One launch for the whole batch.  With `wdrr_weights` (one per member) the claim order is
+        weighted deficit round robin (oc_fetch_batch_wdrr, Alg. A2 line 7); `hold_rates` paces
+        member i at wdrr_weights[i] bytes/s (Alg. A2 line 6)."""
         o = CFetchOpts(FETCH_PERSISTENT, COPY_BULK, int(max_ctas), int(unit_bytes), 0.0)
-        _check(_lib.oc_fetch_batch(self._h, ctypes.byref(o), _stream(stream)))
+        if wdrr_weights is None:
+            _check(_lib.oc_fetch_batch(self._h, ctypes.byref(o), _stream(stream)))
+            return
+        w, opts = _wdrr_opts(wdrr_weights, quantum_bytes, entry_units, hold_rates)
+        if len(w) != len(self.descs):
+            raise ValueError("one WDRR weight per batch member")
+        _check(_lib.oc_fetch_batch_wdrr(self._h, ctypes.byref(o), ctypes.byref(opts), _stream(stream)))
 
     def close(self, _free=_lib.oc_batch_free):  # bound early: safe during interpreter exit
         if getattr(self, "_h", None):
@@ -438,7 +458,30 @@ class Batch:
         self.close()
 
 
-def fetch_batch(descs: Sequence[Descriptor], stream=None, **opts) -> Batch:
+def _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates):
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    opts = CWdrrOpts(w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(quantum_bytes), int(entry_units),
+                     1 if hold_rates else 0)
+    return w, opts
+
+
+def wdrr_plan(n_units, tile_bytes, weights, quantum_bytes=0, entry_units=0, hold_rates=False):
+    """The WDRR claim order the library builds (host only): arrays (request, first unit, count,
+    release us) of the entries."""
+    nu = np.ascontiguousarray(np.asarray(n_units, dtype=np.uint64))
+    tb = np.ascontiguousarray(np.asarray(tile_bytes, dtype=np.uint32))
+    w, opts = _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates)
+    if len(w) != len(nu):
+        raise ValueError("one weight per request")
+    n = ctypes.c_uint64()
+    args = (nu.ctypes.data_as(c_u64p), len(nu), tb.ctypes.data_as(c_u32p), len(tb), ctypes.byref(opts))
+    rc = _lib.oc_wdrr_plan(*args, None, None, None, None, 0, ctypes.byref(n))  # size query
+    if rc != OC_ERANGE or n.value == 0:
+        _check(rc)
+    out = [np.zeros(n.value, dtype=np.uint32) for _ in range(4)]
+    _check(_lib.oc_wdrr_plan(*args, *[o.ctypes.data_as(c_u32p) for o in out], n.value, ctypes.byref(n)))
+    return tuple(out)
+
     """Create a batch of descriptors and fetch it once; returns the (reusable) batch."""
     b = Batch(descs)
     b.fetch(stream, **opts)
@@ -448,11 +491,14 @@ def fetch_batch(descs: Sequence[Descriptor], stream=None, **opts) -> Batch:
 class TenantPool:
     """Epoch admission of concurrent layerwise requests under a shared cap (Sec. 3.6, Alg. A2)."""
 
-    def __init__(self, policy, cap_Bps: float, delta_Bps: float = 0.0, theta_bytes: int = 0):
+    def __init__(self, policy, cap_Bps: float, delta_Bps: float = 0.0, theta_bytes: int = 0,
+                 dispatch: int = DISPATCH_INDEPENDENT):
         code = POLICIES[policy] if isinstance(policy, str) else int(policy)
         h = _vp()
         _check(_lib.oc_pool_create(code, float(cap_Bps), float(delta_Bps), int(theta_bytes), ctypes.byref(h)))
         self._h = h
+        if dispatch != DISPATCH_INDEPENDENT:
+            _check(_lib.oc_pool_set_dispatch(h, int(dispatch)))
         self._descs = []
 
     def submit(self, desc: Descriptor, compute_per_layer_s: float, stream=None) -> int:

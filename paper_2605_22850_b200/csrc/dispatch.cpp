@@ -1,0 +1,137 @@
+// Weighted deficit round robin dispatch of layer payloads (PAPER.md Alg. A2 lines 6-7,
+// P:2595-2596; Sec. 3.6).
+//
+// The requests of one epoch share a link; Alg. A2 holds each request's rate r_i for the epoch and
+// dispatches layer payloads with weighted deficit round robin.  On B200 the dispatcher is the
+// claim order of one batched copy kernel: this file turns the requests' unit streams into that
+// order, as a table of claim entries (request, first unit, count <= E) that copy CTAs take in
+// sequence (fetch.cu, fetch_bulk_kernel<kWdrr>).
+//
+// Deficit round robin (Shreedhar & Varghese): a round visits the backlogged requests in index
+// order; a visit adds q_i to D_i and sends units from the request's head while the head unit's
+// bytes are <= D_i; a request that runs out resets D_i = 0 and leaves.  A request's units are its
+// layer-major unit stream (layer 0 of every chunk first), so its layers still complete in order
+// (reading c21).  q_i = floor(Q * w_i / min_j w_j): the lightest request's quantum is Q, which must
+// cover the largest unit (the textbook condition that makes every visit send).  With hold_rates
+// (reading c22) entry e of request i is released no earlier than t0 + (bytes of request i in
+// earlier entries) / r_i -- in whole microseconds, floor(bytes * 1e6 / r_i) -- and never before
+// the previous entry, so releases are monotone along the claim order.
+#include <cmath>
+
+#include "oc_internal.h"
+
+namespace oc {
+
+int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, uint32_t tiles, const oc_wdrr_opts& w,
+              std::vector<WdrrEntry>* out) {
+    out->clear();
+    if (n == 0 || !n_units || !tile_bytes || tiles == 0 || !w.weights)
+        return fail(OC_EINVAL, "wdrr: need n >= 1 requests, weights and tile sizes");
+    uint64_t max_tile = 0, period = 0;
+    std::vector<uint64_t> prefix(tiles + 1, 0);  // bytes of tiles [0, t)
+    for (uint32_t t = 0; t < tiles; t++) {
+        if (tile_bytes[t] == 0) return fail(OC_EINVAL, "wdrr: empty unit");
+        max_tile = std::max<uint64_t>(max_tile, tile_bytes[t]);
+        prefix[t + 1] = prefix[t] + tile_bytes[t];
+    }
+    period = prefix[tiles];
+    const uint64_t Q = w.quantum_bytes ? w.quantum_bytes : std::max<uint64_t>(256 * 1024, max_tile);
+    if (Q < max_tile) return fail(OC_EINVAL, "wdrr: quantum below the largest unit");
+    const uint32_t E = w.entry_units ? w.entry_units : 8;
+    double wmin = INFINITY;
+    for (uint32_t i = 0; i < n; i++) {
+        if (!(w.weights[i] > 0) || !std::isfinite(w.weights[i]))
+            return fail(OC_EINVAL, "wdrr: weights must be finite and > 0 (index " + std::to_string(i) + ")");
+        if (n_units[i] >= (1ull << 32)) return fail(OC_ERANGE, "wdrr: too many units in one request");
+        wmin = std::min(wmin, w.weights[i]);
+    }
+    std::vector<uint64_t> q(n), D(n, 0), head(n, 0);
+    for (uint32_t i = 0; i < n; i++) {
+        const double qi = std::floor((double)Q * w.weights[i] / wmin);
+        if (!(qi < 4.0e18)) return fail(OC_ERANGE, "wdrr: weight ratio too large");
+        q[i] = (uint64_t)qi;
+    }
+    // bytes of units [0, u) of a request: whole periods of `tiles` units, then a partial period
+    auto bytes_upto = [&](uint64_t u) { return (u / tiles) * period + prefix[u % tiles]; };
+    std::vector<uint32_t> active;
+    for (uint32_t i = 0; i < n; i++)
+        if (n_units[i]) active.push_back(i);
+    uint64_t prev_rel = 0;
+    auto emit = [&](uint32_t i, uint64_t first, uint64_t cnt) -> int {
+        for (uint64_t k = 0; k < cnt; k += E) {
+            const uint64_t c = std::min<uint64_t>(E, cnt - k);
+            uint64_t rel = 0;
+            if (w.hold_rates) {
+                const uint64_t b = bytes_upto(first + k);  // request i's bytes before this entry
+                const double t = std::floor((double)b * 1e6 / w.weights[i]);
+                if (!(t < 4294967295.0)) return fail(OC_ERANGE, "wdrr: release time beyond 2^32 us");
+                rel = std::max(prev_rel, (uint64_t)t);
+                prev_rel = rel;
+            }
+            out->push_back(WdrrEntry{i, (uint32_t)(first + k), (uint32_t)c, (uint32_t)rel});
+        }
+        return OC_OK;
+    };
+    uint32_t run_req = 0;
+    uint64_t run_first = 0, run_cnt = 0;  // the dispatch run being extended
+    while (!active.empty()) {
+        size_t keep = 0;
+        for (size_t a = 0; a < active.size(); a++) {
+            const uint32_t i = active[a];
+            D[i] += q[i];
+            const uint64_t start = head[i];
+            // send units while the head unit fits in the deficit: the partial period first, then
+            // whole periods arithmetically, then the rest unit by unit
+            while (head[i] < n_units[i] && head[i] % tiles != 0 && tile_bytes[head[i] % tiles] <= D[i]) {
+                D[i] -= tile_bytes[head[i] % tiles];
+                head[i]++;
+            }
+            if (head[i] % tiles == 0) {
+                const uint64_t periods = std::min<uint64_t>((n_units[i] - head[i]) / tiles, D[i] / period);
+                head[i] += periods * tiles;
+                D[i] -= periods * period;
+                while (head[i] < n_units[i] && tile_bytes[head[i] % tiles] <= D[i]) {
+                    D[i] -= tile_bytes[head[i] % tiles];
+                    head[i]++;
+                }
+            }
+            if (head[i] > start) {  // maximal runs: a visit continuing the previous one extends it
+                if (run_cnt && run_req == i && run_first + run_cnt == start) {
+                    run_cnt += head[i] - start;
+                } else {
+                    if (run_cnt) {
+                        int rc = emit(run_req, run_first, run_cnt);
+                        if (rc) return rc;
+                    }
+                    run_req = i;
+                    run_first = start;
+                    run_cnt = head[i] - start;
+                }
+            }
+            if (head[i] == n_units[i]) D[i] = 0;
+            else active[keep++] = i;
+        }
+        active.resize(keep);
+    }
+    return run_cnt ? emit(run_req, run_first, run_cnt) : OC_OK;
+}
+
+}  // namespace oc
+
+extern "C" OC_API int oc_wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, uint32_t tiles,
+                                   const oc_wdrr_opts* w, uint32_t* ent_req, uint32_t* ent_first, uint32_t* ent_count,
+                                   uint32_t* ent_release_us, uint64_t cap, uint64_t* n_entries) {
+    if (!w || !n_entries) return oc::fail(OC_EINVAL, "wdrr_plan: null pointer");
+    std::vector<oc::WdrrEntry> ents;
+    int rc = oc::wdrr_plan(n_units, n, tile_bytes, tiles, *w, &ents);
+    if (rc) return rc;
+    *n_entries = ents.size();
+    if (ents.size() > cap) return oc::fail(OC_ERANGE, "wdrr_plan: output capacity too small");
+    for (size_t e = 0; e < ents.size(); e++) {
+        if (ent_req) ent_req[e] = ents[e].req;
+        if (ent_first) ent_first[e] = ents[e].first;
+        if (ent_count) ent_count[e] = ents[e].count;
+        if (ent_release_us) ent_release_us[e] = ents[e].rel_us;
+    }
+    return OC_OK;
+}

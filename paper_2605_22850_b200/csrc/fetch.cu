@@ -322,15 +322,25 @@ __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// A batch: several descriptors (same L) fetched by one launch.  Units are claimed in one global
-// order -- layer-major across the batch: layer l of request 0, of request 1, ..., then layer l+1 --
-// so every request sees its layers delivered in order and all requests' early layers go first.
+// Launch flavours of fetch_bulk_kernel.
+//   kSingle  one descriptor; units claimed in its layer-major order.
+//   kBatch   several descriptors (same L) in one launch, claimed layer-major across the batch:
+//            layer l of request 0, of request 1, ..., then layer l+1 -- every request sees its
+//            layers in order and all requests' early layers go first.
+//   kWdrr    several descriptors; the claim order is a table of entries (request, first unit,
+//            count, release us) built by weighted deficit round robin (dispatch.cpp; Alg. A2
+//            lines 6-7), each request's units still in its own layer-major order.
+enum { kSingle = 0, kBatch = 1, kWdrr = 2 };
+
 struct BatchArgs {
     const DevDesc* descs;  // [n] device copies of the requests' descriptors
-    const uint32_t* cum;   // [n + 1] prefix sums of units_per_layer
+    const uint32_t* cum;   // [n + 1] prefix sums of units_per_layer (kBatch)
     uint32_t* claim;       // batch claim counter (monotone across launches)
+    const uint4* ents;     // kWdrr: claim entries {request, first unit, count, release us}
+    unsigned long long* t0_slot;  // kWdrr: the launch's common start time (0 before the launch)
     uint32_t n;
     uint32_t upl_total;    // cum[n]
+    uint32_t paced;        // kWdrr: entries carry release times
     FastDiv div_upl_total;
 };
 
@@ -340,9 +350,9 @@ struct Resolved {
     uint32_t req;  // request index within the batch (0 without a batch)
 };
 
-template <bool BATCH>
+template <int MODE>
 __device__ __forceinline__ Resolved resolve(const DevDesc& d0, const BatchArgs& ba, uint32_t g) {
-    if (!BATCH) return {&d0, g, 0u};
+    if (MODE == kSingle) return {&d0, g, 0u};
     const uint32_t layer = fdiv(g, ba.div_upl_total);
     const uint32_t rem = g - layer * ba.upl_total;
     uint32_t lo = 0, hi = ba.n;  // largest r with cum[r] <= rem
@@ -356,22 +366,40 @@ __device__ __forceinline__ Resolved resolve(const DevDesc& d0, const BatchArgs& 
 }
 
 // Batch observer: lane i announces the layers of requests i, i+32, ...; each request's layers go
-// out in order (same protocol as observe_layers).
+// out in order (same protocol as observe_layers).  The lane polls its requests round-robin without
+// blocking on any one of them -- under WDRR a light request may be many layers behind a heavy one.
+// A request's next layer is read back from its ready word, which only this lane writes during the
+// fetch (it holds (epoch-1)*L when the fetch starts: the previous fetch announced all L layers).
 __device__ void observe_batch(const BatchArgs& ba, uint64_t t0) {
     const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t r = lane; r < ba.n; r += 32) ba.descs[r].ts[0] = t0;
-    const uint32_t L = ba.descs[0].L;
-    for (uint32_t l = 0; l < L; l++)
+    uint32_t left = 0;
+    for (uint32_t r = lane; r < ba.n; r += 32) {
+        ba.descs[r].ts[0] = t0;
+        left++;
+    }
+    uint32_t ns = 32;
+    while (left) {
+        bool moved = false;
         for (uint32_t r = lane; r < ba.n; r += 32) {
             const DevDesc& d = ba.descs[r];
-            uint32_t ns = 32;
-            while ((int32_t)(ld_acquire(&d.unit_cnt[l]) - d.cnt_target) < 0) {
-                __nanosleep(ns);
-                ns = min(ns * 2, 256u);
+            const uint32_t base = (d.epoch - 1u) * d.L;
+            uint32_t l = *(volatile uint32_t*)d.ready - base;
+            if (l >= d.L) continue;
+            while (l < d.L && (int32_t)(ld_acquire(&d.unit_cnt[l]) - d.cnt_target) >= 0) {
+                d.ts[1 + l] = globaltimer();
+                st_release(d.ready, base + l + 1u);
+                l++;
+                moved = true;
             }
-            d.ts[1 + l] = globaltimer();
-            st_release(d.ready, (d.epoch - 1u) * d.L + l + 1u);
+            if (l == d.L) left--;
         }
+        if (moved) {
+            ns = 32;
+        } else {
+            __nanosleep(ns);
+            ns = min(ns * 2, 256u);
+        }
+    }
 }
 
 // CTA 0: observer.  CTA b >= 1: warp 0 claims units and copies them through a `stages`-deep
@@ -379,14 +407,15 @@ __device__ void observe_batch(const BatchArgs& ba, uint64_t t0) {
 // an mbarrier-guarded shared-memory FIFO -- into release reductions, so the copy pipeline never
 // waits on a GPU-scope fence.  A unit is retired once its bulk stores
 // are complete (wait_group with a lag of two units, so stores stay in flight).
-template <bool BATCH>
+template <int MODE>
 __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ DevDesc d0,
                                                         const __grid_constant__ BatchArgs ba, uint32_t g0,
                                                         uint32_t g1, uint32_t grab_base, uint32_t stages,
                                                         uint32_t stage_bytes) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t fifo_req[kFifo], fifo_layer[kFifo], fifo_n[kFifo];
-    __shared__ uint32_t s_unit[32], s_req[32];
+    __shared__ uint32_t s_unit[32], s_req[32], s_rel[32];
+    constexpr bool BATCH = MODE != kSingle;
     __shared__ __align__(8) uint64_t fifo_full[kFifo], fifo_empty[kFifo];
     const uint64_t t0 = globaltimer();
     if (blockIdx.x == 0) {
@@ -440,9 +469,36 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     // overlaps a unit's copy instead of stalling the issue loop -- with a small copy-CTA budget
     // that latency would otherwise cap each CTA at one unit per round trip.
     uint32_t next_raw = lane == 0 ? atomicAdd(claim_ctr, 1u) : 0u;
+    // kWdrr: the entry being consumed (lane 0) and the launch's common start time
+    uint32_t cur_req = 0, cur_next = 0, cur_left = 0, cur_rel = 0;
+    uint64_t t_start = t0;
+    if (MODE == kWdrr && ba.paced && lane == 0) {
+        const unsigned long long old = atomicCAS(ba.t0_slot, 0ull, (unsigned long long)t0);
+        t_start = old ? old : t0;
+    }
     auto claim = [&](uint32_t k) {  // lane 0 only: claim unit k, returns false at the end
         uint32_t g = kEnd, req = 0;
-        if (!exhausted) {
+        if (MODE == kWdrr) {
+            if (!exhausted && cur_left == 0) {  // take the next entry (claims stop past g1 as below)
+                const uint32_t e = g0 + (next_raw - grab_base);
+                if (e >= g1) {
+                    exhausted = true;
+                } else {
+                    next_raw = atomicAdd(claim_ctr, 1u);
+                    const uint4 en = ba.ents[e];
+                    cur_req = en.x;
+                    cur_next = en.y;
+                    cur_left = en.z;
+                    cur_rel = en.w;
+                }
+            }
+            if (!exhausted) {
+                g = cur_next++;
+                cur_left--;
+                req = cur_req;
+                s_rel[k % 32] = cur_rel;
+            }
+        } else if (!exhausted) {
             // Each copy CTA stops after its first claim past g1: a launch advances the counter by
             // exactly (units + copy CTAs), so the host knows the next launch's grab_base.
             const uint32_t gg = g0 + (next_raw - grab_base);
@@ -450,7 +506,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
                 exhausted = true;
             } else {
                 next_raw = atomicAdd(claim_ctr, 1u);
-                const Resolved rs = resolve<BATCH>(d0, ba, gg);
+                const Resolved rs = resolve<MODE>(d0, ba, gg);
                 g = rs.g;
                 req = rs.req;
             }
@@ -468,7 +524,11 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         mbar_expect_tx(&bars[s], bytes);
         bulk_load(buf + (size_t)s * stage_bytes, unit_src(d, u), bytes, &bars[s]);
     };
-    auto release_time = [&](uint32_t k) {  // minimal pacer: layer l released at t0 + l * pace
+    // kSingle: minimal pacer, layer l released at t0 + l * pace.  kWdrr: the entry's
+    // release time after the launch's start (Alg. A2 line 6, reading c22).
+    const bool paced = MODE == kSingle ? d0.pace_ns != 0 : (MODE == kWdrr && ba.paced != 0);
+    auto release_time = [&](uint32_t k) -> uint64_t {
+        if (MODE == kWdrr) return t_start + (uint64_t)s_rel[k % 32] * 1000ull;
         const DevDesc& d = desc_of(k);
         return t0 + (uint64_t)fdiv(s_unit[k % 32], d.div_upl) * d.pace_ns;
     };
@@ -492,7 +552,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     if (lane == 0)
         for (uint32_t k = 0; k + 1 < stages; k++) {
             if (!claim(k)) break;
-            if (!BATCH && d0.pace_ns)
+            if (paced)
                 while (globaltimer() < release_time(k)) __nanosleep(2000);
             issue_load(k);
         }
@@ -540,7 +600,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         if (lane == 0) got = claim(kl) ? 1u : 0u;
         got = __shfl_sync(0xffffffffu, got, 0);
         if (got) {
-            if (!BATCH && d0.pace_ns) {
+            if (paced) {
                 uint32_t hold = lane == 0 ? (globaltimer() < release_time(kl) ? 1u : 0u) : 0u;
                 hold = __shfl_sync(0xffffffffu, hold, 0);
                 if (hold) {  // retire everything copied so far before idling until the release
@@ -748,11 +808,11 @@ BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units
     return p;
 }
 
-template <bool BATCH>
+template <int MODE>
 cudaError_t set_bulk_smem(uint32_t smem) {
     static uint32_t attr_set = 0;
     if (smem <= attr_set) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute((const void*)fetch_bulk_kernel<BATCH>,
+    cudaError_t e = cudaFuncSetAttribute((const void*)fetch_bulk_kernel<MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<uint32_t>(smem, 48 * 1024));
     if (e == cudaSuccess) attr_set = smem;
@@ -763,8 +823,8 @@ cudaError_t set_bulk_smem(uint32_t smem) {
 // d->grab_ctr and advances that counter by (units + copy CTAs) -- see claim_unit.
 int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
     if (p.stages < 2) return fail(OC_ENOTSUP, "bulk engine: two units do not fit in shared memory (use LDST)");
-    OC_CUDA(set_bulk_smem<false>(p.smem));
-    fetch_bulk_kernel<false><<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
+    OC_CUDA(set_bulk_smem<kSingle>(p.smem));
+    fetch_bulk_kernel<kSingle><<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
                                                                  p.stage_bytes);
     OC_CUDA(cudaGetLastError());
     d->grab_ctr += (g1 - g0) + p.copy_ctas;
@@ -887,19 +947,47 @@ struct Batch {
     uint64_t dev_class = 0;
     void* stage = nullptr;     // pinned staging of the upload area
     uint64_t stage_class = 0;
-    cudaEvent_t staged = nullptr;  // the last upload has finished reading `stage`
+    cudaEvent_t staged = nullptr;  // the last upload has finished reading `stage` (and `ent_stage`)
     uint32_t grab_ctr = 0;
     uint32_t* claim = nullptr;
+    // WDRR claim table: [t0 slot (16 B)][entries], device block and pinned stage, grown on demand
+    void* ent_dev = nullptr;
+    uint64_t ent_dev_class = 0;
+    void* ent_stage = nullptr;
+    uint64_t ent_stage_class = 0;
+    size_t ent_cap = 0;  // bytes of both blocks
 };
 
-int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
+// Grow the WDRR table blocks to `bytes`.  The old device block may still be read by this batch's
+// previous launch, so it is released only after every member's last fetch has completed.
+int ensure_ent_capacity(Batch* b, size_t bytes) {
+    if (bytes <= b->ent_cap) return OC_OK;
+    for (Desc* d : b->descs)
+        if (d->fetched && d->done_ev) OC_CUDA(cudaEventSynchronize(d->done_ev));
+    dev_pool_free(b->device, b->ent_dev, b->ent_dev_class);
+    dev_pool_free(-1, b->ent_stage, b->ent_stage_class);
+    b->ent_dev = dev_pool_alloc(b->device, bytes, &b->ent_dev_class);
+    b->ent_stage = dev_pool_alloc(-1, bytes, &b->ent_stage_class);
+    if (!b->ent_dev || !b->ent_stage) {
+        dev_pool_free(b->device, b->ent_dev, b->ent_dev_class);
+        dev_pool_free(-1, b->ent_stage, b->ent_stage_class);
+        b->ent_dev = b->ent_stage = nullptr;
+        b->ent_cap = 0;
+        return fail(OC_ENOMEM, "fetch_batch_wdrr: claim table allocation failed");
+    }
+    b->ent_cap = bytes;
+    return OC_OK;
+}
+
+int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cudaStream_t s) {
     if (o.mode != OC_FETCH_PERSISTENT) return fail(OC_ENOTSUP, "fetch_batch: batches use PERSISTENT mode");
     if (o.engine != OC_COPY_BULK) return fail(OC_ENOTSUP, "fetch_batch: batches use the BULK engine");
-    if (o.pace_Bps != 0) return fail(OC_ENOTSUP, "fetch_batch: pacing is per request (fetch_layerwise)");
+    if (o.pace_Bps != 0)
+        return fail(OC_ENOTSUP, "fetch_batch: pace_Bps is per request (fetch_layerwise); WDRR batches use hold_rates");
     for (Desc* d : b->descs)
         if (d->poisoned) return fail(OC_ECUDA, "fetch_batch: a descriptor is unusable after a failed launch");
     DeviceGuard dg(b->device);
-    OC_CUDA(cudaEventSynchronize(b->staged));  // previous upload done with the staging buffer
+    OC_CUDA(cudaEventSynchronize(b->staged));  // previous upload done with the staging buffers
     DevDesc* st = (DevDesc*)b->stage;
     uint32_t* cum = (uint32_t*)((uint8_t*)b->stage + sizeof(DevDesc) * b->n);
     uint64_t host_chunks = 0, chunks = 0, total = 0;
@@ -924,10 +1012,34 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
     }
     const uint32_t L = b->descs[0]->geo.L;
     if (total * L >= (1ull << 32)) return fail(OC_ERANGE, "fetch_batch: too many units in one batch");
+    // WDRR: the claim order (Alg. A2 line 7), uploaded behind a zeroed start-time slot
+    uint64_t n_claims = total * L;  // claim items of the launch: units, or WDRR entries
+    if (wdrr) {
+        const DevDesc& d0 = b->descs[0]->dd;
+        std::vector<uint64_t> n_units(b->n);
+        for (uint32_t i = 0; i < b->n; i++) {
+            if (b->descs[i]->dd.tiles != d0.tiles || b->descs[i]->dd.rows_per_unit != d0.rows_per_unit)
+                return fail(OC_EINVAL, "fetch_batch_wdrr: members planned with different units");
+            n_units[i] = (uint64_t)b->descs[i]->dd.units_per_layer * L;
+        }
+        std::vector<uint32_t> tile_bytes(d0.tiles);
+        for (uint32_t t = 0; t < d0.tiles; t++)
+            tile_bytes[t] = (uint32_t)(std::min(d0.rows_per_unit, 2 * d0.G - t * d0.rows_per_unit) * d0.row);
+        std::vector<WdrrEntry> ents;
+        int rc = wdrr_plan(n_units.data(), b->n, tile_bytes.data(), d0.tiles, *wdrr, &ents);
+        if (rc) return rc;
+        rc = ensure_ent_capacity(b, 16 + ents.size() * sizeof(WdrrEntry));
+        if (rc) return rc;
+        std::memset(b->ent_stage, 0, 16);
+        std::memcpy((uint8_t*)b->ent_stage + 16, ents.data(), ents.size() * sizeof(WdrrEntry));
+        OC_CUDA(cudaMemcpyAsync(b->ent_dev, b->ent_stage, 16 + ents.size() * sizeof(WdrrEntry),
+                                cudaMemcpyHostToDevice, s));
+        n_claims = ents.size();
+    }
     uint32_t max_ctas = o.max_ctas;
     if (!max_ctas && host_chunks * 2 > chunks) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8));
     const int sms = device_sm_count(b->device);
-    const BulkPlan p = plan_bulk(b->descs[0]->dd, sms, max_ctas, total * L);
+    const BulkPlan p = plan_bulk(b->descs[0]->dd, sms, max_ctas, n_claims);
     OC_CUDA(cudaMemcpyAsync(b->dev, b->stage, b->upload_bytes, cudaMemcpyHostToDevice, s));
     OC_CUDA(cudaEventRecord(b->staged, s));
     for (Desc* d : b->descs) {  // from the launch on, the device counters belong to the new epoch
@@ -942,12 +1054,21 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, cudaStream_t s) {
     ba.n = b->n;
     ba.upl_total = (uint32_t)total;
     ba.div_upl_total = make_fastdiv((uint32_t)total);
+    ba.ents = wdrr ? (const uint4*)((uint8_t*)b->ent_dev + 16) : nullptr;
+    ba.t0_slot = wdrr ? (unsigned long long*)b->ent_dev : nullptr;
+    ba.paced = wdrr && wdrr->hold_rates ? 1u : 0u;
     if (p.stages < 2) return fail(OC_ENOTSUP, "fetch_batch: two units do not fit in shared memory");
-    OC_CUDA(set_bulk_smem<true>(p.smem));
-    fetch_bulk_kernel<true><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)(total * L), b->grab_ctr,
-                                                                p.stages, p.stage_bytes);
+    if (wdrr) {
+        OC_CUDA(set_bulk_smem<kWdrr>(p.smem));
+        fetch_bulk_kernel<kWdrr><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
+                                                                     b->grab_ctr, p.stages, p.stage_bytes);
+    } else {
+        OC_CUDA(set_bulk_smem<kBatch>(p.smem));
+        fetch_bulk_kernel<kBatch><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
+                                                                      b->grab_ctr, p.stages, p.stage_bytes);
+    }
     OC_CUDA(cudaGetLastError());
-    b->grab_ctr += (uint32_t)(total * L) + p.copy_ctas;
+    b->grab_ctr += (uint32_t)n_claims + p.copy_ctas;
     for (Desc* d : b->descs) {
         OC_CUDA(cudaEventRecord(d->done_ev, s));
         d->poisoned = false;
@@ -1016,7 +1137,16 @@ OC_API int oc_fetch_batch(oc_batch* h, const oc_fetch_opts* opts, void* stream) 
     o.mode = OC_FETCH_PERSISTENT;
     o.engine = OC_COPY_BULK;
     if (opts) o = *opts;
-    return oc::fetch_batch((oc::Batch*)h, o, (cudaStream_t)stream);
+    return oc::fetch_batch((oc::Batch*)h, o, nullptr, (cudaStream_t)stream);
+}
+
+OC_API int oc_fetch_batch_wdrr(oc_batch* h, const oc_fetch_opts* opts, const oc_wdrr_opts* wdrr, void* stream) {
+    if (!h || !wdrr) return oc::fail(OC_EINVAL, "fetch_batch_wdrr: null pointer");
+    oc_fetch_opts o{};
+    o.mode = OC_FETCH_PERSISTENT;
+    o.engine = OC_COPY_BULK;
+    if (opts) o = *opts;
+    return oc::fetch_batch((oc::Batch*)h, o, wdrr, (cudaStream_t)stream);
 }
 
 OC_API int oc_batch_free(oc_batch* h) {
@@ -1032,6 +1162,8 @@ OC_API int oc_batch_free(oc_batch* h) {
         }
         oc::dev_pool_free(b->device, b->dev, b->dev_class);
         oc::dev_pool_free(-1, b->stage, b->stage_class);
+        oc::dev_pool_free(b->device, b->ent_dev, b->ent_dev_class);
+        oc::dev_pool_free(-1, b->ent_stage, b->ent_stage_class);
         cudaGetLastError();
     }
     delete b;

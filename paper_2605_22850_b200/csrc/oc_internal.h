@@ -181,6 +181,13 @@ void dev_pool_free(int device, void* p, uint64_t cls);
 // Plan work units of about `unit_bytes` bytes and fill the unit fields of d->dd.
 void plan_units(Desc* d, uint32_t unit_bytes);
 
+// WDRR claim order (dispatch.cpp; Alg. A2 lines 6-7): entry = request, first unit, units, release us.
+struct WdrrEntry {
+    uint32_t req, first, count, rel_us;
+};
+int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, uint32_t tiles, const oc_wdrr_opts& w,
+              std::vector<WdrrEntry>* out);
+
 // kernel launchers (fetch.cu)
 int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s);
 // Offload gather: new chunk j (slot dd.src[j]) <- the paged rows of request chunk pos[j].

@@ -5,8 +5,12 @@
 // and Alg. A2: at each scheduling epoch the pool admits the waiting
 // layerwise requests under a fixed total budget, gives each a stable target rate for the whole of
 // its KV load (Stall-opt / Calibrated Stall-opt or a baseline policy), and bandwidth released by
-// a request that finishes early returns to the pool only at the next epoch.  Rates are enforced
-// by the fetch kernel's pacer (a10): layer l of a request is released at t0 + l * N*S / r.
+// a request that finishes early returns to the pool only at the next epoch.  Dispatch:
+//   INDEPENDENT  each admitted request is its own fetch, paced by the kernel's minimal pacer (a10):
+//                layer l released at t0 + l * N*S / r;
+//   WDRR         the epoch's admitted requests are one batched launch whose claim order is
+//                weighted deficit round robin with weights r_i, each request held at r_i
+//                (Alg. A2 lines 6-7; dispatch.cpp), on the first admitted request's stream.
 #include <cmath>
 
 #include "oc_internal.h"
@@ -25,8 +29,14 @@ struct TenantPool {
     int policy;
     double cap, delta;
     uint64_t theta;
+    int dispatch = OC_DISPATCH_INDEPENDENT;
     std::mutex mu;
     std::vector<Tenant> tenants;  // ticket = index
+    struct EpochBatch {
+        oc_batch* batch;
+        std::vector<size_t> members;  // tickets
+    };
+    std::vector<EpochBatch> batches;  // WDRR launches, freed once every member has finished
     uint64_t epochs = 0;
 };
 
@@ -46,6 +56,16 @@ OC_API int oc_pool_create(int policy, double cap_Bps, double delta_Bps, uint64_t
     p->delta = delta_Bps;
     p->theta = theta_bytes;
     *out = (oc_tenant_pool*)p;
+    return OC_OK;
+}
+
+OC_API int oc_pool_set_dispatch(oc_tenant_pool* h, int dispatch) {
+    if (!h) return oc::fail(OC_EINVAL, "pool_set_dispatch: null pool");
+    if (dispatch != OC_DISPATCH_INDEPENDENT && dispatch != OC_DISPATCH_WDRR)
+        return oc::fail(OC_EINVAL, "pool_set_dispatch: unknown dispatch");
+    oc::TenantPool* p = (oc::TenantPool*)h;
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->dispatch = dispatch;
     return OC_OK;
 }
 
@@ -98,6 +118,16 @@ OC_API int oc_pool_epoch(oc_tenant_pool* h, uint64_t* n_admitted) {
             return oc::cuda_fail(e, "pool_epoch: fetch failed");
         }
     }
+    for (size_t k = 0; k < p->batches.size();) {  // WDRR launches whose members have all finished
+        bool live = false;
+        for (size_t i : p->batches[k].members) live |= p->tenants[i].state == OC_TENANT_RUNNING;
+        if (live) {
+            k++;
+        } else {
+            oc_batch_free(p->batches[k].batch);
+            p->batches.erase(p->batches.begin() + k);
+        }
+    }
     // 2. Admit every waiting request with rates from the budget the running ones leave.
     std::vector<size_t> waiting;
     for (size_t i = 0; i < p->tenants.size(); i++)
@@ -111,7 +141,32 @@ OC_API int oc_pool_epoch(oc_tenant_pool* h, uint64_t* n_admitted) {
     std::vector<double> rates(waiting.size());
     int rc = oc_schedule_bandwidth(p->policy, prof.data(), prof.size(), budget, p->delta, rates.data());
     if (rc) return rc;
-    // 3. Launch the admitted fetches, each paced at its rate for the whole load.
+    // 3. Launch the admitted fetches, each held at its rate for the whole load.
+    if (p->dispatch == OC_DISPATCH_WDRR) {  // one launch, WDRR claim order (Alg. A2 lines 6-7)
+        std::vector<oc_desc*> ds(waiting.size());
+        for (size_t k = 0; k < waiting.size(); k++) ds[k] = (oc_desc*)p->tenants[waiting[k]].desc;
+        oc_batch* b = nullptr;
+        rc = oc_batch_create(ds.data(), (uint32_t)ds.size(), &b);
+        if (rc) return rc;
+        oc_fetch_opts o{};
+        o.mode = OC_FETCH_PERSISTENT;
+        o.engine = OC_COPY_BULK;
+        oc_wdrr_opts w{};
+        w.weights = rates.data();
+        w.hold_rates = 1;
+        rc = oc_fetch_batch_wdrr(b, &o, &w, p->tenants[waiting[0]].stream);
+        if (rc) {
+            oc_batch_free(b);
+            return rc;
+        }
+        p->batches.push_back({b, waiting});
+        for (size_t k = 0; k < waiting.size(); k++) {
+            p->tenants[waiting[k]].rate = rates[k];
+            p->tenants[waiting[k]].state = OC_TENANT_RUNNING;
+        }
+        if (n_admitted) *n_admitted = waiting.size();
+        return OC_OK;
+    }
     for (size_t k = 0; k < waiting.size(); k++) {
         oc::Tenant& t = p->tenants[waiting[k]];
         oc_fetch_opts o{};
@@ -139,6 +194,8 @@ OC_API int oc_pool_status(oc_tenant_pool* h, uint64_t ticket, int* state, double
 }
 
 OC_API int oc_pool_destroy(oc_tenant_pool* h) {
+    if (!h) return OC_OK;
+    for (auto& eb : ((oc::TenantPool*)h)->batches) oc_batch_free(eb.batch);  // waits for its launch
     delete (oc::TenantPool*)h;
     return OC_OK;
 }

@@ -115,3 +115,135 @@ def test_batch_errors():
     b.close()
     st.close()
     st2.close()
+
+
+# ---- WDRR claim order (Alg. A2 lines 6-7) ------------------------------------------------------
+@pytest.mark.parametrize("lay,unit_bytes", [(OLayout(3, 2, 64, 2, 16), 0), (OLayout(2, 4, 32, 2, 20), 3072),
+                                            (OLayout(2, 4, 32, 2, 20), 1024)])
+@pytest.mark.parametrize("hold", [False, True])
+@pytest.mark.parametrize("E", [0, 1, 3])
+def test_wdrr_parity(lay, unit_bytes, hold, E):
+    """Every byte lands as in the oracle whatever the interleaving (ragged units included: 3072 B
+    units of 12 rows cut a 40-row slice into 12+12+12+4), and each request's layers are announced
+    in order."""
+    st, items = setup_batch(lay, SPECS)
+    b = oc.Batch([it["desc"] for it in items])
+    s = torch.cuda.Stream()
+    weights = [2e9, 0.5e9, 7e9, 1e9, 3.3e9]
+    b.fetch(s, unit_bytes=unit_bytes, wdrr_weights=weights, quantum_bytes=unit_bytes or 0, entry_units=E,
+            hold_rates=hold)
+    for it in items:
+        it["desc"].sync_layer(lay.num_layers - 1)
+    torch.cuda.synchronize()
+    check(lay, items)
+    for it in items:
+        t = it["desc"].layer_times().astype(np.int64)
+        assert np.all(np.diff(t[1:]) >= 0) and t[1] >= t[0]
+    b.close()
+    st.close()
+
+
+def test_wdrr_refetch_mixed_with_other_orders():
+    """Epoch bookkeeping across WDRR, layer-major batch and single fetches of the same descriptors
+    (the WDRR observer reads each request's next layer back from its ready word)."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    st, items = setup_batch(lay, SPECS)
+    b = oc.Batch([it["desc"] for it in items])
+    s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+    for rnd in range(6):
+        with torch.cuda.stream(s):
+            for it in items:
+                it["buf"].fill_(0xA5)
+        if rnd in (0, 3, 5):
+            b.fetch(s, wdrr_weights=[1e9 * (k + 1) for k in range(len(items))], hold_rates=rnd == 3,
+                    max_ctas=2 if rnd == 5 else 0)
+        elif rnd == 1:
+            b.fetch(s)
+        else:
+            for it in items:
+                it["desc"].fetch_layerwise(s)
+        for it in items:
+            it["desc"].wait_layer(lay.num_layers - 1, cons)
+        cons.synchronize()
+        torch.cuda.synchronize()
+        check(lay, items)
+    b.close()
+    st.close()
+
+
+def test_wdrr_pinned_host_and_errors():
+    lay = OLayout(2, 4, 32, 2, 16)
+    st, items = setup_batch(lay, SPECS, tier=oc.TIER_PINNED_HOST)
+    b = oc.Batch([it["desc"] for it in items])
+    b.fetch(torch.cuda.current_stream(), wdrr_weights=[1.0, 2.0, 3.0, 4.0, 5.0])
+    torch.cuda.synchronize()
+    check(lay, items)
+    with pytest.raises(ValueError):
+        b.fetch(None, wdrr_weights=[1.0])
+    with pytest.raises(oc.ObjcacheError) as e:
+        b.fetch(None, wdrr_weights=[1.0, 1.0, 0.0, 1.0, 1.0])
+    assert e.value.code == oc.OC_EINVAL
+    b.close()
+    st.close()
+
+
+def big_pair(n_chunks):
+    """Two Llama-3-8B-layout requests of n_chunks chunks each, HBM store, NHD paged targets."""
+    import synth
+    lay = synth.LLAMA3_8B.as_tuple()
+    L, G, Bs = lay[0], lay[4], 16
+    row, S, chunk = oc.geometry(lay)
+    st = oc.Store(lay, capacity=2 * n_chunks)
+    descs, caches = [], []
+    for r in range(2):
+        (tok,), _ = synth.family_streams(100 + r, G, 0, [n_chunks])
+        keys = oc.chunk_keys(tok, G)
+        for b0 in range(0, n_chunks, 64):
+            b1 = min(n_chunks, b0 + 64)
+            st.put_chunks(keys[b0:b1], torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device="cuda"))
+        need = n_chunks * G // Bs
+        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device="cuda")
+        per_kv = need * Bs * row
+        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay[2] * lay[3], Bs,
+                             synth.block_table(r, need, need), 0)
+        descs.append(oc.build_descriptor(st, keys, lay, tgt))
+        caches.append(cache)
+    return st, descs, caches, n_chunks * S * L
+
+
+def finish_ms(d):
+    t = d.layer_times().astype(np.int64)
+    return (t[-1] - t[0]) / 1e6
+
+
+def test_wdrr_work_conserving_shares():
+    """Unpaced WDRR over a saturated link (HBM here) with weights 1:3 and equal payloads: the
+    heavy request gets 3/4 of the bandwidth until it finishes, so its finish time is (4/3)/2 = 2/3
+    of the light request's."""
+    st, descs, caches, W = big_pair(1024)                        # 2 x 2 GiB
+    b = oc.Batch(descs)
+    s = torch.cuda.Stream()
+    for _ in range(2):
+        b.fetch(s, wdrr_weights=[1.0, 3.0])
+        s.synchronize()
+    ratio = finish_ms(descs[1]) / finish_ms(descs[0])
+    assert 0.6 < ratio < 0.74, ratio
+    b.close()
+    st.close()
+
+
+def test_wdrr_hold_rates():
+    """hold_rates: request i is delivered at weights[i] bytes/s (Alg. A2 line 6): the last layer
+    of a request lands at about W / r_i (the last entry's release plus one entry's copy)."""
+    st, descs, caches, W = big_pair(256)                          # 2 x 512 MiB
+    rates = [50e9, 150e9]
+    b = oc.Batch(descs)
+    s = torch.cuda.Stream()
+    b.fetch(s, wdrr_weights=rates, hold_rates=True)
+    s.synchronize()
+    for d, r in zip(descs, rates):
+        want = W / r * 1e3
+        assert abs(finish_ms(d) - want) < 0.05 * want + 0.2, (finish_ms(d), want)
+    b.close()
+    st.close()

@@ -28,14 +28,15 @@ def make_requests(lay, st, specs):
     return out
 
 
-def test_pool_epochs_rates_and_bytes():
+@pytest.mark.parametrize("dispatch", [oc.DISPATCH_INDEPENDENT, oc.DISPATCH_WDRR])
+def test_pool_epochs_rates_and_bytes(dispatch):
     lay = OLayout(4, 2, 64, 2, 16)
     S = chunk_layer_bytes(lay)
     with oc.Store(lay, capacity=64) as st:
         rs = make_requests(lay, st, [(1, 8), (2, 16), (3, 4)])
         c = [2e-3, 1e-3, 3e-3]                                        # compute windows (s/layer)
         cap = 0.6 * sum(r["s"] / ci for r, ci in zip(rs, c))         # oversubscribed: rates are cut
-        pool = oc.TenantPool("stall_opt", cap)
+        pool = oc.TenantPool("stall_opt", cap, dispatch=dispatch)
         t0 = pool.submit(rs[0]["d"], c[0], rs[0]["stream"])
         t1 = pool.submit(rs[1]["d"], c[1], rs[1]["stream"])
         assert pool.status(t0)[0] == oc.TENANT_WAITING
@@ -90,6 +91,7 @@ def test_pool_errors():
     with pytest.raises(oc.ObjcacheError):
         oc.TenantPool("equal", 1e9, -1.0)
     pool = oc.TenantPool("equal", 1e9)
+    assert oc._lib.oc_pool_set_dispatch(pool._h, 7) == oc.OC_EINVAL
     with pytest.raises(oc.ObjcacheError) as e:
         pool.status(3)
     assert e.value.code == oc.OC_ERANGE

@@ -1,0 +1,71 @@
+"""The library's WDRR claim order (oc_wdrr_plan, host code; Alg. A2 lines 6-7) against the oracle:
+identical entries and release times on random batches, ragged units included."""
+import random
+import time
+
+import numpy as np
+import pytest
+
+import paper_2605_22850_b200 as oc
+from oracle import dispatch as dp
+
+
+def lib_plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=0, hold=False):
+    req, first, cnt, rel = oc.wdrr_plan([n * L * tiles for n in n_chunks], tile_bytes, weights,
+                                        quantum_bytes=Q, entry_units=E, hold_rates=hold)
+    return list(zip(req.tolist(), first.tolist(), cnt.tolist())), rel.tolist()
+
+
+def test_random_batches_match_oracle():
+    rng = random.Random(2605)
+    for case in range(120):
+        n = rng.randint(1, 6)
+        L = rng.randint(1, 4)
+        tiles = rng.randint(1, 3)
+        tile_bytes = [rng.choice([2048, 16384, 32768]) for _ in range(tiles)]
+        n_chunks = [rng.randint(0, 12) for _ in range(n)]
+        if sum(n_chunks) == 0:
+            n_chunks[0] = 1
+        weights = [rng.choice([1.0, 2.0, 3.7, 0.5, 12.25]) * 1e9 for _ in range(n)]
+        Q = rng.choice([0, max(tile_bytes), 3 * max(tile_bytes) + 5])
+        E = rng.choice([0, 1, 3, 8])
+        hold = rng.random() < 0.5
+        got, rel = lib_plan(n_chunks, L, tiles, tile_bytes, weights, Q, E, hold)
+        want, wrel = dp.plan(n_chunks, L, tiles, tile_bytes, weights, Q=Q, E=E or 8,
+                             rates=weights if hold else None)
+        assert got == want, case
+        assert rel == (wrel if hold else [0] * len(want)), case
+
+
+def test_errors():
+    with pytest.raises(oc.ObjcacheError) as e:
+        oc.wdrr_plan([4, 4], [32768], [1.0, 0.0])
+    assert e.value.code == oc.OC_EINVAL
+    with pytest.raises(oc.ObjcacheError) as e:
+        oc.wdrr_plan([4], [32768], [1.0], quantum_bytes=4096)       # Q below the largest unit
+    assert e.value.code == oc.OC_EINVAL
+    with pytest.raises(oc.ObjcacheError) as e:                     # 2^32 us of release time
+        oc.wdrr_plan([1 << 20], [32768], [1.0], hold_rates=True)
+    assert e.value.code == oc.OC_ERANGE
+    with pytest.raises(ValueError):
+        oc.wdrr_plan([4, 4], [32768], [1.0])
+
+
+def test_config4_scale():
+    """BASELINE config 4 (70B layout, 16 x 32K at 50% / 87.5% hit, 32 KiB units): the plan of the
+    whole epoch is host work before layer 0, so it must be cheap; every unit appears once, in
+    per-request order, and the first round gives each request its quantum."""
+    n_chunks = [1024 if i % 2 == 0 else 1792 for i in range(16)]
+    n_units = [n * 80 * 2 for n in n_chunks]
+    rates = [(n * 65536) / 0.03 for n in n_chunks]
+    t = time.perf_counter()
+    req, first, cnt, rel = oc.wdrr_plan(n_units, [32768, 32768], rates, hold_rates=True)
+    dt = time.perf_counter() - t
+    assert dt < 0.5, dt
+    for i in range(16):
+        m = req == i
+        f, c = first[m].astype(np.int64), cnt[m].astype(np.int64)
+        assert f[0] == 0 and np.all(f[1:] == f[:-1] + c[:-1]) and f[-1] + c[-1] == n_units[i]
+    assert np.all(np.diff(rel.astype(np.int64)) >= 0)
+    # round 1: the light requests send Q = 256 KiB (8 units), the heavy ones 1792/1024 x that
+    assert cnt[0] == 8 and req[0] == 0
