@@ -1166,6 +1166,8 @@ def batch_leg(args, oc, torch, dev, lay_t):
     res = {"requests": f"{n4} x 4K + {n64} x 64K (families: {fam4} x 4K, {fam64} x 64K)",
            "bytes_rw": total_bytes,
            "batched_one_launch": timed(lambda a: batch.fetch(s0)),
+           # WDRR claim order (Alg. A2 line 7), weights = each request's bytes (equal finish times)
+           "batched_wdrr_by_size": timed(lambda a: batch.fetch(s0, wdrr_weights=[float(n) for _, _, n in reqs])),
            "per_request_one_stream": timed(lambda a: [d.fetch_layerwise(s0) for d in descs]),
            "per_request_own_streams": timed(lambda a: [(st.wait_event(a), d.fetch_layerwise(st))
                                                        for d, st in zip(descs, streams)])}
@@ -1259,8 +1261,12 @@ def sched_leg(args, oc, torch, dev, lay_t):
             reqs.append({"cell": label, "N": N, "s": N * S, "c": c, "d": d, "cache": cache,
                          "copy": torch.cuda.Stream(device=dev), "cons": torch.cuda.Stream(device=dev)})
 
-        def run(rates):
-            """All requests concurrently; rates None = unpaced.  Returns TTFT per request (ms)."""
+        batch = oc.Batch([r["d"] for r in reqs])
+
+        def run(rates, dispatch="independent"):
+            """All requests concurrently; rates None = unpaced.  dispatch "independent": one fetch per
+            request paced by its own kernel (a10); "wdrr": one batched launch in WDRR order with
+            every request held at its rate (Alg. A2 lines 6-7).  Returns TTFT per request (ms)."""
             torch.cuda.synchronize()
             start = torch.cuda.Event(enable_timing=True)
             start.record(torch.cuda.current_stream())
@@ -1268,8 +1274,11 @@ def sched_leg(args, oc, torch, dev, lay_t):
             for r in reqs:
                 r["copy"].wait_event(start)
                 r["cons"].wait_event(start)
-            for i, r in enumerate(reqs):
-                r["d"].fetch_layerwise(r["copy"], pace_Bps=0.0 if rates is None else float(rates[i]))
+            if dispatch == "wdrr":
+                batch.fetch(reqs[0]["copy"], wdrr_weights=[float(x) for x in rates], hold_rates=True)
+            else:
+                for i, r in enumerate(reqs):
+                    r["d"].fetch_layerwise(r["copy"], pace_Bps=0.0 if rates is None else float(rates[i]))
             for l in range(L):                              # enqueue layer by layer across requests
                 for r in reqs:
                     r["d"].wait_layer(l, r["cons"])
@@ -1294,15 +1303,24 @@ def sched_leg(args, oc, torch, dev, lay_t):
             ttft = run(rates)
             # Eq. 3 with uniform X = s/r and C = c: added = X + (L-1) max(0, X - C)
             model = [s / r + (L - 1) * max(0.0, s / r - c) for s, c, r in zip(s_i, c_i, rates)]
+            ttft_w = run(rates, "wdrr")
             res["policies"][pol] = {"rates_gbps": [round(r / GB, 2) for r in rates],
                                     "ttft_ms": [round(x, 1) for x in ttft],
                                     "dttft_ms": round(sum(t - b for t, b in zip(ttft, base)), 1),
+                                    "wdrr_ttft_ms": [round(x, 1) for x in ttft_w],
+                                    "wdrr_dttft_ms": round(sum(t - b for t, b in zip(ttft_w, base)), 1),
                                     "model_dttft_ms": round(sum(model) * 1e3, 1)}
         res["equal_over_cal"] = round(res["policies"]["equal"]["dttft_ms"] /
                                       max(1e-9, res["policies"]["cal_stall_opt"]["dttft_ms"]), 3)
         res["equal_over_stall_opt"] = round(res["policies"]["equal"]["dttft_ms"] /
                                             max(1e-9, res["policies"]["stall_opt"]["dttft_ms"]), 3)
+        res["wdrr_equal_over_cal"] = round(res["policies"]["equal"]["wdrr_dttft_ms"] /
+                                           max(1e-9, res["policies"]["cal_stall_opt"]["wdrr_dttft_ms"]), 3)
+        res["dispatch"] = ("dttft_ms: one fetch per request, each paced by its own kernel; wdrr_dttft_ms: "
+                           "one batched launch in WDRR claim order, requests held at their rates "
+                           "(Alg. A2 lines 6-7)")
         out[wl] = res
+        batch.close()
         for r in reqs:
             r["d"].close()
         del reqs
