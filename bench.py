@@ -1141,6 +1141,7 @@ def batch_leg(args, oc, torch, dev, lay_t):
     descs = [r[0] for r in reqs]
     total_bytes = sum(2 * n * S * L for _, _, n in reqs)
     batch = oc.Batch(descs)
+    batch_pos = oc.Batch(descs, order=oc.BATCH_BY_POSITION)
     s0 = torch.cuda.Stream(device=dev)
     streams = [torch.cuda.Stream(device=dev) for _ in descs]
 
@@ -1166,12 +1167,16 @@ def batch_leg(args, oc, torch, dev, lay_t):
     res = {"requests": f"{n4} x 4K + {n64} x 64K (families: {fam4} x 4K, {fam64} x 64K)",
            "bytes_rw": total_bytes,
            "batched_one_launch": timed(lambda a: batch.fetch(s0)),
+           # position-major inside each layer: members sharing a family prefix read each shared
+           # slice together (HBM once, L2 for the rest)
+           "batched_by_position": timed(lambda a: batch_pos.fetch(s0)),
            # WDRR claim order (Alg. A2 line 7), weights = each request's bytes (equal finish times)
            "batched_wdrr_by_size": timed(lambda a: batch.fetch(s0, wdrr_weights=[float(n) for _, _, n in reqs])),
            "per_request_one_stream": timed(lambda a: [d.fetch_layerwise(s0) for d in descs]),
            "per_request_own_streams": timed(lambda a: [(st.wait_event(a), d.fetch_layerwise(st))
                                                        for d, st in zip(descs, streams)])}
     batch.close()
+    batch_pos.close()
     for d, _, _ in reqs:
         d.close()
     del reqs

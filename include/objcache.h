@@ -247,6 +247,17 @@ OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out);
 OC_API int oc_fetch_batch(oc_batch* batch, const oc_fetch_opts* opts, void* copy_stream);
 OC_API int oc_batch_free(oc_batch* batch);
 
+/* Order of a batch's units inside each layer (oc_fetch_batch; every order is layer-major, so every
+ * request's layers arrive in order):
+ *   BY_REQUEST  (default) request 0's units of layer l, then request 1's, ...;
+ *   BY_POSITION chunk position j of every member holding one (tile by tile, members in order of
+ *               decreasing N), then position j+1.  Members that share a prefix -- the same chunk
+ *               at the same position -- read each shared slice at the same moment, so HBM serves
+ *               it once and the other reads hit L2; a member's layer l completes only when the
+ *               longest member's layer l does. */
+enum { OC_BATCH_BY_REQUEST = 0, OC_BATCH_BY_POSITION = 1 };
+OC_API int oc_batch_set_order(oc_batch* batch, int order);
+
 /* Weighted deficit round robin dispatch (Alg. A2 lines 6-7: "Hold per-request
  * rates stable for this epoch. Dispatch layer payloads with weighted deficit round robin.").
  * The batch's requests become one claim order: each request's copy units in layer-major order

@@ -34,6 +34,7 @@ TARGET_PAGED, TARGET_FLAT = 0, 1
 FETCH_PERSISTENT, FETCH_PER_LAYER = 0, 1
 TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
+BATCH_BY_REQUEST, BATCH_BY_POSITION = 0, 1
 COPY_LDST, COPY_BULK = 0, 1
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
@@ -96,6 +97,7 @@ _SIGS = {
     "oc_batch_create": [ctypes.POINTER(_vp), ctypes.c_uint32, ctypes.POINTER(_vp)],
     "oc_fetch_batch": [_vp, ctypes.POINTER(CFetchOpts), _vp],
     "oc_batch_free": [_vp],
+    "oc_batch_set_order": [_vp, ctypes.c_int],
     "oc_fetch_batch_wdrr": [_vp, ctypes.POINTER(CFetchOpts), ctypes.POINTER(CWdrrOpts), _vp],
     "oc_wdrr_plan": [c_u64p, ctypes.c_uint32, c_u32p, ctypes.c_uint32, ctypes.POINTER(CWdrrOpts), c_u32p, c_u32p,
                      c_u32p, c_u32p, ctypes.c_uint64, c_u64p],
@@ -428,12 +430,17 @@ def build_descriptor(store: Store, keys, layout, target, delivery: int = DELIVER
 class Batch:
     """Several descriptors fetched by one launch (layer-major across the batch)."""
 
-    def __init__(self, descs: Sequence[Descriptor]):
+    def __init__(self, descs: Sequence[Descriptor], order: int = BATCH_BY_REQUEST):
         self.descs = list(descs)
         arr = (_vp * len(self.descs))(*[d._h for d in self.descs])
         h = _vp()
         _check(_lib.oc_batch_create(arr, len(self.descs), ctypes.byref(h)))
         self._h = h
+        if order != BATCH_BY_REQUEST:
+            _check(_lib.oc_batch_set_order(h, int(order)))
+
+    def set_order(self, order: int):
+        _check(_lib.oc_batch_set_order(self._h, int(order)))
 
     def fetch(self, stream=None, max_ctas=0, unit_bytes=0, wdrr_weights=None, quantum_bytes=0, entry_units=0,
               hold_rates=False):

@@ -330,7 +330,11 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 //   kWdrr    several descriptors; the claim order is a table of entries (request, first unit,
 //            count, release us) built by weighted deficit round robin (dispatch.cpp; Alg. A2
 //            lines 6-7), each request's units still in its own layer-major order.
-enum { kSingle = 0, kBatch = 1, kWdrr = 2 };
+//   kByPos   several descriptors, layer-major, and inside a layer position-major: chunk position
+//            j of every request holding one, tile by tile, before position j+1.  Requests that
+//            share a prefix (same chunk at the same position) then read each shared slice at the
+//            same moment, so HBM serves it once and the duplicates hit L2.
+enum { kSingle = 0, kBatch = 1, kWdrr = 2, kByPos = 3 };
 
 struct BatchArgs {
     const DevDesc* descs;  // [n] device copies of the requests' descriptors
@@ -342,6 +346,15 @@ struct BatchArgs {
     uint32_t upl_total;    // cum[n]
     uint32_t paced;        // kWdrr: entries carry release times
     FastDiv div_upl_total;
+    // kByPos: members sorted by N (descending) into runs of positions with a constant number of
+    // members: seg_cum[k] = units of a layer before run k, seg_pos[k] = its first position,
+    // seg_cnt[k] = members holding those positions (the first seg_cnt[k] of `sorted`)
+    const uint32_t* seg_cum;  // [nseg + 1]
+    const uint32_t* seg_pos;  // [nseg]
+    const uint32_t* seg_cnt;  // [nseg]
+    const uint32_t* sorted;   // [n] member indices, N descending
+    uint32_t nseg;
+    uint32_t tiles;           // units per chunk-layer slice (the same for every member)
 };
 
 struct Resolved {
@@ -355,6 +368,23 @@ __device__ __forceinline__ Resolved resolve(const DevDesc& d0, const BatchArgs& 
     if (MODE == kSingle) return {&d0, g, 0u};
     const uint32_t layer = fdiv(g, ba.div_upl_total);
     const uint32_t rem = g - layer * ba.upl_total;
+    if (MODE == kByPos) {
+        uint32_t lo = 0, hi = ba.nseg;  // largest k with seg_cum[k] <= rem
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&ba.seg_cum[mid]) <= rem) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t cnt = __ldg(&ba.seg_cnt[lo]);
+        const uint32_t o = rem - __ldg(&ba.seg_cum[lo]);
+        const uint32_t per_pos = cnt * ba.tiles;  // units of one position across its members
+        const uint32_t jj = o / per_pos;
+        const uint32_t rest = o - jj * per_pos;
+        const uint32_t tile = rest / cnt;        // tile-major, member-minor: equal sources adjacent
+        const uint32_t req = __ldg(&ba.sorted[rest - tile * cnt]);
+        const DevDesc* d = &ba.descs[req];
+        return {d, layer * d->units_per_layer + (__ldg(&ba.seg_pos[lo]) + jj) * ba.tiles + tile, req};
+    }
     uint32_t lo = 0, hi = ba.n;  // largest r with cum[r] <= rem
     while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -623,8 +653,10 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         // retired as soon as its stores complete, so the layer is announced promptly.  Inside a
         // layer at most 8 units stay unretired -- a small copy-CTA budget (a CTA owning many
         // units per layer) keeps 4-8 units of stores in flight instead of waiting on each.
+        // kByPos changes request at every unit, but a member's layer completes only at the end of
+        // the layer: there only a layer change is a boundary.
         const uint32_t gn = s_unit[(k + 1) % 32];  // claimed already: claims run stages-1 ahead
-        bool boundary = gn == kEnd || s_req[(k + 1) % 32] != s_req[k % 32];
+        bool boundary = gn == kEnd || (MODE != kByPos && s_req[(k + 1) % 32] != s_req[k % 32]);
         if (!boundary)
             boundary = fdiv(gn, desc_of(k + 1).div_upl) != fdiv(g, d.div_upl);
         if (boundary) {
@@ -942,7 +974,8 @@ struct Batch {
     std::vector<Desc*> descs;
     int device = 0;
     uint32_t n = 0;
-    size_t upload_bytes = 0;   // DevDesc[n] | cum[n+1]
+    size_t upload_bytes = 0;   // DevDesc[n] | cum[n+1] | seg_cum[n+1] | seg_pos[n] | seg_cnt[n] | sorted[n]
+    int order = OC_BATCH_BY_REQUEST;
     void* dev = nullptr;       // upload area + claim counter
     uint64_t dev_class = 0;
     void* stage = nullptr;     // pinned staging of the upload area
@@ -990,6 +1023,10 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
     OC_CUDA(cudaEventSynchronize(b->staged));  // previous upload done with the staging buffers
     DevDesc* st = (DevDesc*)b->stage;
     uint32_t* cum = (uint32_t*)((uint8_t*)b->stage + sizeof(DevDesc) * b->n);
+    uint32_t* seg_cum = cum + (b->n + 1);
+    uint32_t* seg_pos = seg_cum + (b->n + 1);
+    uint32_t* seg_cnt = seg_pos + b->n;
+    uint32_t* sorted = seg_cnt + b->n;
     uint64_t host_chunks = 0, chunks = 0, total = 0;
     cum[0] = 0;
     for (uint32_t i = 0; i < b->n; i++) {
@@ -1012,6 +1049,27 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
     }
     const uint32_t L = b->descs[0]->geo.L;
     if (total * L >= (1ull << 32)) return fail(OC_ERANGE, "fetch_batch: too many units in one batch");
+    // By position: members sorted by N descending; run k holds the positions where exactly
+    // seg_cnt[k] members still have a chunk
+    uint32_t nseg = 0;
+    const bool by_pos = !wdrr && b->order == OC_BATCH_BY_POSITION;
+    if (by_pos) {
+        for (uint32_t i = 0; i < b->n; i++) sorted[i] = i;
+        std::stable_sort(sorted, sorted + b->n, [&](uint32_t x, uint32_t y) { return b->descs[x]->N > b->descs[y]->N; });
+        const uint32_t tiles = b->descs[0]->dd.tiles;
+        seg_cum[0] = 0;
+        for (uint32_t cnt = b->n; cnt >= 1; cnt--) {
+            const uint64_t p0 = cnt == b->n ? 0 : b->descs[sorted[cnt]]->N;
+            const uint64_t p1 = b->descs[sorted[cnt - 1]]->N;
+            if (p1 <= p0) continue;
+            seg_pos[nseg] = (uint32_t)p0;
+            seg_cnt[nseg] = cnt;
+            seg_cum[nseg + 1] = seg_cum[nseg] + (uint32_t)((p1 - p0) * cnt * tiles);
+            nseg++;
+        }
+        for (Desc* d : b->descs)
+            if (d->dd.tiles != tiles) return fail(OC_EINVAL, "fetch_batch: members planned with different units");
+    }
     // WDRR: the claim order (Alg. A2 line 7), uploaded behind a zeroed start-time slot
     uint64_t n_claims = total * L;  // claim items of the launch: units, or WDRR entries
     if (wdrr) {
@@ -1057,11 +1115,24 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
     ba.ents = wdrr ? (const uint4*)((uint8_t*)b->ent_dev + 16) : nullptr;
     ba.t0_slot = wdrr ? (unsigned long long*)b->ent_dev : nullptr;
     ba.paced = wdrr && wdrr->hold_rates ? 1u : 0u;
+    {
+        const uint32_t* dcum = ba.cum + (b->n + 1);
+        ba.seg_cum = dcum;
+        ba.seg_pos = dcum + (b->n + 1);
+        ba.seg_cnt = ba.seg_pos + b->n;
+        ba.sorted = ba.seg_cnt + b->n;
+        ba.nseg = nseg;
+        ba.tiles = b->descs[0]->dd.tiles;
+    }
     if (p.stages < 2) return fail(OC_ENOTSUP, "fetch_batch: two units do not fit in shared memory");
     if (wdrr) {
         OC_CUDA(set_bulk_smem<kWdrr>(p.smem));
         fetch_bulk_kernel<kWdrr><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
                                                                      b->grab_ctr, p.stages, p.stage_bytes);
+    } else if (by_pos) {
+        OC_CUDA(set_bulk_smem<kByPos>(p.smem));
+        fetch_bulk_kernel<kByPos><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
+                                                                      b->grab_ctr, p.stages, p.stage_bytes);
     } else {
         OC_CUDA(set_bulk_smem<kBatch>(p.smem));
         fetch_bulk_kernel<kBatch><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
@@ -1109,7 +1180,7 @@ OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out) {
     }
     b->n = n;
     b->device = b->descs[0]->device;
-    b->upload_bytes = sizeof(oc::DevDesc) * n + 4 * (n + 1);
+    b->upload_bytes = sizeof(oc::DevDesc) * n + 4 * (n + 1) * 2 + 4 * n * 3;
     const size_t dev_bytes = ((b->upload_bytes + 15) & ~size_t(15)) + 16;
     oc::DeviceGuard dg(b->device);
     b->dev = oc::dev_pool_alloc(b->device, dev_bytes, &b->dev_class);
@@ -1138,6 +1209,14 @@ OC_API int oc_fetch_batch(oc_batch* h, const oc_fetch_opts* opts, void* stream) 
     o.engine = OC_COPY_BULK;
     if (opts) o = *opts;
     return oc::fetch_batch((oc::Batch*)h, o, nullptr, (cudaStream_t)stream);
+}
+
+OC_API int oc_batch_set_order(oc_batch* h, int order) {
+    if (!h) return oc::fail(OC_EINVAL, "batch_set_order: null batch");
+    if (order != OC_BATCH_BY_REQUEST && order != OC_BATCH_BY_POSITION)
+        return oc::fail(OC_EINVAL, "batch_set_order: unknown order");
+    ((oc::Batch*)h)->order = order;
+    return OC_OK;
 }
 
 OC_API int oc_fetch_batch_wdrr(oc_batch* h, const oc_fetch_opts* opts, const oc_wdrr_opts* wdrr, void* stream) {

@@ -28,6 +28,9 @@ for kind in ("nhd", "hnd"):
                     b = oc.Batch([d])
                     b.fetch(s)
                     d.sync_layer(1)
+                    b.fetch(s, wdrr_weights=[1e9], hold_rates=True, entry_units=3)   # WDRR order
+                    d.sync_layer(1)
+                    assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 3, req, dest))
                     b.close()
                     src = make_dest(lay, 5, kind, Bs=8, first_token=3, seed=1)
                     st2 = oc.Store(lay, capacity=8)
@@ -67,5 +70,26 @@ with oc.Store(lay, capacity=8) as st:
         assert np.array_equal(b0.cpu().numpy(), oracle_result(lay, 4, req, de0))
         d0.close()
         ok += 1
+# a WDRR batch of three requests with uneven weights and held rates
+with oc.Store(lay, capacity=24) as st:
+    items = []
+    for seed, n in ((5, 3), (6, 7), (7, 2)):
+        r = requests_family(lay, seed, 0, [n])[0]
+        k = oc.chunk_keys(r.tokens, 16)
+        st.put_chunks(k, payload_stack(lay, seed, r.payload_ids))
+        dest = make_dest(lay, n, "nhd", Bs=16, seed=seed)
+        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        items.append((seed, r, dest, buf, oc.build_descriptor(st, k, lay, lib_target(oc, dest, buf.data_ptr()))))
+    b = oc.Batch([it[4] for it in items])
+    s = torch.cuda.Stream()
+    for hold in (False, True):
+        b.fetch(s, unit_bytes=1024, wdrr_weights=[1e9, 3e9, 0.5e9], quantum_bytes=1024, hold_rates=hold)
+        for it in items:
+            it[4].sync_layer(1)
+            assert np.array_equal(it[3].cpu().numpy(), oracle_result(lay, it[0], it[1], it[2]))
+            ok += 1
+    b.close()
+    for it in items:
+        it[4].close()
 torch.cuda.synchronize()
 print("sanitize workload ok", ok)

@@ -39,10 +39,11 @@ SPECS = [(1, 3, "nhd", 16, 0), (2, 7, "hnd", 8, 5), (3, 1, "flat", 16, 0), (4, 1
 
 
 @pytest.mark.parametrize("lay", [OLayout(3, 2, 64, 2, 16), OLayout(2, 4, 32, 2, 20)])
-@pytest.mark.parametrize("unit_bytes", [0, 1024])
-def test_batch_parity(lay, unit_bytes):
+@pytest.mark.parametrize("unit_bytes", [0, 1024, 3072])
+@pytest.mark.parametrize("order", [oc.BATCH_BY_REQUEST, oc.BATCH_BY_POSITION])
+def test_batch_parity(lay, unit_bytes, order):
     st, items = setup_batch(lay, SPECS)
-    b = oc.Batch([it["desc"] for it in items])
+    b = oc.Batch([it["desc"] for it in items], order=order)
     s = torch.cuda.Stream()
     b.fetch(s, unit_bytes=unit_bytes)
     for it in items:
@@ -247,3 +248,31 @@ def test_wdrr_hold_rates():
         assert abs(finish_ms(d) - want) < 0.05 * want + 0.2, (finish_ms(d), want)
     b.close()
     st.close()
+
+
+@pytest.mark.parametrize("order", [oc.BATCH_BY_REQUEST, oc.BATCH_BY_POSITION])
+def test_batch_shared_prefix_family(order):
+    """Requests of one prefix family (8 shared chunks, then own chunks; one request is the bare
+    shared prefix) through one store: every member's bytes as the oracle, both orders, refetched."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    reqs = requests_family(lay, 21, 8, [2, 0, 5, 3])
+    with oc.Store(lay, capacity=64) as st:
+        items = []
+        for i, req in enumerate(reqs):
+            keys = oc.chunk_keys(req.tokens, lay.chunk_tokens)
+            st.put_chunks(keys, payload_stack(lay, 21, req.payload_ids))
+            dest = make_dest(lay, req.n_chunks, "nhd" if i % 2 else "hnd", Bs=8, first_token=i, seed=40 + i)
+            buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+            desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+            items.append({"seed": 21, "req": req, "dest": dest, "buf": buf, "desc": desc})
+        b = oc.Batch([it["desc"] for it in items], order=order)
+        s = torch.cuda.Stream()
+        for rnd in range(3):
+            with torch.cuda.stream(s):
+                for it in items:
+                    it["buf"].fill_(0xA5)
+            b.fetch(s, max_ctas=2 if rnd == 1 else 0, unit_bytes=1024 if rnd == 2 else 0)
+            s.synchronize()
+            check(lay, items)
+        b.close()
+        assert oc._lib.oc_batch_set_order(None, 1) == oc.OC_EINVAL
