@@ -6,11 +6,12 @@ import numpy as np
 import torch
 import paper_2605_22850_b200 as oc
 from oracle.geometry import Layout
-from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family
+from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer
 
 lay = Layout(2, 2, 64, 2, 16)
 ok = 0
-for kind in ("nhd", "hnd"):
+SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3").split(",")
+for kind in (("nhd", "hnd") if "1" in SECTIONS else ()):
     for engine in (oc.COPY_BULK, oc.COPY_LDST):
         for mode in (oc.FETCH_PERSISTENT, oc.FETCH_PER_LAYER):
             req = requests_family(lay, 3, 0, [5])[0]
@@ -18,7 +19,7 @@ for kind in ("nhd", "hnd"):
                 keys = oc.chunk_keys(req.tokens, 16)
                 st.put_chunks(keys, payload_stack(lay, 3, req.payload_ids))
                 dest = make_dest(lay, 5, kind, Bs=8, first_token=3, seed=1)
-                buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+                buf = sentinel_buffer(dest.size)
                 d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
                 s = torch.cuda.Stream()
                 d.fetch_layerwise(s, engine=engine, mode=mode, unit_bytes=1024)
@@ -43,53 +44,65 @@ for kind in ("nhd", "hnd"):
 # with a consumer that waits on its last layer and runs a compute-window spin
 req = requests_family(lay, 4, 0, [6])[0]
 with oc.Store(lay, capacity=8) as st:
-    keys = oc.chunk_keys(req.tokens, 16)
-    st.put_chunks(keys, payload_stack(lay, 4, req.payload_ids))
-    streams = [torch.cuda.Stream() for _ in range(4)]
-    cons = torch.cuda.Stream()
-    stamps = torch.zeros(2, dtype=torch.int64, device="cuda")
-    live = []
-    for i in range(12):
-        dest = make_dest(lay, 6, "nhd", Bs=16, seed=10 + i)
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
-        d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
-        s = streams[i % 4]
-        s.wait_stream(torch.cuda.current_stream())
-        d.fetch_layerwise(s)
-        d.wait_layer(1, cons)
-        oc.emulate_compute(1000, cons, stamps)
-        live.append((d, buf, dest))
-        if len(live) > 4:
-            d0, b0, de0 = live.pop(0)
-            d0.sync_layer(1)
-            assert np.array_equal(b0.cpu().numpy(), oracle_result(lay, 4, req, de0))
-            d0.close()
-            ok += 1
-    for d0, b0, de0 in live:
-        d0.sync_layer(1)
-        assert np.array_equal(b0.cpu().numpy(), oracle_result(lay, 4, req, de0))
-        d0.close()
-        ok += 1
+  if "2" in SECTIONS:
+      keys = oc.chunk_keys(req.tokens, 16)
+      st.put_chunks(keys, payload_stack(lay, 4, req.payload_ids))
+      streams = [torch.cuda.Stream() for _ in range(4)]
+      cons = torch.cuda.Stream()
+      stamps = torch.zeros(2, dtype=torch.int64, device="cuda")
+      live = []
+      for i in range(12):
+          dest = make_dest(lay, 6, "nhd", Bs=16, seed=10 + i)
+          buf = sentinel_buffer(dest.size)
+          d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+          s = streams[i % 4]
+          s.wait_stream(torch.cuda.current_stream())
+          d.fetch_layerwise(s)
+          d.wait_layer(1, cons)
+          oc.emulate_compute(1000, cons, stamps)
+          live.append((d, buf, dest))
+          if len(live) > 4:
+              d0, b0, de0 = live.pop(0)
+              d0.sync_layer(1)
+              assert np.array_equal(b0.cpu().numpy(), oracle_result(lay, 4, req, de0))
+              d0.close()
+              ok += 1
+      for d0, b0, de0 in live:
+          d0.sync_layer(1)
+          assert np.array_equal(b0.cpu().numpy(), oracle_result(lay, 4, req, de0))
+          d0.close()
+          ok += 1
 # a WDRR batch of three requests with uneven weights and held rates
 with oc.Store(lay, capacity=24) as st:
-    items = []
-    for seed, n in ((5, 3), (6, 7), (7, 2)):
-        r = requests_family(lay, seed, 0, [n])[0]
-        k = oc.chunk_keys(r.tokens, 16)
-        st.put_chunks(k, payload_stack(lay, seed, r.payload_ids))
-        dest = make_dest(lay, n, "nhd", Bs=16, seed=seed)
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
-        items.append((seed, r, dest, buf, oc.build_descriptor(st, k, lay, lib_target(oc, dest, buf.data_ptr()))))
-    b = oc.Batch([it[4] for it in items])
-    s = torch.cuda.Stream()
-    for hold in (False, True):
-        b.fetch(s, unit_bytes=1024, wdrr_weights=[1e9, 3e9, 0.5e9], quantum_bytes=1024, hold_rates=hold)
-        for it in items:
-            it[4].sync_layer(1)
-            assert np.array_equal(it[3].cpu().numpy(), oracle_result(lay, it[0], it[1], it[2]))
-            ok += 1
-    b.close()
-    for it in items:
-        it[4].close()
+  if "3" in SECTIONS:
+      items = []
+      for seed, n in ((5, 3), (6, 7), (7, 2)):
+          r = requests_family(lay, seed, 0, [n])[0]
+          k = oc.chunk_keys(r.tokens, 16)
+          st.put_chunks(k, payload_stack(lay, seed, r.payload_ids))
+          dest = make_dest(lay, n, "nhd", Bs=16, seed=seed)
+          buf = sentinel_buffer(dest.size)
+          items.append((seed, r, dest, buf, oc.build_descriptor(st, k, lay, lib_target(oc, dest, buf.data_ptr()))))
+      b = oc.Batch([it[4] for it in items])
+      s = torch.cuda.Stream()
+      s.wait_stream(torch.cuda.current_stream())  # the sentinel fills are on the current stream
+      for hold in (False, True):
+          b.fetch(s, unit_bytes=1024, wdrr_weights=[1e9, 3e9, 0.5e9], quantum_bytes=1024, hold_rates=hold)
+          for i, it in enumerate(items):
+              it[4].sync_layer(1)
+              want = oracle_result(lay, it[0], it[1], it[2])
+              got = it[3].cpu().numpy()
+              if not np.array_equal(got, want):
+                  diff = np.nonzero(got != want)[0]
+                  torch.cuda.synchronize()
+                  late = np.array_equal(it[3].cpu().numpy(), want)
+                  t = it[4].layer_times().astype(np.int64)
+                  raise AssertionError(f"WDRR hold={hold} request {i}: {len(diff)} bytes differ (first at "
+                                       f"{diff[:4].tolist()}), equal after a device sync: {late}, layer "
+                                       f"times {(t - t[0]).tolist()}")
+              ok += 1
+      b.close()
+      for it in items:
+          it[4].close()
 torch.cuda.synchronize()
 print("sanitize workload ok", ok)

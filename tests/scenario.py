@@ -100,6 +100,16 @@ def oracle_target(dest: Dest):
 
 
 # ---- library side --------------------------------------------------------------------------------
+def sentinel_buffer(size: int, device="cuda"):
+    """A destination buffer of 0xA5 bytes, filled before any later work on ANY stream: the fill runs
+    on torch's current stream, the fetches on the tests' own non-blocking streams, which are not
+    ordered after it."""
+    import torch
+    buf = torch.full((int(size),), 0xA5, dtype=torch.uint8, device=device)
+    torch.cuda.current_stream(buf.device).synchronize()
+    return buf
+
+
 def lib_target(oc, dest: Dest, base: int):
     if dest.kind == "flat":
         return oc.FlatTarget(base + dest.flat_off, dest.flat_cap)

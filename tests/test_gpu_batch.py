@@ -6,7 +6,7 @@ torch = pytest.importorskip("torch")
 
 import paper_2605_22850_b200 as oc  # noqa: E402
 from oracle.geometry import Layout as OLayout  # noqa: E402
-from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family  # noqa: E402
+from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -21,9 +21,10 @@ def setup_batch(lay, specs, tier=oc.TIER_HBM):
         keys = oc.chunk_keys(req.tokens, lay.chunk_tokens)
         st.put_chunks(keys, payload_stack(lay, seed, req.payload_ids))
         dest = make_dest(lay, n, kind, Bs=Bs, first_token=first, seed=seed)
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         desc = oc.build_descriptor(st, st.match_prefix(req.tokens), lay, lib_target(oc, dest, buf.data_ptr()))
         items.append({"seed": seed, "req": req, "dest": dest, "buf": buf, "desc": desc})
+    torch.cuda.synchronize()  # the sentinel fills (current stream) land before fetches on other streams
     return st, items
 
 
@@ -210,6 +211,7 @@ def big_pair(n_chunks):
                              synth.block_table(r, need, need), 0)
         descs.append(oc.build_descriptor(st, keys, lay, tgt))
         caches.append(cache)
+    torch.cuda.synchronize()
     return st, descs, caches, n_chunks * S * L
 
 
@@ -262,9 +264,10 @@ def test_batch_shared_prefix_family(order):
             keys = oc.chunk_keys(req.tokens, lay.chunk_tokens)
             st.put_chunks(keys, payload_stack(lay, 21, req.payload_ids))
             dest = make_dest(lay, req.n_chunks, "nhd" if i % 2 else "hnd", Bs=8, first_token=i, seed=40 + i)
-            buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+            buf = sentinel_buffer(dest.size)
             desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
             items.append({"seed": 21, "req": req, "dest": dest, "buf": buf, "desc": desc})
+        torch.cuda.synchronize()
         b = oc.Batch([it["desc"] for it in items], order=order)
         s = torch.cuda.Stream()
         for rnd in range(3):

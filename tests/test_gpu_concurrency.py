@@ -9,7 +9,7 @@ torch = pytest.importorskip("torch")
 
 import paper_2605_22850_b200 as oc  # noqa: E402
 from oracle.geometry import Layout as OLayout  # noqa: E402
-from scenario import Request, lib_target, make_dest, oracle_result, payload_stack, requests_family  # noqa: E402
+from scenario import Request, lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -40,7 +40,7 @@ def test_streams_of_requests_with_recycled_descriptors(engine):
             req = Request(fams[f].tokens, fams[f].payload_ids, n)
             dest = make_dest(lay, n, "nhd", Bs=int(rng.choice([8, 16, 32])), seed=i)
             want = oracle_result(lay, 900 + f, req, dest)
-            buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+            buf = sentinel_buffer(dest.size)
             d = oc.build_descriptor(st, keys[f][:n], lay, lib_target(oc, dest, buf.data_ptr()))
             s = streams[i % len(streams)]
             s.wait_stream(torch.cuda.current_stream())          # buf's fill happened on the current stream
@@ -76,7 +76,7 @@ def test_consumer_wait_on_fresh_descriptor():
             torch.cuda.synchronize()
             old.close()
             del scratch
-            buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+            buf = sentinel_buffer(dest.size)
             copy_s, cons = torch.cuda.Stream(), torch.cuda.Stream()
             copy_s.wait_stream(torch.cuda.current_stream())
             d = oc.build_descriptor(st, k, lay, lib_target(oc, dest, buf.data_ptr()))

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 def _owner(q, done):
     import paper_2605_22850_b200 as oc
     from oracle.geometry import Layout
-    from scenario import payload_stack, requests_family
+    from scenario import payload_stack, requests_family, sentinel_buffer
     torch.cuda.set_device(0)
     lay = Layout(2, 2, 64, 2, 16)
     req = requests_family(lay, 31, 0, [12])[0]
@@ -48,7 +48,7 @@ def test_export_import_across_processes():
         got_keys = local.match_prefix(req.tokens)
         assert got_keys.shape[0] == 12
         dest = make_dest(lay, 12, "nhd", Bs=16, first_token=4, seed=3)
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         for engine in (oc.COPY_LDST, oc.COPY_BULK):
             buf.fill_(0xA5)
             desc = oc.build_descriptor(local, got_keys, lay, lib_target(oc, dest, buf.data_ptr()))

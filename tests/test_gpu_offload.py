@@ -10,7 +10,7 @@ from oracle.assemble import fetch_layerwise, offload_paged  # noqa: E402
 from oracle.descriptor import FlatTarget as OFlat, build_descriptor as obuild  # noqa: E402
 from oracle.geometry import Layout as OLayout, chunk_layer_bytes  # noqa: E402
 from oracle.store import ChunkStore  # noqa: E402
-from scenario import lib_target, make_dest, oracle_target, requests_family  # noqa: E402
+from scenario import lib_target, make_dest, oracle_target, requests_family, sentinel_buffer  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -35,7 +35,7 @@ def test_offload_then_fetch_flat_matches_oracle(monkeypatch, engine, kind, Bs, f
         assert oc.put_from_paged(st, keys, lay, lib_target(oc, src, cache.data_ptr()), s) == 0   # dedup
         # read the new chunks back through a flat (Alg. A1 client buffer) fetch
         W = N * lay.num_layers * chunk_layer_bytes(lay)
-        flat = torch.full((W,), 0xA5, dtype=torch.uint8, device="cuda")
+        flat = sentinel_buffer(W)
         d = oc.build_descriptor(st, keys, lay, oc.FlatTarget(flat.data_ptr(), W))
         d.fetch_layerwise(s)
         d.sync_layer(lay.num_layers - 1)
@@ -61,7 +61,7 @@ def test_offload_round_trip_into_another_cache(monkeypatch, engine):
     b = make_dest(lay, N, "hnd", Bs=8, first_token=3, seed=2)
     gen = torch.Generator(device="cuda").manual_seed(9)
     cache_a = torch.randint(0, 256, (a.size,), dtype=torch.uint8, device="cuda", generator=gen)
-    cache_b = torch.full((b.size,), 0xA5, dtype=torch.uint8, device="cuda")
+    cache_b = sentinel_buffer(b.size)
     keys = oc.chunk_keys(req.tokens, 16)
     with oc.Store(lay, capacity=N) as st:
         s = torch.cuda.Stream()
@@ -114,7 +114,7 @@ def test_offload_into_pinned_host_store(monkeypatch, engine):
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         assert oc.put_from_paged(st, keys, lay, lib_target(oc, src, cache.data_ptr()), s) == N
-        flat = torch.full((W,), 0xA5, dtype=torch.uint8, device="cuda")
+        flat = sentinel_buffer(W)
         d = oc.build_descriptor(st, keys, lay, oc.FlatTarget(flat.data_ptr(), W))
         d.fetch_layerwise(s)
         d.sync_layer(lay.num_layers - 1)

@@ -13,7 +13,7 @@ import paper_2605_22850_b200 as oc  # noqa: E402
 import synth  # noqa: E402
 from oracle.geometry import Layout as OLayout, chunk_layer_bytes, row_bytes  # noqa: E402
 from scenario import (lib_target, make_dest, oracle_result, payload_stack,  # noqa: E402
-                      requests_family)
+                      requests_family, sentinel_buffer)
 
 pytestmark = pytest.mark.gpu
 
@@ -34,7 +34,7 @@ def run_lib(lay, seed, req, dest, tier=oc.TIER_HBM, mode=oc.FETCH_PERSISTENT, un
         store.put_chunks(keys, payload_stack(lay, seed, req.payload_ids[:req.n_chunks]))
     keys = store.match_prefix(req.tokens)[:req.n_chunks]
     assert keys.shape[0] == req.n_chunks
-    buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+    buf = sentinel_buffer(dest.size)
     desc = oc.build_descriptor(store, keys, lay, lib_target(oc, dest, buf.data_ptr()), delivery)
     s = torch.cuda.Stream()
     desc.fetch_layerwise(s, mode=mode, unit_bytes=unit_bytes, max_ctas=max_ctas, engine=engine)
@@ -188,7 +188,7 @@ def test_llama8b_64k_sampled_layers():
     with oc.Store(lay, capacity=N) as st:
         keys = oc.chunk_keys(req.tokens, 16)
         assert st.put_chunks(keys, pl) == N
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
         desc.fetch_layerwise(torch.cuda.current_stream())
         desc.sync_layer(31)
@@ -218,7 +218,7 @@ def test_llama70b_layout_sampled_layers():
     with oc.Store(lay, capacity=N) as st:
         keys = oc.chunk_keys(req.tokens, 16)
         assert st.put_chunks(keys, payload_stack(lay, 70, req.payload_ids)) == N
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
         desc.fetch_layerwise(torch.cuda.current_stream())
         desc.sync_layer(79)
@@ -245,7 +245,7 @@ def test_wait_layer_orders_consumer(monkeypatch, wait_kernel, engine):
     with oc.Store(lay, capacity=8) as st:
         keys = oc.chunk_keys(req.tokens, 16)
         st.put_chunks(keys, payload_stack(lay, 21, req.payload_ids))
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
         copy_s, cons = torch.cuda.Stream(), torch.cuda.Stream()
         layer_bytes = 8 * chunk_layer_bytes(lay)
@@ -277,7 +277,7 @@ def test_refetch_epochs_and_sync(engine):
     with oc.Store(lay, capacity=8) as st:
         keys = oc.chunk_keys(req.tokens, 16)
         st.put_chunks(keys, payload_stack(lay, 5, req.payload_ids))
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
         s = torch.cuda.Stream()
         for it in range(5):
@@ -309,7 +309,7 @@ def test_errors():
         with pytest.raises(oc.ObjcacheError) as e:
             st.put_chunks(other, payload_stack(lay, 99, [(9, 0), (9, 1)]))
         assert e.value.code == oc.OC_EFULL and e.value.bad_index == 1
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         tgt = lib_target(oc, dest, buf.data_ptr())
         missing = np.concatenate([keys[:2], oc.chunk_keys(synth.tokens(7, 16), 16), keys[2:]])
         with pytest.raises(oc.ObjcacheError) as e:
@@ -366,7 +366,7 @@ def test_alternating_engines_and_unit_sizes_on_one_descriptor():
     with oc.Store(lay, capacity=9) as st:
         keys = oc.chunk_keys(req.tokens, 16)
         st.put_chunks(keys, payload_stack(lay, 12, req.payload_ids))
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         desc = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
         s, cons = torch.cuda.Stream(), torch.cuda.Stream()
         plan = [(oc.COPY_BULK, 0, oc.FETCH_PERSISTENT), (oc.COPY_LDST, 1024, oc.FETCH_PERSISTENT),

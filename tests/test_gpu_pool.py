@@ -9,7 +9,7 @@ torch = pytest.importorskip("torch")
 import paper_2605_22850_b200 as oc  # noqa: E402
 from oracle import scheduler as osch  # noqa: E402
 from oracle.geometry import Layout as OLayout, chunk_layer_bytes  # noqa: E402
-from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family  # noqa: E402
+from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -21,7 +21,7 @@ def make_requests(lay, st, specs):
         keys = oc.chunk_keys(req.tokens, lay.chunk_tokens)
         st.put_chunks(keys, payload_stack(lay, seed, req.payload_ids))
         dest = make_dest(lay, n, "nhd", Bs=16, seed=seed)
-        buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+        buf = sentinel_buffer(dest.size)
         d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
         out.append({"seed": seed, "req": req, "dest": dest, "buf": buf, "d": d, "s": n * chunk_layer_bytes(lay),
                     "stream": torch.cuda.Stream()})

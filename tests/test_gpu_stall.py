@@ -10,7 +10,7 @@ torch = pytest.importorskip("torch")
 import paper_2605_22850_b200 as oc  # noqa: E402
 from oracle import stall as ostall  # noqa: E402
 from oracle.geometry import Layout as OLayout, chunk_layer_bytes  # noqa: E402
-from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family  # noqa: E402
+from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -38,7 +38,7 @@ def _setup(st, lay, seed, n, delivery=oc.DELIVER_LAYER_MAJOR):
     dest = make_dest(lay, n, "nhd", Bs=16, seed=seed)
     keys = oc.chunk_keys(req.tokens, lay.chunk_tokens)
     st.put_chunks(keys, payload_stack(lay, seed, req.payload_ids))
-    buf = torch.full((dest.size,), 0xA5, dtype=torch.uint8, device="cuda")
+    buf = sentinel_buffer(dest.size)
     d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()), delivery)
     return req, dest, buf, d
 
