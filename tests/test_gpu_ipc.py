@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 def _owner(q, done):
     import paper_2605_22850_b200 as oc
     from oracle.geometry import Layout
-    from scenario import payload_stack, requests_family, sentinel_buffer
+    from scenario import payload_stack, requests_family
     torch.cuda.set_device(0)
     lay = Layout(2, 2, 64, 2, 16)
     req = requests_family(lay, 31, 0, [12])[0]
@@ -28,7 +28,7 @@ def _owner(q, done):
 def test_export_import_across_processes():
     import paper_2605_22850_b200 as oc
     from oracle.geometry import Layout
-    from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family
+    from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer
     ctx = mp.get_context("spawn")
     q, done = ctx.Queue(), ctx.Event()
     p = ctx.Process(target=_owner, args=(q, done))
