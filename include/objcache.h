@@ -250,11 +250,12 @@ OC_API int oc_batch_free(oc_batch* batch);
 /* Order of a batch's units inside each layer (oc_fetch_batch; every order is layer-major, so every
  * request's layers arrive in order):
  *   BY_REQUEST  (default) request 0's units of layer l, then request 1's, ...;
- *   BY_POSITION chunk position j of every member holding one (tile by tile, members in order of
- *               decreasing N), then position j+1.  Members that share a prefix -- the same chunk
- *               at the same position -- read each shared slice at the same moment, so HBM serves
- *               it once and the other reads hit L2; a member's layer l completes only when the
- *               longest member's layer l does. */
+ *   BY_POSITION blocks of B consecutive chunk positions (B*S ~ 4 MiB; env OC_BYPOS_BLOCK_KIB):
+ *               block b of every member holding it (members in order of decreasing N, each
+ *               member's B positions tile by tile), then block b+1.  Members that share a prefix
+ *               -- the same chunk at the same position -- re-read each shared slice ~B*S bytes
+ *               after the first read, while L2 still holds it, so HBM serves it once; a member's
+ *               layer l completes only when the longest member's layer l does. */
 enum { OC_BATCH_BY_REQUEST = 0, OC_BATCH_BY_POSITION = 1 };
 OC_API int oc_batch_set_order(oc_batch* batch, int order);
 

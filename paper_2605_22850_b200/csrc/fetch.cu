@@ -330,10 +330,12 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 //   kWdrr    several descriptors; the claim order is a table of entries (request, first unit,
 //            count, release us) built by weighted deficit round robin (dispatch.cpp; Alg. A2
 //            lines 6-7), each request's units still in its own layer-major order.
-//   kByPos   several descriptors, layer-major, and inside a layer position-major: chunk position
-//            j of every request holding one, tile by tile, before position j+1.  Requests that
-//            share a prefix (same chunk at the same position) then read each shared slice at the
-//            same moment, so HBM serves it once and the duplicates hit L2.
+//   kByPos   several descriptors, layer-major, and inside a layer position-major in blocks: a
+//            block of B consecutive chunk positions of every request holding them (request by
+//            request, each request's B positions tile by tile) before the next block.  Requests that
+//            share a prefix (same chunk at the same position) then re-read each shared slice about
+//            B*S bytes after the first read -- close enough that L2 still holds it, far enough
+//            that the readers do not collide on the same L2 lines at once -- so HBM serves it once.
 enum { kSingle = 0, kBatch = 1, kWdrr = 2, kByPos = 3 };
 
 struct BatchArgs {
@@ -352,9 +354,10 @@ struct BatchArgs {
     const uint32_t* seg_cum;  // [nseg + 1]
     const uint32_t* seg_pos;  // [nseg]
     const uint32_t* seg_cnt;  // [nseg]
-    const uint32_t* sorted;   // [n] member indices, N descending
+    const uint2* memb;        // [n] {member index, its units per layer}, N descending
     uint32_t nseg;
     uint32_t tiles;           // units per chunk-layer slice (the same for every member)
+    uint32_t pos_block;       // B: positions per block
 };
 
 struct Resolved {
@@ -363,27 +366,44 @@ struct Resolved {
     uint32_t req;  // request index within the batch (0 without a batch)
 };
 
+// kByPos: the run of positions the previous claim fell in (a CTA's consecutive claims are ~one
+// grid apart, so they usually stay in one run): lane-0 registers, refreshed by a binary search
+// only on a miss.
+struct SegCache {
+    uint32_t c0 = 1, c1 = 0;  // units [c0, c1) of a layer (empty until the first search)
+    uint32_t cnt = 0, pos0 = 0, len = 0;
+};
+
 template <int MODE>
-__device__ __forceinline__ Resolved resolve(const DevDesc& d0, const BatchArgs& ba, uint32_t g) {
+__device__ __forceinline__ Resolved resolve(const DevDesc& d0, const BatchArgs& ba, uint32_t g, SegCache& sc) {
     if (MODE == kSingle) return {&d0, g, 0u};
     const uint32_t layer = fdiv(g, ba.div_upl_total);
     const uint32_t rem = g - layer * ba.upl_total;
     if (MODE == kByPos) {
-        uint32_t lo = 0, hi = ba.nseg;  // largest k with seg_cum[k] <= rem
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(&ba.seg_cum[mid]) <= rem) lo = mid;
-            else hi = mid;
+        if (rem < sc.c0 || rem >= sc.c1) {
+            uint32_t lo = 0, hi = ba.nseg;  // largest k with seg_cum[k] <= rem
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (__ldg(&ba.seg_cum[mid]) <= rem) lo = mid;
+                else hi = mid;
+            }
+            sc.c0 = __ldg(&ba.seg_cum[lo]);
+            sc.c1 = __ldg(&ba.seg_cum[lo + 1]);
+            sc.cnt = __ldg(&ba.seg_cnt[lo]);
+            sc.pos0 = __ldg(&ba.seg_pos[lo]);
+            sc.len = (sc.c1 - sc.c0) / (sc.cnt * ba.tiles);  // positions in the run
         }
-        const uint32_t cnt = __ldg(&ba.seg_cnt[lo]);
-        const uint32_t o = rem - __ldg(&ba.seg_cum[lo]);
-        const uint32_t per_pos = cnt * ba.tiles;  // units of one position across its members
-        const uint32_t jj = o / per_pos;
-        const uint32_t rest = o - jj * per_pos;
-        const uint32_t tile = rest / cnt;        // tile-major, member-minor: equal sources adjacent
-        const uint32_t req = __ldg(&ba.sorted[rest - tile * cnt]);
-        const DevDesc* d = &ba.descs[req];
-        return {d, layer * d->units_per_layer + (__ldg(&ba.seg_pos[lo]) + jj) * ba.tiles + tile, req};
+        const uint32_t per_pos = sc.cnt * ba.tiles;   // units of one position across its members
+        const uint32_t o = rem - sc.c0;
+        const uint32_t per_blk = ba.pos_block * per_pos;
+        const uint32_t bi = o / per_blk;              // block of positions
+        const uint32_t r1 = o - bi * per_blk;
+        const uint32_t blen = min(ba.pos_block, sc.len - bi * ba.pos_block);
+        const uint32_t m = r1 / (blen * ba.tiles);    // member, then its positions, then tiles
+        const uint32_t r2 = r1 - m * blen * ba.tiles;
+        const uint32_t pos = sc.pos0 + bi * ba.pos_block + r2 / ba.tiles;
+        const uint2 mb = __ldg(&ba.memb[m]);          // {member, units per layer}
+        return {&ba.descs[mb.x], layer * mb.y + pos * ba.tiles + (r2 % ba.tiles), mb.x};
     }
     uint32_t lo = 0, hi = ba.n;  // largest r with cum[r] <= rem
     while (hi - lo > 1) {
@@ -501,6 +521,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     uint32_t next_raw = lane == 0 ? atomicAdd(claim_ctr, 1u) : 0u;
     // kWdrr: the entry being consumed (lane 0) and the launch's common start time
     uint32_t cur_req = 0, cur_next = 0, cur_left = 0, cur_rel = 0;
+    SegCache seg_cache;  // kByPos (lane 0)
     uint64_t t_start = t0;
     if (MODE == kWdrr && ba.paced && lane == 0) {
         const unsigned long long old = atomicCAS(ba.t0_slot, 0ull, (unsigned long long)t0);
@@ -536,7 +557,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
                 exhausted = true;
             } else {
                 next_raw = atomicAdd(claim_ctr, 1u);
-                const Resolved rs = resolve<MODE>(d0, ba, gg);
+                const Resolved rs = resolve<MODE>(d0, ba, gg, seg_cache);
                 g = rs.g;
                 req = rs.req;
             }
@@ -974,7 +995,7 @@ struct Batch {
     std::vector<Desc*> descs;
     int device = 0;
     uint32_t n = 0;
-    size_t upload_bytes = 0;   // DevDesc[n] | cum[n+1] | seg_cum[n+1] | seg_pos[n] | seg_cnt[n] | sorted[n]
+    size_t upload_bytes = 0;   // DevDesc[n] | cum[n+1] | seg_cum[n+1] | seg_pos[n] | seg_cnt[n] | memb[n] (uint2)
     int order = OC_BATCH_BY_REQUEST;
     void* dev = nullptr;       // upload area + claim counter
     uint64_t dev_class = 0;
@@ -1026,7 +1047,8 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
     uint32_t* seg_cum = cum + (b->n + 1);
     uint32_t* seg_pos = seg_cum + (b->n + 1);
     uint32_t* seg_cnt = seg_pos + b->n;
-    uint32_t* sorted = seg_cnt + b->n;
+    uint32_t* memb = seg_cnt + b->n;  // [n] x {member, units per layer}
+    std::vector<uint32_t> sorted(b->n);
     uint64_t host_chunks = 0, chunks = 0, total = 0;
     cum[0] = 0;
     for (uint32_t i = 0; i < b->n; i++) {
@@ -1055,7 +1077,8 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
     const bool by_pos = !wdrr && b->order == OC_BATCH_BY_POSITION;
     if (by_pos) {
         for (uint32_t i = 0; i < b->n; i++) sorted[i] = i;
-        std::stable_sort(sorted, sorted + b->n, [&](uint32_t x, uint32_t y) { return b->descs[x]->N > b->descs[y]->N; });
+        std::stable_sort(sorted.begin(), sorted.end(),
+                         [&](uint32_t x, uint32_t y) { return b->descs[x]->N > b->descs[y]->N; });
         const uint32_t tiles = b->descs[0]->dd.tiles;
         seg_cum[0] = 0;
         for (uint32_t cnt = b->n; cnt >= 1; cnt--) {
@@ -1069,6 +1092,10 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         }
         for (Desc* d : b->descs)
             if (d->dd.tiles != tiles) return fail(OC_EINVAL, "fetch_batch: members planned with different units");
+        for (uint32_t i = 0; i < b->n; i++) {  // units_per_layer was set by plan_units above
+            memb[2 * i] = sorted[i];
+            memb[2 * i + 1] = b->descs[sorted[i]]->dd.units_per_layer;
+        }
     }
     // WDRR: the claim order (Alg. A2 line 7), uploaded behind a zeroed start-time slot
     uint64_t n_claims = total * L;  // claim items of the launch: units, or WDRR entries
@@ -1120,9 +1147,12 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         ba.seg_cum = dcum;
         ba.seg_pos = dcum + (b->n + 1);
         ba.seg_cnt = ba.seg_pos + b->n;
-        ba.sorted = ba.seg_cnt + b->n;
+        ba.memb = (const uint2*)(ba.seg_cnt + b->n);
         ba.nseg = nseg;
         ba.tiles = b->descs[0]->dd.tiles;
+        // B = ~4 MiB of one request's slices per block (profiles/r01_batch_dram.json)
+        const uint64_t blk_bytes = (uint64_t)std::max(1, env_int("OC_BYPOS_BLOCK_KIB", 4096)) << 10;
+        ba.pos_block = (uint32_t)std::max<uint64_t>(1, blk_bytes / b->descs[0]->geo.S);
     }
     if (p.stages < 2) return fail(OC_ENOTSUP, "fetch_batch: two units do not fit in shared memory");
     if (wdrr) {
@@ -1180,7 +1210,7 @@ OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out) {
     }
     b->n = n;
     b->device = b->descs[0]->device;
-    b->upload_bytes = sizeof(oc::DevDesc) * n + 4 * (n + 1) * 2 + 4 * n * 3;
+    b->upload_bytes = sizeof(oc::DevDesc) * n + 4 * (n + 1) * 2 + 4 * n * 4;
     const size_t dev_bytes = ((b->upload_bytes + 15) & ~size_t(15)) + 16;
     oc::DeviceGuard dg(b->device);
     b->dev = oc::dev_pool_alloc(b->device, dev_bytes, &b->dev_class);

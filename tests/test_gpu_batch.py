@@ -41,8 +41,11 @@ SPECS = [(1, 3, "nhd", 16, 0), (2, 7, "hnd", 8, 5), (3, 1, "flat", 16, 0), (4, 1
 
 @pytest.mark.parametrize("lay", [OLayout(3, 2, 64, 2, 16), OLayout(2, 4, 32, 2, 20)])
 @pytest.mark.parametrize("unit_bytes", [0, 1024, 3072])
-@pytest.mark.parametrize("order", [oc.BATCH_BY_REQUEST, oc.BATCH_BY_POSITION])
-def test_batch_parity(lay, unit_bytes, order):
+@pytest.mark.parametrize("order,blk_kib", [(oc.BATCH_BY_REQUEST, 0), (oc.BATCH_BY_POSITION, 16),
+                                           (oc.BATCH_BY_POSITION, 4096)])
+def test_batch_parity(lay, unit_bytes, order, blk_kib, monkeypatch):
+    if blk_kib:   # 16 KiB: blocks of 1-2 positions, partial last blocks in every run
+        monkeypatch.setenv("OC_BYPOS_BLOCK_KIB", str(blk_kib))
     st, items = setup_batch(lay, SPECS)
     b = oc.Batch([it["desc"] for it in items], order=order)
     s = torch.cuda.Stream()
@@ -252,8 +255,11 @@ def test_wdrr_hold_rates():
     st.close()
 
 
-@pytest.mark.parametrize("order", [oc.BATCH_BY_REQUEST, oc.BATCH_BY_POSITION])
-def test_batch_shared_prefix_family(order):
+@pytest.mark.parametrize("order,blk_kib", [(oc.BATCH_BY_REQUEST, 0), (oc.BATCH_BY_POSITION, 24),
+                                           (oc.BATCH_BY_POSITION, 4096)])
+def test_batch_shared_prefix_family(order, blk_kib, monkeypatch):
+    if blk_kib:
+        monkeypatch.setenv("OC_BYPOS_BLOCK_KIB", str(blk_kib))
     """Requests of one prefix family (8 shared chunks, then own chunks; one request is the bare
     shared prefix) through one store: every member's bytes as the oracle, both orders, refetched."""
     lay = OLayout(3, 2, 64, 2, 16)
