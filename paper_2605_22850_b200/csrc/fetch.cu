@@ -366,8 +366,9 @@ struct Resolved {
     uint32_t req;  // request index within the batch (0 without a batch)
 };
 
-// kByPos: the run of positions the previous claim fell in (a CTA's consecutive claims are ~one
-// grid apart, so they usually stay in one run): lane-0 registers, refreshed by a binary search
+// The batch segment the previous claim fell in -- kByPos: a run of positions; kBatch: a member's
+// units of a layer (cnt = member, len = its units per layer).  A CTA's consecutive claims are ~one
+// grid apart, so they usually stay in one segment: lane-0 registers, refreshed by a binary search
 // only on a miss.
 struct SegCache {
     uint32_t c0 = 1, c1 = 0;  // units [c0, c1) of a layer (empty until the first search)
@@ -405,14 +406,19 @@ __device__ __forceinline__ Resolved resolve(const DevDesc& d0, const BatchArgs& 
         const uint2 mb = __ldg(&ba.memb[m]);          // {member, units per layer}
         return {&ba.descs[mb.x], layer * mb.y + pos * ba.tiles + (r2 % ba.tiles), mb.x};
     }
-    uint32_t lo = 0, hi = ba.n;  // largest r with cum[r] <= rem
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(&ba.cum[mid]) <= rem) lo = mid;
-        else hi = mid;
+    if (rem < sc.c0 || rem >= sc.c1) {  // kBatch: the cache holds the member of the last claim
+        uint32_t lo = 0, hi = ba.n;  // largest r with cum[r] <= rem
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(&ba.cum[mid]) <= rem) lo = mid;
+            else hi = mid;
+        }
+        sc.c0 = __ldg(&ba.cum[lo]);
+        sc.c1 = __ldg(&ba.cum[lo + 1]);
+        sc.cnt = lo;
+        sc.len = sc.c1 - sc.c0;  // the member's units per layer
     }
-    const DevDesc* d = &ba.descs[lo];
-    return {d, layer * d->units_per_layer + (rem - __ldg(&ba.cum[lo])), lo};
+    return {&ba.descs[sc.cnt], layer * sc.len + (rem - sc.c0), sc.cnt};
 }
 
 // Batch observer: lane i announces the layers of requests i, i+32, ...; each request's layers go
