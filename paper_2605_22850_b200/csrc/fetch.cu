@@ -72,6 +72,13 @@ __device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// Release pattern in two parts: one fence for a group of relaxed reductions.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ void red_add_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ---- unit geometry -------------------------------------------------------------------------------
 // Layer l of chunk j is 2G rows at [lS, (l+1)S) of the slot: K rows 0..G-1, then V rows G..2G-1
 // (KV_L2TD, reading c2).  A unit is R consecutive rows q0 .. q0+R-1 of that slice -- contiguous
@@ -279,6 +286,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+// Non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
@@ -497,14 +519,43 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     __syncthreads();
     if (threadIdx.x >= 32) {  // ---- signaler warp
         if (threadIdx.x != 32) return;
-        for (uint32_t h = 0;; h++) {  // slot h % kFifo, round h / kFifo
-            const uint32_t f = h % kFifo;
-            mbar_wait(&fifo_full[f], (h / kFifo) & 1u);  // acquire: the record is visible
-            const uint32_t req = fifo_req[f], layer = fifo_layer[f], n = fifo_n[f];
-            mbar_arrive(&fifo_empty[f]);                 // release: the slot may be reused
-            if (layer == 0xffffffffu) return;
-            complete_units(BATCH ? ba.descs[req] : d0, layer, n);
+        // Each round takes every record already in the FIFO (waiting only for the first), merges
+        // records of the same (request, layer), then publishes them with ONE GPU-scope release
+        // fence followed by relaxed reductions (a PTX release pattern) -- a fence per record
+        // (MEMBAR.GPU + ERRBAR) throttled batches that change request at every unit.
+        constexpr int kBatchRec = 8;
+        uint32_t h = 0;  // slot h % kFifo, round h / kFifo
+        bool done = false;
+        while (!done) {
+            uint32_t rq[kBatchRec], ly[kBatchRec], nn[kBatchRec];
+            int m = 0;
+            for (int taken = 0; taken < kBatchRec; taken++, h++) {
+                const uint32_t f = h % kFifo;
+                if (taken == 0) mbar_wait(&fifo_full[f], (h / kFifo) & 1u);  // acquire: the record is visible
+                else if (!mbar_test(&fifo_full[f], (h / kFifo) & 1u)) break;
+                const uint32_t req = fifo_req[f], layer = fifo_layer[f], n = fifo_n[f];
+                mbar_arrive(&fifo_empty[f]);                 // release: the slot may be reused
+                if (layer == 0xffffffffu) {
+                    done = true;
+                    h++;
+                    break;
+                }
+                int e = 0;
+                while (e < m && !(rq[e] == req && ly[e] == layer)) e++;
+                if (e == m) {
+                    rq[m] = req;
+                    ly[m] = layer;
+                    nn[m++] = n;
+                } else {
+                    nn[e] += n;
+                }
+            }
+            if (m) {
+                fence_acq_rel_gpu();
+                for (int e = 0; e < m; e++) red_add_relaxed(&(BATCH ? ba.descs[rq[e]] : d0).unit_cnt[ly[e]], nn[e]);
+            }
         }
+        return;
     }
     // ---- copy warp
     constexpr uint32_t kEnd = 0xffffffffu;
