@@ -212,6 +212,11 @@ typedef enum {
 typedef enum {
     OC_COPY_LDST = 0,        /* 16-byte vector loads/stores through registers */
     OC_COPY_BULK = 1,        /* TMA bulk copies through a shared-memory ring  */
+    OC_COPY_CE = 2,          /* pinned-host chunks only (ENOTSUP otherwise): per layer, one
+                                strided copy-engine transfer per run of consecutive store slots
+                                into a double-buffered HBM stage (2*N*S bytes, owned by the
+                                descriptor), then the BULK kernel scatters the stage into the
+                                target and announces the layer.  PERSISTENT mode, unpaced.  */
 } oc_copy_engine;
 
 typedef struct {

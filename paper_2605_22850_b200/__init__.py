@@ -35,7 +35,7 @@ FETCH_PERSISTENT, FETCH_PER_LAYER = 0, 1
 TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
 BATCH_BY_REQUEST, BATCH_BY_POSITION = 0, 1
-COPY_LDST, COPY_BULK = 0, 1
+COPY_LDST, COPY_BULK, COPY_CE = 0, 1, 2
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)

@@ -315,6 +315,17 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     d->N = n;
     d->nb = v.bt.size();
     d->host_chunks = host_chunks;
+    if (host_chunks == n) {  // CE engine: maximal runs of chunks in consecutive slots
+        for (uint64_t i = 0; i < n; i++) {
+            if (i > 0 && src[i] == src[i - 1] + g.chunk) {
+                d->run_len.back()++;
+            } else {
+                d->run_first.push_back(i);
+                d->run_len.push_back(1);
+                d->run_src.push_back(src[i]);
+            }
+        }
+    }
     oc::DeviceGuard dg(d->device);
     rc = oc::upload_block(d->device, g, src, v, nullptr, "build_descriptor", &d->dev_mem, &d->dev_mem_class, &d->dd,
                           nullptr, &d->up, false, nullptr);
@@ -417,6 +428,11 @@ OC_API int oc_desc_free(oc_desc* h) {
         if (d->done_ev) cudaEventDestroy(d->done_ev);
         if (d->sync_ev) cudaEventDestroy(d->sync_ev);
         if (d->sync_stream) cudaStreamDestroy(d->sync_stream);
+        for (auto ev : d->ce_done) cudaEventDestroy(ev);
+        for (auto ev : d->scat_done) cudaEventDestroy(ev);
+        if (d->ce_start) cudaEventDestroy(d->ce_start);
+        if (d->ce_stream) cudaStreamDestroy(d->ce_stream);
+        oc::dev_pool_free(d->device, d->stage_mem, d->stage_class);
         oc::dev_pool_free(d->device, d->dev_mem, d->dev_mem_class);
         cudaGetLastError();
     }

@@ -99,6 +99,8 @@ __device__ __forceinline__ UnitGeo unit_geo(const DevDesc& d, uint32_t g) {
 }
 
 __device__ __forceinline__ const uint8_t* unit_src(const DevDesc& d, const UnitGeo& u) {
+    if (d.staged)  // CE engine: layer l of chunk j was staged at stage_base[l & 1] + j*S
+        return (const uint8_t*)d.stage_base[u.layer & 1] + (uint64_t)u.j * d.S + (uint64_t)u.q0 * d.row;
     return (const uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + (uint64_t)u.q0 * d.row;
 }
 
@@ -985,10 +987,84 @@ int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStrea
     return OC_OK;
 }
 
+// CE engine for pinned-host chunks: per layer, one strided copy-engine transfer per run of
+// consecutive slots (width S, source pitch L*S) lands the layer's N slices contiguously in an HBM
+// stage (double-buffered by layer), then the bulk kernel scatters the stage into the paged target
+// and announces the layer.  The copy engine reads PCIe at ~55 GB/s where SM zero-copy reads stop
+// at ~51 GB/s (profiles/r01_ce_probe.txt, r01_ce2d.txt); the scatter of layer l overlaps the copy
+// of layer l+1 (copies on a private stream, events in both directions).
+int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
+    if (o.mode != OC_FETCH_PERSISTENT) return fail(OC_ENOTSUP, "fetch_layerwise: the CE engine uses PERSISTENT mode");
+    if (o.pace_Bps != 0) return fail(OC_ENOTSUP, "fetch_layerwise: the CE engine is unpaced");
+    if (d->host_chunks != d->N || d->run_first.empty())
+        return fail(OC_ENOTSUP, "fetch_layerwise: the CE engine needs every chunk in the pinned host tier");
+    if (d->poisoned) return fail(OC_ECUDA, "fetch_layerwise: descriptor unusable after a failed launch");
+    DeviceGuard dg(d->device);
+    int urc = upload_order(&d->up, s);
+    if (urc) return urc;
+    const uint32_t L = d->geo.L;
+    const uint64_t NS = d->N * d->geo.S;
+    if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
+    if (!d->ce_stream) OC_CUDA(cudaStreamCreateWithFlags(&d->ce_stream, cudaStreamNonBlocking));
+    if (!d->ce_start) OC_CUDA(cudaEventCreateWithFlags(&d->ce_start, cudaEventDisableTiming));
+    if (d->ce_done.empty()) {
+        d->ce_done.resize(L, nullptr);
+        d->scat_done.resize(L, nullptr);
+        for (uint32_t l = 0; l < L; l++) {
+            OC_CUDA(cudaEventCreateWithFlags(&d->ce_done[l], cudaEventDisableTiming));
+            OC_CUDA(cudaEventCreateWithFlags(&d->scat_done[l], cudaEventDisableTiming));
+        }
+    }
+    if (!d->stage_mem) {
+        d->stage_mem = dev_pool_alloc(d->device, 2 * NS, &d->stage_class);
+        if (!d->stage_mem) return fail(OC_ENOMEM, "fetch_layerwise: CE stage allocation failed");
+    }
+    plan_units(d, o.unit_bytes ? o.unit_bytes : default_unit_bytes(o.max_ctas, device_sm_count(d->device)));
+    DevDesc& dd = d->dd;
+    const uint64_t total_units = (uint64_t)dd.units_per_layer * L;
+    if (total_units >= (1ull << 32)) return fail(OC_ERANGE, "fetch_layerwise: too many units");
+    uint32_t epoch = d->epoch + 1;
+    if (epoch == 0) epoch = 1;
+    dd.epoch = epoch;
+    dd.cnt_target = d->cnt_base + dd.units_per_layer;
+    dd.pace_ns = 0;
+    dd.staged = 1;
+    dd.stage_base[0] = (uint64_t)d->stage_mem;
+    dd.stage_base[1] = (uint64_t)d->stage_mem + NS;
+    const BulkPlan p = plan_bulk(dd, device_sm_count(d->device), o.max_ctas, dd.units_per_layer);
+    d->epoch = epoch;
+    d->cnt_base = dd.cnt_target;
+    d->poisoned = true;
+    const uint32_t upl = dd.units_per_layer;
+    OC_CUDA(cudaEventRecord(d->ce_start, s));  // the copies follow the caller's earlier work
+    OC_CUDA(cudaStreamWaitEvent(d->ce_stream, d->ce_start, 0));
+    for (uint32_t l = 0; l < L; l++) {
+        if (l >= 2) OC_CUDA(cudaStreamWaitEvent(d->ce_stream, d->scat_done[l - 2], 0));  // stage l&1 free
+        uint8_t* stage = (uint8_t*)d->stage_mem + (l & 1) * NS;
+        for (size_t r = 0; r < d->run_first.size(); r++)
+            OC_CUDA(cudaMemcpy2DAsync(stage + d->run_first[r] * d->geo.S, d->geo.S,
+                                      (const void*)(d->run_src[r] + (uint64_t)l * d->geo.S), d->geo.chunk,
+                                      d->geo.S, d->run_len[r], cudaMemcpyDefault, d->ce_stream));
+        OC_CUDA(cudaEventRecord(d->ce_done[l], d->ce_stream));
+        OC_CUDA(cudaStreamWaitEvent(s, d->ce_done[l], 0));
+        int rc = launch_bulk(d, p, l * upl, (l + 1) * upl, s);
+        if (rc) return rc;
+        OC_CUDA(cudaEventRecord(d->scat_done[l], s));
+    }
+    OC_CUDA(cudaEventRecord(d->done_ev, s));
+    d->poisoned = false;
+    d->last_mode = OC_FETCH_PERSISTENT;
+    d->last_stream = s;
+    d->fetched = true;
+    return OC_OK;
+}
+
 int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     if (o.mode != OC_FETCH_PERSISTENT && o.mode != OC_FETCH_PER_LAYER)
         return fail(OC_EINVAL, "fetch_layerwise: unknown mode");
+    if (o.engine == OC_COPY_CE) return launch_fetch_ce(d, o, s);
     if (o.engine != OC_COPY_LDST && o.engine != OC_COPY_BULK) return fail(OC_EINVAL, "fetch_layerwise: unknown engine");
+    d->dd.staged = 0;
     if (o.pace_Bps < 0) return fail(OC_EINVAL, "fetch_layerwise: pace must be >= 0");
     if (o.pace_Bps > 0 && o.mode != OC_FETCH_PERSISTENT)
         return fail(OC_ENOTSUP, "fetch_layerwise: pacing needs PERSISTENT mode");
@@ -1120,6 +1196,7 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         dd.epoch = epoch;
         dd.cnt_target = d->cnt_base + dd.units_per_layer;
         dd.pace_ns = 0;
+        dd.staged = 0;
         st[i] = dd;
         total += dd.units_per_layer;
         cum[i + 1] = (uint32_t)total;

@@ -139,6 +139,8 @@ struct DevDesc {
     uint32_t cnt_target;      // unit_cnt[l] value once this fetch's units of layer l are done
     uint32_t chunk_major;     // 1: only the completion of the whole prefix is announced
     uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
+    uint64_t stage_base[2];   // CE engine: layer l's slices were staged at stage_base[l & 1] as [N][S]
+    uint32_t staged;          // 1: read sources from stage_base (CE engine), 0: from src[]
     FastDiv div_upl;          // units_per_layer
     FastDiv div_tiles;        // tiles per chunk-layer slice
     FastDiv div_vpr;
@@ -170,6 +172,14 @@ struct Desc {
     cudaStream_t last_stream = nullptr;
     cudaStream_t sync_stream = nullptr;  // oc_sync_layer in PERSISTENT mode
     cudaEvent_t sync_ev = nullptr;
+    // CE engine (pinned-host chunks): runs of chunks in consecutive slots, copied per layer by one
+    // strided copy-engine transfer into a double-buffered HBM stage, then scattered by the kernel
+    std::vector<uint64_t> run_first, run_len, run_src;
+    void* stage_mem = nullptr;
+    uint64_t stage_class = 0;
+    cudaStream_t ce_stream = nullptr;
+    cudaEvent_t ce_start = nullptr;
+    std::vector<cudaEvent_t> ce_done, scat_done;
 };
 
 // Pooled memory (pool.cpp): power-of-two blocks of device memory on `device`, or of pinned host

@@ -1,0 +1,106 @@
+"""CE engine (pinned-host chunks: strided copy-engine transfers into an HBM stage, then the bulk
+scatter kernel) vs the oracle, byte for byte, including chains whose slots form several runs."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2605_22850_b200 as oc  # noqa: E402
+from oracle.geometry import Layout as OLayout  # noqa: E402
+from scenario import (lib_target, make_dest, oracle_result, payload_stack,  # noqa: E402
+                      requests_family, sentinel_buffer)
+
+pytestmark = pytest.mark.gpu
+
+
+def fetch_and_check(st, lay, seed, req, dest, keys=None, delivery=oc.DELIVER_LAYER_MAJOR, **opts):
+    keys = st.match_prefix(req.tokens)[:req.n_chunks] if keys is None else keys
+    buf = sentinel_buffer(dest.size)
+    d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()), delivery)
+    s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+    d.fetch_layerwise(s, engine=oc.COPY_CE, **opts)
+    d.wait_layer(lay.num_layers - 1, cons)
+    cons.synchronize()
+    assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, seed, req, dest))
+    t = d.layer_times().astype(np.int64)
+    assert np.all(np.diff(t[1:]) >= 0)
+    return d, buf
+
+
+@pytest.mark.parametrize("lay", [OLayout(3, 2, 64, 2, 16), OLayout(2, 4, 32, 2, 20), OLayout(5, 1, 16, 2, 16)])
+@pytest.mark.parametrize("kind,Bs,first", [("nhd", 16, 0), ("nhd", 8, 5), ("hnd", 16, 3), ("flat", 16, 0),
+                                           ("nhd", 1, 2)])
+@pytest.mark.parametrize("unit_bytes", [0, 1024])
+def test_ce_parity_one_run(lay, kind, Bs, first, unit_bytes):
+    req = requests_family(lay, 7, 0, [9])[0]
+    with oc.Store(lay, capacity=16, tier=oc.TIER_PINNED_HOST) as st:
+        st.put_chunks(oc.chunk_keys(req.tokens, lay.chunk_tokens), payload_stack(lay, 7, req.payload_ids))
+        dest = make_dest(lay, req.n_chunks, kind, Bs=Bs, first_token=first, seed=3)
+        d, _ = fetch_and_check(st, lay, 7, req, dest, unit_bytes=unit_bytes)
+        d.close()
+
+
+def test_ce_several_runs_and_refetch():
+    """Request B's chain: the family's 8 shared chunks (put with A), then its own 3 chunks put after
+    an unrelated request's -- three runs of slots; refetched with every engine in turn."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    a, b = requests_family(lay, 11, 8, [2, 3])
+    other = requests_family(lay, 12, 0, [4])[0]
+    with oc.Store(lay, capacity=32, tier=oc.TIER_PINNED_HOST) as st:
+        ka, kb, ko = (oc.chunk_keys(r.tokens, 16) for r in (a, b, other))
+        st.put_chunks(ka, payload_stack(lay, 11, a.payload_ids))
+        st.put_chunks(ko, payload_stack(lay, 12, other.payload_ids))
+        st.put_chunks(kb[8:10], payload_stack(lay, 11, b.payload_ids[8:10]))
+        st.put_chunks(ko[:1], payload_stack(lay, 12, other.payload_ids[:1]))      # dedup, no slot
+        st.put_chunks(kb[10:], payload_stack(lay, 11, b.payload_ids[10:]))
+        slots = st.lookup(kb)
+        runs = 1 + int(np.count_nonzero(np.diff(slots.astype(np.int64)) != 2 * 16 * 256 * 3))
+        assert runs == 2
+        dest = make_dest(lay, b.n_chunks, "nhd", Bs=8, first_token=1, seed=5)
+        d, buf = fetch_and_check(st, lay, 11, b, dest)
+        s = torch.cuda.Stream()
+        for engine in (oc.COPY_BULK, oc.COPY_CE, oc.COPY_LDST, oc.COPY_CE, oc.COPY_CE):
+            with torch.cuda.stream(s):
+                buf.fill_(0xA5)
+            d.fetch_layerwise(s, engine=engine, max_ctas=3 if engine == oc.COPY_CE else 0)
+            d.sync_layer(lay.num_layers - 1)
+            s.synchronize()
+            assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 11, b, dest)), engine
+        d.close()
+
+
+def test_ce_chunk_major_delivery():
+    lay = OLayout(4, 2, 64, 2, 16)
+    req = requests_family(lay, 21, 0, [6])[0]
+    with oc.Store(lay, capacity=8, tier=oc.TIER_PINNED_HOST) as st:
+        st.put_chunks(oc.chunk_keys(req.tokens, 16), payload_stack(lay, 21, req.payload_ids))
+        dest = make_dest(lay, req.n_chunks, "hnd", Bs=16, seed=2)
+        d, _ = fetch_and_check(st, lay, 21, req, dest, delivery=oc.DELIVER_CHUNK_MAJOR)
+        d.close()
+
+
+def test_ce_errors():
+    lay = OLayout(2, 2, 64, 2, 16)
+    req = requests_family(lay, 31, 0, [3])[0]
+    keys = oc.chunk_keys(req.tokens, 16)
+    dest = make_dest(lay, 3, "nhd", Bs=16)
+    buf = sentinel_buffer(dest.size)
+    with oc.Store(lay, capacity=4) as hbm:                       # HBM store: no CE path
+        hbm.put_chunks(keys, payload_stack(lay, 31, req.payload_ids))
+        d = oc.build_descriptor(hbm, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+        with pytest.raises(oc.ObjcacheError) as e:
+            d.fetch_layerwise(None, engine=oc.COPY_CE)
+        assert e.value.code == oc.OC_ENOTSUP
+        d.close()
+    with oc.Store(lay, capacity=4, tier=oc.TIER_PINNED_HOST) as st:
+        st.put_chunks(keys, payload_stack(lay, 31, req.payload_ids))
+        d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+        for kw in ({"pace_Bps": 1e9}, {"mode": oc.FETCH_PER_LAYER}):
+            with pytest.raises(oc.ObjcacheError) as e:
+                d.fetch_layerwise(None, engine=oc.COPY_CE, **kw)
+            assert e.value.code == oc.OC_ENOTSUP
+        d.fetch_layerwise(None, engine=oc.COPY_CE)               # still usable after the refusals
+        d.sync_layer(1)
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 31, req, dest))
+        d.close()
