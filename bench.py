@@ -471,6 +471,7 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
     L, G, Bs = lay_t[0], lay_t[4], 16
     row, S, chunk = oc.geometry(lay_t)
     stamps = torch.zeros((L, 2), dtype=torch.int64, device=dev)
+    cur = {"fo": fopts}                            # fetch options of the tier being measured
 
     def chain(copy_s, cons_s, d, C_ns, fetch=True, events=None):
         """Returns (TTFT ms from the launch event, stamps [L,2] ns)."""
@@ -479,7 +480,7 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
         a.record(copy_s)
         cons_s.wait_event(a)
         if d is not None and fetch:
-            d.fetch_layerwise(copy_s, **fopts)
+            d.fetch_layerwise(copy_s, **cur["fo"])
         elif events is not None:
             events(copy_s)
         for l in range(L):
@@ -496,7 +497,7 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
     if cells is None:
         cells = [("4k", 4096, 3584, 63.47)] + ([("64k", 65536, 57344, 2423.90)] if args.stall64k else [])
     if tiers is None:
-        tiers = (("hbm", oc.TIER_HBM), ("pinned_host", oc.TIER_PINNED_HOST))
+        tiers = (("hbm", oc.TIER_HBM), ("pinned_host", oc.TIER_PINNED_HOST), ("pinned_host_ce", oc.TIER_PINNED_HOST))
     for name, ctx, cached, t_total_ms in cells:
         N = cached // G
         windows = {"a100": t_total_ms / L if t_total_ms else None,             # Table A5 (A100)
@@ -510,6 +511,7 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
         tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs, bt, 0)
         copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         for tier_name, tier in tiers:
+            cur["fo"] = {"engine": oc.COPY_CE} if tier_name.endswith("_ce") else fopts
             store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
             (tok,), _ = synth.family_streams(9000 + N, G, 0, [N])
             keys = oc.chunk_keys(tok, G)
@@ -539,7 +541,7 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
                 ol = _OL()
             for wname, C_ms in windows.items():
                 C_ns = int(round(C_ms * 1e6))
-                d.fetch_layerwise(copy_s, **fopts)
+                d.fetch_layerwise(copy_s, **cur["fo"])
                 torch.cuda.synchronize()
                 base_runs = [chain(copy_s, cons_s, d, C_ns, fetch=False) for _ in range(3)]
                 base, bst = min(base_runs, key=lambda r: r[0])

@@ -428,11 +428,7 @@ OC_API int oc_desc_free(oc_desc* h) {
         if (d->done_ev) cudaEventDestroy(d->done_ev);
         if (d->sync_ev) cudaEventDestroy(d->sync_ev);
         if (d->sync_stream) cudaStreamDestroy(d->sync_stream);
-        for (auto ev : d->ce_done) cudaEventDestroy(ev);
-        for (auto ev : d->scat_done) cudaEventDestroy(ev);
-        if (d->ce_start) cudaEventDestroy(d->ce_start);
-        if (d->ce_stream) cudaStreamDestroy(d->ce_stream);
-        oc::dev_pool_free(d->device, d->stage_mem, d->stage_class);
+        oc::ce_release(d);
         oc::dev_pool_free(d->device, d->dev_mem, d->dev_mem_class);
         cudaGetLastError();
     }

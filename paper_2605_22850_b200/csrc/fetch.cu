@@ -993,6 +993,54 @@ int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStrea
 // and announces the layer.  The copy engine reads PCIe at ~55 GB/s where SM zero-copy reads stop
 // at ~51 GB/s (profiles/r01_ce_probe.txt, r01_ce2d.txt); the scatter of layer l overlaps the copy
 // of layer l+1 (copies on a private stream, events in both directions).
+// A copy stream with its per-layer events; kits are recycled per (device, L) because creating a
+// stream and 2L+1 events per request cost ~0.2 ms of host time per fetch.
+struct CeKit {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t start = nullptr;
+    std::vector<cudaEvent_t> ce_done, scat_done;
+};
+
+namespace {
+std::mutex g_kit_mu;
+std::unordered_map<uint64_t, std::vector<CeKit*>> g_kits;
+
+int ce_kit_get(int device, uint32_t L, CeKit** out) {
+    const uint64_t key = ((uint64_t)(uint32_t)device << 32) | L;
+    {
+        std::lock_guard<std::mutex> lk(g_kit_mu);
+        auto& v = g_kits[key];
+        if (!v.empty()) {
+            *out = v.back();
+            v.pop_back();
+            return OC_OK;
+        }
+    }
+    auto k = std::make_unique<CeKit>();
+    OC_CUDA(cudaStreamCreateWithFlags(&k->stream, cudaStreamNonBlocking));
+    OC_CUDA(cudaEventCreateWithFlags(&k->start, cudaEventDisableTiming));
+    k->ce_done.resize(L, nullptr);
+    k->scat_done.resize(L, nullptr);
+    for (uint32_t l = 0; l < L; l++) {
+        OC_CUDA(cudaEventCreateWithFlags(&k->ce_done[l], cudaEventDisableTiming));
+        OC_CUDA(cudaEventCreateWithFlags(&k->scat_done[l], cudaEventDisableTiming));
+    }
+    *out = k.release();
+    return OC_OK;
+}
+}  // namespace
+
+// Called by oc_desc_free after the descriptor's last fetch has completed.
+void ce_release(Desc* d) {
+    if (d->ce_kit) {
+        std::lock_guard<std::mutex> lk(g_kit_mu);
+        g_kits[((uint64_t)(uint32_t)d->device << 32) | d->geo.L].push_back(d->ce_kit);
+        d->ce_kit = nullptr;
+    }
+    dev_pool_free(d->device, d->stage_mem, d->stage_class);
+    d->stage_mem = nullptr;
+}
+
 int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     if (o.mode != OC_FETCH_PERSISTENT) return fail(OC_ENOTSUP, "fetch_layerwise: the CE engine uses PERSISTENT mode");
     if (o.pace_Bps != 0) return fail(OC_ENOTSUP, "fetch_layerwise: the CE engine is unpaced");
@@ -1005,16 +1053,11 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     const uint32_t L = d->geo.L;
     const uint64_t NS = d->N * d->geo.S;
     if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
-    if (!d->ce_stream) OC_CUDA(cudaStreamCreateWithFlags(&d->ce_stream, cudaStreamNonBlocking));
-    if (!d->ce_start) OC_CUDA(cudaEventCreateWithFlags(&d->ce_start, cudaEventDisableTiming));
-    if (d->ce_done.empty()) {
-        d->ce_done.resize(L, nullptr);
-        d->scat_done.resize(L, nullptr);
-        for (uint32_t l = 0; l < L; l++) {
-            OC_CUDA(cudaEventCreateWithFlags(&d->ce_done[l], cudaEventDisableTiming));
-            OC_CUDA(cudaEventCreateWithFlags(&d->scat_done[l], cudaEventDisableTiming));
-        }
+    if (!d->ce_kit) {
+        int krc = ce_kit_get(d->device, L, &d->ce_kit);
+        if (krc) return krc;
     }
+    CeKit& kit = *d->ce_kit;
     if (!d->stage_mem) {
         d->stage_mem = dev_pool_alloc(d->device, 2 * NS, &d->stage_class);
         if (!d->stage_mem) return fail(OC_ENOMEM, "fetch_layerwise: CE stage allocation failed");
@@ -1036,20 +1079,20 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     d->cnt_base = dd.cnt_target;
     d->poisoned = true;
     const uint32_t upl = dd.units_per_layer;
-    OC_CUDA(cudaEventRecord(d->ce_start, s));  // the copies follow the caller's earlier work
-    OC_CUDA(cudaStreamWaitEvent(d->ce_stream, d->ce_start, 0));
+    OC_CUDA(cudaEventRecord(kit.start, s));  // the copies follow the caller's earlier work
+    OC_CUDA(cudaStreamWaitEvent(kit.stream, kit.start, 0));
     for (uint32_t l = 0; l < L; l++) {
-        if (l >= 2) OC_CUDA(cudaStreamWaitEvent(d->ce_stream, d->scat_done[l - 2], 0));  // stage l&1 free
+        if (l >= 2) OC_CUDA(cudaStreamWaitEvent(kit.stream, kit.scat_done[l - 2], 0));  // stage l&1 free
         uint8_t* stage = (uint8_t*)d->stage_mem + (l & 1) * NS;
         for (size_t r = 0; r < d->run_first.size(); r++)
             OC_CUDA(cudaMemcpy2DAsync(stage + d->run_first[r] * d->geo.S, d->geo.S,
                                       (const void*)(d->run_src[r] + (uint64_t)l * d->geo.S), d->geo.chunk,
-                                      d->geo.S, d->run_len[r], cudaMemcpyDefault, d->ce_stream));
-        OC_CUDA(cudaEventRecord(d->ce_done[l], d->ce_stream));
-        OC_CUDA(cudaStreamWaitEvent(s, d->ce_done[l], 0));
+                                      d->geo.S, d->run_len[r], cudaMemcpyDefault, kit.stream));
+        OC_CUDA(cudaEventRecord(kit.ce_done[l], kit.stream));
+        OC_CUDA(cudaStreamWaitEvent(s, kit.ce_done[l], 0));
         int rc = launch_bulk(d, p, l * upl, (l + 1) * upl, s);
         if (rc) return rc;
-        OC_CUDA(cudaEventRecord(d->scat_done[l], s));
+        OC_CUDA(cudaEventRecord(kit.scat_done[l], s));
     }
     OC_CUDA(cudaEventRecord(d->done_ev, s));
     d->poisoned = false;

@@ -177,10 +177,11 @@ struct Desc {
     std::vector<uint64_t> run_first, run_len, run_src;
     void* stage_mem = nullptr;
     uint64_t stage_class = 0;
-    cudaStream_t ce_stream = nullptr;
-    cudaEvent_t ce_start = nullptr;
-    std::vector<cudaEvent_t> ce_done, scat_done;
+    struct CeKit* ce_kit = nullptr;  // copy stream + per-layer events, pooled per (device, L)
 };
+
+// CE engine resources returned to their pool when a descriptor is freed (fetch.cu).
+void ce_release(Desc* d);
 
 // Pooled memory (pool.cpp): power-of-two blocks of device memory on `device`, or of pinned host
 // memory (device = -1), recycled instead of returned to the driver.
