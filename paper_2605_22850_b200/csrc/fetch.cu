@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         if (BATCH) {
             if (threadIdx.x < 32) observe_batch(ba, t0);
         } else if (threadIdx.x == 0) {
-            if (g0 == 0) d0.ts[0] = t0;
+            if (g0 == 0 && !d0.staged) d0.ts[0] = t0;  // CE engine: stamped when the copies start
             observe_layers(d0, g0 / d0.units_per_layer, g1 / d0.units_per_layer);
         }
         return;
@@ -846,6 +846,8 @@ __global__ void __launch_bounds__(32) offload_bulk_kernel(const __grid_constant_
     if (lane == 0) bulk_wait<0>();  // the slots are written before the kernel ends
 }
 
+__global__ void stamp_kernel(uint64_t* ts) { ts[0] = globaltimer(); }
+
 __global__ void wait_geq_kernel(const uint32_t* addr, uint32_t value) {
     while ((int32_t)(ld_acquire(addr) - value) < 0) __nanosleep(256);
 }
@@ -1081,6 +1083,8 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     const uint32_t upl = dd.units_per_layer;
     OC_CUDA(cudaEventRecord(kit.start, s));  // the copies follow the caller's earlier work
     OC_CUDA(cudaStreamWaitEvent(kit.stream, kit.start, 0));
+    stamp_kernel<<<1, 1, 0, kit.stream>>>(dd.ts);  // layer_times()[0] = the start of the copies
+    OC_CUDA(cudaGetLastError());
     for (uint32_t l = 0; l < L; l++) {
         if (l >= 2) OC_CUDA(cudaStreamWaitEvent(kit.stream, kit.scat_done[l - 2], 0));  // stage l&1 free
         uint8_t* stage = (uint8_t*)d->stage_mem + (l & 1) * NS;
