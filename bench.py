@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--serve", type=int, default=0, help="config 5 on one GPU: this many mixed 4K/64K requests "
                    "streaming through a bounded paged pool with FIFO block admission")
     p.add_argument("--no-offload", action="store_true", help="skip the offload (put_from_paged) leg")
+    p.add_argument("--no-p2p", action="store_true", help="N>1: skip the cross-GPU leg (every rank fetches a "
+                   "4K request whose chunks live on the next rank's GPU, NVLink P2P reads)")
     p.add_argument("--sensitivity", action="store_true", help="Fig. 14 analog: TTFT increase at a 10 Gbps vs "
                    "100 Gbps cap, layerwise vs chunkwise, Table A5 cells")
     p.add_argument("--crossover", action="store_true", help="Eq. 2 / Fig. 13 analog: layerwise vs chunkwise "
@@ -368,6 +370,10 @@ def main_ours(args):
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_granularity and not args.profile:
         out["granularity"] = granularity_leg(args, oc, torch, dev, lay_t, fopts)
+    if ws > 1 and not args.no_p2p:                 # every rank: chunks homed on the next GPU (a11)
+        res = p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
+        if rank == 0:
+            out["p2p"] = res
     if args.serve:                                 # every rank serves its share (config 5)
         res = serve_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
         if rank == 0:
@@ -391,6 +397,77 @@ def main_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend="nccl"):
+    """SURVEY 8(a) a11 / config 5's cross-GPU reads: rank r's store holds a 4K-token request's
+    chunks in its HBM; the stores are exchanged once (CUDA IPC export blobs over all_gather_object)
+    and rank r fetches the request homed on rank (r+1) mod N into its own paged cache -- the same
+    fused kernel, its TMA loads crossing NVLink.  All ranks fetch concurrently; time = max over
+    ranks of the device time of K fetches.  GB/s counts r+w (2*N*S*L) per fetch; the NVLink
+    ingress per GPU is half of it.  Rank 0 checks two sampled layers byte for byte against the
+    payload regenerated from the peer's seed."""
+    import synth
+    from paper_2605_22850_b200 import dist as odist
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    N = N_CHUNKS_4K
+    seed_of = lambda r: 31000 + r
+    store = oc.Store(lay_t, capacity=N, tier=oc.TIER_HBM, device=dev.index)
+    (tok,), (ids,) = synth.family_streams(seed_of(rank), G, 0, [N])
+    store.put_chunks(oc.chunk_keys(tok, G), torch.from_numpy(synth.payloads(seed_of(rank), ids, chunk)).to(dev))
+    torch.cuda.synchronize()
+    blobs = odist.exchange_blobs(store.export())
+    src_rank = (rank + 1) % ws
+    peer = oc.Store.import_(blobs[src_rank], device=dev.index)
+    local = oc.Store(lay_t, capacity=1, tier=oc.TIER_HBM, device=dev.index)   # resolves through its peer
+    local.attach_peer(peer)
+    (ptok,), (pids,) = synth.family_streams(seed_of(src_rank), G, 0, [N])
+    keys = local.match_prefix(ptok)
+    need = N * G // Bs
+    bt = synth.block_table(55 + rank, need, need + need // 4)
+    cache = torch.empty((L, 2, need + need // 4, Bs, row), dtype=torch.uint8, device=dev)
+    per_kv = cache.shape[2] * Bs * row
+    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+    tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs, bt, 0)
+    d = oc.build_descriptor(local, keys, lay_t, tgt)
+    s = torch.cuda.Stream(device=dev)
+    steps = max(5, min(args.steps, 50))
+    for _ in range(3):
+        d.fetch_layerwise(s)
+    s.synchronize()
+    ok = None
+    if rank == 0:                                   # sampled check of what crossed NVLink
+        pl = synth.payloads(seed_of(src_rank), pids, chunk)
+        slots = bt[np.arange(N * G) // Bs].astype(np.int64) * Bs + np.arange(N * G) % Bs
+        ok = True
+        for l in (0, L - 1):
+            want = pl[:, l * S:(l + 1) * S].reshape(N, 2, G, row)
+            for kv in (0, 1):
+                got = cache[l, kv].reshape(-1, row)[torch.from_numpy(slots).to(dev)].cpu().numpy()
+                ok &= bool(np.array_equal(got, want[:, kv].reshape(N * G, row)))
+    if ws > 1:
+        torch.distributed.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(steps):
+        d.fetch_layerwise(s)
+    b.record(s)
+    s.synchronize()
+    ms = odist.max_over_ranks(a.elapsed_time(b), device=dev if backend == "nccl" else None)
+    d.close()
+    if ws > 1:
+        torch.distributed.barrier()                 # peers done reading before any store goes away
+    local.close()
+    peer.close()
+    store.close()
+    del cache
+    torch.cuda.empty_cache()
+    rw = 2 * N * S * L
+    return {"workload": f"each rank fetches a 4K-token hit (N={N}) homed on the next rank's GPU",
+            "ranks": ws, "steps": steps, "GBps_rw_aggregate": round(ws * rw * steps / ms / 1e6, 1),
+            "nvlink_ingress_GBps_per_gpu": round(rw / 2 * steps / ms / 1e6, 1),
+            "ms_per_fetch_max_over_ranks": round(ms / steps, 4), "rank0_sampled_layers_bit_exact": ok}
 
 
 def e2e_leg(args, oc, torch, dev, lay_t, fopts, ws=1, backend="nccl"):
