@@ -467,7 +467,8 @@ def p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend="nccl"):
     return {"workload": f"each rank fetches a 4K-token hit (N={N}) homed on the next rank's GPU",
             "ranks": ws, "steps": steps, "GBps_rw_aggregate": round(ws * rw * steps / ms / 1e6, 1),
             "nvlink_ingress_GBps_per_gpu": round(rw / 2 * steps / ms / 1e6, 1),
-            "ms_per_fetch_max_over_ranks": round(ms / steps, 4), "rank0_sampled_layers_bit_exact": ok}
+            "ms_per_fetch_max_over_ranks": round(ms / steps, 4), "rank0_sampled_layers_bit_exact": ok,
+            "peers_share_one_gpu": torch.cuda.device_count() < ws}
 
 
 def e2e_leg(args, oc, torch, dev, lay_t, fopts, ws=1, backend="nccl"):
