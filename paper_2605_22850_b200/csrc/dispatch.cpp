@@ -54,8 +54,14 @@ int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, u
     // bytes of units [0, u) of a request: whole periods of `tiles` units, then a partial period
     auto bytes_upto = [&](uint64_t u) { return (u / tiles) * period + prefix[u % tiles]; };
     std::vector<uint32_t> active;
-    for (uint32_t i = 0; i < n; i++)
+    uint64_t total_units = 0, visits = 0;  // reserve: ~one entry per visit plus one per E units
+    for (uint32_t i = 0; i < n; i++) {
         if (n_units[i]) active.push_back(i);
+        total_units += n_units[i];
+        const uint64_t bytes_i = bytes_upto(n_units[i]);
+        visits += bytes_i / std::max<uint64_t>(1, q[i]) + 1;
+    }
+    out->reserve(total_units / E + visits + 16);
     uint64_t prev_rel = 0;
     auto emit = [&](uint32_t i, uint64_t first, uint64_t cnt) -> int {
         for (uint64_t k = 0; k < cnt; k += E) {
