@@ -382,6 +382,8 @@ struct BatchArgs {
     uint32_t nseg;
     uint32_t tiles;           // units per chunk-layer slice (the same for every member)
     uint32_t pos_block;       // B: positions per block
+    uint32_t pos_claim;       // kByPos: units per claim
+    uint32_t n_units;         // kByPos: units of the launch
 };
 
 struct Resolved {
@@ -607,6 +609,25 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
                 cur_left--;
                 req = cur_req;
                 s_rel[k % 32] = cur_rel;
+            }
+        } else if (MODE == kByPos) {
+            // claims of pos_claim consecutive units of the position-major order: one atomic per
+            // claim, and a CTA streams one member's run of positions
+            if (!exhausted && cur_left == 0) {
+                const uint32_t c = g0 + (next_raw - grab_base);
+                if (c >= g1) {
+                    exhausted = true;
+                } else {
+                    next_raw = atomicAdd(claim_ctr, 1u);
+                    cur_next = c * ba.pos_claim;
+                    cur_left = min(ba.pos_claim, ba.n_units - cur_next);
+                }
+            }
+            if (!exhausted) {
+                const Resolved rs = resolve<MODE>(d0, ba, cur_next++, seg_cache);
+                cur_left--;
+                g = rs.g;
+                req = rs.req;
             }
         } else if (!exhausted) {
             // Each copy CTA stops after its first claim past g1: a launch advances the counter by
@@ -1279,7 +1300,9 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         }
     }
     // WDRR: the claim order (Alg. A2 line 7), uploaded behind a zeroed start-time slot
-    uint64_t n_claims = total * L;  // claim items of the launch: units, or WDRR entries
+    // claim items of the launch: units, WDRR entries, or by-position claims of pos_claim units
+    const uint32_t pos_claim = by_pos ? (uint32_t)std::max(1, env_int("OC_BYPOS_CLAIM", 8)) : 1u;
+    uint64_t n_claims = (total * L + pos_claim - 1) / pos_claim;
     if (wdrr) {
         const DevDesc& d0 = b->descs[0]->dd;
         std::vector<uint64_t> n_units(b->n);
@@ -1334,6 +1357,8 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         // B = ~4 MiB of one request's slices per block (profiles/r01_batch_dram.json)
         const uint64_t blk_bytes = (uint64_t)std::max(1, env_int("OC_BYPOS_BLOCK_KIB", 4096)) << 10;
         ba.pos_block = (uint32_t)std::max<uint64_t>(1, blk_bytes / b->descs[0]->geo.S);
+        ba.pos_claim = pos_claim;
+        ba.n_units = (uint32_t)(total * L);
     }
     if (p.stages < 2) return fail(OC_ENOTSUP, "fetch_batch: two units do not fit in shared memory");
     if (wdrr) {

@@ -41,11 +41,13 @@ SPECS = [(1, 3, "nhd", 16, 0), (2, 7, "hnd", 8, 5), (3, 1, "flat", 16, 0), (4, 1
 
 @pytest.mark.parametrize("lay", [OLayout(3, 2, 64, 2, 16), OLayout(2, 4, 32, 2, 20)])
 @pytest.mark.parametrize("unit_bytes", [0, 1024, 3072])
-@pytest.mark.parametrize("order,blk_kib", [(oc.BATCH_BY_REQUEST, 0), (oc.BATCH_BY_POSITION, 16),
-                                           (oc.BATCH_BY_POSITION, 4096)])
-def test_batch_parity(lay, unit_bytes, order, blk_kib, monkeypatch):
+@pytest.mark.parametrize("order,blk_kib,claim", [(oc.BATCH_BY_REQUEST, 0, 0), (oc.BATCH_BY_POSITION, 16, 3),
+                                                 (oc.BATCH_BY_POSITION, 4096, 8), (oc.BATCH_BY_POSITION, 16, 1)])
+def test_batch_parity(lay, unit_bytes, order, blk_kib, claim, monkeypatch):
     if blk_kib:   # 16 KiB: blocks of 1-2 positions, partial last blocks in every run
         monkeypatch.setenv("OC_BYPOS_BLOCK_KIB", str(blk_kib))
+    if claim:     # units per claim; 3 leaves a ragged last claim
+        monkeypatch.setenv("OC_BYPOS_CLAIM", str(claim))
     st, items = setup_batch(lay, SPECS)
     b = oc.Batch([it["desc"] for it in items], order=order)
     s = torch.cuda.Stream()
