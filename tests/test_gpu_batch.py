@@ -126,7 +126,7 @@ def test_batch_errors():
 
 # ---- WDRR claim order (Alg. A2 lines 6-7) ------------------------------------------------------
 @pytest.mark.parametrize("lay,unit_bytes", [(OLayout(3, 2, 64, 2, 16), 0), (OLayout(2, 4, 32, 2, 20), 3072),
-                                            (OLayout(2, 4, 32, 2, 20), 1024)])
+                                            (OLayout(2, 4, 32, 2, 20), 1024), (OLayout(1, 1, 16, 2, 8), 0)])
 @pytest.mark.parametrize("hold", [False, True])
 @pytest.mark.parametrize("E", [0, 1, 3])
 def test_wdrr_parity(lay, unit_bytes, hold, E):
@@ -287,3 +287,19 @@ def test_batch_shared_prefix_family(order, blk_kib, monkeypatch):
             check(lay, items)
         b.close()
         assert oc._lib.oc_batch_set_order(None, 1) == oc.OC_EINVAL
+
+
+def test_wdrr_single_member_batch():
+    """n = 1: WDRR degenerates to the member's own layer-major order (held rate or not)."""
+    lay = OLayout(2, 2, 64, 2, 16)
+    st, items = setup_batch(lay, SPECS[1:2])
+    b = oc.Batch([items[0]["desc"]])
+    s = torch.cuda.Stream()
+    for hold in (False, True):
+        with torch.cuda.stream(s):
+            items[0]["buf"].fill_(0xA5)
+        b.fetch(s, wdrr_weights=[2e9], hold_rates=hold, entry_units=1)
+        s.synchronize()
+        check(lay, items)
+    b.close()
+    st.close()
