@@ -48,7 +48,26 @@ def build(force=False, verbose=False):
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
+    build_demo(force, verbose)
     return LIB
+
+
+DEMO_SRC = os.path.join(ROOT, "examples", "fetch_demo.c")
+DEMO = os.path.join(ROOT, "examples", "fetch_demo")
+CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
+
+
+def build_demo(force=False, verbose=False):
+    """The C-ABI usage example (examples/fetch_demo.c): plain C, linked against libobjcache.so."""
+    if not os.path.exists(DEMO_SRC) or not (force or _newer(DEMO, [DEMO_SRC, LIB])):
+        return DEMO
+    cmd = ["gcc", "-O2", "-Wall", "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(CUDA_HOME, "include"),
+           DEMO_SRC, "-o", DEMO, "-L" + HERE, "-lobjcache", "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcudart",
+           "-Wl,-rpath," + HERE + ":" + os.path.join(CUDA_HOME, "lib64")]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return DEMO
 
 
 if __name__ == "__main__":
