@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--serve", type=int, default=0, help="config 5 on one GPU: this many mixed 4K/64K requests "
                    "streaming through a bounded paged pool with FIFO block admission")
     p.add_argument("--no-offload", action="store_true", help="skip the offload (put_from_paged) leg")
+    p.add_argument("--no-config3", action="store_true", help="skip BASELINE config 3 (64K-token hit, 8 GiB: "
+                   "HBM store vs pinned-host store with SM zero-copy and copy-engine paths)")
     p.add_argument("--no-p2p", action="store_true", help="N>1: skip the cross-GPU leg (every rank fetches a "
                    "4K request whose chunks live on the next rank's GPU, NVLink P2P reads)")
     p.add_argument("--sensitivity", action="store_true", help="Fig. 14 analog: TTFT increase at a 10 Gbps vs "
@@ -380,6 +382,8 @@ def main_ours(args):
             out["serve"] = res
     if rank == 0 and not args.no_offload and not args.profile:
         out["offload"] = offload_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and not args.no_config3 and not args.profile:
+        out["config3"] = config3_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.sensitivity:
         out["sensitivity"] = sensitivity_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.crossover:
@@ -397,6 +401,77 @@ def main_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
+
+
+def config3_leg(args, oc, torch, dev, lay_t):
+    """BASELINE config 3: Llama-3-8B layout, one request with a 64K-token prefix hit (N = 4096
+    chunks, 8 GiB of KV), from an HBM store and from a pinned-host store (SM zero-copy reads and the
+    copy-engine path), into a fragmented paged cache.  GB/s counts r+w (2*N*S*L) per fetch; the
+    pinned rows also give the PCIe read rate against an in-harness pinned->device copy of 1 GiB."""
+    import synth
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    N = 65536 // G
+    need = N * G // Bs
+    cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
+    per_kv = need * Bs * row
+    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+    tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+                         synth.block_table(64, need, need), 0)
+    (tok,), _ = synth.family_streams(6464, G, 0, [N])
+    keys = oc.chunk_keys(tok, G)
+    h = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()      # in-harness PCIe reference
+    dd = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    best_h2d = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dd.copy_(h, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best_h2d = max(best_h2d, (1 << 30) / a.elapsed_time(b) / 1e6)
+    del h, dd
+    peak, _ = peaks()
+    rw = 2 * N * S * L
+    out = {"workload": f"llama3-8b KV layout, one request, 64K-token prefix hit (N={N}, {N * chunk / 2**30:.0f} GiB)",
+           "h2d_copy_GBps": round(best_h2d, 1)}
+    gen = torch.Generator(device=dev).manual_seed(64)
+    for tier_name, tier, engines in (("hbm", oc.TIER_HBM, (("bulk", oc.COPY_BULK),)),
+                                     ("pinned_host", oc.TIER_PINNED_HOST, (("bulk_zero_copy", oc.COPY_BULK),
+                                                                           ("copy_engine", oc.COPY_CE)))):
+        store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
+        for b0 in range(0, N, 512):
+            pl = torch.randint(0, 256, (512, chunk), dtype=torch.uint8, device=dev, generator=gen)
+            store.put_chunks(keys[b0:b0 + 512], pl)
+            del pl
+        d = oc.build_descriptor(store, keys, lay_t, tgt)
+        s = torch.cuda.Stream(device=dev)
+        for eng_name, eng in engines:
+            d.fetch_layerwise(s, engine=eng)
+            s.synchronize()
+            ms = []
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                d.fetch_layerwise(s, engine=eng)
+                b.record(s)
+                s.synchronize()
+                ms.append(a.elapsed_time(b))
+            t = min(ms)
+            t_ = d.layer_times().astype(np.int64)
+            row_out = {"ms": round(t, 3), "GBps_rw": round(rw / t / 1e6, 1), "X0_ms": round((t_[1] - t_[0]) / 1e6, 4)}
+            if tier == oc.TIER_HBM:
+                row_out["frac_of_hbm_peak"] = round(rw / t / 1e6 / peak, 3)
+            else:
+                row_out["pcie_read_GBps"] = round(rw / 2 / t / 1e6, 1)
+                row_out["frac_of_h2d_copy"] = round(rw / 2 / t / 1e6 / best_h2d, 3)
+            out[f"{tier_name}_{eng_name}"] = row_out
+        d.close()
+        store.close()
+        torch.cuda.empty_cache()
+    del cache
+    torch.cuda.empty_cache()
+    return out
 
 
 def p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend="nccl"):
