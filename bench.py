@@ -68,6 +68,9 @@ def parse():
                    "added TTFT over 1K-64K contexts, HBM and pinned-host tiers")
     p.add_argument("--sweep", action="store_true", help="rate sweep (Fig. 15 analog): added TTFT of one "
                    "paced request vs rate / r*, against Eq. 3 (adds a 'sweep' object)")
+    p.add_argument("--pool", type=int, default=0, help="streaming multi-tenant runtime: this many requests "
+                   "arrive over time (Poisson) into oc.TenantPool epochs (100 ms) under a shared cap, per policy "
+                   "and dispatch (adds a 'pool' object)")
     p.add_argument("--batch", default="", help="NxM: N 4K-token + M 64K-token concurrent requests (config 5, "
                    "one GPU): one batched launch vs per-request launches (adds a 'batch' object)")
     p.add_argument("--sched", default="", help="comma list of paper scheduler workloads to run (A,B,C): "
@@ -370,6 +373,8 @@ def main_ours(args):
         out["sched"] = sched_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.batch:
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and args.pool:
+        out["pool"] = pool_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_granularity and not args.profile:
         out["granularity"] = granularity_leg(args, oc, torch, dev, lay_t, fopts)
     if ws > 1 and not args.no_p2p:                 # every rank: chunks homed on the next GPU (a11)
@@ -1447,6 +1452,102 @@ def sched_workloads():
     w["70B"] = (synth.LLAMA3_70B, round(sum_rstar / 2 * 8 / 1e9, 3), c70,
                 "FLOP model at 50% of the measured sustained bf16 rate (B200)")
     return w
+
+
+def pool_leg(args, oc, torch, dev, lay_t, epoch_s=0.1, cap_gbps=50.0, delta_gbps=5.0):
+    """Alg. A2 as a running system (Sec. 3.6): requests arrive over time (Poisson) and
+    are submitted to an oc.TenantPool; every 100 ms (reading c16) the host calls pool.epoch(), which
+    retires finished requests, admits the waiting ones under the cap the running ones leave (rates
+    from the policy), and launches them -- as independently paced fetches, or as one WDRR batch per
+    epoch with held rates.  Chunks live in the pinned-host tier (PCIe as the shared link); each
+    request's consumer runs wait_layer(l) + a compute window c_i per layer (Table A5 windows).
+    TTFT_i = end of its last window - its arrival, both stamped on the GPU clock; the no-limit TTFT
+    is L * c_i.  Reported per (policy, dispatch): mean / p50 / p90 TTFT and the sum of added TTFT."""
+    import synth
+    GB = 1e9 / 8
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    cells = [(16384, 0.5), (16384, 0.875), (32768, 0.5), (32768, 0.875), (65536, 0.5), (65536, 0.875)]
+    R = args.pool
+    rng = np.random.default_rng(2605)
+    kinds = [cells[i % len(cells)] for i in rng.permutation(R)]
+    bytes_total = sum(int(c * h) // G * S * L for c, h in kinds)
+    mean_gap = bytes_total / (cap_gbps * GB) / R / 0.9      # offered load ~0.9 of the cap
+    arrivals = np.cumsum(rng.exponential(mean_gap, R))
+    arrivals -= arrivals[0]
+    n_max = max(int(c * h) // G for c, h in kinds)
+    store = oc.Store(lay_t, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
+    (tok,), _ = synth.family_streams(4343, G, 0, [n_max])
+    keys = oc.chunk_keys(tok, G)
+    gen = torch.Generator(device=dev).manual_seed(4343)
+    for b0 in range(0, n_max, 128):
+        b1 = min(n_max, b0 + 128)
+        pl = torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
+        store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
+        del pl
+    caches = {}
+    for c, h in set(kinds):                                  # one destination per kind, reused
+        N = int(c * h) // G
+        need = N * G // Bs
+        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
+        per_kv = need * Bs * row
+        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+        caches[(c, h)] = (cache, oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3],
+                                                Bs, synth.block_table(N, need, need), 0))
+    copy_streams = [torch.cuda.Stream(device=dev) for _ in range(R)]
+    cons_streams = [torch.cuda.Stream(device=dev) for _ in range(R)]
+    stamps = torch.zeros((R, L + 1, 2), dtype=torch.int64, device=dev)
+
+    def run(policy, dispatch):
+        pool = oc.TenantPool(policy, cap_gbps * GB, delta_gbps * GB, 0, dispatch=dispatch)
+        torch.cuda.synchronize()
+        descs, tickets, chained = [None] * R, [None] * R, [False] * R
+        c_of = [TABLE_A5_T_TOTAL_MS[k] / L / 1e3 for k in kinds]
+        t0 = time.perf_counter()
+        nxt, next_epoch = 0, 0.0
+        while True:
+            now = time.perf_counter() - t0
+            while nxt < R and arrivals[nxt] <= now:
+                i = nxt
+                c, h = kinds[i]
+                N = int(c * h) // G
+                descs[i] = oc.build_descriptor(store, keys[:N], lay_t, caches[(c, h)][1])
+                oc.emulate_compute(0, cons_streams[i], stamps[i, 0])          # arrival stamp
+                tickets[i] = pool.submit(descs[i], c_of[i], copy_streams[i])
+                nxt += 1
+            if now >= next_epoch:
+                pool.epoch()
+                next_epoch += epoch_s
+                for i in range(nxt):
+                    if not chained[i] and pool.status(tickets[i])[0] != oc.TENANT_WAITING:
+                        for l in range(L):                    # prefill of layer l after its KV
+                            descs[i].wait_layer(l, cons_streams[i])
+                            oc.emulate_compute(int(c_of[i] * 1e9), cons_streams[i], stamps[i, 1 + l])
+                        chained[i] = True
+            if nxt == R and all(chained):
+                break
+            time.sleep(0.002)
+        torch.cuda.synchronize()
+        st = stamps.cpu().numpy().astype(np.int64)
+        ttft = (st[:, L, 1] - st[:, 0, 0]) / 1e6
+        base = np.array([L * c * 1e3 for c in c_of])
+        pool.close()
+        for d in descs:
+            d.close()
+        return {"ttft_ms_mean": round(float(ttft.mean()), 1), "ttft_ms_p50": round(float(np.median(ttft)), 1),
+                "ttft_ms_p90": round(float(np.percentile(ttft, 90)), 1),
+                "added_ms_sum": round(float((ttft - base).sum()), 1)}
+
+    out = {"requests": R, "cap_gbps": cap_gbps, "delta_gbps": delta_gbps, "epoch_ms": epoch_s * 1e3,
+           "offered_load_of_cap": 0.9, "mix": "Workload C cells (16K/32K/64K x 50%/87.5%), Table A5 windows",
+           "runs": {}}
+    for policy in ("equal", "stall_opt", "cal_stall_opt"):
+        for dname, disp in (("independent", oc.DISPATCH_INDEPENDENT), ("wdrr", oc.DISPATCH_WDRR)):
+            out["runs"][f"{policy}/{dname}"] = run(policy, disp)
+    store.close()
+    del caches
+    torch.cuda.empty_cache()
+    return out
 
 
 def sched_leg(args, oc, torch, dev, lay_t):
