@@ -232,6 +232,11 @@ typedef struct {
     double pace_Bps;         /* minimal pacer: layer l is released no
                                 earlier than t0 + l*(N*S)/pace_Bps; 0 = off.
                                 PERSISTENT mode only.                           */
+    uint32_t pace_strict;    /* 1: byte-granular pacing instead -- byte b of the
+                                fetch (layer-major) is released no earlier than
+                                t0 + b/pace_Bps, so the request never exceeds its
+                                rate (the held rate of Alg. A2 line 6)          */
+    uint32_t reserved;       /* 0 */
 } oc_fetch_opts;
 
 /* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and

@@ -59,7 +59,8 @@ class CTarget(ctypes.Structure):
 
 class CFetchOpts(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_uint32), ("engine", ctypes.c_uint32), ("max_ctas", ctypes.c_uint32),
-                ("unit_bytes", ctypes.c_uint32), ("pace_Bps", ctypes.c_double)]
+                ("unit_bytes", ctypes.c_uint32), ("pace_Bps", ctypes.c_double), ("pace_strict", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
 
 
 class CWdrrOpts(ctypes.Structure):
@@ -370,8 +371,9 @@ class Descriptor:
         return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
 
     def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_BULK, max_ctas=0, unit_bytes=0,
-                        pace_Bps=0.0):
-        o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps))
+                        pace_Bps=0.0, pace_strict=False):
+        o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
+                       1 if pace_strict else 0, 0)
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))
 
     def wait_layer(self, layer: int, stream=None):

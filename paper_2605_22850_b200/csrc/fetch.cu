@@ -657,10 +657,16 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     };
     // kSingle: minimal pacer, layer l released at t0 + l * pace.  kWdrr: the entry's
     // release time after the launch's start (Alg. A2 line 6, reading c22).
-    const bool paced = MODE == kSingle ? d0.pace_ns != 0 : (MODE == kWdrr && ba.paced != 0);
+    const bool paced = MODE == kSingle ? (d0.pace_ns != 0 || d0.pace_ns_per_byte > 0.0)
+                                       : (MODE == kWdrr && ba.paced != 0);
     auto release_time = [&](uint32_t k) -> uint64_t {
         if (MODE == kWdrr) return t_start + (uint64_t)s_rel[k % 32] * 1000ull;
         const DevDesc& d = desc_of(k);
+        if (d.pace_ns_per_byte > 0.0) {  // strict: the unit's first byte in the layer-major fetch
+            const UnitGeo u = unit_geo(d, s_unit[k % 32]);
+            const double b = (double)u.layer * d.N * d.S + (double)u.j * d.S + (double)u.q0 * d.row;
+            return t0 + (uint64_t)(b * d.pace_ns_per_byte);
+        }
         return t0 + (uint64_t)fdiv(s_unit[k % 32], d.div_upl) * d.pace_ns;
     };
     // Retired units are batched per (request, layer): one record per change.
@@ -1094,6 +1100,7 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     dd.epoch = epoch;
     dd.cnt_target = d->cnt_base + dd.units_per_layer;
     dd.pace_ns = 0;
+    dd.pace_ns_per_byte = 0.0;
     dd.staged = 1;
     dd.stage_base[0] = (uint64_t)d->stage_mem;
     dd.stage_base[1] = (uint64_t)d->stage_mem + NS;
@@ -1136,6 +1143,8 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     if (o.pace_Bps < 0) return fail(OC_EINVAL, "fetch_layerwise: pace must be >= 0");
     if (o.pace_Bps > 0 && o.mode != OC_FETCH_PERSISTENT)
         return fail(OC_ENOTSUP, "fetch_layerwise: pacing needs PERSISTENT mode");
+    if (o.pace_Bps > 0 && o.pace_strict && o.engine != OC_COPY_BULK)
+        return fail(OC_ENOTSUP, "fetch_layerwise: strict pacing needs the BULK engine");
     if (d->poisoned) return fail(OC_ECUDA, "fetch_layerwise: descriptor unusable after a failed launch");
     DeviceGuard dg(d->device);
     int urc = upload_order(&d->up, s);  // the kernel reads the descriptor block
@@ -1162,7 +1171,8 @@ int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     if (epoch == 0) epoch = 1;  // epochs count from 1: layer l of epoch e is ready at (e-1)*L + l + 1
     dd.epoch = epoch;
     dd.cnt_target = d->cnt_base + dd.units_per_layer;  // the unit size may change between fetches
-    dd.pace_ns = o.pace_Bps > 0 ? (uint64_t)((double)d->N * d->geo.S / o.pace_Bps * 1e9) : 0;
+    dd.pace_ns = o.pace_Bps > 0 && !o.pace_strict ? (uint64_t)((double)d->N * d->geo.S / o.pace_Bps * 1e9) : 0;
+    dd.pace_ns_per_byte = o.pace_Bps > 0 && o.pace_strict ? 1e9 / o.pace_Bps : 0.0;
     const int sms = device_sm_count(d->device);
     // From the first launch on, the device counters belong to this epoch.
     d->epoch = epoch;
@@ -1264,6 +1274,7 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         dd.epoch = epoch;
         dd.cnt_target = d->cnt_base + dd.units_per_layer;
         dd.pace_ns = 0;
+        dd.pace_ns_per_byte = 0.0;
         dd.staged = 0;
         st[i] = dd;
         total += dd.units_per_layer;

@@ -139,6 +139,7 @@ struct DevDesc {
     uint32_t cnt_target;      // unit_cnt[l] value once this fetch's units of layer l are done
     uint32_t chunk_major;     // 1: only the completion of the whole prefix is announced
     uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
+    double pace_ns_per_byte;  // strict pacing: unit released at t0 + (fetch bytes before it) * this
     uint64_t stage_base[2];   // CE engine: layer l's slices were staged at stage_base[l & 1] as [N][S]
     uint32_t staged;          // 1: read sources from stage_base (CE engine), 0: from src[]
     FastDiv div_upl;          // units_per_layer

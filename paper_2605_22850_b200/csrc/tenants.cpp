@@ -6,8 +6,8 @@
 // layerwise requests under a fixed total budget, gives each a stable target rate for the whole of
 // its KV load (Stall-opt / Calibrated Stall-opt or a baseline policy), and bandwidth released by
 // a request that finishes early returns to the pool only at the next epoch.  Dispatch:
-//   INDEPENDENT  each admitted request is its own fetch, paced by the kernel's minimal pacer (a10):
-//                layer l released at t0 + l * N*S / r;
+//   INDEPENDENT  each admitted request is its own fetch, paced byte by byte at its rate (byte b
+//                released at t0 + b / r; the minimal layer pacer of a10 would let each layer burst);
 //   WDRR         the epoch's admitted requests are one batched launch whose claim order is
 //                weighted deficit round robin with weights r_i, each request held at r_i
 //                (Alg. A2 lines 6-7; dispatch.cpp), on the first admitted request's stream.
@@ -173,6 +173,7 @@ OC_API int oc_pool_epoch(oc_tenant_pool* h, uint64_t* n_admitted) {
         o.mode = OC_FETCH_PERSISTENT;
         o.engine = OC_COPY_BULK;
         o.pace_Bps = rates[k];
+        o.pace_strict = 1;  // a held rate (Alg. A2 line 6): never above r_i, not only on average
         rc = oc::launch_fetch(t.desc, o, t.stream);
         if (rc) return rc;
         t.rate = rates[k];

@@ -98,3 +98,29 @@ def test_chunkwise_delivery_holds_every_window():
         assert start[0] >= t[L] - t[0]
         assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 33, req, dest))
         d.close()
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_pacer_release_schedule(strict):
+    """Minimal pacer (c20): layer l starts at t0 + l*X and is copied at full speed, so it is ready
+    just after l*X.  Strict pacing: byte b is released at t0 + b/r, so layer l (8 units) is ready
+    only after its last unit's release at l*X + 7X/8."""
+    lay = OLayout(8, 2, 64, 2, 16)
+    L = lay.num_layers
+    X = 0.5e-3
+    with oc.Store(lay, capacity=8) as st:
+        req, dest, buf, d = _setup(st, lay, 41, 8)
+        s = torch.cuda.Stream()
+        d.fetch_layerwise(s, pace_Bps=8 * chunk_layer_bytes(lay) / X, pace_strict=strict)
+        d.sync_layer(L - 1)
+        t = d.layer_times().astype(np.int64)
+        ready = (t[1:] - t[0]) / 1e9
+        for l in range(L):
+            lo = l * X + (7 * X / 8 if strict else 0.0)
+            assert lo - 20e-6 <= ready[l] <= lo + 150e-6, (l, ready[l], lo)
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 41, req, dest))
+        with pytest.raises(oc.ObjcacheError) as e:
+            d.fetch_layerwise(s, pace_Bps=1e9, pace_strict=True, engine=oc.COPY_LDST)
+        assert e.value.code == oc.OC_ENOTSUP
+        d.close()
