@@ -23,6 +23,11 @@ struct Tenant {
     cudaStream_t stream;  // the request's copy stream
     double rate = 0;      // assigned at admission (bytes/s); 0 while waiting or if chunkwise
     int state = 0;        // OC_TENANT_*
+    // WDRR members share one launch, whose completion event fires only when the LAST member is
+    // done; a member's own completion is its last layer's ready word, turned into an event on a
+    // private stream so its bandwidth returns at the next epoch after IT finishes.
+    cudaStream_t done_stream = nullptr;
+    cudaEvent_t layers_done = nullptr;
 };
 
 struct TenantPool {
@@ -109,7 +114,7 @@ OC_API int oc_pool_epoch(oc_tenant_pool* h, uint64_t* n_admitted) {
     for (auto& t : p->tenants) {
         if (t.state != OC_TENANT_RUNNING) continue;
         oc::DeviceGuard dg(t.desc->device);
-        cudaError_t e = cudaEventQuery(t.desc->done_ev);
+        cudaError_t e = cudaEventQuery(t.layers_done ? t.layers_done : t.desc->done_ev);
         if (e == cudaSuccess) {
             t.state = OC_TENANT_DONE;
         } else if (e == cudaErrorNotReady) {
@@ -161,8 +166,15 @@ OC_API int oc_pool_epoch(oc_tenant_pool* h, uint64_t* n_admitted) {
         }
         p->batches.push_back({b, waiting});
         for (size_t k = 0; k < waiting.size(); k++) {
-            p->tenants[waiting[k]].rate = rates[k];
-            p->tenants[waiting[k]].state = OC_TENANT_RUNNING;
+            oc::Tenant& t = p->tenants[waiting[k]];
+            t.rate = rates[k];
+            t.state = OC_TENANT_RUNNING;
+            oc::DeviceGuard dg(t.desc->device);
+            if (!t.done_stream) OC_CUDA(cudaStreamCreateWithFlags(&t.done_stream, cudaStreamNonBlocking));
+            if (!t.layers_done) OC_CUDA(cudaEventCreateWithFlags(&t.layers_done, cudaEventDisableTiming));
+            rc = oc_wait_layer((oc_desc*)t.desc, t.desc->geo.L - 1, t.done_stream);
+            if (rc) return rc;
+            OC_CUDA(cudaEventRecord(t.layers_done, t.done_stream));
         }
         if (n_admitted) *n_admitted = waiting.size();
         return OC_OK;
@@ -197,6 +209,13 @@ OC_API int oc_pool_status(oc_tenant_pool* h, uint64_t ticket, int* state, double
 OC_API int oc_pool_destroy(oc_tenant_pool* h) {
     if (!h) return OC_OK;
     for (auto& eb : ((oc::TenantPool*)h)->batches) oc_batch_free(eb.batch);  // waits for its launch
+    for (auto& t : ((oc::TenantPool*)h)->tenants) {
+        if (t.done_stream) {
+            cudaStreamSynchronize(t.done_stream);
+            cudaStreamDestroy(t.done_stream);
+        }
+        if (t.layers_done) cudaEventDestroy(t.layers_done);
+    }
     delete (oc::TenantPool*)h;
     return OC_OK;
 }
