@@ -935,8 +935,9 @@ def serve_leg(args, oc, torch, dev, lay_t, ws=1, rank=0, backend="nccl"):
 
     run()                                               # warm-up pass (descriptor pool, modules)
     total_bytes, dev_ms, host_s, fetch_us, waits = run()
-    run_batched()
-    tb_b, dev_ms_b, host_s_b, n_batches, sizes = run_batched()
+    mb = int(os.environ.get("OC_SERVE_MAX_BATCH", "64"))
+    run_batched(mb)
+    tb_b, dev_ms_b, host_s_b, n_batches, sizes = run_batched(mb)
     red_dev = dev if backend == "nccl" else None
     max_ms = odist.max_over_ranks(dev_ms, device=red_dev)
     all_bytes = odist.sum_over_ranks(total_bytes, device=red_dev)
@@ -954,7 +955,7 @@ def serve_leg(args, oc, torch, dev, lay_t, ws=1, rank=0, backend="nccl"):
            "admission_stalls_rank0": waits}
     max_ms_b = odist.max_over_ranks(dev_ms_b, device=red_dev)
     res["batched_by_position"] = {
-        "how": "each admission step launches its admitted requests (<= 64) as one position-major batch",
+        "how": f"each admission step launches its admitted requests (<= {mb}) as one position-major batch",
         "GBps_device": round(odist.sum_over_ranks(tb_b, device=red_dev) / max_ms_b / 1e6, 1),
         "GBps_rank0_host_wall": round(tb_b / host_s_b / 1e9, 1),
         "device_ms_max_over_ranks": round(max_ms_b, 2), "batches_rank0": n_batches,
