@@ -935,7 +935,7 @@ def serve_leg(args, oc, torch, dev, lay_t, ws=1, rank=0, backend="nccl"):
 
     run()                                               # warm-up pass (descriptor pool, modules)
     total_bytes, dev_ms, host_s, fetch_us, waits = run()
-    mb = int(os.environ.get("OC_SERVE_MAX_BATCH", "64"))
+    mb = int(os.environ.get("OC_SERVE_MAX_BATCH", "16"))    # profiles/r01_serve.json: 4..64 swept
     run_batched(mb)
     tb_b, dev_ms_b, host_s_b, n_batches, sizes = run_batched(mb)
     red_dev = dev if backend == "nccl" else None
