@@ -10,7 +10,7 @@ from scenario import lib_target, make_dest, oracle_result, payload_stack, reques
 
 lay = Layout(2, 2, 64, 2, 16)
 ok = 0
-SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3").split(",")
+SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3,4").split(",")
 for kind in (("nhd", "hnd") if "1" in SECTIONS else ()):
     for engine in (oc.COPY_BULK, oc.COPY_LDST):
         for mode in (oc.FETCH_PERSISTENT, oc.FETCH_PER_LAYER):
@@ -104,5 +104,25 @@ with oc.Store(lay, capacity=24) as st:
       b.close()
       for it in items:
           it[4].close()
+# the copy-engine path from a pinned-host store (two runs of slots), and strict pacing
+if "4" in SECTIONS:
+    fam = requests_family(lay, 8, 4, [2, 3])
+    with oc.Store(lay, capacity=16, tier=oc.TIER_PINNED_HOST) as st:
+        ka, kb = (oc.chunk_keys(r.tokens, 16) for r in fam)
+        st.put_chunks(ka, payload_stack(lay, 8, fam[0].payload_ids))
+        st.put_chunks(kb, payload_stack(lay, 8, fam[1].payload_ids))
+        dest = make_dest(lay, fam[1].n_chunks, "hnd", Bs=8, first_token=2, seed=9)
+        buf = sentinel_buffer(dest.size)
+        d = oc.build_descriptor(st, kb, lay, lib_target(oc, dest, buf.data_ptr()))
+        s = torch.cuda.Stream()
+        for opts in ({"engine": oc.COPY_CE}, {"pace_Bps": 2e9, "pace_strict": True}, {"engine": oc.COPY_CE}):
+            with torch.cuda.stream(s):
+                buf.fill_(0xA5)
+            d.fetch_layerwise(s, **opts)
+            d.sync_layer(1)
+            s.synchronize()
+            assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 8, fam[1], dest)), opts
+            ok += 1
+        d.close()
 torch.cuda.synchronize()
 print("sanitize workload ok", ok)
