@@ -212,6 +212,9 @@ typedef enum {
 typedef enum {
     OC_COPY_LDST = 0,        /* 16-byte vector loads/stores through registers */
     OC_COPY_BULK = 1,        /* TMA bulk copies through a shared-memory ring  */
+    OC_COPY_AUTO = 3,        /* BULK when destination rows are contiguous (NHD, flat
+                                target) or strict pacing is asked for, else LDST
+                                (head-split targets such as HND); the default   */
     OC_COPY_CE = 2,          /* pinned-host chunks only (ENOTSUP otherwise): per layer, one
                                 strided copy-engine transfer per run of consecutive store slots
                                 into a double-buffered HBM stage (2*N*S bytes, owned by the
@@ -242,7 +245,7 @@ typedef struct {
 /* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and
  * return at once.  One fetch may be in flight per descriptor at a time; a
  * second fetch must be ordered after the first (same stream or an event).
- * opts = NULL selects the defaults (persistent, BULK, auto grid, unpaced). */
+ * opts = NULL selects the defaults (persistent, AUTO engine, auto grid, unpaced). */
 OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* copy_stream);
 
 /* Batches: concurrent requests (P:467-598 treats them as tenants sharing one link) fetched by

@@ -35,7 +35,7 @@ FETCH_PERSISTENT, FETCH_PER_LAYER = 0, 1
 TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
 BATCH_BY_REQUEST, BATCH_BY_POSITION = 0, 1
-COPY_LDST, COPY_BULK, COPY_CE = 0, 1, 2
+COPY_LDST, COPY_BULK, COPY_CE, COPY_AUTO = 0, 1, 2, 3
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -370,7 +370,7 @@ class Descriptor:
         _check(_lib.oc_desc_info(self._h, ctypes.byref(n), ctypes.byref(W), ctypes.byref(u)))
         return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
 
-    def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_BULK, max_ctas=0, unit_bytes=0,
+    def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_AUTO, max_ctas=0, unit_bytes=0,
                         pace_Bps=0.0, pace_strict=False):
         o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
                        1 if pace_strict else 0, 0)

@@ -1134,9 +1134,16 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     return OC_OK;
 }
 
-int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
+int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
+    oc_fetch_opts o = oin;
     if (o.mode != OC_FETCH_PERSISTENT && o.mode != OC_FETCH_PER_LAYER)
         return fail(OC_EINVAL, "fetch_layerwise: unknown mode");
+    // AUTO: the TMA engine where destination rows are contiguous (NHD, flat); with a head-split
+    // target (HND) every row becomes n_kv stores of d*p bytes, which holds the TMA engine to
+    // 4.2 TB/s at 4K while 16-byte LD/ST streams at 6.3 (profiles/r01_hnd_probe.txt).  Strict
+    // pacing exists only in the TMA engine.
+    if (o.engine == OC_COPY_AUTO)
+        o.engine = (d->dd.nhd || (o.pace_Bps > 0 && o.pace_strict)) ? OC_COPY_BULK : OC_COPY_LDST;
     if (o.engine == OC_COPY_CE) return launch_fetch_ce(d, o, s);
     if (o.engine != OC_COPY_LDST && o.engine != OC_COPY_BULK) return fail(OC_EINVAL, "fetch_layerwise: unknown engine");
     d->dd.staged = 0;
@@ -1246,7 +1253,8 @@ int ensure_ent_capacity(Batch* b, size_t bytes) {
 
 int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cudaStream_t s) {
     if (o.mode != OC_FETCH_PERSISTENT) return fail(OC_ENOTSUP, "fetch_batch: batches use PERSISTENT mode");
-    if (o.engine != OC_COPY_BULK) return fail(OC_ENOTSUP, "fetch_batch: batches use the BULK engine");
+    if (o.engine != OC_COPY_BULK && o.engine != OC_COPY_AUTO)
+        return fail(OC_ENOTSUP, "fetch_batch: batches use the BULK engine");
     if (o.pace_Bps != 0)
         return fail(OC_ENOTSUP, "fetch_batch: pace_Bps is per request (fetch_layerwise); WDRR batches use hold_rates");
     for (Desc* d : b->descs)
@@ -1407,7 +1415,7 @@ OC_API int oc_fetch_layerwise(oc_desc* h, const oc_fetch_opts* opts, void* strea
     if (!h) return oc::fail(OC_EINVAL, "fetch_layerwise: null descriptor");
     oc_fetch_opts o{};
     o.mode = OC_FETCH_PERSISTENT;
-    o.engine = OC_COPY_BULK;
+    o.engine = OC_COPY_AUTO;
     if (opts) o = *opts;
     return oc::launch_fetch((Desc*)h, o, (cudaStream_t)stream);
 }
