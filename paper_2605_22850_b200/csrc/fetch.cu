@@ -54,14 +54,6 @@ __device__ __forceinline__ void st_global(uint64_t addr, const uint4& v) {
                  : "memory");
 }
 
-__device__ __forceinline__ uint4 ld_shared_v4(const void* p) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
-    return v;
-}
-
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -726,38 +718,16 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
                     bulk_store(dst, sbuf + (size_t)r * d.row, (uint32_t)(len * d.row));
                 }
             }
-        } else {
-            // Head-split target (e.g. HND): a row is n_kv pieces of d*p bytes in different places.
-            // One TMA store per piece (256 B at Llama layouts) holds the engine to ~4.2 TB/s, so
-            // the warp writes the staged unit itself with 16-byte stores (shared -> registers ->
-            // global), 8 vectors in flight per lane.  These generic stores are ordered before the
-            // unit's completion count by the warp barrier, the FIFO's mbarrier and the signaler's
-            // GPU-scope release fence.
-            const uint32_t nvec = u.nrows * d.vpr;
-            const uint32_t hdv = d.div_hdv.d;
-            for (uint32_t v0 = 0; v0 < nvec; v0 += 32 * 8) {
-                uint4 val[8];
-#pragma unroll
-                for (int t = 0; t < 8; t++) {
-                    const uint32_t v = v0 + lane + 32u * t;
-                    if (v < nvec) val[t] = ld_shared_v4(sbuf + (size_t)v * 16);
-                }
-#pragma unroll
-                for (int t = 0; t < 8; t++) {
-                    const uint32_t v = v0 + lane + 32u * t;
-                    if (v < nvec) {
-                        const uint32_t r = fdiv(v, d.div_vpr);
-                        const uint32_t c = v - r * d.vpr;
-                        const uint32_t h = fdiv(c, d.div_hdv);
-                        const uint64_t dst = row_addr(d, u.layer, u.j, u.q0 + r, nullptr) + (uint64_t)h * d.head_stride +
-                                             (uint64_t)(c - h * hdv) * 16;
-                        st_global(dst, val[t]);
-                    }
-                }
+        } else {  // one store per (row, head)
+            const uint32_t hdv = d.div_hdv.d;  // 16-byte pieces per head
+            const uint32_t heads = d.vpr / hdv;
+            const uint32_t hbytes = hdv * 16;
+            for (uint32_t p = lane; p < u.nrows * heads; p += 32) {
+                const uint32_t r = p / heads;
+                const uint32_t h = p - r * heads;
+                const uint64_t dst = row_addr(d, u.layer, u.j, u.q0 + r, nullptr) + (uint64_t)h * d.head_stride;
+                bulk_store(dst, sbuf + (size_t)r * d.row + (size_t)h * hbytes, hbytes);
             }
-            // the stage is read by generic loads; the TMA load that next overwrites it is an
-            // async-proxy write
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         bulk_commit();
         bulk_wait_read<1>();  // unit k-1's stage is free once its stores have read shared memory
