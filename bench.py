@@ -60,8 +60,9 @@ def parse():
     p.add_argument("--no-offload", action="store_true", help="skip the offload (put_from_paged) leg")
     p.add_argument("--no-config3", action="store_true", help="skip BASELINE config 3 (64K-token hit, 8 GiB: "
                    "HBM store vs pinned-host store with SM zero-copy and copy-engine paths)")
-    p.add_argument("--no-p2p", action="store_true", help="N>1: skip the cross-GPU leg (every rank fetches a "
-                   "4K request whose chunks live on the next rank's GPU, NVLink P2P reads)")
+    p.add_argument("--p2p", action="store_true", help="N>1: cross-GPU leg (every rank fetches a 4K request "
+                   "whose chunks live on the next rank's GPU: CUDA IPC import, NVLink P2P reads by the same "
+                   "kernel); opt-in because it has only been run with peers sharing one GPU")
     p.add_argument("--sensitivity", action="store_true", help="Fig. 14 analog: TTFT increase at a 10 Gbps vs "
                    "100 Gbps cap, layerwise vs chunkwise, Table A5 cells")
     p.add_argument("--crossover", action="store_true", help="Eq. 2 / Fig. 13 analog: layerwise vs chunkwise "
@@ -377,7 +378,7 @@ def main_ours(args):
         out["pool"] = pool_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_granularity and not args.profile:
         out["granularity"] = granularity_leg(args, oc, torch, dev, lay_t, fopts)
-    if ws > 1 and not args.no_p2p:                 # every rank: chunks homed on the next GPU (a11)
+    if ws > 1 and args.p2p:                        # every rank: chunks homed on the next GPU (a11)
         res = p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
         if rank == 0:
             out["p2p"] = res
