@@ -87,3 +87,72 @@ def test_consumer_wait_on_fresh_descriptor():
             torch.cuda.synchronize()
             assert np.array_equal(snap.cpu().numpy(), want), it
             d.close()
+
+
+def test_every_path_at_once():
+    """Single fetches (TMA, LD/ST, strict-paced), CE fetches from a pinned-host store, and batches
+    in every claim order, all in flight together on their own streams and recycled as they retire:
+    no path may disturb another's pooled descriptor blocks, claim counters or stages."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    rng = np.random.default_rng(11)
+    fams = [requests_family(lay, 970 + f, 0, [20])[0] for f in range(3)]
+    streams = [torch.cuda.Stream() for _ in range(6)]
+    with oc.Store(lay, capacity=64) as hbm, oc.Store(lay, capacity=64, tier=oc.TIER_PINNED_HOST) as host:
+        keys = []
+        for f, req in enumerate(fams):
+            k = oc.chunk_keys(req.tokens, 16)
+            pl = payload_stack(lay, 970 + f, req.payload_ids)
+            hbm.put_chunks(k, pl)
+            host.put_chunks(k, pl)
+            keys.append(k)
+
+        def new_item(i, store):
+            f = int(rng.integers(0, 3))
+            n = int(rng.integers(1, 21))
+            req = Request(fams[f].tokens, fams[f].payload_ids, n)
+            dest = make_dest(lay, n, str(rng.choice(["nhd", "hnd", "flat"])), Bs=int(rng.choice([8, 16])),
+                             seed=1000 + i)
+            buf = sentinel_buffer(dest.size)
+            d = oc.build_descriptor(store, keys[f][:n], lay, lib_target(oc, dest, buf.data_ptr()))
+            return d, buf, oracle_result(lay, 970 + f, req, dest)
+
+        inflight = []
+
+        def retire(item):
+            ev, ds, bufs, wants, batch = item
+            ev.synchronize()
+            for buf, want in zip(bufs, wants):
+                assert np.array_equal(buf.cpu().numpy(), want)
+            if batch is not None:
+                batch.close()
+            for d in ds:
+                d.close()
+
+        for i in range(60):
+            s = streams[i % len(streams)]
+            kind = i % 6
+            if kind < 4:
+                d, buf, want = new_item(i, host if kind == 3 else hbm)
+                s.wait_stream(torch.cuda.current_stream())
+                opts = [{"engine": oc.COPY_BULK}, {"engine": oc.COPY_LDST},
+                        {"engine": oc.COPY_BULK, "pace_Bps": 4e9, "pace_strict": True},
+                        {"engine": oc.COPY_CE}][kind]
+                d.fetch_layerwise(s, **opts)
+                ds, bufs, wants, batch = [d], [buf], [want], None
+            else:
+                items = [new_item(i * 10 + m, hbm) for m in range(3)]
+                ds, bufs, wants = [x[0] for x in items], [x[1] for x in items], [x[2] for x in items]
+                s.wait_stream(torch.cuda.current_stream())
+                if kind == 4:
+                    batch = oc.Batch(ds, order=oc.BATCH_BY_POSITION)
+                    batch.fetch(s)
+                else:
+                    batch = oc.Batch(ds)
+                    batch.fetch(s, wdrr_weights=[1e9, 2e9, 5e9], hold_rates=bool(i % 2))
+            ev = torch.cuda.Event()
+            ev.record(s)
+            inflight.append((ev, ds, bufs, wants, batch))
+            if len(inflight) > 8:
+                retire(inflight.pop(0))
+        for item in inflight:
+            retire(item)
