@@ -253,8 +253,9 @@ OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* co
  * then layer l+1 -- so every request's layers arrive in order and all requests' early layers go
  * first.  Descriptors must share layout and device, and stay alive (not freed) until the batch
  * is freed.  Each member keeps its own layer-ready state: wait_layer / sync_layer / layer_times
- * work per descriptor as after fetch_layerwise.  PERSISTENT mode, BULK engine, unpaced only
- * (ENOTSUP otherwise); a batch may be fetched repeatedly, one fetch in flight at a time. */
+ * work per descriptor as after fetch_layerwise.  PERSISTENT mode, unpaced only (ENOTSUP
+ * otherwise); engine BULK, LDST or AUTO (LDST as soon as one member's target is head-split);
+ * a batch may be fetched repeatedly, one fetch in flight at a time. */
 typedef struct oc_batch oc_batch;
 OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out);
 OC_API int oc_fetch_batch(oc_batch* batch, const oc_fetch_opts* opts, void* copy_stream);

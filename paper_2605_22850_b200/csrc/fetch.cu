@@ -794,6 +794,126 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     }
 }
 
+// Batched claims for the LD/ST engine: the same three orders as fetch_bulk_kernel (layer-major
+// by request, by position in claims of pos_claim units, WDRR entries), produced one unit at a
+// time by thread 0.
+template <int MODE>
+struct BatchClaimer {
+    uint32_t next_raw = 0, cur_req = 0, cur_next = 0, cur_left = 0, cur_rel = 0;
+    bool exhausted = false;
+    SegCache sc;
+    // the next unit (request, unit within it, release us); false once the launch's claims are out
+    __device__ bool next(const BatchArgs& ba, uint32_t g0, uint32_t g1, uint32_t grab_base, uint32_t& req,
+                         uint32_t& g, uint32_t& rel) {
+        rel = 0;
+        if (MODE == kBatch) {
+            if (exhausted) return false;
+            const uint32_t gg = g0 + (next_raw - grab_base);
+            if (gg >= g1) {
+                exhausted = true;
+                return false;
+            }
+            next_raw = atomicAdd(ba.claim, 1u);
+            const Resolved rs = resolve<MODE>(DevDesc{}, ba, gg, sc);
+            req = rs.req;
+            g = rs.g;
+            return true;
+        }
+        if (!exhausted && cur_left == 0) {
+            const uint32_t c = g0 + (next_raw - grab_base);
+            if (c >= g1) {
+                exhausted = true;
+            } else {
+                next_raw = atomicAdd(ba.claim, 1u);
+                if (MODE == kWdrr) {
+                    const uint4 en = ba.ents[c];
+                    cur_req = en.x;
+                    cur_next = en.y;
+                    cur_left = en.z;
+                    cur_rel = en.w;
+                } else {
+                    cur_next = c * ba.pos_claim;
+                    cur_left = min(ba.pos_claim, ba.n_units - cur_next);
+                }
+            }
+        }
+        if (exhausted) return false;
+        cur_left--;
+        if (MODE == kWdrr) {
+            req = cur_req;
+            g = cur_next++;
+            rel = cur_rel;
+        } else {
+            const Resolved rs = resolve<MODE>(DevDesc{}, ba, cur_next++, sc);
+            req = rs.req;
+            g = rs.g;
+        }
+        return true;
+    }
+};
+
+// LD/ST engine for batches (head-split targets, where per-piece TMA stores are slow): the loop of
+// fetch_ldst_kernel with units from a BatchClaimer; CTA 0's first warp is the batch observer.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) fetch_ldst_batch_kernel(const __grid_constant__ BatchArgs ba,
+                                                                        uint32_t g0, uint32_t g1, uint32_t grab_base) {
+    __shared__ uint64_t s_dst[2][kMaxRows];
+    __shared__ uint32_t s_g[2], s_req[2], s_rel[2], s_ok[2];
+    const uint64_t t0 = globaltimer();
+    if (blockIdx.x == 0) {
+        if (threadIdx.x < 32) observe_batch(ba, t0);
+        return;
+    }
+    uint64_t t_start = t0;
+    BatchClaimer<MODE> cl;
+    if (threadIdx.x == 0) {
+        if (MODE == kWdrr && ba.paced) {
+            const unsigned long long old = atomicCAS(ba.t0_slot, 0ull, (unsigned long long)t0);
+            t_start = old ? old : t0;
+        }
+        cl.next_raw = atomicAdd(ba.claim, 1u);
+        uint32_t rq = 0, g = 0, rel = 0;
+        s_ok[0] = cl.next(ba, g0, g1, grab_base, rq, g, rel) ? 1u : 0u;
+        s_req[0] = rq;
+        s_g[0] = g;
+        s_rel[0] = rel;
+    }
+    __syncthreads();
+    uint32_t pending_req = 0, pending_layer = 0;
+    bool pending = false;
+    for (uint32_t k = 0;; k++) {
+        const uint32_t b = k & 1;
+        if (!s_ok[b]) break;  // uniform: every thread read the same slot after the last barrier
+        const DevDesc& d = ba.descs[s_req[b]];
+        const UnitGeo u = unit_geo(d, s_g[b]);
+        if (MODE == kWdrr && ba.paced) {  // held rate (c22): wait for the entry's release time
+            const uint64_t rel = t_start + (uint64_t)s_rel[b] * 1000ull;
+            if (__syncthreads_or(threadIdx.x == 0 && globaltimer() < rel)) {
+                if (threadIdx.x == 0 && pending) complete_units(ba.descs[pending_req], pending_layer, 1);
+                pending = false;
+                while (globaltimer() < rel) __nanosleep(2000);
+            }
+        }
+        uint64_t* tab = s_dst[b];
+        for (uint32_t r = threadIdx.x; r < u.nrows; r += kThreads) tab[r] = row_addr(d, u.layer, u.j, u.q0 + r, nullptr);
+        if (threadIdx.x == 0) {  // publish unit k+1 (read after the barrier below)
+            uint32_t rq = 0, g = 0, rel = 0;
+            s_ok[b ^ 1] = cl.next(ba, g0, g1, grab_base, rq, g, rel) ? 1u : 0u;
+            s_req[b ^ 1] = rq;
+            s_g[b ^ 1] = g;
+            s_rel[b ^ 1] = rel;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && pending) complete_units(ba.descs[pending_req], pending_layer, 1);
+        copy_rows(d, unit_src(d, u), u.nrows, tab);
+        pending = true;
+        pending_req = s_req[b];
+        pending_layer = u.layer;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && pending) complete_units(ba.descs[pending_req], pending_layer, 1);
+}
+
 // Offload on the TMA (put_from_paged): the mirror of fetch_bulk_kernel.  A unit is R rows of
 // one new chunk's layer slice; its rows are gathered from their paged slots (one bulk load per
 // contiguous run, all completing on the stage's mbarrier) into shared memory, then written to the
@@ -1253,8 +1373,8 @@ int ensure_ent_capacity(Batch* b, size_t bytes) {
 
 int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cudaStream_t s) {
     if (o.mode != OC_FETCH_PERSISTENT) return fail(OC_ENOTSUP, "fetch_batch: batches use PERSISTENT mode");
-    if (o.engine != OC_COPY_BULK && o.engine != OC_COPY_AUTO)
-        return fail(OC_ENOTSUP, "fetch_batch: batches use the BULK engine");
+    if (o.engine != OC_COPY_BULK && o.engine != OC_COPY_LDST && o.engine != OC_COPY_AUTO)
+        return fail(OC_ENOTSUP, "fetch_batch: batches use the BULK or LDST engine");
     if (o.pace_Bps != 0)
         return fail(OC_ENOTSUP, "fetch_batch: pace_Bps is per request (fetch_layerwise); WDRR batches use hold_rates");
     for (Desc* d : b->descs)
@@ -1379,22 +1499,39 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         ba.pos_claim = pos_claim;
         ba.n_units = (uint32_t)(total * L);
     }
-    if (p.stages < 2) return fail(OC_ENOTSUP, "fetch_batch: two units do not fit in shared memory");
-    if (wdrr) {
-        OC_CUDA(set_bulk_smem<kWdrr>(p.smem));
-        fetch_bulk_kernel<kWdrr><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
-                                                                     b->grab_ctr, p.stages, p.stage_bytes);
-    } else if (by_pos) {
-        OC_CUDA(set_bulk_smem<kByPos>(p.smem));
-        fetch_bulk_kernel<kByPos><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
-                                                                      b->grab_ctr, p.stages, p.stage_bytes);
+    // AUTO: the LD/ST engine as soon as one member's target is head-split (see launch_fetch)
+    bool ldst = o.engine == OC_COPY_LDST;
+    if (o.engine == OC_COPY_AUTO)
+        for (Desc* d : b->descs) ldst |= !d->dd.nhd;
+    if (ldst) {
+        static int occ = occupancy((const void*)fetch_ldst_batch_kernel<kBatch>, kThreads, 0);
+        uint64_t grid = (uint64_t)occ * sms - 1;  // one CTA slot of the first wave is the observer's
+        if (max_ctas) grid = std::min<uint64_t>(grid, max_ctas);
+        grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, n_claims));
+        const unsigned gb = (unsigned)grid + 1;
+        if (wdrr) fetch_ldst_batch_kernel<kWdrr><<<gb, kThreads, 0, s>>>(ba, 0u, (uint32_t)n_claims, b->grab_ctr);
+        else if (by_pos) fetch_ldst_batch_kernel<kByPos><<<gb, kThreads, 0, s>>>(ba, 0u, (uint32_t)n_claims, b->grab_ctr);
+        else fetch_ldst_batch_kernel<kBatch><<<gb, kThreads, 0, s>>>(ba, 0u, (uint32_t)n_claims, b->grab_ctr);
+        OC_CUDA(cudaGetLastError());
+        b->grab_ctr += (uint32_t)n_claims + (uint32_t)grid;
     } else {
-        OC_CUDA(set_bulk_smem<kBatch>(p.smem));
-        fetch_bulk_kernel<kBatch><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
-                                                                      b->grab_ctr, p.stages, p.stage_bytes);
+        if (p.stages < 2) return fail(OC_ENOTSUP, "fetch_batch: two units do not fit in shared memory");
+        if (wdrr) {
+            OC_CUDA(set_bulk_smem<kWdrr>(p.smem));
+            fetch_bulk_kernel<kWdrr><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
+                                                                         b->grab_ctr, p.stages, p.stage_bytes);
+        } else if (by_pos) {
+            OC_CUDA(set_bulk_smem<kByPos>(p.smem));
+            fetch_bulk_kernel<kByPos><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
+                                                                          b->grab_ctr, p.stages, p.stage_bytes);
+        } else {
+            OC_CUDA(set_bulk_smem<kBatch>(p.smem));
+            fetch_bulk_kernel<kBatch><<<p.copy_ctas + 1, 64, p.smem, s>>>(DevDesc{}, ba, 0u, (uint32_t)n_claims,
+                                                                          b->grab_ctr, p.stages, p.stage_bytes);
+        }
+        OC_CUDA(cudaGetLastError());
+        b->grab_ctr += (uint32_t)n_claims + p.copy_ctas;
     }
-    OC_CUDA(cudaGetLastError());
-    b->grab_ctr += (uint32_t)n_claims + p.copy_ctas;
     for (Desc* d : b->descs) {
         OC_CUDA(cudaEventRecord(d->done_ev, s));
         d->poisoned = false;

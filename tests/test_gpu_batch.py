@@ -43,7 +43,8 @@ SPECS = [(1, 3, "nhd", 16, 0), (2, 7, "hnd", 8, 5), (3, 1, "flat", 16, 0), (4, 1
 @pytest.mark.parametrize("unit_bytes", [0, 1024, 3072])
 @pytest.mark.parametrize("order,blk_kib,claim", [(oc.BATCH_BY_REQUEST, 0, 0), (oc.BATCH_BY_POSITION, 16, 3),
                                                  (oc.BATCH_BY_POSITION, 4096, 8), (oc.BATCH_BY_POSITION, 16, 1)])
-def test_batch_parity(lay, unit_bytes, order, blk_kib, claim, monkeypatch):
+@pytest.mark.parametrize("engine", [oc.COPY_BULK, oc.COPY_LDST])
+def test_batch_parity(lay, unit_bytes, order, blk_kib, claim, engine, monkeypatch):
     if blk_kib:   # 16 KiB: blocks of 1-2 positions, partial last blocks in every run
         monkeypatch.setenv("OC_BYPOS_BLOCK_KIB", str(blk_kib))
     if claim:     # units per claim; 3 leaves a ragged last claim
@@ -51,7 +52,7 @@ def test_batch_parity(lay, unit_bytes, order, blk_kib, claim, monkeypatch):
     st, items = setup_batch(lay, SPECS)
     b = oc.Batch([it["desc"] for it in items], order=order)
     s = torch.cuda.Stream()
-    b.fetch(s, unit_bytes=unit_bytes)
+    b.fetch(s, unit_bytes=unit_bytes, engine=engine)
     for it in items:
         it["desc"].sync_layer(lay.num_layers - 1)
     torch.cuda.synchronize()
@@ -129,7 +130,8 @@ def test_batch_errors():
                                             (OLayout(2, 4, 32, 2, 20), 1024), (OLayout(1, 1, 16, 2, 8), 0)])
 @pytest.mark.parametrize("hold", [False, True])
 @pytest.mark.parametrize("E", [0, 1, 3])
-def test_wdrr_parity(lay, unit_bytes, hold, E):
+@pytest.mark.parametrize("engine", [oc.COPY_BULK, oc.COPY_AUTO])
+def test_wdrr_parity(lay, unit_bytes, hold, E, engine):
     """Every byte lands as in the oracle whatever the interleaving (ragged units included: 3072 B
     units of 12 rows cut a 40-row slice into 12+12+12+4), and each request's layers are announced
     in order."""
@@ -138,7 +140,7 @@ def test_wdrr_parity(lay, unit_bytes, hold, E):
     s = torch.cuda.Stream()
     weights = [2e9, 0.5e9, 7e9, 1e9, 3.3e9]
     b.fetch(s, unit_bytes=unit_bytes, wdrr_weights=weights, quantum_bytes=unit_bytes or 0, entry_units=E,
-            hold_rates=hold)
+            hold_rates=hold, engine=engine)
     for it in items:
         it["desc"].sync_layer(lay.num_layers - 1)
     torch.cuda.synchronize()
