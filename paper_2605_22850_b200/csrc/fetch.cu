@@ -905,9 +905,10 @@ __global__ void __launch_bounds__(kThreads, 4) fetch_ldst_batch_kernel(const __g
         }
         __syncthreads();
         if (threadIdx.x == 0 && pending) complete_units(ba.descs[pending_req], pending_layer, 1);
+        // only thread 0 completes units: read the slot before it republishes it next iteration
+        if (threadIdx.x == 0) pending_req = s_req[b];
         copy_rows(d, unit_src(d, u), u.nrows, tab);
         pending = true;
-        pending_req = s_req[b];
         pending_layer = u.layer;
     }
     __syncthreads();
