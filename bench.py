@@ -536,6 +536,21 @@ def p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend="nccl"):
     b.record(s)
     s.synchronize()
     ms = odist.max_over_ranks(a.elapsed_time(b), device=dev if backend == "nccl" else None)
+    # in-harness P2P reference: a copy-engine copy of the peer's slab into local HBM
+    from cuda.bindings import runtime as cudart
+    pbase, pbytes = peer.slab()
+    nb = int(min(pbytes, 1 << 30))
+    scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(3):
+        a.record(s)
+        err, = cudart.cudaMemcpyAsync(scratch.data_ptr(), pbase, nb, cudart.cudaMemcpyKind.cudaMemcpyDefault,
+                                      s.cuda_stream)
+        b.record(s)
+        s.synchronize()
+        if err == cudart.cudaError_t.cudaSuccess:
+            best = max(best, nb / a.elapsed_time(b) / 1e6)
+    del scratch
     d.close()
     if ws > 1:
         torch.distributed.barrier()                 # peers done reading before any store goes away
@@ -549,6 +564,8 @@ def p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend="nccl"):
             "ranks": ws, "steps": steps, "GBps_rw_aggregate": round(ws * rw * steps / ms / 1e6, 1),
             "nvlink_ingress_GBps_per_gpu": round(rw / 2 * steps / ms / 1e6, 1),
             "ms_per_fetch_max_over_ranks": round(ms / steps, 4), "rank0_sampled_layers_bit_exact": ok,
+            "p2p_copy_engine_GBps_rank0": round(best, 1),
+            "ingress_frac_of_p2p_copy": round(rw / 2 * steps / ms / 1e6 / best, 3) if best else None,
             "peers_share_one_gpu": torch.cuda.device_count() < ws}
 
 
