@@ -538,7 +538,7 @@ def p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend="nccl"):
     ms = odist.max_over_ranks(a.elapsed_time(b), device=dev if backend == "nccl" else None)
     # in-harness P2P reference: a copy-engine copy of the peer's slab into local HBM
     from cuda.bindings import runtime as cudart
-    pbase, pbytes = peer.slab()
+    pbase, pbytes = peer.slab
     nb = int(min(pbytes, 1 << 30))
     scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
     best = 0.0
