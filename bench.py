@@ -1110,8 +1110,9 @@ def sensitivity_leg(args, oc, torch, dev, lay_t):
 def granularity_leg(args, oc, torch, dev, lay_t, fopts):
     """Config 2's chunk-size sweep: the 4K-token hit at G = 16, 64, 256
     (N = 256, 64, 16) through the fused kernel, plus the unfused comparison at G = 16: the same
-    kernel into the paper's flat client buffer [L][N*S] (Alg. A1's B_l), then a torch index_copy_
-    scatter per layer into the paged cache -- 4*N*S bytes per layer instead of 2*N*S.  GB/s are
+    kernel into the paper's flat client buffer [L][N*S] (Alg. A1's B_l), then the client-side
+    scatter into the paged cache (oc scatter_flat; a torch index_copy_ per layer beside it) --
+    4*N*S bytes per layer instead of 2*N*S.  GB/s are
     algorithmic (2*N*S*L) over device time, best of 20 after warm-up, rotating 2 request sets."""
     import synth
     L, Bs = lay_t[0], 16
@@ -1169,18 +1170,30 @@ def granularity_leg(args, oc, torch, dev, lay_t, fopts):
                     for l in range(L):
                         src = flatb[l].view(N, 2, G, row).permute(1, 0, 2, 3).reshape(2, N * G, row)
                         cache[l].view(2, -1, row).index_copy_(1, slots, src)
+            def unfused_ours(i):                  # the same two steps, both in our kernels
+                d, cache, (flatb, df, slots) = sets[i % 2]
+                df.fetch_layerwise(s, **fopts)
+                d.scatter_flat(flatb.data_ptr(), flatb.numel(), s)
             ms_u = timed(unfused)
-            cell["unfused_flat_then_scatter"] = {"GBps_algorithmic": round(2 * N * S * L / ms_u / 1e6, 1),
-                                                 "ms": round(ms_u, 4), "traffic_bytes": 4 * N * S * L,
-                                                 "scatter": "torch permute+index_copy_ per layer"}
-            # correctness of the comparison path: same bytes as the fused kernel
+            ms_o = timed(unfused_ours)
+            cell["unfused_flat_then_scatter"] = {"GBps_algorithmic": round(2 * N * S * L / ms_o / 1e6, 1),
+                                                 "ms": round(ms_o, 4), "traffic_bytes": 4 * N * S * L,
+                                                 "scatter": "oc scatter_flat (bulk kernel, flat source)",
+                                                 "torch_scatter_GBps_algorithmic": round(2 * N * S * L / ms_u / 1e6, 1),
+                                                 "torch_scatter": "torch permute+index_copy_ per layer"}
+            # correctness of the comparison paths: same bytes as the fused kernel
             d, cache, _ = sets[0]
-            unfused(0)
-            torch.cuda.synchronize()
-            ref = cache.clone()
-            d.fetch_layerwise(s, **fopts)
-            torch.cuda.synchronize()
-            cell["unfused_equals_fused"] = bool(torch.equal(ref, cache))
+            same = True
+            for fn in (unfused, unfused_ours):
+                with torch.cuda.stream(s):
+                    cache.zero_()
+                fn(0)
+                torch.cuda.synchronize()
+                ref = cache.clone()
+                d.fetch_layerwise(s, **fopts)
+                torch.cuda.synchronize()
+                same &= bool(torch.equal(ref, cache))
+            cell["unfused_equals_fused"] = same
         out[f"G{G}"] = cell
         for d, cache, flat in sets:
             d.close()

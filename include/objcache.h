@@ -248,6 +248,15 @@ typedef struct {
  * opts = NULL selects the defaults (persistent, AUTO engine, auto grid, unpaced). */
 OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* copy_stream);
 
+/* scatter_flat -- the client half of the paper's unfused flow (Alg. A1 line 6 RDMA-writes B_l into
+ * the client buffer; the client then copies it into its paged KV cache): a
+ * layer-major payload at flat_base (device address, [L][N][S]: layer l, chunk j at
+ * (l*N + j)*S, 16-byte aligned, flat_capacity >= N*L*S) is scattered into the descriptor's
+ * target with the same per-layer completion as a fetch (wait_layer, layer_times).  opts: unit
+ * size and copy-CTA cap (PERSISTENT, unpaced; ENOTSUP otherwise).  ERANGE / EALIGN as stated. */
+OC_API int oc_scatter_flat(oc_desc* desc, uint64_t flat_base, uint64_t flat_capacity, const oc_fetch_opts* opts,
+                           void* stream);
+
 /* Batches: concurrent requests (P:467-598 treats them as tenants sharing one link) fetched by
  * ONE persistent launch.  Units are claimed in a single global order -- layer l of every request,
  * then layer l+1 -- so every request's layers arrive in order and all requests' early layers go

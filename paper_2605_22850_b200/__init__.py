@@ -99,6 +99,7 @@ _SIGS = {
     "oc_fetch_batch": [_vp, ctypes.POINTER(CFetchOpts), _vp],
     "oc_batch_free": [_vp],
     "oc_batch_set_order": [_vp, ctypes.c_int],
+    "oc_scatter_flat": [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(CFetchOpts), _vp],
     "oc_fetch_batch_wdrr": [_vp, ctypes.POINTER(CFetchOpts), ctypes.POINTER(CWdrrOpts), _vp],
     "oc_wdrr_plan": [c_u64p, ctypes.c_uint32, c_u32p, ctypes.c_uint32, ctypes.POINTER(CWdrrOpts), c_u32p, c_u32p,
                      c_u32p, c_u32p, ctypes.c_uint64, c_u64p],
@@ -375,6 +376,12 @@ class Descriptor:
         o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
                        1 if pace_strict else 0, 0)
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))
+
+    def scatter_flat(self, flat_base: int, flat_capacity: int, stream=None, max_ctas=0, unit_bytes=0):
+        """Scatter a layer-major payload [L][N][S] at device address flat_base into this
+        descriptor's target (the client half of the paper's unfused flow)."""
+        o = CFetchOpts(FETCH_PERSISTENT, COPY_BULK, int(max_ctas), int(unit_bytes), 0.0, 0, 0)
+        _check(_lib.oc_scatter_flat(self._h, int(flat_base), int(flat_capacity), ctypes.byref(o), _stream(stream)))
 
     def wait_layer(self, layer: int, stream=None):
         _check(_lib.oc_wait_layer(self._h, int(layer), _stream(stream)))

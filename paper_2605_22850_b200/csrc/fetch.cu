@@ -99,8 +99,10 @@ __device__ __forceinline__ UnitGeo unit_geo(const DevDesc& d, uint32_t g) {
 }
 
 __device__ __forceinline__ const uint8_t* unit_src(const DevDesc& d, const UnitGeo& u) {
-    if (d.staged)  // CE engine: layer l of chunk j was staged at stage_base[l & 1] + j*S
+    if (d.staged == 1)  // CE engine: layer l of chunk j was staged at stage_base[l & 1] + j*S
         return (const uint8_t*)d.stage_base[u.layer & 1] + (uint64_t)u.j * d.S + (uint64_t)u.q0 * d.row;
+    if (d.staged == 2)  // flat payload [L][N][S]
+        return (const uint8_t*)d.stage_base[0] + ((uint64_t)u.layer * d.N + u.j) * d.S + (uint64_t)u.q0 * d.row;
     return (const uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + (uint64_t)u.q0 * d.row;
 }
 
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         if (BATCH) {
             if (threadIdx.x < 32) observe_batch(ba, t0);
         } else if (threadIdx.x == 0) {
-            if (g0 == 0 && !d0.staged) d0.ts[0] = t0;  // CE engine: stamped when the copies start
+            if (g0 == 0 && d0.staged != 1) d0.ts[0] = t0;  // CE engine: stamped when the copies start
             observe_layers(d0, g0 / d0.units_per_layer, g1 / d0.units_per_layer);
         }
         return;
@@ -1255,6 +1257,46 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     return OC_OK;
 }
 
+// The client half of the paper's unfused flow (Alg. A1 writes B_l into the client buffer, the
+// client then copies it into its paged cache, iffalse): a layer-major payload
+// [L][N][S] already in device memory is scattered into the descriptor's target by the bulk
+// kernel, with the descriptor's per-layer completion.  2*N*S bytes per layer, like a fetch.
+int launch_scatter_flat(Desc* d, uint64_t flat, uint64_t cap, const oc_fetch_opts& o, cudaStream_t s) {
+    if (o.mode != OC_FETCH_PERSISTENT || o.pace_Bps != 0)
+        return fail(OC_ENOTSUP, "scatter_flat: PERSISTENT mode, unpaced");
+    if (cap < d->N * d->geo.L * d->geo.S) return fail(OC_ERANGE, "scatter_flat: flat payload smaller than N*L*S");
+    if (flat % 16) return fail(OC_EALIGN, "scatter_flat: flat base not 16-byte aligned");
+    if (d->poisoned) return fail(OC_ECUDA, "scatter_flat: descriptor unusable after a failed launch");
+    DeviceGuard dg(d->device);
+    int urc = upload_order(&d->up, s);
+    if (urc) return urc;
+    if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
+    plan_units(d, o.unit_bytes ? o.unit_bytes : default_unit_bytes(o.max_ctas, device_sm_count(d->device)));
+    DevDesc& dd = d->dd;
+    const uint64_t total_units = (uint64_t)dd.units_per_layer * dd.L;
+    if (total_units >= (1ull << 32)) return fail(OC_ERANGE, "scatter_flat: too many units");
+    uint32_t epoch = d->epoch + 1;
+    if (epoch == 0) epoch = 1;
+    dd.epoch = epoch;
+    dd.cnt_target = d->cnt_base + dd.units_per_layer;
+    dd.pace_ns = 0;
+    dd.pace_ns_per_byte = 0.0;
+    dd.staged = 2;
+    dd.stage_base[0] = flat;
+    d->epoch = epoch;
+    d->cnt_base = dd.cnt_target;
+    d->poisoned = true;
+    const BulkPlan p = plan_bulk(dd, device_sm_count(d->device), o.max_ctas, total_units);
+    int rc = launch_bulk(d, p, 0, (uint32_t)total_units, s);
+    if (rc) return rc;
+    OC_CUDA(cudaEventRecord(d->done_ev, s));
+    d->poisoned = false;
+    d->last_mode = OC_FETCH_PERSISTENT;
+    d->last_stream = s;
+    d->fetched = true;
+    return OC_OK;
+}
+
 int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     oc_fetch_opts o = oin;
     if (o.mode != OC_FETCH_PERSISTENT && o.mode != OC_FETCH_PER_LAYER)
@@ -1602,6 +1644,16 @@ OC_API int oc_fetch_batch(oc_batch* h, const oc_fetch_opts* opts, void* stream) 
     o.engine = OC_COPY_BULK;
     if (opts) o = *opts;
     return oc::fetch_batch((oc::Batch*)h, o, nullptr, (cudaStream_t)stream);
+}
+
+OC_API int oc_scatter_flat(oc_desc* h, uint64_t flat_base, uint64_t flat_capacity, const oc_fetch_opts* opts,
+                           void* stream) {
+    if (!h) return oc::fail(OC_EINVAL, "scatter_flat: null descriptor");
+    oc_fetch_opts o{};
+    o.mode = OC_FETCH_PERSISTENT;
+    o.engine = OC_COPY_BULK;
+    if (opts) o = *opts;
+    return oc::launch_scatter_flat((Desc*)h, flat_base, flat_capacity, o, (cudaStream_t)stream);
 }
 
 OC_API int oc_batch_set_order(oc_batch* h, int order) {

@@ -141,7 +141,8 @@ struct DevDesc {
     uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
     double pace_ns_per_byte;  // strict pacing: unit released at t0 + (fetch bytes before it) * this
     uint64_t stage_base[2];   // CE engine: layer l's slices were staged at stage_base[l & 1] as [N][S]
-    uint32_t staged;          // 1: read sources from stage_base (CE engine), 0: from src[]
+    uint32_t staged;          // 0: sources from src[]; 1: CE stage (stage_base[l & 1]); 2: a flat
+                              // layer-major payload [L][N][S] at stage_base[0] (oc_scatter_flat)
     FastDiv div_upl;          // units_per_layer
     FastDiv div_tiles;        // tiles per chunk-layer slice
     FastDiv div_vpr;

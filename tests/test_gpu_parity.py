@@ -381,3 +381,43 @@ def test_alternating_engines_and_unit_sizes_on_one_descriptor():
             assert_same(buf.cpu().numpy(), want)
             torch.cuda.synchronize()
         desc.close()
+
+
+# ---- the paper's unfused flow: gather into the flat client buffer, then scatter it ---------------
+@pytest.mark.parametrize("kind,Bs,first", [("nhd", 16, 0), ("hnd", 8, 3), ("nhd", 32, 17)])
+@pytest.mark.parametrize("unit_bytes", [0, 1024])
+def test_gather_to_flat_then_scatter_flat(kind, Bs, first, unit_bytes):
+    """Alg. A1 into the flat client buffer B_0..B_{L-1}, then oc_scatter_flat into a paged cache:
+    both the flat payload and the paged result equal the oracle's."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    req = requests_family(lay, 77, 0, [9])[0]
+    with oc.Store(lay, capacity=12) as st:
+        keys = oc.chunk_keys(req.tokens, 16)
+        st.put_chunks(keys, payload_stack(lay, 77, req.payload_ids))
+        fdest = make_dest(lay, 9, "flat")
+        fbuf = sentinel_buffer(fdest.size)
+        df = oc.build_descriptor(st, keys, lay, lib_target(oc, fdest, fbuf.data_ptr()))
+        pdest = make_dest(lay, 9, kind, Bs=Bs, first_token=first, seed=5)
+        pbuf = sentinel_buffer(pdest.size)
+        dp = oc.build_descriptor(st, keys, lay, lib_target(oc, pdest, pbuf.data_ptr()))
+        s = torch.cuda.Stream()
+        df.fetch_layerwise(s, unit_bytes=unit_bytes)
+        dp.scatter_flat(fbuf.data_ptr() + fdest.flat_off, fdest.flat_cap, s, unit_bytes=unit_bytes)
+        dp.sync_layer(lay.num_layers - 1)
+        s.synchronize()
+        assert_same(fbuf.cpu().numpy(), oracle_result(lay, 77, req, fdest))
+        assert_same(pbuf.cpu().numpy(), oracle_result(lay, 77, req, pdest))
+        t = dp.layer_times().astype(np.int64)
+        assert t[0] > 0 and np.all(np.diff(t[1:]) >= 0)
+        dp.fetch_layerwise(s)                                    # a normal fetch afterwards still works
+        dp.sync_layer(lay.num_layers - 1)
+        s.synchronize()
+        assert_same(pbuf.cpu().numpy(), oracle_result(lay, 77, req, pdest))
+        with pytest.raises(oc.ObjcacheError) as e:
+            dp.scatter_flat(fbuf.data_ptr() + fdest.flat_off, fdest.flat_cap - 16, s)
+        assert e.value.code == oc.OC_ERANGE
+        with pytest.raises(oc.ObjcacheError) as e:
+            dp.scatter_flat(fbuf.data_ptr() + fdest.flat_off + 8, fdest.flat_cap, s)
+        assert e.value.code == oc.OC_EALIGN
+        df.close()
+        dp.close()
