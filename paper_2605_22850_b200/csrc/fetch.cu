@@ -1072,6 +1072,17 @@ BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units
     return p;
 }
 
+// Paced launches keep a 2-unit ring: a CTA claims and loads its ring ahead of time, and the
+// prologue (or a hold) waits for each claimed unit's release -- with a deep ring a CTA that
+// claimed units across a release boundary would hold its earlier units' stores until the later
+// release (a paced layer 0 seen ready only after layer 1's release time).
+void shallow_ring(BulkPlan* p) {
+    if (p->stages > 2) {
+        p->stages = 2;
+        p->smem = 128 + 2 * p->stage_bytes;
+    }
+}
+
 template <int MODE>
 cudaError_t set_bulk_smem(uint32_t smem) {
     static uint32_t attr_set = 0;
@@ -1350,9 +1361,10 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     d->poisoned = true;
     const uint32_t upl = dd.units_per_layer;
     if (o.mode == OC_FETCH_PERSISTENT) {
-        int rc = o.engine == OC_COPY_BULK
-                     ? launch_bulk(d, plan_bulk(dd, sms, max_ctas, total_units), 0, (uint32_t)total_units, s)
-                     : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
+        BulkPlan p = plan_bulk(dd, sms, max_ctas, total_units);
+        if (dd.pace_ns || dd.pace_ns_per_byte > 0.0) shallow_ring(&p);
+        int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, 0, (uint32_t)total_units, s)
+                                          : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
         if (rc) return rc;
     } else {
         const BulkPlan p = plan_bulk(dd, sms, max_ctas, upl);
@@ -1510,7 +1522,8 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
     uint32_t max_ctas = o.max_ctas;
     if (!max_ctas && host_chunks * 2 > chunks) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8));
     const int sms = device_sm_count(b->device);
-    const BulkPlan p = plan_bulk(b->descs[0]->dd, sms, max_ctas, n_claims);
+    BulkPlan p = plan_bulk(b->descs[0]->dd, sms, max_ctas, n_claims);
+    if (wdrr && wdrr->hold_rates) shallow_ring(&p);
     OC_CUDA(cudaMemcpyAsync(b->dev, b->stage, b->upload_bytes, cudaMemcpyHostToDevice, s));
     OC_CUDA(cudaEventRecord(b->staged, s));
     for (Desc* d : b->descs) {  // from the launch on, the device counters belong to the new epoch
