@@ -118,6 +118,11 @@ def test_pacer_release_schedule(strict):
         for l in range(L):
             lo = l * X + (7 * X / 8 if strict else 0.0)
             assert lo - 20e-6 <= ready[l] <= lo + 150e-6, (l, ready[l], lo)
+        if strict:   # over windows of >= 10 pacing quanta, delivered / elapsed <= 1.05 r
+            s_layer = 8 * chunk_layer_bytes(lay)
+            for i in range(L):
+                for j in range(i + 2, L):
+                    assert (j - i) * s_layer / (ready[j] - ready[i]) <= 1.05 * s_layer / X, (i, j)
         torch.cuda.synchronize()
         assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 41, req, dest))
         with pytest.raises(oc.ObjcacheError) as e:
