@@ -72,6 +72,8 @@ def parse():
     p.add_argument("--pool", type=int, default=0, help="streaming multi-tenant runtime: this many requests "
                    "arrive over time (Poisson) into oc.TenantPool epochs (100 ms) under a shared cap, per policy "
                    "and dispatch (adds a 'pool' object)")
+    p.add_argument("--hash", type=int, default=0, help="chain keys of this many 4K-token requests: one GPU launch "
+                   "(oc_chunk_keys_batch) vs the host's SHA-extension loop (adds a 'hash' object)")
     p.add_argument("--batch", default="", help="NxM: N 4K-token + M 64K-token concurrent requests (config 5, "
                    "one GPU): one batched launch vs per-request launches (adds a 'batch' object)")
     p.add_argument("--sched", default="", help="comma list of paper scheduler workloads to run (A,B,C): "
@@ -374,6 +376,8 @@ def main_ours(args):
         out["sched"] = sched_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.batch:
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and args.hash:
+        out["hash"] = hash_leg(args, oc, torch, dev)
     if rank == 0 and args.pool:
         out["pool"] = pool_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and not args.no_granularity and not args.profile:
@@ -1484,6 +1488,40 @@ def sched_workloads():
     w["70B"] = (synth.LLAMA3_70B, round(sum_rstar / 2 * 8 / 1e9, 3), c70,
                 "FLOP model at 50% of the measured sustained bf16 rate (B200)")
     return w
+
+
+def hash_leg(args, oc, torch, dev, G=16, ctx=4096):
+    """Chain keys (reading c1) of R requests of 4K tokens (256 keys each): one GPU launch
+    (oc_chunk_keys_batch, one thread per chain; device time from CUDA events around the launch
+    alone) vs the host library's loop over oc_chunk_keys (SHA extensions, one core)."""
+    import synth
+    R = args.hash
+    streams = [synth.tokens(77000 + i, ctx) for i in range(R)]
+    t = time.perf_counter()
+    for st in streams:
+        oc.chunk_keys(st, G)
+    host_s = time.perf_counter() - t
+    flat = torch.from_numpy(np.concatenate(streams).view(np.int32)).to(dev)
+    off = torch.from_numpy((np.arange(R, dtype=np.int64) * ctx)).to(dev)
+    lens = torch.full((R,), ctx, dtype=torch.int64, device=dev)
+    koff = torch.from_numpy(np.arange(R, dtype=np.int64) * (ctx // G)).to(dev)
+    out = torch.empty((R * (ctx // G), 32), dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    run = lambda: oc._check(oc._lib.oc_chunk_keys_batch(flat.data_ptr(), off.data_ptr(), lens.data_ptr(), R, G, None,
+                                                       out.data_ptr(), koff.data_ptr(), s.cuda_stream))
+    run()
+    s.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    run()
+    b.record(s)
+    s.synchronize()
+    gpu_ms = a.elapsed_time(b)
+    same = bool(np.array_equal(out[:ctx // G].cpu().numpy(), oc.chunk_keys(streams[0], G)))
+    keys = R * (ctx // G)
+    return {"requests": R, "keys": keys, "host_ms": round(host_s * 1e3, 2), "gpu_ms": round(gpu_ms, 3),
+            "host_keys_per_s": round(keys / host_s), "gpu_keys_per_s": round(keys / (gpu_ms / 1e3)),
+            "first_request_equal": same}
 
 
 def pool_leg(args, oc, torch, dev, lay_t, epoch_s=0.1, cap_gbps=50.0, delta_gbps=5.0):

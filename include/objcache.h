@@ -91,6 +91,17 @@ OC_API int oc_sha256(const void* data, uint64_t n, uint8_t out[32]);
 OC_API int oc_chunk_keys(const uint32_t* tokens, uint64_t n_tokens, uint32_t chunk_tokens,
                          const oc_key* parent, oc_key* out, uint64_t cap, uint64_t* n_out);
 
+/* chunk_keys_batch: the same keys computed on the GPU for a batch of token streams (the offload
+ * path's keys).  Request r's tokens are tokens[tok_off[r] .. + n_tokens[r]),
+ * its floor(n_tokens[r]/G) keys are written to out[key_off[r] ..], chained from parents[r]
+ * (parents NULL = the root for every request).  tokens, tok_off, n_tokens, parents, out and
+ * key_off are DEVICE arrays of the current device; the caller sizes them (no bounds are checked).
+ * One thread per request (a chain is sequential): a single chain is slower than oc_chunk_keys on
+ * the host, a batch of hundreds of requests is much faster.  Asynchronous on `stream`. */
+OC_API int oc_chunk_keys_batch(const uint32_t* tokens, const uint64_t* tok_off, const uint64_t* n_tokens,
+                               uint32_t n_requests, uint32_t chunk_tokens, const oc_key* parents, oc_key* out,
+                               const uint64_t* key_off, void* stream);
+
 /* ---- chunk store -------------------------------------------------------- */
 typedef enum { OC_TIER_HBM = 0, OC_TIER_PINNED_HOST = 1 } oc_tier;
 typedef struct oc_store oc_store;

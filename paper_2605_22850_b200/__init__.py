@@ -78,6 +78,7 @@ _SIGS = {
     "oc_select_mode": [ctypes.c_uint64, ctypes.c_uint64],
     "oc_sha256": [_vp, ctypes.c_uint64, c_u8p],
     "oc_chunk_keys": [c_u32p, ctypes.c_uint64, ctypes.c_uint32, _vp, _vp, ctypes.c_uint64, c_u64p],
+    "oc_chunk_keys_batch": [_vp, _vp, _vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp, _vp],
     "oc_store_create": [ctypes.POINTER(CLayout), ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(_vp)],
     "oc_store_destroy": [_vp],
     "oc_store_count": [_vp, c_u64p],
@@ -218,6 +219,33 @@ def chunk_keys(tokens, chunk_tokens: int, parent: Optional[bytes] = None) -> np.
     _check(_lib.oc_chunk_keys(t.ctypes.data_as(c_u32p), t.size, int(chunk_tokens),
                               par.ctypes.data if par is not None else None, out.ctypes.data, n, ctypes.byref(cnt)))
     return out[:cnt.value]
+
+
+def chunk_keys_batch(token_streams, chunk_tokens: int, stream=None, parents=None):
+    """Chain keys of many token streams in one GPU launch (oc_chunk_keys_batch): a list of uint32
+    arrays in, a list of (floor(len/G), 32) uint8 arrays out.  `parents`: optional (R, 32) bytes."""
+    import torch
+    G = int(chunk_tokens)
+    lens = [int(len(t)) for t in token_streams]
+    nk = [n // G for n in lens] if G > 0 else [0] * len(lens)
+    tok_off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64) if lens else np.zeros(0, np.uint64)
+    key_off = np.concatenate([[0], np.cumsum(nk)[:-1]]).astype(np.uint64) if nk else np.zeros(0, np.uint64)
+    flat = np.concatenate([np.asarray(t, dtype=np.uint32) for t in token_streams]) if lens else np.zeros(0, np.uint32)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64 else
+                                    np.ascontiguousarray(a).view(np.int32)).to(dev)
+    t_tok, t_toff, t_len, t_koff = to(flat), to(tok_off), to(np.asarray(lens, np.uint64)), to(key_off)
+    out = torch.empty((max(1, sum(nk)), 32), dtype=torch.uint8, device=dev)
+    par = None
+    if parents is not None:
+        par = torch.from_numpy(np.ascontiguousarray(np.asarray(parents, dtype=np.uint8).reshape(-1, 32))).to(dev)
+    s = torch.cuda.current_stream() if stream is None else stream
+    _check(_lib.oc_chunk_keys_batch(t_tok.data_ptr(), t_toff.data_ptr(), t_len.data_ptr(), len(lens), G,
+                                    par.data_ptr() if par is not None else None, out.data_ptr(), t_koff.data_ptr(),
+                                    _stream(s)))
+    s.synchronize()
+    host = out.cpu().numpy()
+    return [host[int(k0):int(k0) + n] for k0, n in zip(key_off, nk)]
 
 
 def schedule_bandwidth(policy, s: Sequence[float], c: Sequence[float], cap_Bps: float,

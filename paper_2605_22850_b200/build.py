@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden,-Wall",
           "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["common.cpp", "sha256.cpp", "scheduler.cpp", "pool.cpp", "store.cpp", "descriptor.cpp", "tenants.cpp", "dispatch.cpp", "fetch.cu"]
+SOURCES = ["common.cpp", "sha256.cpp", "scheduler.cpp", "pool.cpp", "store.cpp", "descriptor.cpp", "tenants.cpp", "dispatch.cpp", "fetch.cu", "hash.cu"]
 
 
 def _newer(target, deps):
