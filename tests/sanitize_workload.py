@@ -10,7 +10,7 @@ from scenario import lib_target, make_dest, oracle_result, payload_stack, reques
 
 lay = Layout(2, 2, 64, 2, 16)
 ok = 0
-SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3,4").split(",")
+SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3,4,5").split(",")
 for kind in (("nhd", "hnd") if "1" in SECTIONS else ()):
     for engine in (oc.COPY_BULK, oc.COPY_LDST):
         for mode in (oc.FETCH_PERSISTENT, oc.FETCH_PER_LAYER):
@@ -124,5 +124,14 @@ if "4" in SECTIONS:
             assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 8, fam[1], dest)), opts
             ok += 1
         d.close()
+# chain keys of a ragged batch on the GPU
+if "5" in SECTIONS:
+    from oracle import keys as okeys
+    streams = [np.arange(n, dtype=np.uint32) * 7 + n for n in (0, 15, 16, 47, 160)]
+    got = oc.chunk_keys_batch(streams, 16)
+    for t, g in zip(streams, got):
+        want = b"".join(okeys.chunk_keys(t, 16))
+        assert g.tobytes() == want
+        ok += 1
 torch.cuda.synchronize()
 print("sanitize workload ok", ok)
