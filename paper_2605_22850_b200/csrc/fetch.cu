@@ -501,13 +501,6 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     __shared__ uint32_t s_unit[32], s_req[32], s_rel[32];
     constexpr bool BATCH = MODE != kSingle;
     __shared__ __align__(8) uint64_t fifo_full[kFifo], fifo_empty[kFifo];
-    if (MODE == kSingle) {
-        // Programmatic dependent launch (single fetches): this grid may be scheduled while the
-        // previous kernel of the stream drains; nothing is read or written before that kernel has
-        // completed (wait), and the next fetch may be scheduled onto SMs this grid frees (trigger).
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    }
     const uint64_t t0 = globaltimer();
     if (blockIdx.x == 0) {
         if (BATCH) {
@@ -1106,24 +1099,8 @@ cudaError_t set_bulk_smem(uint32_t smem) {
 int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
     if (p.stages < 2) return fail(OC_ENOTSUP, "bulk engine: two units do not fit in shared memory (use LDST)");
     OC_CUDA(set_bulk_smem<kSingle>(p.smem));
-    static const bool pdl = env_int("OC_PDL", 1) != 0;
-    if (pdl) {  // back-to-back fetches: the next grid is scheduled during this one's tail
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(p.copy_ctas + 1);
-        cfg.blockDim = dim3(64);
-        cfg.dynamicSmemBytes = p.smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        OC_CUDA(cudaLaunchKernelEx(&cfg, fetch_bulk_kernel<kSingle>, d->dd, BatchArgs{}, g0, g1, d->grab_ctr,
-                                   p.stages, p.stage_bytes));
-    } else {
-        fetch_bulk_kernel<kSingle><<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, BatchArgs{}, g0, g1, d->grab_ctr,
-                                                                     p.stages, p.stage_bytes);
-    }
+    fetch_bulk_kernel<kSingle><<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
+                                                                 p.stage_bytes);
     OC_CUDA(cudaGetLastError());
     d->grab_ctr += (g1 - g0) + p.copy_ctas;
     return OC_OK;
