@@ -86,6 +86,40 @@ __global__ void chain_keys_kernel(const uint32_t* __restrict__ tokens, const uin
         }
         prev[i] = v;
     }
+    if (G == 16) {  // the default chunk size: two blocks per key, next key's tokens loaded ahead
+        uint32_t t[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) t[i] = nkeys ? __ldg(&tok[i]) : 0u;
+        for (uint64_t k = 0; k < nkeys; k++) {
+            uint32_t nt[16];
+            const bool more = k + 1 < nkeys;
+#pragma unroll
+            for (int i = 0; i < 16; i++) nt[i] = more ? __ldg(&tok[(k + 1) * 16 + i]) : 0u;
+            uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+            uint32_t blk[16];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                blk[i] = prev[i];
+                blk[8 + i] = __byte_perm(t[i], 0, 0x0123);
+            }
+            compress(h, blk);
+#pragma unroll
+            for (int i = 0; i < 8; i++) blk[i] = __byte_perm(t[8 + i], 0, 0x0123);
+            blk[8] = 0x80000000u;
+#pragma unroll
+            for (int i = 9; i < 15; i++) blk[i] = 0;
+            blk[15] = (8 + 16) * 32;  // message bits: 32-byte digest + 16 tokens
+            compress(h, blk);
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                prev[i] = h[i];
+                dst[k * 8 + i] = __byte_perm(h[i], 0, 0x0123);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i++) t[i] = nt[i];
+        }
+        return;
+    }
     const uint64_t msg_words = 8 + (uint64_t)G;       // prev digest, then G tokens
     const uint64_t bits = msg_words * 32;
     const uint64_t total = ((msg_words + 1 + 2 + 15) / 16) * 16;  // + 0x80 word + 64-bit length
