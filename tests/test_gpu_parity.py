@@ -156,6 +156,27 @@ def test_peer_store_resolution():
     assert_same(run_lib(lay, 11, req, dest, store=local), oracle_result(lay, 11, req, dest))
 
 
+@pytest.mark.parametrize("engine", [oc.COPY_BULK, oc.COPY_LDST, oc.COPY_AUTO])
+@pytest.mark.parametrize("host_first", [False, True])
+def test_mixed_tier_chain(engine, host_first):
+    """One request whose chain is split between an HBM store and a pinned-host store attached as
+    its peer: one launch reads HBM and host memory (PCIe) and delivers every byte."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    req = requests_family(lay, 12, 0, [11])[0]
+    keys = oc.chunk_keys(req.tokens, 16)
+    pl = payload_stack(lay, 12, req.payload_ids)
+    first_tier, second_tier = (oc.TIER_PINNED_HOST, oc.TIER_HBM) if host_first else (oc.TIER_HBM, oc.TIER_PINNED_HOST)
+    local, peer = oc.Store(lay, capacity=16, tier=first_tier), oc.Store(lay, capacity=16, tier=second_tier)
+    local.put_chunks(keys[:6], pl[:6])
+    peer.put_chunks(keys[6:], pl[6:])
+    local.attach_peer(peer)
+    for kind in ("nhd", "hnd"):
+        dest = make_dest(lay, 11, kind, Bs=8, first_token=3, seed=6)
+        assert_same(run_lib(lay, 12, req, dest, store=local, engine=engine), oracle_result(lay, 12, req, dest))
+    local.close()
+    peer.close()
+
+
 # ---- the bench configuration: Llama-3-8B, 4K-token prefix hit -----------------------------------
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("engine", ENGINES)
