@@ -87,11 +87,13 @@ def test_batch_refetch_and_mix_with_single_fetches():
     st.close()
 
 
-def test_batch_pinned_host_tier():
+@pytest.mark.parametrize("order", [oc.BATCH_BY_REQUEST, oc.BATCH_BY_POSITION])
+@pytest.mark.parametrize("engine", [oc.COPY_BULK, oc.COPY_LDST, oc.COPY_AUTO])
+def test_batch_pinned_host_tier(order, engine):
     lay = OLayout(2, 4, 32, 2, 16)
     st, items = setup_batch(lay, SPECS, tier=oc.TIER_PINNED_HOST)
-    b = oc.Batch([it["desc"] for it in items])
-    b.fetch(torch.cuda.current_stream())
+    b = oc.Batch([it["desc"] for it in items], order=order)
+    b.fetch(torch.cuda.current_stream(), engine=engine)
     torch.cuda.synchronize()
     for it in items:
         it["desc"].sync_layer(1)
