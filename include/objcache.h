@@ -223,14 +223,16 @@ typedef enum {
 typedef enum {
     OC_COPY_LDST = 0,        /* 16-byte vector loads/stores through registers */
     OC_COPY_BULK = 1,        /* TMA bulk copies through a shared-memory ring  */
-    OC_COPY_AUTO = 3,        /* BULK when destination rows are contiguous (NHD, flat
-                                target) or strict pacing is asked for, else LDST
-                                (head-split targets such as HND); the default   */
     OC_COPY_CE = 2,          /* pinned-host chunks only (ENOTSUP otherwise): per layer, one
                                 strided copy-engine transfer per run of consecutive store slots
                                 into a double-buffered HBM stage (2*N*S bytes, owned by the
                                 descriptor), then the BULK kernel scatters the stage into the
-                                target and announces the layer.  PERSISTENT mode, unpaced.  */
+                                target and announces the layer.  PERSISTENT mode, unpaced.
+                                ~55 GB/s of PCIe reads vs ~51 for SM zero-copy; the saturated
+                                PCIe queue adds ~5 us to each launch of other streams.       */
+    OC_COPY_AUTO = 3,        /* BULK when destination rows are contiguous (NHD, flat
+                                target) or strict pacing is asked for, else LDST
+                                (head-split targets such as HND); the default   */
 } oc_copy_engine;
 
 typedef struct {
