@@ -228,6 +228,8 @@ typedef enum {
                                 into a double-buffered HBM stage (2*N*S bytes, owned by the
                                 descriptor), then the BULK kernel scatters the stage into the
                                 target and announces the layer.  PERSISTENT mode, unpaced.
+                                With a FLAT target the copies land in the client buffer
+                                directly (no stage, no scatter kernel).
                                 ~55 GB/s of PCIe reads vs ~51 for SM zero-copy; the saturated
                                 PCIe queue adds ~5 us to each launch of other streams.       */
     OC_COPY_AUTO = 3,        /* BULK when destination rows are contiguous (NHD, flat

@@ -315,6 +315,7 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     d->N = n;
     d->nb = v.bt.size();
     d->host_chunks = host_chunks;
+    if (t->kind == OC_TARGET_FLAT) d->flat_base = t->flat_base;
     if (host_chunks == n) {  // CE engine: maximal runs of chunks in consecutive slots
         for (uint64_t i = 0; i < n; i++) {
             if (i > 0 && src[i] == src[i - 1] + g.chunk) {

@@ -998,6 +998,13 @@ __global__ void __launch_bounds__(32) offload_bulk_kernel(const __grid_constant_
 
 __global__ void stamp_kernel(uint64_t* ts) { ts[0] = globaltimer(); }
 
+// CE engine into a flat client buffer: layer l has landed (the copies before this kernel on the
+// copy stream are complete) -- stamp it and announce it, as the fetch kernel's observer does.
+__global__ void announce_kernel(uint64_t* ts, uint32_t* ready, uint32_t value) {
+    ts[0] = globaltimer();
+    st_release(ready, value);
+}
+
 __global__ void wait_geq_kernel(const uint32_t* addr, uint32_t value) {
     while ((int32_t)(ld_acquire(addr) - value) < 0) __nanosleep(256);
 }
@@ -1221,6 +1228,37 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
         if (krc) return krc;
     }
     CeKit& kit = *d->ce_kit;
+    if (d->flat_base) {
+        // FLAT target (the paper's client buffer): layer l of a run of consecutive slots is one
+        // strided transfer straight into B_l = flat + l*N*S (chunk j at + j*S) -- no stage, no
+        // scatter kernel; a one-thread kernel after each layer's copies announces it.
+        uint32_t epoch = d->epoch + 1;
+        if (epoch == 0) epoch = 1;
+        d->dd.epoch = epoch;
+        d->epoch = epoch;  // the unit counters are untouched: cnt_base stays
+        d->poisoned = true;
+        OC_CUDA(cudaEventRecord(kit.start, s));
+        OC_CUDA(cudaStreamWaitEvent(kit.stream, kit.start, 0));
+        stamp_kernel<<<1, 1, 0, kit.stream>>>(d->dd.ts);
+        OC_CUDA(cudaGetLastError());
+        for (uint32_t l = 0; l < L; l++) {
+            uint8_t* dst = (uint8_t*)d->flat_base + (uint64_t)l * NS;
+            for (size_t r = 0; r < d->run_first.size(); r++)
+                OC_CUDA(cudaMemcpy2DAsync(dst + d->run_first[r] * d->geo.S, d->geo.S,
+                                          (const void*)(d->run_src[r] + (uint64_t)l * d->geo.S), d->geo.chunk,
+                                          d->geo.S, d->run_len[r], cudaMemcpyDefault, kit.stream));
+            announce_kernel<<<1, 1, 0, kit.stream>>>(d->dd.ts + 1 + l, d->dd.ready, (epoch - 1u) * L + l + 1u);
+            OC_CUDA(cudaGetLastError());
+        }
+        OC_CUDA(cudaEventRecord(kit.ce_done[L - 1], kit.stream));
+        OC_CUDA(cudaStreamWaitEvent(s, kit.ce_done[L - 1], 0));  // the caller's stream sees the fetch end
+        OC_CUDA(cudaEventRecord(d->done_ev, s));
+        d->poisoned = false;
+        d->last_mode = OC_FETCH_PERSISTENT;
+        d->last_stream = s;
+        d->fetched = true;
+        return OC_OK;
+    }
     if (!d->stage_mem) {
         d->stage_mem = dev_pool_alloc(d->device, 2 * NS, &d->stage_class);
         if (!d->stage_mem) return fail(OC_ENOMEM, "fetch_layerwise: CE stage allocation failed");

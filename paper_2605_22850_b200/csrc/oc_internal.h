@@ -177,6 +177,7 @@ struct Desc {
     // CE engine (pinned-host chunks): runs of chunks in consecutive slots, copied per layer by one
     // strided copy-engine transfer into a double-buffered HBM stage, then scattered by the kernel
     std::vector<uint64_t> run_first, run_len, run_src;
+    uint64_t flat_base = 0;    // FLAT target: the client buffer [L][N][S] (the CE engine writes it directly)
     void* stage_mem = nullptr;
     uint64_t stage_class = 0;
     struct CeKit* ce_kit = nullptr;  // copy stream + per-layer events, pooled per (device, L)

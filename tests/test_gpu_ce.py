@@ -104,3 +104,30 @@ def test_ce_errors():
         torch.cuda.synchronize()
         assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 31, req, dest))
         d.close()
+
+
+def test_ce_flat_target_direct_and_refetch():
+    """FLAT target: the copy engine writes the client buffer B_l directly (no stage); refetches
+    alternate with the kernel engines on the same descriptor (epochs stay consistent)."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    a, b = requests_family(lay, 31, 5, [3, 2])
+    with oc.Store(lay, capacity=16, tier=oc.TIER_PINNED_HOST) as st:
+        st.put_chunks(oc.chunk_keys(a.tokens, 16), payload_stack(lay, 31, a.payload_ids))
+        st.put_chunks(oc.chunk_keys(b.tokens, 16), payload_stack(lay, 31, b.payload_ids))   # 2 runs for b
+        dest = make_dest(lay, b.n_chunks, "flat")
+        buf = sentinel_buffer(dest.size)
+        d = oc.build_descriptor(st, st.match_prefix(b.tokens), lay, lib_target(oc, dest, buf.data_ptr()))
+        s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+        want = oracle_result(lay, 31, b, dest)
+        for engine in (oc.COPY_CE, oc.COPY_BULK, oc.COPY_CE, oc.COPY_LDST, oc.COPY_CE):
+            with torch.cuda.stream(s):
+                buf.fill_(0xA5)
+            d.fetch_layerwise(s, engine=engine)
+            for l in range(lay.num_layers):
+                d.wait_layer(l, cons)
+            cons.synchronize()
+            s.synchronize()
+            assert np.array_equal(buf.cpu().numpy(), want), engine
+            t = d.layer_times().astype(np.int64)
+            assert np.all(np.diff(t) >= 0)
+        d.close()
