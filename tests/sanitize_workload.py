@@ -124,6 +124,15 @@ if "4" in SECTIONS:
             assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 8, fam[1], dest)), opts
             ok += 1
         d.close()
+        fdest = make_dest(lay, fam[1].n_chunks, "flat")       # CE straight into the client buffer
+        fbuf = sentinel_buffer(fdest.size)
+        d = oc.build_descriptor(st, kb, lay, lib_target(oc, fdest, fbuf.data_ptr()))
+        d.fetch_layerwise(s, engine=oc.COPY_CE)
+        d.sync_layer(1)
+        s.synchronize()
+        assert np.array_equal(fbuf.cpu().numpy(), oracle_result(lay, 8, fam[1], fdest))
+        ok += 1
+        d.close()
 # chain keys of a ragged batch on the GPU
 if "5" in SECTIONS:
     from oracle import keys as okeys
