@@ -72,6 +72,9 @@ def parse():
     p.add_argument("--pool", type=int, default=0, help="streaming multi-tenant runtime: this many requests "
                    "arrive over time (Poisson) into oc.TenantPool epochs (100 ms) under a shared cap, per policy "
                    "and dispatch (adds a 'pool' object)")
+    p.add_argument("--stall-gemm", action="store_true", help="added TTFT with real per-layer prefill compute: "
+                   "each layer's miss tokens through the four projection GEMMs of a Llama-3-8B layer (random "
+                   "bf16 weights) on the consumer stream, instead of timer spins (adds a 'stall_gemm' object)")
     p.add_argument("--hash", type=int, default=0, help="chain keys of this many 4K-token requests: one GPU launch "
                    "(oc_chunk_keys_batch) vs the host's SHA-extension loop (adds a 'hash' object)")
     p.add_argument("--batch", default="", help="NxM: N 4K-token + M 64K-token concurrent requests (config 5, "
@@ -376,6 +379,8 @@ def main_ours(args):
         out["sched"] = sched_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.batch:
         out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and args.stall_gemm:
+        out["stall_gemm"] = stall_gemm_leg(args, oc, torch, dev, lay_t)
     if rank == 0 and args.hash:
         out["hash"] = hash_leg(args, oc, torch, dev)
     if rank == 0 and args.pool:
@@ -1488,6 +1493,82 @@ def sched_workloads():
     w["70B"] = (synth.LLAMA3_70B, round(sum_rstar / 2 * 8 / 1e9, 3), c70,
                 "FLOP model at 50% of the measured sustained bf16 rate (B200)")
     return w
+
+
+def stall_gemm_leg(args, oc, torch, dev, lay_t):
+    """Added TTFT with real prefill compute sharing the GPU ("a shape-true Llama
+    layer (random bf16 weights; only shapes matter) over the miss tokens"): per layer the consumer
+    stream waits for the layer's KV (wait_layer) and then runs the layer's four projection GEMMs
+    (QKV 4096x6144, O 4096x4096, gate+up 4096x28672, down 14336x4096) on the m miss tokens; the
+    attention itself is left out.  TTFT = fetch launch -> end of the last layer's GEMMs (CUDA
+    events); added = TTFT - the same GEMM chain with the KV already resident.  Unlike the timer
+    spins of the stall leg, these GEMMs contend with the fetch for SMs and HBM."""
+    import synth
+    L, G, Bs = lay_t[0], lay_t[4], 16
+    row, S, chunk = oc.geometry(lay_t)
+    w = [torch.randn(k, n, dtype=torch.bfloat16, device=dev) * 0.01
+         for k, n in ((4096, 6144), (4096, 4096), (4096, 28672), (14336, 4096))]
+    out = {}
+    for name, ctx in (("4k", 4096), ("64k", 65536)):
+        cached = ctx * 7 // 8
+        m = ctx - cached
+        N = cached // G
+        x = torch.randn(m, 4096, dtype=torch.bfloat16, device=dev)
+        h = torch.empty(m, 14336, dtype=torch.bfloat16, device=dev)
+        need = N * G // Bs
+        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
+        per_kv = need * Bs * row
+        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
+        tgt = oc.PagedTarget(kb, [x_ + per_kv for x_ in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
+                             synth.block_table(7, need, need), 0)
+        copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+        def layer_gemms():
+            torch.matmul(x, w[0])
+            torch.matmul(x, w[1])
+            gu = torch.matmul(x, w[2])
+            torch.matmul(gu[:, :14336], w[3], out=h[:, :4096])
+
+        def chain(d, fopts):
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(copy_s)
+            cons_s.wait_event(a0)
+            if d is not None:
+                d.fetch_layerwise(copy_s, **fopts)
+            with torch.cuda.stream(cons_s):
+                for l in range(L):
+                    if d is not None:
+                        d.wait_layer(l, cons_s)
+                    layer_gemms()
+            a1.record(cons_s)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1)
+
+        chain(None, {})
+        base = min(chain(None, {}) for _ in range(3))
+        res = {"miss_tokens": m, "hit_chunks": N, "compute_ms_resident": round(base, 3),
+               "compute_ms_per_layer": round(base / L, 4)}
+        for tier_name, tier, fopts in (("hbm", oc.TIER_HBM, {"engine": oc.COPY_BULK}),
+                                       ("pinned_host", oc.TIER_PINNED_HOST, {"engine": oc.COPY_BULK}),
+                                       ("pinned_host_ce", oc.TIER_PINNED_HOST, {"engine": oc.COPY_CE})):
+            store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
+            (tok,), _ = synth.family_streams(9100 + N, G, 0, [N])
+            keys = oc.chunk_keys(tok, G)
+            for b0 in range(0, N, 512):
+                pl = torch.randint(0, 256, (min(N, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev)
+                store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
+                del pl
+            d = oc.build_descriptor(store, keys, lay_t, tgt)
+            chain(d, fopts)
+            t = min(chain(d, fopts) for _ in range(3))
+            res[tier_name] = {"ttft_ms": round(t, 3), "added_ms": round(t - base, 3)}
+            d.close()
+            store.close()
+        out[name] = res
+        del cache
+        torch.cuda.empty_cache()
+    return out
 
 
 def hash_leg(args, oc, torch, dev, G=16, ctx=4096):
