@@ -1514,7 +1514,6 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
         m = ctx - cached
         N = cached // G
         x = torch.randn(m, 4096, dtype=torch.bfloat16, device=dev)
-        h = torch.empty(m, 14336, dtype=torch.bfloat16, device=dev)
         need = N * G // Bs
         cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
         per_kv = need * Bs * row
@@ -1527,7 +1526,7 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
             torch.matmul(x, w[0])
             torch.matmul(x, w[1])
             gu = torch.matmul(x, w[2])
-            torch.matmul(gu[:, :14336], w[3], out=h[:, :4096])
+            torch.matmul(gu[:, :14336], w[3])
 
         def chain(d, fopts):
             torch.cuda.synchronize()
