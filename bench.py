@@ -1548,9 +1548,14 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
         base = min(chain(None, {}) for _ in range(3))
         res = {"miss_tokens": m, "hit_chunks": N, "compute_ms_resident": round(base, 3),
                "compute_ms_per_layer": round(base / L, 4)}
-        for tier_name, tier, fopts in (("hbm", oc.TIER_HBM, {"engine": oc.COPY_BULK}),
-                                       ("pinned_host", oc.TIER_PINNED_HOST, {"engine": oc.COPY_BULK}),
-                                       ("pinned_host_ce", oc.TIER_PINNED_HOST, {"engine": oc.COPY_CE})):
+        for tier_name, tier, variants in (
+                ("hbm", oc.TIER_HBM, (("", {"engine": oc.COPY_BULK}),
+                                      # a copy-CTA budget: the transfer stays ahead of compute on
+                                      # fewer SMs and steals less from the GEMMs
+                                      ("_ctas64", {"engine": oc.COPY_BULK, "max_ctas": 64}),
+                                      ("_ctas16", {"engine": oc.COPY_BULK, "max_ctas": 16}))),
+                ("pinned_host", oc.TIER_PINNED_HOST, (("", {"engine": oc.COPY_BULK}),
+                                                      ("_ce", {"engine": oc.COPY_CE})))):
             store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
             (tok,), _ = synth.family_streams(9100 + N, G, 0, [N])
             keys = oc.chunk_keys(tok, G)
@@ -1559,9 +1564,10 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                 store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
                 del pl
             d = oc.build_descriptor(store, keys, lay_t, tgt)
-            chain(d, fopts)
-            t = min(chain(d, fopts) for _ in range(3))
-            res[tier_name] = {"ttft_ms": round(t, 3), "added_ms": round(t - base, 3)}
+            for suffix, fopts in variants:
+                chain(d, fopts)
+                t = min(chain(d, fopts) for _ in range(3))
+                res[tier_name + suffix] = {"ttft_ms": round(t, 3), "added_ms": round(t - base, 3)}
             d.close()
             store.close()
         out[name] = res
