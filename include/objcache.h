@@ -113,6 +113,14 @@ OC_API int oc_store_create(const oc_layout* layout, int tier, int device, uint64
                            oc_store** out);
 OC_API int oc_store_destroy(oc_store* store);
 OC_API int oc_store_count(const oc_store* store, uint64_t* n_chunks);
+/* Hot layers (pinned-host stores, before the first put): mirror the first `hot_layers` layers of
+ * every chunk in HBM (hot_layers*S bytes per slot, cudaMalloc'd now).  A fetch whose chunks all
+ * carry the mirror reads those layers from HBM with a full grid -- its exposed first-layer
+ * latency X0 drops from one layer over PCIe to one layer at HBM speed -- and the
+ * rest from host memory.  EINVAL: HBM or imported store, or chunks already stored; ERANGE:
+ * hot_layers > L.  put_from_paged into such a store is ENOTSUP. */
+OC_API int oc_store_set_hot_layers(oc_store* store, uint32_t hot_layers);
+
 /* Slab base device address and size in bytes (for IPC export and tests). */
 OC_API int oc_store_slab(const oc_store* store, uint64_t* base, uint64_t* bytes);
 

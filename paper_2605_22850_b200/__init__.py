@@ -83,6 +83,7 @@ _SIGS = {
     "oc_store_destroy": [_vp],
     "oc_store_count": [_vp, c_u64p],
     "oc_store_slab": [_vp, c_u64p, c_u64p],
+    "oc_store_set_hot_layers": [_vp, ctypes.c_uint32],
     "oc_put_chunks": [_vp, _vp, _vp, ctypes.c_uint64, c_u64p, c_u64p],
     "oc_match_prefix": [_vp, c_u32p, ctypes.c_uint64, _vp, _vp, ctypes.c_uint64, c_u64p],
     "oc_store_lookup": [_vp, _vp, ctypes.c_uint64, c_u64p, c_u64p],
@@ -296,6 +297,10 @@ class Store:
         n = ctypes.c_uint64()
         _check(_lib.oc_store_count(self._h, ctypes.byref(n)))
         return n.value
+
+    def set_hot_layers(self, hot_layers: int):
+        """Pinned-host stores: mirror the first `hot_layers` layers of every chunk in HBM."""
+        _check(_lib.oc_store_set_hot_layers(self._h, int(hot_layers)))
 
     @property
     def slab(self):

@@ -84,12 +84,12 @@ int normalize_target(const Geometry& g, uint64_t n, const oc_target* t, const ch
 }
 
 // Device block layout shared by descriptors and offload jobs:
-//   src[N] | k_base[L] | v_base[L] | ts[L+1] | unit_cnt[L] | ready, next | bt[nb] | pos[N]
+//   src[N] | k_base[L] | v_base[L] | ts[L+1] | unit_cnt[L] | ready, next | bt[nb] | pos[N] | hot[N]
 struct BlockLayout {
-    size_t o_src, o_kb, o_vb, o_ts, o_cnt, o_ready, o_next, o_bt, o_pos, total;
+    size_t o_src, o_kb, o_vb, o_ts, o_cnt, o_ready, o_next, o_bt, o_pos, o_hot, total;
 };
 
-BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos) {
+BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos, bool with_hot = false) {
     BlockLayout b;
     b.o_src = 0;
     b.o_kb = align16(b.o_src + n * 8);
@@ -100,7 +100,8 @@ BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos) {
     b.o_next = b.o_ready + 4;
     b.o_bt = align16(b.o_ready + 16);
     b.o_pos = align16(b.o_bt + nb * 4);
-    b.total = align16(b.o_pos + (with_pos ? n * 4 : 0));
+    b.o_hot = align16(b.o_pos + (with_pos ? n * 4 : 0));
+    b.total = align16(b.o_hot + (with_hot ? n * 8 : 0));
     return b;
 }
 
@@ -111,10 +112,11 @@ BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos) {
 // upload stream with up->ev marking completion (see Upload in oc_internal.h).
 int upload_block(int device, const Geometry& g, const std::vector<uint64_t>& src, const PagedView& v,
                  const std::vector<uint32_t>* pos, const char* who, void** mem_out, uint64_t* cls_out, DevDesc* dd,
-                 const uint32_t** pos_dev, Upload* up, bool ordered, cudaStream_t on_stream) {
+                 const uint32_t** pos_dev, Upload* up, bool ordered, cudaStream_t on_stream,
+                 const std::vector<uint64_t>* src_hot = nullptr, uint32_t hot_layers = 0) {
     const uint64_t n = src.size();
     const uint32_t L = g.L;
-    const BlockLayout b = block_layout(n, L, v.bt.size(), pos != nullptr);
+    const BlockLayout b = block_layout(n, L, v.bt.size(), pos != nullptr, src_hot != nullptr);
     uint64_t scls = 0;
     uint8_t* stage = (uint8_t*)dev_pool_alloc(-1, b.total, &scls);
     if (!stage) return fail(OC_ENOMEM, std::string(who) + ": pinned staging allocation failed");
@@ -124,6 +126,7 @@ int upload_block(int device, const Geometry& g, const std::vector<uint64_t>& src
     std::memcpy(stage + b.o_vb, v.vb.data(), L * 8);
     std::memcpy(stage + b.o_bt, v.bt.data(), v.bt.size() * 4);
     if (pos) std::memcpy(stage + b.o_pos, pos->data(), n * 4);
+    if (src_hot) std::memcpy(stage + b.o_hot, src_hot->data(), n * 8);
     uint64_t cls = 0;
     void* mem = dev_pool_alloc(device, b.total, &cls);
     if (!mem) {
@@ -160,6 +163,10 @@ int upload_block(int device, const Geometry& g, const std::vector<uint64_t>& src
     dd->next_unit = (uint32_t*)(m + b.o_next);
     dd->bt = (const int32_t*)(m + b.o_bt);
     if (pos_dev) *pos_dev = pos ? (const uint32_t*)(m + b.o_pos) : nullptr;
+    if (src_hot) {
+        dd->src_hot = (const uint64_t*)(m + b.o_hot);
+        dd->hot_layers = hot_layers;
+    }
     dd->S = g.S;
     dd->row = g.row;
     dd->block_stride = v.block_stride;
@@ -291,12 +298,15 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
         return oc::fail(OC_ERANGE, "build_descriptor: prefix longer than 2^31 tokens");
 
     // Resolve every key (first missing key reported by index, in prefix order).
-    std::vector<uint64_t> src(n);
+    std::vector<uint64_t> src(n), hot(n);
     uint64_t host_chunks = 0;
+    uint32_t hot_layers = ~0u;  // leading layers mirrored in HBM for EVERY chunk
     for (uint64_t i = 0; i < n; i++) {
         int tier = OC_TIER_HBM;
-        const bool found = oc::store_resolve(s, keys[i], &src[i], &tier);
+        uint32_t hl = 0;
+        const bool found = oc::store_resolve(s, keys[i], &src[i], &tier, &hot[i], &hl);
         host_chunks += tier == OC_TIER_PINNED_HOST;
+        hot_layers = std::min(hot_layers, found ? hl : 0u);
         if (!found) {
             if (bad_index) *bad_index = i;
             return oc::fail(OC_ENOTFOUND, "build_descriptor: chunk key " + std::to_string(i) + " not found");
@@ -328,8 +338,12 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
         }
     }
     oc::DeviceGuard dg(d->device);
+    if (hot_layers == ~0u) hot_layers = 0;
+    d->hot_layers = hot_layers;
+    if (hot_layers)  // runs of consecutive slots have consecutive mirrors
+        for (uint64_t r = 0; r < d->run_first.size(); r++) d->run_hot.push_back(hot[d->run_first[r]]);
     rc = oc::upload_block(d->device, g, src, v, nullptr, "build_descriptor", &d->dev_mem, &d->dev_mem_class, &d->dd,
-                          nullptr, &d->up, false, nullptr);
+                          nullptr, &d->up, false, nullptr, hot_layers ? &hot : nullptr, hot_layers);
     if (rc) return rc;
     d->dd.chunk_major = delivery == OC_DELIVER_CHUNK_MAJOR;
     oc::plan_units(d.get(), 0);
@@ -346,6 +360,7 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
     if (n == 0) return OC_OK;
     if (!keys) return oc::fail(OC_EINVAL, "put_from_paged: null keys");
     if (s->read_only) return oc::fail(OC_EINVAL, "put_from_paged: store is a read-only imported peer");
+    if (s->hot_layers) return oc::fail(OC_ENOTSUP, "put_from_paged: store mirrors hot layers (use put_chunks)");
     if (t->kind != OC_TARGET_PAGED) return oc::fail(OC_EINVAL, "put_from_paged: source must be a paged cache");
     if (!oc::same_layout(*layout, s->layout)) return oc::fail(OC_EINVAL, "put_from_paged: layout differs from the store's");
     const oc::Geometry& g = s->geo;

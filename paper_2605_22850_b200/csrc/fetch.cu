@@ -103,7 +103,8 @@ __device__ __forceinline__ const uint8_t* unit_src(const DevDesc& d, const UnitG
         return (const uint8_t*)d.stage_base[u.layer & 1] + (uint64_t)u.j * d.S + (uint64_t)u.q0 * d.row;
     if (d.staged == 2)  // flat payload [L][N][S]
         return (const uint8_t*)d.stage_base[0] + ((uint64_t)u.layer * d.N + u.j) * d.S + (uint64_t)u.q0 * d.row;
-    return (const uint8_t*)d.src[u.j] + (uint64_t)u.layer * d.S + (uint64_t)u.q0 * d.row;
+    const uint64_t base = u.layer < d.hot_layers ? d.src_hot[u.j] : d.src[u.j];  // hot layers: HBM mirror
+    return (const uint8_t*)base + (uint64_t)u.layer * d.S + (uint64_t)u.q0 * d.row;
 }
 
 // Destination of row q of chunk `pos`'s layer-l slice: matrix kv = q >= G, token t = q - kv*G,
@@ -1243,10 +1244,12 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
         OC_CUDA(cudaGetLastError());
         for (uint32_t l = 0; l < L; l++) {
             uint8_t* dst = (uint8_t*)d->flat_base + (uint64_t)l * NS;
+            const bool hot = l < d->hot_layers;  // from the HBM mirror (pitch hot_layers*S)
             for (size_t r = 0; r < d->run_first.size(); r++)
                 OC_CUDA(cudaMemcpy2DAsync(dst + d->run_first[r] * d->geo.S, d->geo.S,
-                                          (const void*)(d->run_src[r] + (uint64_t)l * d->geo.S), d->geo.chunk,
-                                          d->geo.S, d->run_len[r], cudaMemcpyDefault, kit.stream));
+                                          (const void*)((hot ? d->run_hot[r] : d->run_src[r]) + (uint64_t)l * d->geo.S),
+                                          hot ? (uint64_t)d->hot_layers * d->geo.S : d->geo.chunk, d->geo.S,
+                                          d->run_len[r], cudaMemcpyDefault, kit.stream));
             announce_kernel<<<1, 1, 0, kit.stream>>>(d->dd.ts + 1 + l, d->dd.ready, (epoch - 1u) * L + l + 1u);
             OC_CUDA(cudaGetLastError());
         }
@@ -1288,10 +1291,12 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     for (uint32_t l = 0; l < L; l++) {
         if (l >= 2) OC_CUDA(cudaStreamWaitEvent(kit.stream, kit.scat_done[l - 2], 0));  // stage l&1 free
         uint8_t* stage = (uint8_t*)d->stage_mem + (l & 1) * NS;
+        const bool hot = l < d->hot_layers;  // from the HBM mirror (pitch hot_layers*S)
         for (size_t r = 0; r < d->run_first.size(); r++)
             OC_CUDA(cudaMemcpy2DAsync(stage + d->run_first[r] * d->geo.S, d->geo.S,
-                                      (const void*)(d->run_src[r] + (uint64_t)l * d->geo.S), d->geo.chunk,
-                                      d->geo.S, d->run_len[r], cudaMemcpyDefault, kit.stream));
+                                      (const void*)((hot ? d->run_hot[r] : d->run_src[r]) + (uint64_t)l * d->geo.S),
+                                      hot ? (uint64_t)d->hot_layers * d->geo.S : d->geo.chunk, d->geo.S,
+                                      d->run_len[r], cudaMemcpyDefault, kit.stream));
         OC_CUDA(cudaEventRecord(kit.ce_done[l], kit.stream));
         OC_CUDA(cudaStreamWaitEvent(s, kit.ce_done[l], 0));
         int rc = launch_bulk(d, p, l * upl, (l + 1) * upl, s);
@@ -1398,9 +1403,23 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     d->cnt_base = dd.cnt_target;
     d->poisoned = true;
     const uint32_t upl = dd.units_per_layer;
-    if (o.mode == OC_FETCH_PERSISTENT) {
+    const bool paced = dd.pace_ns || dd.pace_ns_per_byte > 0.0;
+    if (o.mode == OC_FETCH_PERSISTENT && dd.hot_layers && host_src && !paced) {
+        // Hot layers mirrored in HBM: they go first with an HBM-sized grid (X0 at HBM speed), the
+        // rest follows from host memory with the PCIe-sized grid; each launch announces its layers.
+        const uint32_t k_units = std::min(dd.hot_layers, dd.L) * upl;
+        const uint32_t ranges[2][2] = {{0, k_units}, {k_units, (uint32_t)total_units}};
+        const uint32_t caps[2] = {o.max_ctas, max_ctas};
+        for (int part = 0; part < 2; part++) {
+            const uint32_t g0 = ranges[part][0], g1 = ranges[part][1];
+            if (g1 <= g0) continue;
+            int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, plan_bulk(dd, sms, caps[part], g1 - g0), g0, g1, s)
+                                              : launch_ldst(d, sms, caps[part], g0, g1, s);
+            if (rc) return rc;
+        }
+    } else if (o.mode == OC_FETCH_PERSISTENT) {
         BulkPlan p = plan_bulk(dd, sms, max_ctas, total_units);
-        if (dd.pace_ns || dd.pace_ns_per_byte > 0.0) shallow_ring(&p);
+        if (paced) shallow_ring(&p);
         int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, 0, (uint32_t)total_units, s)
                                           : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
         if (rc) return rc;

@@ -96,9 +96,16 @@ struct Store {
     std::vector<Store*> peers;
     mutable std::shared_mutex mu;
     cudaStream_t put_stream = nullptr;
+    // Pinned-host stores may mirror the first hot_layers layers of every chunk in HBM (slot i's
+    // mirror: hot_slab + i * hot_layers * S, the same layout as the slot's first layers), so a
+    // fetch's first layers -- its exposed X0 -- come from HBM.
+    uint32_t hot_layers = 0;
+    uint8_t* hot_slab = nullptr;
 };
-// Resolve a key to a device address (and the tier holding it): local slots first, then peers.
-bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier = nullptr);
+// Resolve a key to a device address (and the tier holding it; and its HBM mirror and mirrored
+// layer count, 0 if none): local slots first, then peers.
+bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier = nullptr, uint64_t* hot = nullptr,
+                   uint32_t* hot_layers = nullptr);
 
 // Host -> device upload of a descriptor/offload block (descriptor.cpp).  The bytes are staged in
 // pooled pinned memory and copied on a private non-blocking stream of the device; `ev` completes
@@ -140,6 +147,8 @@ struct DevDesc {
     uint32_t chunk_major;     // 1: only the completion of the whole prefix is announced
     uint64_t pace_ns;         // persistent mode: ns between layer releases (0 = off)
     double pace_ns_per_byte;  // strict pacing: unit released at t0 + (fetch bytes before it) * this
+    const uint64_t* src_hot;  // [N] HBM mirror of each chunk's first hot_layers layers
+    uint32_t hot_layers;      // layers l < hot_layers are read from src_hot (0: none)
     uint64_t stage_base[2];   // CE engine: layer l's slices were staged at stage_base[l & 1] as [N][S]
     uint32_t staged;          // 0: sources from src[]; 1: CE stage (stage_base[l & 1]); 2: a flat
                               // layer-major payload [L][N][S] at stage_base[0] (oc_scatter_flat)
@@ -176,7 +185,8 @@ struct Desc {
     cudaEvent_t sync_ev = nullptr;
     // CE engine (pinned-host chunks): runs of chunks in consecutive slots, copied per layer by one
     // strided copy-engine transfer into a double-buffered HBM stage, then scattered by the kernel
-    std::vector<uint64_t> run_first, run_len, run_src;
+    std::vector<uint64_t> run_first, run_len, run_src, run_hot;  // run_hot: the runs' HBM mirrors
+    uint32_t hot_layers = 0;   // leading layers with an HBM mirror for every chunk (0: none)
     uint64_t flat_base = 0;    // FLAT target: the client buffer [L][N][S] (the CE engine writes it directly)
     void* stage_mem = nullptr;
     uint64_t stage_class = 0;

@@ -26,18 +26,20 @@ struct ExportHeader {
 
 }  // namespace
 
-bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier) {
+bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier, uint64_t* hot, uint32_t* hot_layers) {
     {
         std::shared_lock<std::shared_mutex> lk(s->mu);
         auto it = s->index.find(k);
         if (it != s->index.end()) {
             *addr = (uint64_t)(uintptr_t)s->slab + it->second * s->geo.chunk;
             if (tier) *tier = s->tier;
+            if (hot) *hot = s->hot_layers ? (uint64_t)(uintptr_t)s->hot_slab + it->second * s->hot_layers * s->geo.S : 0;
+            if (hot_layers) *hot_layers = s->hot_layers;
             return true;
         }
     }
     for (Store* p : s->peers)
-        if (store_resolve(p, k, addr, tier)) return true;
+        if (store_resolve(p, k, addr, tier, hot, hot_layers)) return true;
     return false;
 }
 
@@ -103,6 +105,7 @@ OC_API int oc_store_destroy(oc_store* h) {
     {
         oc::DeviceGuard dg(s->device);
         if (s->put_stream) cudaStreamDestroy(s->put_stream);
+        if (s->hot_slab) cudaFree(s->hot_slab);
         if (s->ipc_mapped) cudaIpcCloseMemHandle(s->slab);
         else if (s->owns_slab) {
             if (s->tier == OC_TIER_HBM) cudaFree(s->slab);
@@ -111,6 +114,27 @@ OC_API int oc_store_destroy(oc_store* h) {
         cudaGetLastError();
     }
     delete s;
+    return OC_OK;
+}
+
+OC_API int oc_store_set_hot_layers(oc_store* h, uint32_t hot_layers) {
+    if (!h) return oc::fail(OC_EINVAL, "store_set_hot_layers: null store");
+    Store* s = (Store*)h;
+    if (s->tier != OC_TIER_PINNED_HOST || s->read_only)
+        return oc::fail(OC_EINVAL, "store_set_hot_layers: only for an own pinned-host store");
+    if (hot_layers > s->geo.L) return oc::fail(OC_ERANGE, "store_set_hot_layers: more layers than the model has");
+    std::unique_lock<std::shared_mutex> lk(s->mu);
+    if (s->count) return oc::fail(OC_EINVAL, "store_set_hot_layers: the store already holds chunks");
+    oc::DeviceGuard dg(s->device);
+    if (s->hot_slab) {
+        cudaFree(s->hot_slab);
+        s->hot_slab = nullptr;
+    }
+    s->hot_layers = 0;
+    if (hot_layers) {
+        OC_CUDA(cudaMalloc((void**)&s->hot_slab, s->capacity * hot_layers * s->geo.S));
+        s->hot_layers = hot_layers;
+    }
     return OC_OK;
 }
 
@@ -181,6 +205,10 @@ OC_API int oc_put_chunks(oc_store* h, const oc_key* keys, const void* payloads, 
         }
         uint64_t slot = s->count;
         OC_CUDA(cudaMemcpyAsync(s->slab + slot * cb, src + i * cb, cb, cudaMemcpyDefault, s->put_stream));
+        if (s->hot_layers) {  // the chunk's first layers are its first hot_layers * S bytes
+            const uint64_t hb = (uint64_t)s->hot_layers * s->geo.S;
+            OC_CUDA(cudaMemcpyAsync(s->hot_slab + slot * hb, src + i * cb, hb, cudaMemcpyDefault, s->put_stream));
+        }
         s->index.emplace(keys[i], slot);
         s->count++;
         fresh++;

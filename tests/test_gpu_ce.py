@@ -131,3 +131,58 @@ def test_ce_flat_target_direct_and_refetch():
             t = d.layer_times().astype(np.int64)
             assert np.all(np.diff(t) >= 0)
         d.close()
+
+
+@pytest.mark.parametrize("hot", [1, 2, 3])
+def test_hot_layer_mirror(hot):
+    """A pinned-host store mirroring its chunks' first `hot` layers in HBM: every engine (split
+    launches for the kernel engines; mirror copies for the CE engine) delivers the oracle's bytes,
+    for a chain of two slot runs, into paged and flat targets."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    a, b = requests_family(lay, 41, 4, [2, 3])
+    with oc.Store(lay, capacity=16, tier=oc.TIER_PINNED_HOST) as st:
+        st.set_hot_layers(hot)
+        st.put_chunks(oc.chunk_keys(a.tokens, 16), payload_stack(lay, 41, a.payload_ids))
+        st.put_chunks(oc.chunk_keys(b.tokens, 16), payload_stack(lay, 41, b.payload_ids))
+        for kind in ("nhd", "hnd", "flat"):
+            dest = make_dest(lay, b.n_chunks, kind, Bs=8, first_token=2 if kind != "flat" else 0, seed=9)
+            buf = sentinel_buffer(dest.size)
+            d = oc.build_descriptor(st, st.match_prefix(b.tokens), lay, lib_target(oc, dest, buf.data_ptr()))
+            s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+            want = oracle_result(lay, 41, b, dest)
+            for engine in (oc.COPY_AUTO, oc.COPY_BULK, oc.COPY_LDST, oc.COPY_CE):
+                with torch.cuda.stream(s):
+                    buf.fill_(0xA5)
+                d.fetch_layerwise(s, engine=engine)
+                for l in range(lay.num_layers):
+                    d.wait_layer(l, cons)
+                cons.synchronize()
+                s.synchronize()
+                assert np.array_equal(buf.cpu().numpy(), want), (kind, engine)
+                t = d.layer_times().astype(np.int64)
+                assert np.all(np.diff(t) >= 0)
+            d.close()
+
+
+def test_hot_layer_errors():
+    lay = OLayout(2, 2, 64, 2, 16)
+    req = requests_family(lay, 42, 0, [2])[0]
+    keys = oc.chunk_keys(req.tokens, 16)
+    with oc.Store(lay, capacity=4) as hbm:
+        with pytest.raises(oc.ObjcacheError) as e:
+            hbm.set_hot_layers(1)
+        assert e.value.code == oc.OC_EINVAL
+    with oc.Store(lay, capacity=4, tier=oc.TIER_PINNED_HOST) as st:
+        with pytest.raises(oc.ObjcacheError) as e:
+            st.set_hot_layers(3)
+        assert e.value.code == oc.OC_ERANGE
+        st.set_hot_layers(1)
+        st.put_chunks(keys, payload_stack(lay, 42, req.payload_ids))
+        with pytest.raises(oc.ObjcacheError) as e:
+            st.set_hot_layers(2)
+        assert e.value.code == oc.OC_EINVAL
+        src = make_dest(lay, 2, "nhd")
+        cache = sentinel_buffer(src.size)
+        with pytest.raises(oc.ObjcacheError) as e:
+            oc.put_from_paged(st, keys, lay, lib_target(oc, src, cache.data_ptr()))
+        assert e.value.code == oc.OC_ENOTSUP
