@@ -682,7 +682,8 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
     if cells is None:
         cells = [("4k", 4096, 3584, 63.47)] + ([("64k", 65536, 57344, 2423.90)] if args.stall64k else [])
     if tiers is None:
-        tiers = (("hbm", oc.TIER_HBM), ("pinned_host", oc.TIER_PINNED_HOST), ("pinned_host_ce", oc.TIER_PINNED_HOST))
+        tiers = (("hbm", oc.TIER_HBM), ("pinned_host", oc.TIER_PINNED_HOST), ("pinned_host_ce", oc.TIER_PINNED_HOST),
+                 ("pinned_host_hot1", oc.TIER_PINNED_HOST))
     for name, ctx, cached, t_total_ms in cells:
         N = cached // G
         windows = {"a100": t_total_ms / L if t_total_ms else None,             # Table A5 (A100)
@@ -698,6 +699,8 @@ def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, window
         for tier_name, tier in tiers:
             cur["fo"] = {"engine": oc.COPY_CE} if tier_name.endswith("_ce") else fopts
             store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
+            if tier_name.endswith("_hot1"):            # layer 0 of every chunk mirrored in HBM
+                store.set_hot_layers(1)
             (tok,), _ = synth.family_streams(9000 + N, G, 0, [N])
             keys = oc.chunk_keys(tok, G)
             gen = torch.Generator(device=dev).manual_seed(N)
