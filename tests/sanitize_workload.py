@@ -133,6 +133,26 @@ if "4" in SECTIONS:
         assert np.array_equal(fbuf.cpu().numpy(), oracle_result(lay, 8, fam[1], fdest))
         ok += 1
         d.close()
+# a pinned-host store mirroring layer 0 in HBM: split launches and CE mirror copies
+if "4" in SECTIONS:
+    fam = requests_family(lay, 9, 3, [2])
+    with oc.Store(lay, capacity=8, tier=oc.TIER_PINNED_HOST) as st:
+        st.set_hot_layers(1)
+        kf = oc.chunk_keys(fam[0].tokens, 16)
+        st.put_chunks(kf, payload_stack(lay, 9, fam[0].payload_ids))
+        dest = make_dest(lay, fam[0].n_chunks, "nhd", Bs=8, seed=4)
+        buf = sentinel_buffer(dest.size)
+        d = oc.build_descriptor(st, kf, lay, lib_target(oc, dest, buf.data_ptr()))
+        s = torch.cuda.Stream()
+        for engine in (oc.COPY_BULK, oc.COPY_LDST, oc.COPY_CE):
+            with torch.cuda.stream(s):
+                buf.fill_(0xA5)
+            d.fetch_layerwise(s, engine=engine)
+            d.sync_layer(1)
+            s.synchronize()
+            assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 9, fam[0], dest)), engine
+            ok += 1
+        d.close()
 # chain keys of a ragged batch on the GPU
 if "5" in SECTIONS:
     from oracle import keys as okeys
