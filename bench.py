@@ -1558,8 +1558,20 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                                       ("_ctas64", {"engine": oc.COPY_BULK, "max_ctas": 64}),
                                       ("_ctas16", {"engine": oc.COPY_BULK, "max_ctas": 16}))),
                 ("pinned_host", oc.TIER_PINNED_HOST, (("", {"engine": oc.COPY_BULK}),
-                                                      ("_ce", {"engine": oc.COPY_CE})))):
+                                                      ("_ce", {"engine": oc.COPY_CE}))),
+                # layer-0 mirror, and the mirror depth that Eq. 3 says removes the stall:
+                # K >= L - (L-1) * C / X with X = one layer over PCIe, C = one layer of compute
+                ("pinned_host_hot1", oc.TIER_PINNED_HOST, (("", {"engine": oc.COPY_BULK}),)),
+                ("pinned_host_hotK", oc.TIER_PINNED_HOST, (("", {"engine": oc.COPY_BULK}),))):
             store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
+            if tier_name.endswith("_hot1"):
+                store.set_hot_layers(1)
+            elif tier_name.endswith("_hotK"):
+                X = N * S / 51.4e9 * 1e3                      # ms per layer over PCIe (SM path)
+                C = base / L
+                K = max(1, min(L, int(np.ceil(L - (L - 1) * C / X))))
+                store.set_hot_layers(K)
+                res["hotK_layers"] = K
             (tok,), _ = synth.family_streams(9100 + N, G, 0, [N])
             keys = oc.chunk_keys(tok, G)
             for b0 in range(0, N, 512):
