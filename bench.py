@@ -1569,7 +1569,7 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
             elif tier_name.endswith("_hotK"):
                 X = N * S / 51.4e9 * 1e3                      # ms per layer over PCIe (SM path)
                 C = base / L
-                K = max(1, min(L, int(np.ceil(L - (L - 1) * C / X))))
+                K = oc.hot_layers_for(X, C, L)
                 store.set_hot_layers(K)
                 res["hotK_layers"] = K
             (tok,), _ = synth.family_streams(9100 + N, G, 0, [N])

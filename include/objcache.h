@@ -121,6 +121,12 @@ OC_API int oc_store_count(const oc_store* store, uint64_t* n_chunks);
  * hot_layers > L.  put_from_paged into such a store is ENOTSUP. */
 OC_API int oc_store_set_hot_layers(oc_store* store, uint32_t hot_layers);
 
+/* The mirror depth that hides the host link (Eq. 3): with X seconds per layer over the
+ * link and C seconds of compute per layer, the smallest K >= 1 such that mirroring layers < K lets
+ * the free-running pipeline add no TTFT: K = max(1, ceil(L - (L-1) C / X)), clamped to L.  Pure.
+ * EINVAL if X or C is not finite and > 0, or L = 0. */
+OC_API int oc_hot_layers_for(double X_s, double C_s, uint32_t L, uint32_t* K);
+
 /* Slab base device address and size in bytes (for IPC export and tests). */
 OC_API int oc_store_slab(const oc_store* store, uint64_t* base, uint64_t* bytes);
 

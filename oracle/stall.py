@@ -12,6 +12,11 @@ to back), so the device pipeline is
 with added TTFT = end_{L-1} - sum_l C_l and stall_l = start_l - end_{l-1}.
 Both models coincide when X and C are uniform across layers (the paper's
 footnote); otherwise Eq. 3 is an upper bound.
+
+Hot-layer mirror (DESIGN reading c24): with the first K layers already in
+HBM (ready at t = 0) and the others streamed back to back at X per layer,
+ready_l = (l - K + 1) X for l >= K.  The smallest K >= 1 whose free-running
+pipeline adds no TTFT is the mirror depth that hides the host link.
 """
 
 
@@ -76,3 +81,18 @@ def simulate(X, C, prefetch_depth):
         c_start[l] = max(x_end[l], c_end[l - 1] if l > 0 else 0.0)
         c_end[l] = c_start[l] + C[l]
     return c_end[-1]
+
+
+def mirrored_ready(K, X, L):
+    """Ready times with layers < K mirrored (ready at 0) and the rest streamed at X each."""
+    return [0.0 if l < K else (l - K + 1) * X for l in range(L)]
+
+
+def hot_layers_for(X, C, L, eps=1e-12):
+    """Smallest K in [1, L] whose free-running pipeline (uniform X, C) adds no TTFT: brute force
+    over K with the recurrence above."""
+    for K in range(1, L + 1):
+        ttft = free_running(mirrored_ready(K, X, L), [C] * L)[0]
+        if added_ttft(ttft, [C] * L) <= eps * max(1.0, L * C):
+            return K
+    return L

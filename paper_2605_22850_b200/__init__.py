@@ -84,6 +84,7 @@ _SIGS = {
     "oc_store_count": [_vp, c_u64p],
     "oc_store_slab": [_vp, c_u64p, c_u64p],
     "oc_store_set_hot_layers": [_vp, ctypes.c_uint32],
+    "oc_hot_layers_for": [ctypes.c_double, ctypes.c_double, ctypes.c_uint32, c_u32p],
     "oc_put_chunks": [_vp, _vp, _vp, ctypes.c_uint64, c_u64p, c_u64p],
     "oc_match_prefix": [_vp, c_u32p, ctypes.c_uint64, _vp, _vp, ctypes.c_uint64, c_u64p],
     "oc_store_lookup": [_vp, _vp, ctypes.c_uint64, c_u64p, c_u64p],
@@ -247,6 +248,13 @@ def chunk_keys_batch(token_streams, chunk_tokens: int, stream=None, parents=None
     s.synchronize()
     host = out.cpu().numpy()
     return [host[int(k0):int(k0) + n] for k0, n in zip(key_off, nk)]
+
+
+def hot_layers_for(X_s: float, C_s: float, L: int) -> int:
+    """Mirror depth (layers kept in HBM) that lets a host-tier fetch add no TTFT (Eq. 3)."""
+    k = ctypes.c_uint32()
+    _check(_lib.oc_hot_layers_for(float(X_s), float(C_s), int(L), ctypes.byref(k)))
+    return k.value
 
 
 def schedule_bandwidth(policy, s: Sequence[float], c: Sequence[float], cap_Bps: float,

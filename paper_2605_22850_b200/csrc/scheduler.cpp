@@ -81,3 +81,17 @@ extern "C" OC_API int oc_schedule_bandwidth(int policy, const oc_profile* prof, 
     }
     return oc::fail(OC_EINVAL, "schedule_bandwidth: no feasible split (numerical)");
 }
+
+// Mirror depth for a pinned-host store (oc_store_set_hot_layers; DESIGN reading c24).  With the
+// first K layers in HBM (ready at once) and the rest streamed back to back at X seconds per layer,
+// layer l >= K is ready at (l - K + 1) X and the free-running pipeline of Eq. 3 adds no
+// TTFT iff (l - K + 1) X <= l C for every l >= K; the binding case is the last layer, so
+// K = max(1, ceil(L - (L - 1) C / X)), clamped to L.
+extern "C" OC_API int oc_hot_layers_for(double X_s, double C_s, uint32_t L, uint32_t* K) {
+    if (!K) return oc::fail(OC_EINVAL, "hot_layers_for: null out");
+    if (!(X_s > 0) || !(C_s > 0) || !std::isfinite(X_s) || !std::isfinite(C_s) || L == 0)
+        return oc::fail(OC_EINVAL, "hot_layers_for: X, C must be finite and > 0, L >= 1");
+    const double k = std::ceil((double)L - (double)(L - 1) * C_s / X_s - 1e-12);
+    *K = (uint32_t)std::max(1.0, std::min((double)L, k));
+    return OC_OK;
+}

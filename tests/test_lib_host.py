@@ -150,3 +150,17 @@ def test_sha256_padding_boundaries_vs_hashlib():
     data = bytes(range(256)) * 8
     for n in (0, 1, 55, 56, 57, 63, 64, 65, 96, 119, 120, 127, 128, 129, 1000, 2048):
         assert oc.sha256(data[:n]) == hashlib.sha256(data[:n]).digest(), n
+
+
+def test_hot_layers_for_equals_oracle():
+    import random
+    from oracle import stall as ostall
+    rng = random.Random(24)
+    for _ in range(500):
+        L = rng.randint(1, 80)
+        X, C = rng.uniform(0.01, 5.0), rng.uniform(0.01, 5.0)
+        assert oc.hot_layers_for(X, C, L) == ostall.hot_layers_for(X, C, L), (X, C, L)
+    for bad in ((0.0, 1.0, 4), (1.0, -1.0, 4), (1.0, 1.0, 0), (float("inf"), 1.0, 4)):
+        with pytest.raises(oc.ObjcacheError) as e:
+            oc.hot_layers_for(*bad)
+        assert e.value.code == oc.OC_EINVAL

@@ -45,3 +45,23 @@ def test_free_running_stall_accounting():
     assert start == [1.0, 2.0, 3.0, 6.0] and end == [2.0, 3.0, 4.0, 7.0]
     assert st == [1.0, 0.0, 0.0, 2.0]
     assert ttft == 7.0 and stall.added_ttft(ttft, C) == 3.0 == sum(st)
+
+
+def test_hot_layers_for_closed_form_and_invariants():
+    """The brute-force mirror depth equals the closed form K = max(1, ceil(L - (L-1) C / X)) that
+    follows from requiring (l - K + 1) X <= l C for the last layer; K - 1 layers leave a stall."""
+    import math
+    import random
+    rng = random.Random(3)
+    for _ in range(300):
+        L = rng.randint(1, 80)
+        X = rng.uniform(0.01, 5.0)
+        C = rng.uniform(0.01, 5.0)
+        K = stall.hot_layers_for(X, C, L)
+        closed = max(1, min(L, math.ceil(L - (L - 1) * C / X - 1e-12)))
+        assert K == closed, (L, X, C, K, closed)
+        if K > 1:
+            ttft = stall.free_running(stall.mirrored_ready(K - 1, X, L), [C] * L)[0]
+            assert stall.added_ttft(ttft, [C] * L) > 0
+    assert stall.hot_layers_for(1.0, 2.0, 32) == 1          # compute outpaces the link: mirror layer 0 only
+    assert stall.hot_layers_for(2.0, 1.0, 33) == 17         # X = 2C: half the layers (33 - 32/2 = 17)
