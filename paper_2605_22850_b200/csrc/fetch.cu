@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(kThreads, 4) fetch_ldst_kernel(const DevDesc d
         if (g >= g1) break;  // uniform: every thread read the same slot after the last barrier
         const UnitGeo u = unit_geo(d, g);
         if (d.pace_ns) {  // minimal pacer: layer l released at t0 + l * pace
-            const uint64_t rel = t0 + (uint64_t)u.layer * d.pace_ns;
+            // mirrored (hot) layers do not cross the paced link: the schedule starts after them
+            const uint64_t rel = t0 + (uint64_t)(u.layer < d.hot_layers ? 0u : u.layer - d.hot_layers) * d.pace_ns;
             // CTA-uniform decision (also the barrier that orders unit k-1's stores)
             if (__syncthreads_or(threadIdx.x == 0 && globaltimer() < rel)) {  // announce, then idle
                 if (threadIdx.x == 0 && pending) complete_units(d, pending_layer, 1);
@@ -665,12 +666,16 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     auto release_time = [&](uint32_t k) -> uint64_t {
         if (MODE == kWdrr) return t_start + (uint64_t)s_rel[k % 32] * 1000ull;
         const DevDesc& d = desc_of(k);
-        if (d.pace_ns_per_byte > 0.0) {  // strict: the unit's first byte in the layer-major fetch
+        // Mirrored (hot) layers do not cross the paced link: they go at once, and the link's
+        // schedule counts only the layers after them.
+        if (d.pace_ns_per_byte > 0.0) {  // strict: the unit's first byte among the link's bytes
             const UnitGeo u = unit_geo(d, s_unit[k % 32]);
-            const double b = (double)u.layer * d.N * d.S + (double)u.j * d.S + (double)u.q0 * d.row;
+            if (u.layer < d.hot_layers) return t0;
+            const double b = (double)(u.layer - d.hot_layers) * d.N * d.S + (double)u.j * d.S + (double)u.q0 * d.row;
             return t0 + (uint64_t)(b * d.pace_ns_per_byte);
         }
-        return t0 + (uint64_t)fdiv(s_unit[k % 32], d.div_upl) * d.pace_ns;
+        const uint32_t layer = fdiv(s_unit[k % 32], d.div_upl);
+        return t0 + (uint64_t)(layer < d.hot_layers ? 0u : layer - d.hot_layers) * d.pace_ns;
     };
     // Retired units are batched per (request, layer): one record per change.
     uint32_t pend_req = 0, pend_layer = 0, pend_cnt = 0;

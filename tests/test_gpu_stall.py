@@ -129,3 +129,25 @@ def test_pacer_release_schedule(strict):
             d.fetch_layerwise(s, pace_Bps=1e9, pace_strict=True, engine=oc.COPY_LDST)
         assert e.value.code == oc.OC_ENOTSUP
         d.close()
+
+
+@pytest.mark.parametrize("strict", [False, True])
+def test_pacer_skips_mirrored_layers(strict):
+    """A pinned-host store mirroring layers 0-1 in HBM: the mirrored layers do not cross the paced
+    link, so they are ready at once and the link's schedule starts with layer 2."""
+    lay = OLayout(8, 2, 64, 2, 16)
+    L, K, X = lay.num_layers, 2, 0.5e-3
+    with oc.Store(lay, capacity=8, tier=oc.TIER_PINNED_HOST) as st:
+        st.set_hot_layers(K)
+        req, dest, buf, d = _setup(st, lay, 43, 8)
+        s = torch.cuda.Stream()
+        d.fetch_layerwise(s, pace_Bps=8 * chunk_layer_bytes(lay) / X, pace_strict=strict)
+        d.sync_layer(L - 1)
+        t = d.layer_times().astype(np.int64)
+        ready = (t[1:] - t[0]) / 1e9
+        for l in range(L):
+            lo = 0.0 if l < K else (l - K) * X + (7 * X / 8 if strict else 0.0)
+            assert lo - 20e-6 <= ready[l] <= lo + 200e-6, (l, ready[l], lo)
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 43, req, dest))
+        d.close()
