@@ -1745,6 +1745,8 @@ def sched_leg(args, oc, torch, dev, lay_t):
         row, S, chunk = oc.geometry(lay)
         n_max = max(int(ctx * hit) // G for _, ctx, hit, _ in cells)
         store = oc.Store(lay, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
+        store_hot = oc.Store(lay, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
+        store_hot.set_hot_layers(1)                        # the same corpus with layer 0 mirrored in HBM
         (tok,), _ = synth.family_streams(4242, G, 0, [n_max])
         keys = oc.chunk_keys(tok, G)                       # one shared-prefix corpus
         gen = torch.Generator(device=dev).manual_seed(4242)
@@ -1752,6 +1754,7 @@ def sched_leg(args, oc, torch, dev, lay_t):
             b1 = min(n_max, b0 + 128)
             pl = torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
             store.put_chunks(keys[b0:b1], pl)
+            store_hot.put_chunks(keys[b0:b1], pl)
             del pl
         reqs = []
         for label, ctx, hit, c in cells:
@@ -1764,6 +1767,7 @@ def sched_leg(args, oc, torch, dev, lay_t):
                                  synth.block_table(N, need, need), 0)
             d = oc.build_descriptor(store, keys[:N], lay, tgt)
             reqs.append({"cell": label, "N": N, "s": N * S, "c": c, "d": d, "cache": cache,
+                         "d_hot": oc.build_descriptor(store_hot, keys[:N], lay, tgt),
                          "copy": torch.cuda.Stream(device=dev), "cons": torch.cuda.Stream(device=dev)})
 
         batch = oc.Batch([r["d"] for r in reqs])
@@ -1782,12 +1786,14 @@ def sched_leg(args, oc, torch, dev, lay_t):
             if dispatch == "wdrr":
                 batch.fetch(reqs[0]["copy"], wdrr_weights=[float(x) for x in rates], hold_rates=True)
             else:
+                dk = "d_hot" if dispatch == "hot_strict" else "d"
                 for i, r in enumerate(reqs):
-                    r["d"].fetch_layerwise(r["copy"], pace_Bps=0.0 if rates is None else float(rates[i]),
-                                           pace_strict=dispatch == "strict")
+                    r[dk].fetch_layerwise(r["copy"], pace_Bps=0.0 if rates is None else float(rates[i]),
+                                          pace_strict=dispatch in ("strict", "hot_strict"))
+            dk = "d_hot" if dispatch == "hot_strict" else "d"
             for l in range(L):                              # enqueue layer by layer across requests
                 for r in reqs:
-                    r["d"].wait_layer(l, r["cons"])
+                    r[dk].wait_layer(l, r["cons"])
                     with torch.cuda.stream(r["cons"]):
                         torch.cuda._sleep(int(r["c"] * 1e3 * cyc_per_ms))
             for r in reqs:
@@ -1811,12 +1817,17 @@ def sched_leg(args, oc, torch, dev, lay_t):
             model = [s / r + (L - 1) * max(0.0, s / r - c) for s, c, r in zip(s_i, c_i, rates)]
             ttft_w = run(rates, "wdrr")
             ttft_s = run(rates, "strict")
+            ttft_h = run(rates, "hot_strict")
             res["policies"][pol] = {"rates_gbps": [round(r / GB, 2) for r in rates],
                                     "ttft_ms": [round(x, 1) for x in ttft],
                                     "dttft_ms": round(sum(t - b for t, b in zip(ttft, base)), 1),
                                     "wdrr_ttft_ms": [round(x, 1) for x in ttft_w],
                                     "wdrr_dttft_ms": round(sum(t - b for t, b in zip(ttft_w, base)), 1),
                                     "strict_dttft_ms": round(sum(t - b for t, b in zip(ttft_s, base)), 1),
+                                    "hot_strict_dttft_ms": round(sum(t - b for t, b in zip(ttft_h, base)), 1),
+                                    # Eq. 3 with layer 0 local: ready_l = l*X, added = (L-1) max(0, X - C)
+                                    "model_hot_dttft_ms": round(sum((L - 1) * max(0.0, s_ / r_ - c_)
+                                                                    for s_, c_, r_ in zip(s_i, c_i, rates)) * 1e3, 1),
                                     "model_dttft_ms": round(sum(model) * 1e3, 1)}
         res["equal_over_cal"] = round(res["policies"]["equal"]["dttft_ms"] /
                                       max(1e-9, res["policies"]["cal_stall_opt"]["dttft_ms"]), 3)
@@ -1827,13 +1838,16 @@ def sched_leg(args, oc, torch, dev, lay_t):
         res["dispatch"] = ("dttft_ms: one fetch per request, each paced by its own kernel's minimal pacer "
                            "(layer release times); strict_dttft_ms: the same fetches paced byte by byte; "
                            "wdrr_dttft_ms: one batched launch in WDRR claim order, requests held at their "
-                           "rates (Alg. A2 lines 6-7)")
+                           "rates (Alg. A2 lines 6-7); hot_strict_dttft_ms: strict pacing from a store that "
+                           "mirrors layer 0 in HBM (the link carries layers 1..L-1 only)")
         out[wl] = res
         batch.close()
         for r in reqs:
             r["d"].close()
+            r["d_hot"].close()
         del reqs
         store.close()
+        store_hot.close()
         torch.cuda.empty_cache()
     return out
 
