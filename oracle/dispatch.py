@@ -21,7 +21,9 @@ Readings (DESIGN.md):
   c22  hold rates: request i's units are released no earlier than t0 + (bytes of request i
        dispatched before them) / r_i; a dispatched run is released at the max of that and the
        previous run's release, so releases are monotone along the dispatch order.  Release
-       times are whole microseconds, floor(bytes * 1e6 / r_i).
+       times are whole microseconds, floor(bytes * 1e6 / r_i).  With a hot-layer mirror (c24)
+       a request's first free_i packets are read from HBM, not over the paced link: they are
+       not counted in its bytes (and so are released at t0, subject to the monotone max).
 
 The dispatch order is returned as runs (flow, first packet, count); `entries` splits the runs
 into claim entries of at most E packets, the granularity at which copy CTAs take work.
@@ -88,16 +90,17 @@ def entries(rs, E):
     return out
 
 
-def release_us(ents, sizes, rates):
-    """c22: release time (whole us after t0) of every entry, monotone along the order."""
-    sent = [0] * len(sizes)
+def release_us(ents, sizes, rates, free=None):
+    """c22: release time (whole us after t0) of every entry, monotone along the order.  free[f]:
+    leading packets of flow f that do not count toward its rate (they never cross the paced link)."""
     out = []
     prev = 0
     for f, first, cnt in ents:
-        t = int(math.floor(sent[f] * 1e6 / rates[f]))
+        fu = free[f] if free else 0
+        paced_before = sum(sizes[f][fu:first]) if first > fu else 0
+        t = int(math.floor(paced_before * 1e6 / rates[f]))
         prev = max(prev, t)
         out.append(prev)
-        sent[f] += sum(sizes[f][first:first + cnt])
     return out
 
 
@@ -106,7 +109,7 @@ def unit_sizes(n_chunks, L, tiles, tile_bytes):
     return [tile_bytes[u % tiles] for u in range(n_chunks * L * tiles)]
 
 
-def plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=8, rates=None):
+def plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=8, rates=None, free=None):
     """The whole dispatch plan of a batch: claim entries (flow, first unit, count) and, when
     `rates` is given, their release times in us (c22)."""
     sizes = [unit_sizes(n, L, tiles, tile_bytes) for n in n_chunks]
@@ -114,5 +117,5 @@ def plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=8, rates=None):
     if Qe < max(tile_bytes):
         raise ValueError("quantum below the largest packet")
     ents = entries(runs(drr_order(sizes, quanta(weights, Qe))), E)
-    rel = release_us(ents, sizes, rates) if rates is not None else None
+    rel = release_us(ents, sizes, rates, free) if rates is not None else None
     return ents, rel

@@ -65,7 +65,8 @@ class CFetchOpts(ctypes.Structure):
 
 class CWdrrOpts(ctypes.Structure):
     _fields_ = [("weights", ctypes.POINTER(ctypes.c_double)), ("quantum_bytes", ctypes.c_uint64),
-                ("entry_units", ctypes.c_uint32), ("hold_rates", ctypes.c_uint32)]
+                ("entry_units", ctypes.c_uint32), ("hold_rates", ctypes.c_uint32),
+                ("free_units", ctypes.POINTER(ctypes.c_uint64))]
 
 
 class CProfile(ctypes.Structure):
@@ -515,20 +516,26 @@ class Batch:
         self.close()
 
 
-def _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates):
+def _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units=None):
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
     opts = CWdrrOpts(w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(quantum_bytes), int(entry_units),
                      1 if hold_rates else 0)
+    if free_units is not None:
+        fu = np.ascontiguousarray(np.asarray(free_units, dtype=np.uint64))
+        if len(fu) != len(w):
+            raise ValueError("one free-unit count per request")
+        opts.free_units = fu.ctypes.data_as(c_u64p)
+        w = (w, fu)  # keep both arrays alive with the options
     return w, opts
 
 
-def wdrr_plan(n_units, tile_bytes, weights, quantum_bytes=0, entry_units=0, hold_rates=False):
+def wdrr_plan(n_units, tile_bytes, weights, quantum_bytes=0, entry_units=0, hold_rates=False, free_units=None):
     """The WDRR claim order the library builds (host only): arrays (request, first unit, count,
-    release us) of the entries."""
+    release us) of the entries.  free_units[i]: request i's leading units that are not paced."""
     nu = np.ascontiguousarray(np.asarray(n_units, dtype=np.uint64))
     tb = np.ascontiguousarray(np.asarray(tile_bytes, dtype=np.uint32))
-    w, opts = _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates)
-    if len(w) != len(nu):
+    keep, opts = _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units)
+    if len(weights) != len(nu):
         raise ValueError("one weight per request")
     n = ctypes.c_uint64()
     args = (nu.ctypes.data_as(c_u64p), len(nu), tb.ctypes.data_as(c_u32p), len(tb), ctypes.byref(opts))

@@ -15,7 +15,9 @@
 // cover the largest unit (the textbook condition that makes every visit send).  With hold_rates
 // (reading c22) entry e of request i is released no earlier than t0 + (bytes of request i in
 // earlier entries) / r_i -- in whole microseconds, floor(bytes * 1e6 / r_i) -- and never before
-// the previous entry, so releases are monotone along the claim order.
+// the previous entry, so releases are monotone along the claim order.  Units a request reads from
+// HBM (free_units[i] leading units: the layers a pinned-host store mirrors, reading c24) never
+// cross the paced link, so they neither wait nor count toward the request's bytes.
 #include <cmath>
 
 #include "oc_internal.h"
@@ -68,7 +70,9 @@ int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, u
             const uint64_t c = std::min<uint64_t>(E, cnt - k);
             uint64_t rel = 0;
             if (w.hold_rates) {
-                const uint64_t b = bytes_upto(first + k);  // request i's bytes before this entry
+                // request i's link bytes before this entry: its bytes so far minus its free units'
+                const uint64_t fu = w.free_units ? w.free_units[i] : 0;
+                const uint64_t b = first + k <= fu ? 0 : bytes_upto(first + k) - bytes_upto(fu);
                 const double t = std::floor((double)b * 1e6 / w.weights[i]);
                 if (!(t < 4294967295.0)) return fail(OC_ERANGE, "wdrr: release time beyond 2^32 us");
                 rel = std::max(prev_rel, (uint64_t)t);

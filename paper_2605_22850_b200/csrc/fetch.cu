@@ -1570,8 +1570,16 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         std::vector<uint32_t> tile_bytes(d0.tiles);
         for (uint32_t t = 0; t < d0.tiles; t++)
             tile_bytes[t] = (uint32_t)(std::min(d0.rows_per_unit, 2 * d0.G - t * d0.rows_per_unit) * d0.row);
+        // layers a member reads from the store's HBM mirror are not paced (reading c24)
+        std::vector<uint64_t> free_units(b->n);
+        oc_wdrr_opts wo = *wdrr;
+        if (!wo.free_units) {
+            for (uint32_t i = 0; i < b->n; i++)
+                free_units[i] = (uint64_t)b->descs[i]->dd.units_per_layer * b->descs[i]->dd.hot_layers;
+            wo.free_units = free_units.data();
+        }
         std::vector<WdrrEntry> ents;
-        int rc = wdrr_plan(n_units.data(), b->n, tile_bytes.data(), d0.tiles, *wdrr, &ents);
+        int rc = wdrr_plan(n_units.data(), b->n, tile_bytes.data(), d0.tiles, wo, &ents);
         if (rc) return rc;
         rc = ensure_ent_capacity(b, 16 + ents.size() * sizeof(WdrrEntry));
         if (rc) return rc;

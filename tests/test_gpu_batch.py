@@ -307,3 +307,38 @@ def test_wdrr_single_member_batch():
         check(lay, items)
     b.close()
     st.close()
+
+
+def test_wdrr_hold_rates_skip_mirrored_layers():
+    """hold_rates on a pinned-host store that mirrors its chunks' first K layers in HBM (reading
+    c24): the mirrored layers never cross the paced link, so they land at once and the request's
+    pace covers only the other L-K layers -- the last layer lands at about (L-K)/L * W / r_i, not
+    W / r_i.  Bytes equal the oracle's."""
+    lay, K, n = OLayout(8, 2, 64, 2, 16), 2, 64
+    rates = [200e6, 400e6]
+    st = oc.Store(lay, capacity=2 * n + 2, tier=oc.TIER_PINNED_HOST)
+    st.set_hot_layers(K)
+    items = []
+    for i, seed in enumerate((71, 72)):
+        req = requests_family(lay, seed, 0, [n])[0]
+        st.put_chunks(oc.chunk_keys(req.tokens, 16), payload_stack(lay, seed, req.payload_ids))
+        dest = make_dest(lay, n, "nhd", Bs=16, first_token=3 * i, seed=seed)
+        buf = sentinel_buffer(dest.size)
+        desc = oc.build_descriptor(st, st.match_prefix(req.tokens), lay, lib_target(oc, dest, buf.data_ptr()))
+        items.append({"seed": seed, "req": req, "dest": dest, "buf": buf, "desc": desc})
+    W = n * lay.num_layers * 2 * 16 * 256                       # one request's bytes
+    b = oc.Batch([it["desc"] for it in items])
+    s = torch.cuda.Stream()
+    # Q = one request's mirrored bytes: both requests' mirrored units come first in the order
+    # (releases are monotone along it, so a mirrored unit queued behind a paced one would wait)
+    b.fetch(s, wdrr_weights=rates, hold_rates=True, quantum_bytes=K * n * 2 * 16 * 256)
+    s.synchronize()
+    check(lay, items)
+    for it, r in zip(items, rates):
+        t = it["desc"].layer_times().astype(np.int64)
+        assert (t[K - 1] - t[0]) / 1e6 < 0.5                     # mirrored layers: no pacing
+        want = (lay.num_layers - K) / lay.num_layers * W / r * 1e3
+        got = (t[-1] - t[0]) / 1e6
+        assert abs(got - want) < 0.08 * want + 0.3, (got, want)
+    b.close()
+    st.close()

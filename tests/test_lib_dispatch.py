@@ -10,9 +10,9 @@ import paper_2605_22850_b200 as oc
 from oracle import dispatch as dp
 
 
-def lib_plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=0, hold=False):
+def lib_plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=0, hold=False, free=None):
     req, first, cnt, rel = oc.wdrr_plan([n * L * tiles for n in n_chunks], tile_bytes, weights,
-                                        quantum_bytes=Q, entry_units=E, hold_rates=hold)
+                                        quantum_bytes=Q, entry_units=E, hold_rates=hold, free_units=free)
     return list(zip(req.tolist(), first.tolist(), cnt.tolist())), rel.tolist()
 
 
@@ -30,9 +30,11 @@ def test_random_batches_match_oracle():
         Q = rng.choice([0, max(tile_bytes), 3 * max(tile_bytes) + 5])
         E = rng.choice([0, 1, 3, 8])
         hold = rng.random() < 0.5
-        got, rel = lib_plan(n_chunks, L, tiles, tile_bytes, weights, Q, E, hold)
+        # mirrored leading layers (reading c24): whole layers of units, sometimes none
+        free = [rng.randint(0, L) * n * tiles for n in n_chunks] if rng.random() < 0.5 else None
+        got, rel = lib_plan(n_chunks, L, tiles, tile_bytes, weights, Q, E, hold, free)
         want, wrel = dp.plan(n_chunks, L, tiles, tile_bytes, weights, Q=Q, E=E or 8,
-                             rates=weights if hold else None)
+                             rates=weights if hold else None, free=free)
         assert got == want, case
         assert rel == (wrel if hold else [0] * len(want)), case
 

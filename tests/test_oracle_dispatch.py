@@ -158,6 +158,20 @@ def test_release_times_monotone_max_rule():
         ents = dp.entries(dp.runs(dp.drr_order(sizes, q)), 4)
         rel = dp.release_us(ents, sizes, [x * 1e6 for x in w])
         assert rel == sorted(rel)
+        # no free packets is the plain rule; every packet free releases everything at t0
+        assert dp.release_us(ents, sizes, [x * 1e6 for x in w], [0] * len(sizes)) == rel
+        assert dp.release_us(ents, sizes, [x * 1e6 for x in w], [len(s) for s in sizes]) == [0] * len(ents)
+
+
+def test_release_times_free_packets():
+    """Reading c24 applied to c22: flow 0's first packet is mirrored (free), so its second entry
+    has 0 paced bytes before it -> released 0 instead of 4; flow 1 unchanged (8 bytes at 4/us = 2).
+    A free prefix that ends inside an entry counts only the paced bytes before that entry."""
+    sizes = [[4, 4], [4, 4, 4]]
+    ents = [(0, 0, 1), (1, 0, 2), (0, 1, 1), (1, 2, 1)]
+    assert dp.release_us(ents, sizes, [1e6, 4e6], [1, 0]) == [0, 0, 0, 2]
+    assert dp.release_us(ents, sizes, [1e6, 4e6], [0, 1]) == [0, 0, 4, 4]      # (1,2,1): 4 B / 4 = 1 -> max 4
+    assert dp.release_us([(0, 0, 3), (0, 3, 3)], [[2] * 6], [1e6], [2]) == [0, 2]
 
 
 def test_plan_layer_major_units():
