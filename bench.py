@@ -1771,6 +1771,7 @@ def sched_leg(args, oc, torch, dev, lay_t):
                          "copy": torch.cuda.Stream(device=dev), "cons": torch.cuda.Stream(device=dev)})
 
         batch = oc.Batch([r["d"] for r in reqs])
+        batch_hot = oc.Batch([r["d_hot"] for r in reqs])
 
         def run(rates, dispatch="independent"):
             """All requests concurrently; rates None = unpaced.  dispatch "independent": one fetch per
@@ -1783,14 +1784,15 @@ def sched_leg(args, oc, torch, dev, lay_t):
             for r in reqs:
                 r["copy"].wait_event(start)
                 r["cons"].wait_event(start)
-            if dispatch == "wdrr":
-                batch.fetch(reqs[0]["copy"], wdrr_weights=[float(x) for x in rates], hold_rates=True)
+            if dispatch in ("wdrr", "hot_wdrr"):
+                (batch_hot if dispatch == "hot_wdrr" else batch).fetch(
+                    reqs[0]["copy"], wdrr_weights=[float(x) for x in rates], hold_rates=True)
             else:
                 dk = "d_hot" if dispatch == "hot_strict" else "d"
                 for i, r in enumerate(reqs):
                     r[dk].fetch_layerwise(r["copy"], pace_Bps=0.0 if rates is None else float(rates[i]),
                                           pace_strict=dispatch in ("strict", "hot_strict"))
-            dk = "d_hot" if dispatch == "hot_strict" else "d"
+            dk = "d_hot" if dispatch.startswith("hot_") else "d"
             for l in range(L):                              # enqueue layer by layer across requests
                 for r in reqs:
                     r[dk].wait_layer(l, r["cons"])
@@ -1818,6 +1820,7 @@ def sched_leg(args, oc, torch, dev, lay_t):
             ttft_w = run(rates, "wdrr")
             ttft_s = run(rates, "strict")
             ttft_h = run(rates, "hot_strict")
+            ttft_hw = run(rates, "hot_wdrr")
             res["policies"][pol] = {"rates_gbps": [round(r / GB, 2) for r in rates],
                                     "ttft_ms": [round(x, 1) for x in ttft],
                                     "dttft_ms": round(sum(t - b for t, b in zip(ttft, base)), 1),
@@ -1825,6 +1828,7 @@ def sched_leg(args, oc, torch, dev, lay_t):
                                     "wdrr_dttft_ms": round(sum(t - b for t, b in zip(ttft_w, base)), 1),
                                     "strict_dttft_ms": round(sum(t - b for t, b in zip(ttft_s, base)), 1),
                                     "hot_strict_dttft_ms": round(sum(t - b for t, b in zip(ttft_h, base)), 1),
+                                    "hot_wdrr_dttft_ms": round(sum(t - b for t, b in zip(ttft_hw, base)), 1),
                                     # Eq. 3 with layer 0 local: ready_l = l*X, added = (L-1) max(0, X - C)
                                     "model_hot_dttft_ms": round(sum((L - 1) * max(0.0, s_ / r_ - c_)
                                                                     for s_, c_, r_ in zip(s_i, c_i, rates)) * 1e3, 1),
@@ -1839,9 +1843,11 @@ def sched_leg(args, oc, torch, dev, lay_t):
                            "(layer release times); strict_dttft_ms: the same fetches paced byte by byte; "
                            "wdrr_dttft_ms: one batched launch in WDRR claim order, requests held at their "
                            "rates (Alg. A2 lines 6-7); hot_strict_dttft_ms: strict pacing from a store that "
-                           "mirrors layer 0 in HBM (the link carries layers 1..L-1 only)")
+                           "mirrors layer 0 in HBM (the link carries layers 1..L-1 only); hot_wdrr_dttft_ms: "
+                           "the WDRR launch from that store (mirrored units first, unpaced; reading c25)")
         out[wl] = res
         batch.close()
+        batch_hot.close()
         for r in reqs:
             r["d"].close()
             r["d_hot"].close()

@@ -24,6 +24,11 @@ Readings (DESIGN.md):
        times are whole microseconds, floor(bytes * 1e6 / r_i).  With a hot-layer mirror (c24)
        a request's first free_i packets are read from HBM, not over the paced link: they are
        not counted in its bytes (and so are released at t0, subject to the monotone max).
+  c25  mirrored packets are not link traffic, so DRR does not schedule them: with free_i given,
+       every flow's first free_i packets are dispatched first (flow 0's, then flow 1's, ...,
+       split into entries of E), then DRR runs over the remaining packets of every flow.  With
+       hold rates the front entries are all released at t0 -- the mirror's layers land at HBM
+       speed for every request of the batch, not one DRR round at a time.
 
 The dispatch order is returned as runs (flow, first packet, count); `entries` splits the runs
 into claim entries of at most E packets, the granularity at which copy CTAs take work.
@@ -116,6 +121,13 @@ def plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=8, rates=None, free=Non
     Qe = Q if Q else default_quantum(max(tile_bytes))
     if Qe < max(tile_bytes):
         raise ValueError("quantum below the largest packet")
-    ents = entries(runs(drr_order(sizes, quanta(weights, Qe))), E)
+    if not free:
+        ents = entries(runs(drr_order(sizes, quanta(weights, Qe))), E)
+    else:
+        # c25: the free (mirrored) packets first, flow by flow; then DRR over the paced packets
+        fu = [min(f, len(s)) for f, s in zip(free, sizes)]
+        front = [(f, 0, fu[f]) for f in range(len(sizes)) if fu[f] > 0]
+        rest = drr_order([s[k:] for s, k in zip(sizes, fu)], quanta(weights, Qe))
+        ents = entries(front, E) + entries(runs([(f, p + fu[f]) for f, p in rest]), E)
     rel = release_us(ents, sizes, rates, free) if rates is not None else None
     return ents, rel

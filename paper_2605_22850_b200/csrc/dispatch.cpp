@@ -17,7 +17,8 @@
 // earlier entries) / r_i -- in whole microseconds, floor(bytes * 1e6 / r_i) -- and never before
 // the previous entry, so releases are monotone along the claim order.  Units a request reads from
 // HBM (free_units[i] leading units: the layers a pinned-host store mirrors, reading c24) never
-// cross the paced link, so they neither wait nor count toward the request's bytes.
+// cross the paced link, so they neither wait nor count toward the request's bytes; nor does DRR
+// schedule them: they are dispatched first, request by request (reading c25).
 #include <cmath>
 
 #include "oc_internal.h"
@@ -82,6 +83,21 @@ int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, u
         }
         return OC_OK;
     };
+    // reading c25: units a request reads from a store's HBM mirror are not link traffic -- they
+    // go first, request by request, and DRR schedules the rest
+    if (w.free_units) {
+        size_t keep = 0;
+        for (size_t a = 0; a < active.size(); a++) {
+            const uint32_t i = active[a];
+            head[i] = std::min(w.free_units[i], n_units[i]);
+            if (head[i]) {
+                int rc = emit(i, 0, head[i]);
+                if (rc) return rc;
+            }
+            if (head[i] < n_units[i]) active[keep++] = i;
+        }
+        active.resize(keep);
+    }
     uint32_t run_req = 0;
     uint64_t run_first = 0, run_cnt = 0;  // the dispatch run being extended
     while (!active.empty()) {

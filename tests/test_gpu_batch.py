@@ -329,9 +329,9 @@ def test_wdrr_hold_rates_skip_mirrored_layers():
     W = n * lay.num_layers * 2 * 16 * 256                       # one request's bytes
     b = oc.Batch([it["desc"] for it in items])
     s = torch.cuda.Stream()
-    # Q = one request's mirrored bytes: both requests' mirrored units come first in the order
-    # (releases are monotone along it, so a mirrored unit queued behind a paced one would wait)
-    b.fetch(s, wdrr_weights=rates, hold_rates=True, quantum_bytes=K * n * 2 * 16 * 256)
+    # the default Q (256 KiB) is a quarter of one request's mirrored bytes: the mirrored units
+    # still all go first (reading c25), so no mirrored unit waits behind a paced one
+    b.fetch(s, wdrr_weights=rates, hold_rates=True)
     s.synchronize()
     check(lay, items)
     for it, r in zip(items, rates):

@@ -163,6 +163,18 @@ def test_release_times_monotone_max_rule():
         assert dp.release_us(ents, sizes, [x * 1e6 for x in w], [len(s) for s in sizes]) == [0] * len(ents)
 
 
+def test_plan_free_packets_first():
+    """c25 by hand: flows of 4 equal 4-byte packets, Q = 4, flow 0's first 2 packets free.
+    Front: (0, 0, 2).  DRR over the rest -- round 1: flow 0 packet 2, flow 1 packet 0; round 2:
+    flow 0 packet 3, flow 1 packet 1; rounds 3-4: flow 1 alone, packets 2 and 3 (one run with 1)."""
+    ents, rel = dp.plan([2, 2], L=2, tiles=1, tile_bytes=[4], weights=[1.0, 1.0], Q=4, E=8,
+                        rates=[1e6, 1e6], free=[2, 0])
+    assert ents == [(0, 0, 2), (0, 2, 1), (1, 0, 1), (0, 3, 1), (1, 1, 3)]
+    assert rel == [0, 0, 0, 4, 4]
+    # no free packets: the plain DRR plan
+    assert dp.plan([2, 2], 2, 1, [4], [1.0, 1.0], Q=4, free=[0, 0])[0] == dp.plan([2, 2], 2, 1, [4], [1.0, 1.0], Q=4)[0]
+
+
 def test_release_times_free_packets():
     """Reading c24 applied to c22: flow 0's first packet is mirrored (free), so its second entry
     has 0 paced bytes before it -> released 0 instead of 4; flow 1 unchanged (8 bytes at 4/us = 2).
