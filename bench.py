@@ -148,6 +148,28 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+def in_harness_copy(torch, dev, stream, nbytes):
+    """Read+write GB/s of a plain device-to-device copy_ of nbytes (the MEASURED_PEAKS method, run
+    in this process under this run's clocks)."""
+    src = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    dst = torch.empty_like(src)
+    ts = []
+    with torch.cuda.stream(stream):
+        src.fill_(1)
+        for i in range(23):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dst.copy_(src)
+            b.record(stream)
+            if i >= 3:
+                ts.append((a, b))
+    stream.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ts)
+    del src, dst
+    torch.cuda.empty_cache()
+    return 2 * nbytes / (ms / 1e3) / 1e9
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -342,6 +364,7 @@ def main_ours(args):
     peak, peak_src = peaks()
     mean_launch_ms = statistics.mean(launch_ms)
     achieved = bytes_per_step / (mean_launch_ms / 1e3) / 1e9
+    harness_copy = in_harness_copy(torch, dev, copy_s, bytes_per_step // 2) if not args.profile else None
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -350,6 +373,12 @@ def main_ours(args):
         "config": bench_config(args, lay_t, ws),
         "kv_delivered_GBps": value / 2,
         "frac_of_spec_8TBps": value / 8000.0,
+        # SURVEY 8(d) second denominator: a device-to-device torch copy_ of the step's size, timed here
+        "in_harness_copy": None if harness_copy is None else {
+            "GBps": round(harness_copy, 1), "kernel_frac": round(achieved / harness_copy, 4),
+            "value_frac": round(value / ws / harness_copy, 4),
+            "method": "torch copy_ of %d MiB device to device on the copy stream, read + write counted, "
+                      "median of 20 after 3 warm-ups" % (bytes_per_step // 2 >> 20)},
         "launch_us": {q: float(np.percentile(launch_ms, p)) * 1e3 for q, p in (("p10", 10), ("p50", 50), ("p90", 90))},
         "gpu_launches": args.steps * (1 if mode == oc.FETCH_PERSISTENT else L),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
