@@ -440,6 +440,8 @@ def main_ours(args):
         out["stall"] = stall_leg(args, oc, torch, dev, lay_t, fopts)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_leg()
+        if "config3" in out:   # the oracle's GB/s next to the GPU's for config 3 too
+            out["config3"]["oracle_cpu"] = cpu_config3_leg()
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -1905,6 +1907,21 @@ def cpu_baseline_leg():
     return {"value": tot_b / tot_s / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{len(layers)} of 32 layers of the 4K request (N=256, G=16, Bs=16), "
                       f"{tot_s:.1f} s, single-threaded Python+numpy (host has {ncpu} cpus, affinity {c})"}
+
+
+def cpu_config3_leg():
+    """The oracle on one layer of the config-3 request (N = 4096 chunks, 256 MiB per layer): the
+    per-layer work depends on N and S only, so the layout is truncated to one layer to keep the
+    host copy of the store at 256 MiB instead of 8 GiB."""
+    import synth
+    from oracle.geometry import Layout
+    L8 = synth.LLAMA3_8B.as_tuple()
+    wl = OracleWorkload(3, 4096, Layout(1, *L8[1:]))
+    b, t = wl.run([0])
+    c, ncpu = cores_used()
+    return {"value": round(b / t / 1e9, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"1 layer of the 64K request (N=4096, 512 MiB read+write), {t:.1f} s, single-threaded "
+                      f"Python+numpy (host has {ncpu} cpus, affinity {c})"}
 
 
 def main():
