@@ -403,10 +403,25 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
     const uint32_t* pos_dev = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     oc::Upload up;
-    rc = oc::upload_block(s->device, g, dst, v, &pos, "put_from_paged", &mem, &cls, &dd, &pos_dev, &up, true, st);
+    // The block goes up on the library's upload stream, not on `st`: a small H2D copy queued
+    // between two back-to-back offload kernels would idle the GPU for its DMA latency.  `st` only
+    // waits on the copy's event, which has long fired when the previous kernel ends.
+    rc = oc::upload_block(s->device, g, dst, v, &pos, "put_from_paged", &mem, &cls, &dd, &pos_dev, &up, false, st);
     if (rc) {
         rollback();
         return rc;
+    }
+    {
+        cudaError_t e = cudaStreamWaitEvent(st, up.ev, 0);
+        cudaEventDestroy(up.ev);
+        up.ev = nullptr;
+        if (e != cudaSuccess) {
+            cudaStreamSynchronize(oc::upload_stream(s->device));
+            oc::dev_pool_free(s->device, mem, cls);
+            oc::dev_pool_free(-1, up.stage, up.stage_cls);
+            rollback();
+            return oc::cuda_fail(e, "put_from_paged: ordering after the upload");
+        }
     }
     oc::plan_into(dd, g, dst.size(), 0);
     rc = oc::launch_offload(dd, pos_dev, s->device, st, s->tier == OC_TIER_PINNED_HOST);
