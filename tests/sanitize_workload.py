@@ -135,7 +135,7 @@ if "4" in SECTIONS:
         d.close()
 # a pinned-host store mirroring layer 0 in HBM: split launches and CE mirror copies
 if "4" in SECTIONS:
-    fam = requests_family(lay, 9, 3, [2])
+    fam = requests_family(lay, 9, 3, [2, 1])
     with oc.Store(lay, capacity=8, tier=oc.TIER_PINNED_HOST) as st:
         st.set_hot_layers(1)
         kf = oc.chunk_keys(fam[0].tokens, 16)
@@ -153,6 +153,24 @@ if "4" in SECTIONS:
             assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 9, fam[0], dest)), engine
             ok += 1
         d.close()
+        # WDRR with held rates over two members of the mirrored store: mirrored units first (c25)
+        kg = oc.chunk_keys(fam[1].tokens, 16)
+        st.put_chunks(kg, payload_stack(lay, 9, fam[1].payload_ids))
+        items = []
+        for i, r in enumerate(fam):
+            dst = make_dest(lay, r.n_chunks, "hnd" if i else "nhd", Bs=8, seed=5 + i)
+            bb = sentinel_buffer(dst.size)
+            items.append((r, dst, bb, oc.build_descriptor(st, st.match_prefix(r.tokens), lay,
+                                                          lib_target(oc, dst, bb.data_ptr()))))
+        b = oc.Batch([it[3] for it in items])
+        b.fetch(s, wdrr_weights=[2e8, 6e8], hold_rates=True, entry_units=2)
+        s.synchronize()
+        for r, dst, bb, dd in items:
+            assert np.array_equal(bb.cpu().numpy(), oracle_result(lay, 9, r, dst))
+            ok += 1
+        b.close()
+        for it in items:
+            it[3].close()
 # chain keys of a ragged batch on the GPU
 if "5" in SECTIONS:
     from oracle import keys as okeys
