@@ -246,9 +246,12 @@ typedef enum {
                                 directly (no stage, no scatter kernel).
                                 ~55 GB/s of PCIe reads vs ~51 for SM zero-copy; the saturated
                                 PCIe queue adds ~5 us to each launch of other streams.       */
-    OC_COPY_AUTO = 3,        /* BULK when destination rows are contiguous (NHD, flat
-                                target) or strict pacing is asked for, else LDST
-                                (head-split targets such as HND); the default   */
+    OC_COPY_AUTO = 3,        /* CE for an unpaced PERSISTENT fetch into a FLAT target
+                                from pinned-host chunks in at most 4 slot runs;
+                                else BULK when destination rows are contiguous
+                                (NHD, flat target) or strict pacing is asked
+                                for, else LDST (head-split targets such as
+                                HND); the default                               */
 } oc_copy_engine;
 
 typedef struct {

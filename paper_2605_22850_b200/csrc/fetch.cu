@@ -1364,8 +1364,16 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     // target (HND) every row becomes n_kv stores of d*p bytes, which holds the TMA engine to
     // 4.2 TB/s at 4K while 16-byte LD/ST streams at 6.3 (profiles/r01_hnd_probe.txt).  Strict
     // pacing exists only in the TMA engine.
-    if (o.engine == OC_COPY_AUTO)
-        o.engine = (d->dd.nhd || (o.pace_Bps > 0 && o.pace_strict)) ? OC_COPY_BULK : OC_COPY_LDST;
+    if (o.engine == OC_COPY_AUTO) {
+        // A FLAT target fed from pinned host memory in a few slot runs: the copy engine writes
+        // B_l directly (no stage, no SMs): 53.3 GB/s of PCIe reads at 1 run, 51.5 at 4, against
+        // 51.4 for SM zero-copy reads (profiles/r01_flat_auto.txt); with many runs per layer its
+        // per-transfer cost wins (45.6 GB/s at 16 runs; profiles/r01_ce2d.txt).
+        const bool ce = d->flat_base && d->host_chunks == d->N && !d->run_first.empty() &&
+                        d->run_first.size() <= 4 && o.pace_Bps == 0 && o.mode == OC_FETCH_PERSISTENT;
+        o.engine = ce ? OC_COPY_CE
+                      : (d->dd.nhd || (o.pace_Bps > 0 && o.pace_strict)) ? OC_COPY_BULK : OC_COPY_LDST;
+    }
     if (o.engine == OC_COPY_CE) return launch_fetch_ce(d, o, s);
     if (o.engine != OC_COPY_LDST && o.engine != OC_COPY_BULK) return fail(OC_EINVAL, "fetch_layerwise: unknown engine");
     d->dd.staged = 0;
