@@ -29,7 +29,8 @@ def _newer(target, deps):
 
 def build(force=False, verbose=False):
     os.makedirs(OBJ_DIR, exist_ok=True)
-    headers = [os.path.join(CSRC, "oc_internal.h"), os.path.join(ROOT, "include", "objcache.h")]
+    headers = [os.path.join(CSRC, "oc_internal.h"), os.path.join(CSRC, "fetch_kernels.cuh"),
+               os.path.join(ROOT, "include", "objcache.h")]
     objs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)

@@ -5,7 +5,7 @@
 // dispatches layer payloads with weighted deficit round robin.  On B200 the dispatcher is the
 // claim order of one batched copy kernel: this file turns the requests' unit streams into that
 // order, as a table of claim entries (request, first unit, count <= E) that copy CTAs take in
-// sequence (fetch.cu, fetch_bulk_kernel<kWdrr>).
+// sequence (fetch_kernels.cuh, fetch_bulk_kernel<kWdrr>).
 //
 // Deficit round robin (Shreedhar & Varghese): a round visits the backlogged requests in index
 // order; a visit adds q_i to D_i and sends units from the request's head while the head unit's
