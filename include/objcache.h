@@ -328,10 +328,12 @@ typedef struct {
                                 largest unit); EINVAL if below the largest unit               */
     uint32_t entry_units;    /* E: units per claim entry; 0 = 8                               */
     uint32_t hold_rates;     /* 1: pace request i at weights[i] bytes/s                       */
-    const uint64_t* free_units; /* [n] or NULL: leading units of request i that do not count
-                                toward its held rate (layers mirrored in HBM never cross the
-                                paced link); oc_fetch_batch_wdrr fills it from the members'
-                                hot layers when NULL                                          */
+    const uint64_t* free_units; /* [n] or NULL: leading units of request i read from an HBM
+                                mirror (they never cross the paced link): they are claimed
+                                first, request by request, released at t0, and DRR and the
+                                held rates cover only the rest (reading c25);
+                                oc_fetch_batch_wdrr fills it from the members' hot layers
+                                when NULL                                                     */
 } oc_wdrr_opts;
 
 /* Fetch a batch in WDRR order (instead of layer-major across requests).  Same contract as
