@@ -494,16 +494,17 @@ class Batch:
         _check(_lib.oc_batch_set_order(self._h, int(order)))
 
     def fetch(self, stream=None, max_ctas=0, unit_bytes=0, wdrr_weights=None, quantum_bytes=0, entry_units=0,
-              hold_rates=False, engine=COPY_AUTO):
+              hold_rates=False, engine=COPY_AUTO, free_units=None):
         """One launch for the whole batch.  With `wdrr_weights` (one per member) the claim order is
         weighted deficit round robin (oc_fetch_batch_wdrr, Alg. A2 line 7); `hold_rates` paces
-        member i at wdrr_weights[i] bytes/s (Alg. A2 line 6)."""
+        member i at wdrr_weights[i] bytes/s (Alg. A2 line 6); `free_units` (default: the members'
+        mirrored layers) are claimed first and unpaced (reading c25)."""
         o = CFetchOpts(FETCH_PERSISTENT, int(engine), int(max_ctas), int(unit_bytes), 0.0)
         if wdrr_weights is None:
             _check(_lib.oc_fetch_batch(self._h, ctypes.byref(o), _stream(stream)))
             return
-        w, opts = _wdrr_opts(wdrr_weights, quantum_bytes, entry_units, hold_rates)
-        if len(w) != len(self.descs):
+        keep, opts = _wdrr_opts(wdrr_weights, quantum_bytes, entry_units, hold_rates, free_units)
+        if len(wdrr_weights) != len(self.descs):
             raise ValueError("one WDRR weight per batch member")
         _check(_lib.oc_fetch_batch_wdrr(self._h, ctypes.byref(o), ctypes.byref(opts), _stream(stream)))
 

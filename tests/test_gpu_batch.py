@@ -331,7 +331,16 @@ def test_wdrr_hold_rates_skip_mirrored_layers():
     s = torch.cuda.Stream()
     # the default Q (256 KiB) is a quarter of one request's mirrored bytes: the mirrored units
     # still all go first (reading c25), so no mirrored unit waits behind a paced one
-    b.fetch(s, wdrr_weights=rates, hold_rates=True)
+    b.fetch(s, wdrr_weights=rates, hold_rates=True, free_units=[0, 0])   # mirrors not declared
+    s.synchronize()
+    check(lay, items)
+    t = items[0]["desc"].layer_times().astype(np.int64)
+    want0 = (K - 1) / lay.num_layers * W / rates[0] * 1e3                # layer K-1 paced like the rest
+    assert (t[K - 1] - t[0]) / 1e6 > 0.6 * want0, ((t[K - 1] - t[0]) / 1e6, want0)
+    for it in items:
+        it["buf"].fill_(0xA5)
+    torch.cuda.synchronize()
+    b.fetch(s, wdrr_weights=rates, hold_rates=True)                    # default: the members' mirrors
     s.synchronize()
     check(lay, items)
     for it, r in zip(items, rates):
