@@ -71,3 +71,16 @@ def test_config4_scale():
     assert np.all(np.diff(rel.astype(np.int64)) >= 0)
     # round 1: the light requests send Q = 256 KiB (8 units), the heavy ones 1792/1024 x that
     assert cnt[0] == 8 and req[0] == 0
+
+
+def test_free_units_edge_cases():
+    """free_units beyond a request's units (clamped: all of it is free), zero for some members, and
+    for an empty member: planner = oracle (reading c25)."""
+    n_chunks, L, tiles, tb = [3, 0, 2], 2, 2, [32768, 16384]
+    w = [1e9, 2e9, 3e9]
+    for free in ([100, 0, 1], [0, 5, 0], [12, 0, 8], [3, 0, 0]):
+        got, rel = lib_plan(n_chunks, L, tiles, tb, w, E=3, hold=True, free=free)
+        want, wrel = dp.plan(n_chunks, L, tiles, tb, w, E=3, rates=w, free=free)
+        assert got == want and rel == wrel, free
+    got, rel = lib_plan(n_chunks, L, tiles, tb, w, hold=True, free=[100, 0, 100])
+    assert all(r == 0 for r in rel) and [e[0] for e in got] == [0] * 2 + [2] * 1   # every unit free
