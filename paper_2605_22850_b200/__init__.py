@@ -518,16 +518,18 @@ class Batch:
 
 
 def _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units=None):
+    """(arrays the options point into -- keep them alive across the call, options)."""
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
     opts = CWdrrOpts(w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(quantum_bytes), int(entry_units),
                      1 if hold_rates else 0)
+    keep = [w]
     if free_units is not None:
         fu = np.ascontiguousarray(np.asarray(free_units, dtype=np.uint64))
         if len(fu) != len(w):
             raise ValueError("one free-unit count per request")
         opts.free_units = fu.ctypes.data_as(c_u64p)
-        w = (w, fu)  # keep both arrays alive with the options
-    return w, opts
+        keep.append(fu)
+    return keep, opts
 
 
 def wdrr_plan(n_units, tile_bytes, weights, quantum_bytes=0, entry_units=0, hold_rates=False, free_units=None):
