@@ -156,7 +156,8 @@ OC_API int oc_store_lookup(oc_store* store, const oc_key* keys, uint64_t n, uint
 
 /* Make `peer`'s chunks resolvable through `store` (peer keys are looked up
  * after local ones).  `peer` must outlive `store`'s descriptors, and its slab
- * must be readable from `store`'s GPU (same GPU, peer access, or host tier). */
+ * must be readable from `store`'s GPU (same GPU, peer access, or host tier).
+ * OC_EINVAL if the attachment would close a cycle (peer already reaches store). */
 OC_API int oc_store_attach_peer(oc_store* store, oc_store* peer);
 
 /* Multi-process sharing of an HBM store (config 5, NVLink P2P):

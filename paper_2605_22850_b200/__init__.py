@@ -549,6 +549,8 @@ def wdrr_plan(n_units, tile_bytes, weights, quantum_bytes=0, entry_units=0, hold
     _check(_lib.oc_wdrr_plan(*args, *[o.ctypes.data_as(c_u32p) for o in out], n.value, ctypes.byref(n)))
     return tuple(out)
 
+
+def fetch_batch(descs: Sequence[Descriptor], stream=None, **opts) -> "Batch":
     """Create a batch of descriptors and fetch it once; returns the (reusable) batch."""
     b = Batch(descs)
     b.fetch(stream, **opts)

@@ -299,6 +299,7 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
 
     // Resolve every key (first missing key reported by index, in prefix order).
     std::vector<uint64_t> src(n), hot(n);
+    std::vector<uint32_t> hot_pitch_layers(n);  // layers per mirror slot of the chunk's own store
     uint64_t host_chunks = 0;
     uint32_t hot_layers = ~0u;  // leading layers mirrored in HBM for EVERY chunk
     for (uint64_t i = 0; i < n; i++) {
@@ -306,6 +307,7 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
         uint32_t hl = 0;
         const bool found = oc::store_resolve(s, keys[i], &src[i], &tier, &hot[i], &hl);
         host_chunks += tier == OC_TIER_PINNED_HOST;
+        hot_pitch_layers[i] = hl;
         hot_layers = std::min(hot_layers, found ? hl : 0u);
         if (!found) {
             if (bad_index) *bad_index = i;
@@ -326,22 +328,31 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     d->nb = v.bt.size();
     d->host_chunks = host_chunks;
     if (t->kind == OC_TARGET_FLAT) d->flat_base = t->flat_base;
+    if (hot_layers == ~0u) hot_layers = 0;
     if (host_chunks == n) {  // CE engine: maximal runs of chunks in consecutive slots
+        // With mirrors, a run also needs consecutive mirror slots of ONE pitch: stores (own and
+        // attached peers) may mirror different numbers of layers, and each lays its mirror out with
+        // its own pitch hot_layers*S -- a run crossing stores would read the wrong mirror bytes.
         for (uint64_t i = 0; i < n; i++) {
-            if (i > 0 && src[i] == src[i - 1] + g.chunk) {
+            const uint64_t pitch = (uint64_t)hot_pitch_layers[i] * g.S;
+            const bool cont = i > 0 && src[i] == src[i - 1] + g.chunk &&
+                              (!hot_layers || (hot_pitch_layers[i] == hot_pitch_layers[i - 1] &&
+                                               hot[i] == hot[i - 1] + pitch));
+            if (cont) {
                 d->run_len.back()++;
             } else {
                 d->run_first.push_back(i);
                 d->run_len.push_back(1);
                 d->run_src.push_back(src[i]);
+                if (hot_layers) {
+                    d->run_hot.push_back(hot[i]);
+                    d->run_hot_pitch.push_back(pitch);
+                }
             }
         }
     }
     oc::DeviceGuard dg(d->device);
-    if (hot_layers == ~0u) hot_layers = 0;
     d->hot_layers = hot_layers;
-    if (hot_layers)  // runs of consecutive slots have consecutive mirrors
-        for (uint64_t r = 0; r < d->run_first.size(); r++) d->run_hot.push_back(hot[d->run_first[r]]);
     rc = oc::upload_block(d->device, g, src, v, nullptr, "build_descriptor", &d->dev_mem, &d->dev_mem_class, &d->dd,
                           nullptr, &d->up, false, nullptr, hot_layers ? &hot : nullptr, hot_layers);
     if (rc) return rc;
@@ -394,6 +405,9 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
     auto rollback = [&]() {  // the reserved slots never received their bytes: forget the keys
         std::unique_lock<std::shared_mutex> lk(s->mu);
         for (uint32_t p : pos) s->index.erase(keys[p]);
+        // give the slots back when nobody reserved after them (they are the slab's last ones)
+        const uint64_t first = (dst.front() - (uint64_t)(uintptr_t)s->slab) / g.chunk;
+        if (s->count == first + dst.size()) s->count = first;
         if (n_new) *n_new = 0;
     };
     oc::DeviceGuard dg(s->device);
@@ -443,6 +457,27 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
     {
         std::lock_guard<std::mutex> lk(oc::g_jobs_mu);
         oc::g_jobs.push_back(job);
+    }
+    {  // the store's record of offloads in flight (put_chunks' byte compare waits on them)
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess && cudaEventRecord(ev, st) == cudaSuccess) {
+            std::unique_lock<std::shared_mutex> lk(s->mu);
+            auto& v = s->offload_evs;
+            for (size_t i = 0; i < v.size();) {  // drop the finished ones
+                if (cudaEventQuery(v[i]) == cudaSuccess) {
+                    cudaEventDestroy(v[i]);
+                    v[i] = v.back();
+                    v.pop_back();
+                } else {
+                    i++;
+                }
+            }
+            v.push_back(ev);
+        } else {
+            if (ev) cudaEventDestroy(ev);
+            cudaStreamSynchronize(st);  // no event: make the slots final before returning
+        }
+        cudaGetLastError();
     }
     return status;
 }

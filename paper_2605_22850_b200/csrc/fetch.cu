@@ -21,6 +21,7 @@
 // round trip, no kernel), so layer l's compute starts while layer l+1 is still in flight.  In
 // PER_LAYER mode each layer is its own launch followed by a CUDA event.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -98,15 +99,29 @@ void shallow_ring(BulkPlan* p) {
     }
 }
 
+// cudaFuncSetAttribute applies to the current device only, so the "already raised" cache is per
+// device (a process may hold stores and fetches on several GPUs); racing threads at worst both set it.
+constexpr int kMaxDevices = 64;
+
+cudaError_t raise_smem_attr(const void* fn, std::atomic<uint32_t>* per_dev, uint32_t smem) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::atomic<uint32_t>* slot = dev >= 0 && dev < kMaxDevices ? &per_dev[dev] : nullptr;
+    if (slot && smem <= slot->load(std::memory_order_acquire)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<uint32_t>(smem, 48 * 1024));
+    if (e == cudaSuccess && slot) {
+        uint32_t cur = slot->load(std::memory_order_relaxed);
+        while (cur < smem && !slot->compare_exchange_weak(cur, smem, std::memory_order_acq_rel)) {
+        }
+    }
+    return e;
+}
+
 template <int MODE>
 cudaError_t set_bulk_smem(uint32_t smem) {
-    static uint32_t attr_set = 0;
-    if (smem <= attr_set) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute((const void*)fetch_bulk_kernel<MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)std::max<uint32_t>(smem, 48 * 1024));
-    if (e == cudaSuccess) attr_set = smem;
-    return e;
+    static std::atomic<uint32_t> attr_set[kMaxDevices];
+    return raise_smem_attr((const void*)fetch_bulk_kernel<MODE>, attr_set, smem);
 }
 
 // One launch copies units [g0, g1); it claims them from the descriptor's counter starting at
@@ -144,12 +159,8 @@ int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStrea
         const uint32_t cap = host_dst ? (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8)) : 0;
         const BulkPlan p = plan_bulk(dd, device_sm_count(device), cap, total);
         if (p.stages >= 2) {
-            static uint32_t attr_set = 0;
-            if (p.smem > attr_set) {
-                OC_CUDA(cudaFuncSetAttribute((const void*)offload_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)std::max<uint32_t>(p.smem, 48 * 1024)));
-                attr_set = p.smem;
-            }
+            static std::atomic<uint32_t> attr_set[kMaxDevices];
+            OC_CUDA(raise_smem_attr((const void*)offload_bulk_kernel, attr_set, p.smem));
             // no observer CTA here: the whole first wave copies
             const uint32_t grid = (uint32_t)std::min<uint64_t>(host_dst ? p.copy_ctas : p.copy_ctas + 1, total);
             offload_bulk_kernel<<<grid, 32, p.smem, s>>>(dd, pos, (uint32_t)total, p.stages, p.stage_bytes);
@@ -251,11 +262,11 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
         OC_CUDA(cudaGetLastError());
         for (uint32_t l = 0; l < L; l++) {
             uint8_t* dst = (uint8_t*)d->flat_base + (uint64_t)l * NS;
-            const bool hot = l < d->hot_layers;  // from the HBM mirror (pitch hot_layers*S)
+            const bool hot = l < d->hot_layers;  // from the HBM mirror (the run's store's pitch)
             for (size_t r = 0; r < d->run_first.size(); r++)
                 OC_CUDA(cudaMemcpy2DAsync(dst + d->run_first[r] * d->geo.S, d->geo.S,
                                           (const void*)((hot ? d->run_hot[r] : d->run_src[r]) + (uint64_t)l * d->geo.S),
-                                          hot ? (uint64_t)d->hot_layers * d->geo.S : d->geo.chunk, d->geo.S,
+                                          hot ? d->run_hot_pitch[r] : d->geo.chunk, d->geo.S,
                                           d->run_len[r], cudaMemcpyDefault, kit.stream));
             announce_kernel<<<1, 1, 0, kit.stream>>>(d->dd.ts + 1 + l, d->dd.ready, (epoch - 1u) * L + l + 1u);
             OC_CUDA(cudaGetLastError());
@@ -298,11 +309,11 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
     for (uint32_t l = 0; l < L; l++) {
         if (l >= 2) OC_CUDA(cudaStreamWaitEvent(kit.stream, kit.scat_done[l - 2], 0));  // stage l&1 free
         uint8_t* stage = (uint8_t*)d->stage_mem + (l & 1) * NS;
-        const bool hot = l < d->hot_layers;  // from the HBM mirror (pitch hot_layers*S)
+        const bool hot = l < d->hot_layers;  // from the HBM mirror (the run's store's pitch)
         for (size_t r = 0; r < d->run_first.size(); r++)
             OC_CUDA(cudaMemcpy2DAsync(stage + d->run_first[r] * d->geo.S, d->geo.S,
                                       (const void*)((hot ? d->run_hot[r] : d->run_src[r]) + (uint64_t)l * d->geo.S),
-                                      hot ? (uint64_t)d->hot_layers * d->geo.S : d->geo.chunk, d->geo.S,
+                                      hot ? d->run_hot_pitch[r] : d->geo.chunk, d->geo.S,
                                       d->run_len[r], cudaMemcpyDefault, kit.stream));
         OC_CUDA(cudaEventRecord(kit.ce_done[l], kit.stream));
         OC_CUDA(cudaStreamWaitEvent(s, kit.ce_done[l], 0));

@@ -101,6 +101,9 @@ struct Store {
     // fetch's first layers -- its exposed X0 -- come from HBM.
     uint32_t hot_layers = 0;
     uint8_t* hot_slab = nullptr;
+    // put_from_paged inserts its keys before its kernel (on the caller's stream) has written the
+    // slots; a later put_chunks of one of those keys compares bytes only after these events.
+    std::vector<cudaEvent_t> offload_evs;  // guarded by mu
 };
 // Resolve a key to a device address (and the tier holding it; and its HBM mirror and mirrored
 // layer count, 0 if none): local slots first, then peers.
@@ -186,6 +189,7 @@ struct Desc {
     // CE engine (pinned-host chunks): runs of chunks in consecutive slots, copied per layer by one
     // strided copy-engine transfer into a double-buffered HBM stage, then scattered by the kernel
     std::vector<uint64_t> run_first, run_len, run_src, run_hot;  // run_hot: the runs' HBM mirrors
+    std::vector<uint64_t> run_hot_pitch;  // bytes between consecutive chunks' mirrors in a run
     uint32_t hot_layers = 0;   // leading layers with an HBM mirror for every chunk (0: none)
     uint64_t flat_base = 0;    // FLAT target: the client buffer [L][N][S] (the CE engine writes it directly)
     void* stage_mem = nullptr;

@@ -27,6 +27,7 @@ struct ExportHeader {
 }  // namespace
 
 bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier, uint64_t* hot, uint32_t* hot_layers) {
+    std::vector<Store*> peers;
     {
         std::shared_lock<std::shared_mutex> lk(s->mu);
         auto it = s->index.find(k);
@@ -37,11 +38,28 @@ bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier, uint64_
             if (hot_layers) *hot_layers = s->hot_layers;
             return true;
         }
+        // copy the peer list under the lock: attach_peer may grow (reallocate) it concurrently
+        peers = s->peers;
     }
-    for (Store* p : s->peers)
+    for (Store* p : peers)
         if (store_resolve(p, k, addr, tier, hot, hot_layers)) return true;
     return false;
 }
+
+namespace {
+// Is `target` reachable from `from` along attached peers (including from itself)?
+bool reaches(Store* from, const Store* target) {
+    if (from == target) return true;
+    std::vector<Store*> peers;
+    {
+        std::shared_lock<std::shared_mutex> lk(from->mu);
+        peers = from->peers;
+    }
+    for (Store* p : peers)
+        if (reaches(p, target)) return true;
+    return false;
+}
+}  // namespace
 
 }  // namespace oc
 
@@ -104,6 +122,10 @@ OC_API int oc_store_destroy(oc_store* h) {
     Store* s = (Store*)h;
     {
         oc::DeviceGuard dg(s->device);
+        for (cudaEvent_t ev : s->offload_evs) {  // offloads write the slab until they finish
+            cudaEventSynchronize(ev);
+            cudaEventDestroy(ev);
+        }
         if (s->put_stream) cudaStreamDestroy(s->put_stream);
         if (s->hot_slab) cudaFree(s->hot_slab);
         if (s->ipc_mapped) cudaIpcCloseMemHandle(s->slab);
@@ -184,6 +206,12 @@ OC_API int oc_put_chunks(oc_store* h, const oc_key* keys, const void* payloads, 
         auto it = s->index.find(keys[i]);
         if (it != s->index.end()) {
             // Existing key: identical bytes deduplicate, different bytes violate immutability.
+            // The slot may still be in flight from an offload on another stream: wait for those.
+            for (cudaEvent_t ev : s->offload_evs) {
+                OC_CUDA(cudaEventSynchronize(ev));
+                cudaEventDestroy(ev);
+            }
+            s->offload_evs.clear();
             OC_CUDA(cudaStreamSynchronize(s->put_stream));
             a.resize(cb);
             b.resize(cb);
@@ -257,6 +285,8 @@ OC_API int oc_store_attach_peer(oc_store* h, oc_store* peer_h) {
     Store* s = (Store*)h;
     Store* p = (Store*)peer_h;
     if (!oc::same_layout(s->layout, p->layout)) return oc::fail(OC_EINVAL, "attach_peer: layouts differ");
+    // A cycle (A -> B -> ... -> A) would make every key miss recurse forever.
+    if (oc::reaches(p, s)) return oc::fail(OC_EINVAL, "attach_peer: would close a cycle of attached stores");
     if (p->tier == OC_TIER_HBM && p->device != s->device) {
         int ok = 0;
         OC_CUDA(cudaDeviceCanAccessPeer(&ok, s->device, p->device));

@@ -186,3 +186,48 @@ def test_hot_layer_errors():
         with pytest.raises(oc.ObjcacheError) as e:
             oc.put_from_paged(st, keys, lay, lib_target(oc, src, cache.data_ptr()))
         assert e.value.code == oc.OC_ENOTSUP
+
+
+def test_hot_layer_mirror_pitch_per_store():
+    """Stores with different mirror depths in one chain (own store: 2 mirrored layers, attached
+    pinned-host peer: 1).  The descriptor mirrors min = 1 layer, but each slot run must read its
+    own store's mirror with that store's pitch (hot_layers * S) -- every engine, byte for byte."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    req = requests_family(lay, 43, 0, [9])[0]
+    keys = oc.chunk_keys(req.tokens, 16)
+    pl = payload_stack(lay, 43, req.payload_ids)
+    with oc.Store(lay, capacity=16, tier=oc.TIER_PINNED_HOST) as own, \
+            oc.Store(lay, capacity=16, tier=oc.TIER_PINNED_HOST) as peer:
+        own.set_hot_layers(2)
+        peer.set_hot_layers(1)
+        own.put_chunks(keys[:6], pl[:6])
+        peer.put_chunks(keys[6:], pl[6:])
+        own.attach_peer(peer)
+        for kind in ("nhd", "flat"):
+            dest = make_dest(lay, req.n_chunks, kind, Bs=8, first_token=0, seed=13)
+            buf = sentinel_buffer(dest.size)
+            d = oc.build_descriptor(own, own.match_prefix(req.tokens), lay, lib_target(oc, dest, buf.data_ptr()))
+            want = oracle_result(lay, 43, req, dest)
+            s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+            for engine in (oc.COPY_CE, oc.COPY_BULK, oc.COPY_LDST):
+                with torch.cuda.stream(s):
+                    buf.fill_(0xA5)
+                d.fetch_layerwise(s, engine=engine)
+                d.wait_layer(lay.num_layers - 1, cons)
+                cons.synchronize()
+                s.synchronize()
+                assert np.array_equal(buf.cpu().numpy(), want), (kind, engine)
+            d.close()
+
+
+def test_attach_peer_rejects_cycles():
+    lay = OLayout(2, 2, 64, 2, 16)
+    with oc.Store(lay, capacity=4) as a, oc.Store(lay, capacity=4) as b, oc.Store(lay, capacity=4) as c:
+        a.attach_peer(b)
+        b.attach_peer(c)
+        for x, y in ((b, a), (c, a), (c, b)):
+            with pytest.raises(oc.ObjcacheError) as e:
+                x.attach_peer(y)
+            assert e.value.code == oc.OC_EINVAL
+        req = requests_family(lay, 44, 0, [2])[0]
+        assert a.match_prefix(req.tokens).shape[0] == 0   # a miss walks a -> b -> c and stops
