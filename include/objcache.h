@@ -335,6 +335,12 @@ typedef struct {
                                 held rates cover only the rest (reading c25);
                                 oc_fetch_batch_wdrr fills it from the members' hot layers
                                 when NULL                                                     */
+    uint32_t layer_packets;  /* 0: a DRR packet is one copy unit (reading c21).  L (the model's
+                                layer count): a packet is a request's whole layer payload,
+                                N_i*S bytes -- Alg. A2 line 7 as written; n_units[i] must be
+                                a multiple of L, free_units whole layers, Q >= the largest
+                                payload (default max(256 KiB, largest payload)); EINVAL
+                                otherwise                                                     */
 } oc_wdrr_opts;
 
 /* Fetch a batch in WDRR order (instead of layer-major across requests).  Same contract as

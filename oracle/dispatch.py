@@ -32,6 +32,14 @@ Readings (DESIGN.md):
 
 The dispatch order is returned as runs (flow, first packet, count); `entries` splits the runs
 into claim entries of at most E packets, the granularity at which copy CTAs take work.
+
+Two packet granularities:
+  plan                 c21: packet = one copy unit (the library's default planner)
+  layer_payload_plan   Alg. A2 line 7 literally ("Dispatch layer payloads"): packet =
+                       one request's whole layer-l payload, N_i*S bytes; quantum default
+                       max(256 KiB, largest layer payload) so every visit sends.  The packet
+                       order is expanded into the request's units of that layer (layer-major,
+                       chunk j, then tile) so both plans name the same claimable work.
 """
 import math
 
@@ -131,3 +139,47 @@ def plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=8, rates=None, free=Non
         ents = entries(front, E) + entries(runs([(f, p + fu[f]) for f, p in rest]), E)
     rel = release_us(ents, sizes, rates, free) if rates is not None else None
     return ents, rel
+
+
+def layer_payload_sizes(n_chunks, L, tile_bytes):
+    """Alg. A2 line 7 packets of one request: L layer payloads of N_i * S bytes (S = sum of the
+    tiles of one chunk's layer slice).  A request with no chunks has no payloads at all (it never
+    enters the layerwise pool), not L empty ones."""
+    return [n_chunks * sum(tile_bytes)] * L if n_chunks else []
+
+
+def layer_payload_plan(n_chunks, L, tiles, tile_bytes, weights, Q=0, E=8, rates=None, free_layers=None):
+    """WDRR over whole layer payloads (Alg. A2 line 7, P:2596).  DRR runs over packets = layers;
+    each dispatched layer l of request i becomes its units [l*upl_i, (l+1)*upl_i), upl_i = N_i*tiles,
+    in runs/entries as in `plan`.  free_layers[i] (mirrored layers, reading c25) go first, request
+    by request.  Release times (c22) are per entry over the request's unit bytes, as in `plan`."""
+    sizes = [layer_payload_sizes(n, L, tile_bytes) for n in n_chunks]
+    Qe = Q if Q else default_quantum(max([max(s) for s in sizes if s], default=1))
+    if Qe < max([max(s) for s in sizes if s], default=0):
+        raise ValueError("quantum below the largest layer payload")
+    upl = [n * tiles for n in n_chunks]
+    fl = [min(f, L) for f in free_layers] if free_layers else [0] * len(n_chunks)
+    front = [(f, 0, fl[f] * upl[f]) for f in range(len(n_chunks)) if fl[f] > 0 and upl[f] > 0]
+    order = drr_order([s[k:] for s, k in zip(sizes, fl)], quanta(weights, Qe))
+    unit_runs = runs([(f, p + fl[f]) for f, p in order])           # runs of layers
+    unit_runs = [(f, first * upl[f], cnt * upl[f]) for f, first, cnt in unit_runs]
+    ents = entries(front, E) + entries(unit_runs, E)
+    rel = None
+    if rates is not None:
+        usz = [unit_sizes(n, L, tiles, tile_bytes) for n in n_chunks]
+        rel = release_us(ents, usz, rates, [fl[f] * upl[f] for f in range(len(n_chunks))])
+    return ents, rel
+
+
+def bytes_by_flow_prefix(ents, unit_size_lists):
+    """Byte-level view of a plan: for each entry boundary, (total bytes so far, per-flow bytes)."""
+    n = len(unit_size_lists)
+    per = [0] * n
+    tot = 0
+    out = [(0, tuple(per))]
+    for f, first, cnt in ents:
+        b = sum(unit_size_lists[f][first:first + cnt])
+        per[f] += b
+        tot += b
+        out.append((tot, tuple(per)))
+    return out

@@ -66,7 +66,7 @@ class CFetchOpts(ctypes.Structure):
 class CWdrrOpts(ctypes.Structure):
     _fields_ = [("weights", ctypes.POINTER(ctypes.c_double)), ("quantum_bytes", ctypes.c_uint64),
                 ("entry_units", ctypes.c_uint32), ("hold_rates", ctypes.c_uint32),
-                ("free_units", ctypes.POINTER(ctypes.c_uint64))]
+                ("free_units", ctypes.POINTER(ctypes.c_uint64)), ("layer_packets", ctypes.c_uint32)]
 
 
 class CProfile(ctypes.Structure):
@@ -494,16 +494,17 @@ class Batch:
         _check(_lib.oc_batch_set_order(self._h, int(order)))
 
     def fetch(self, stream=None, max_ctas=0, unit_bytes=0, wdrr_weights=None, quantum_bytes=0, entry_units=0,
-              hold_rates=False, engine=COPY_AUTO, free_units=None):
+              hold_rates=False, engine=COPY_AUTO, free_units=None, layer_packets=0):
         """One launch for the whole batch.  With `wdrr_weights` (one per member) the claim order is
         weighted deficit round robin (oc_fetch_batch_wdrr, Alg. A2 line 7); `hold_rates` paces
         member i at wdrr_weights[i] bytes/s (Alg. A2 line 6); `free_units` (default: the members'
-        mirrored layers) are claimed first and unpaced (reading c25)."""
+        mirrored layers) are claimed first and unpaced (reading c25); `layer_packets` = L makes a
+        DRR packet a whole layer payload (Alg. A2 line 7 as written) instead of one unit."""
         o = CFetchOpts(FETCH_PERSISTENT, int(engine), int(max_ctas), int(unit_bytes), 0.0)
         if wdrr_weights is None:
             _check(_lib.oc_fetch_batch(self._h, ctypes.byref(o), _stream(stream)))
             return
-        keep, opts = _wdrr_opts(wdrr_weights, quantum_bytes, entry_units, hold_rates, free_units)
+        keep, opts = _wdrr_opts(wdrr_weights, quantum_bytes, entry_units, hold_rates, free_units, layer_packets)
         if len(wdrr_weights) != len(self.descs):
             raise ValueError("one WDRR weight per batch member")
         _check(_lib.oc_fetch_batch_wdrr(self._h, ctypes.byref(o), ctypes.byref(opts), _stream(stream)))
@@ -517,11 +518,12 @@ class Batch:
         self.close()
 
 
-def _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units=None):
+def _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units=None, layer_packets=0):
     """(arrays the options point into -- keep them alive across the call, options)."""
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
     opts = CWdrrOpts(w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(quantum_bytes), int(entry_units),
                      1 if hold_rates else 0)
+    opts.layer_packets = int(layer_packets)
     keep = [w]
     if free_units is not None:
         fu = np.ascontiguousarray(np.asarray(free_units, dtype=np.uint64))
@@ -532,12 +534,14 @@ def _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units=None)
     return keep, opts
 
 
-def wdrr_plan(n_units, tile_bytes, weights, quantum_bytes=0, entry_units=0, hold_rates=False, free_units=None):
+def wdrr_plan(n_units, tile_bytes, weights, quantum_bytes=0, entry_units=0, hold_rates=False, free_units=None,
+              layer_packets=0):
     """The WDRR claim order the library builds (host only): arrays (request, first unit, count,
-    release us) of the entries.  free_units[i]: request i's leading units that are not paced."""
+    release us) of the entries.  free_units[i]: request i's leading units that are not paced;
+    layer_packets = L: packets are whole layer payloads (n_units[i] / L units each)."""
     nu = np.ascontiguousarray(np.asarray(n_units, dtype=np.uint64))
     tb = np.ascontiguousarray(np.asarray(tile_bytes, dtype=np.uint32))
-    keep, opts = _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units)
+    keep, opts = _wdrr_opts(weights, quantum_bytes, entry_units, hold_rates, free_units, layer_packets)
     if len(weights) != len(nu):
         raise ValueError("one weight per request")
     n = ctypes.c_uint64()

@@ -19,6 +19,12 @@
 // HBM (free_units[i] leading units: the layers a pinned-host store mirrors, reading c24) never
 // cross the paced link, so they neither wait nor count toward the request's bytes; nor does DRR
 // schedule them: they are dispatched first, request by request (reading c25).
+//
+// Packet granularity: by default a packet is one copy unit (reading c21: a request's layer is many
+// units, so its bytes interleave finely with the other requests'); with layer_packets = L a packet
+// is a whole layer payload of N_i*S bytes, Alg. A2 line 7 as written, and the quantum must cover the
+// largest one.  Both are DRR with the same weights, so their byte shares agree within one round
+// of each (tests/test_oracle_dispatch.py pins the bound; test_lib_dispatch.py checks both planners).
 #include <cmath>
 
 #include "oc_internal.h"
@@ -38,8 +44,27 @@ int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, u
         prefix[t + 1] = prefix[t] + tile_bytes[t];
     }
     period = prefix[tiles];
-    const uint64_t Q = w.quantum_bytes ? w.quantum_bytes : std::max<uint64_t>(256 * 1024, max_tile);
-    if (Q < max_tile) return fail(OC_EINVAL, "wdrr: quantum below the largest unit");
+    // bytes of units [0, u) of a request: whole periods of `tiles` units, then a partial period
+    auto bytes_upto = [&](uint64_t u) { return (u / tiles) * period + prefix[u % tiles]; };
+    // Packets: one unit (reading c21), or with layer_packets = L one request's whole layer payload
+    // (Alg. A2 line 7 as written): request i has L packets of upl_i = n_units[i] / L units.
+    const uint32_t LP = w.layer_packets;
+    std::vector<uint64_t> upl(n, 0), pkt(n, 0);
+    uint64_t max_packet = max_tile;
+    if (LP) {
+        max_packet = 0;
+        for (uint32_t i = 0; i < n; i++) {
+            if (n_units[i] % LP) return fail(OC_EINVAL, "wdrr: layer packets need n_units a multiple of L");
+            upl[i] = n_units[i] / LP;
+            pkt[i] = bytes_upto(upl[i]);
+            if (w.free_units && upl[i] && (std::min(w.free_units[i], n_units[i]) % upl[i]))
+                return fail(OC_EINVAL, "wdrr: layer packets need free_units in whole layers");
+            max_packet = std::max(max_packet, pkt[i]);
+        }
+    }
+    const uint64_t Q = w.quantum_bytes ? w.quantum_bytes : std::max<uint64_t>(256 * 1024, max_packet);
+    if (Q < max_packet) return fail(OC_EINVAL, LP ? "wdrr: quantum below the largest layer payload"
+                                                  : "wdrr: quantum below the largest unit");
     const uint32_t E = w.entry_units ? w.entry_units : 8;
     double wmin = INFINITY;
     for (uint32_t i = 0; i < n; i++) {
@@ -54,8 +79,6 @@ int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, u
         if (!(qi < 4.0e18)) return fail(OC_ERANGE, "wdrr: weight ratio too large");
         q[i] = (uint64_t)qi;
     }
-    // bytes of units [0, u) of a request: whole periods of `tiles` units, then a partial period
-    auto bytes_upto = [&](uint64_t u) { return (u / tiles) * period + prefix[u % tiles]; };
     std::vector<uint32_t> active;
     uint64_t total_units = 0, visits = 0;  // reserve: ~one entry per visit plus one per E units
     for (uint32_t i = 0; i < n; i++) {
@@ -106,13 +129,19 @@ int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, u
             const uint32_t i = active[a];
             D[i] += q[i];
             const uint64_t start = head[i];
+            if (LP) {  // whole layer payloads while they fit in the deficit
+                const uint64_t left = (n_units[i] - head[i]) / upl[i];
+                const uint64_t k = std::min<uint64_t>(left, D[i] / pkt[i]);
+                head[i] += k * upl[i];
+                D[i] -= k * pkt[i];
+            }
             // send units while the head unit fits in the deficit: the partial period first, then
             // whole periods arithmetically, then the rest unit by unit
-            while (head[i] < n_units[i] && head[i] % tiles != 0 && tile_bytes[head[i] % tiles] <= D[i]) {
+            while (!LP && head[i] < n_units[i] && head[i] % tiles != 0 && tile_bytes[head[i] % tiles] <= D[i]) {
                 D[i] -= tile_bytes[head[i] % tiles];
                 head[i]++;
             }
-            if (head[i] % tiles == 0) {
+            if (!LP && head[i] % tiles == 0) {
                 const uint64_t periods = std::min<uint64_t>((n_units[i] - head[i]) / tiles, D[i] / period);
                 head[i] += periods * tiles;
                 D[i] -= periods * period;

@@ -154,6 +154,28 @@ def test_wdrr_parity(lay, unit_bytes, hold, E, engine):
     st.close()
 
 
+@pytest.mark.parametrize("hold", [False, True])
+@pytest.mark.parametrize("engine", [oc.COPY_BULK, oc.COPY_LDST])
+def test_wdrr_layer_packets_parity(hold, engine):
+    """Alg. A2 line 7 as written: DRR packets are whole layer payloads (layer_packets = L) -- the
+    same bytes as the oracle, layers announced in order, through both copy engines."""
+    lay = OLayout(3, 2, 64, 2, 16)
+    st, items = setup_batch(lay, SPECS)
+    b = oc.Batch([it["desc"] for it in items])
+    s = torch.cuda.Stream()
+    b.fetch(s, wdrr_weights=[2e9, 0.5e9, 7e9, 1e9, 3.3e9], hold_rates=hold, engine=engine,
+            layer_packets=lay.num_layers)
+    for it in items:
+        it["desc"].sync_layer(lay.num_layers - 1)
+    torch.cuda.synchronize()
+    check(lay, items)
+    for it in items:
+        t = it["desc"].layer_times().astype(np.int64)
+        assert np.all(np.diff(t[1:]) >= 0) and t[1] >= t[0]
+    b.close()
+    st.close()
+
+
 def test_wdrr_refetch_mixed_with_other_orders():
     """Epoch bookkeeping across WDRR, layer-major batch and single fetches of the same descriptors
     (the WDRR observer reads each request's next layer back from its ready word)."""

@@ -84,3 +84,45 @@ def test_free_units_edge_cases():
         assert got == want and rel == wrel, free
     got, rel = lib_plan(n_chunks, L, tiles, tb, w, hold=True, free=[100, 0, 100])
     assert all(r == 0 for r in rel) and [e[0] for e in got] == [0] * 2 + [2] * 1   # every unit free
+
+
+def test_layer_packet_batches_match_oracle():
+    """layer_packets = L (Alg. A2 line 7 as written: a DRR packet is a request's whole layer payload):
+    the library's planner equals oracle.dispatch.layer_payload_plan entry for entry and in release
+    times, with and without mirrored leading layers."""
+    rng = random.Random(2597)
+    for case in range(120):
+        n = rng.randint(1, 6)
+        L = rng.randint(1, 5)
+        tiles = rng.randint(1, 3)
+        tile_bytes = [rng.choice([2048, 16384, 32768]) for _ in range(tiles)]
+        n_chunks = [rng.randint(0, 12) for _ in range(n)]
+        if sum(n_chunks) == 0:
+            n_chunks[0] = 1
+        weights = [rng.choice([1.0, 2.0, 3.7, 0.5, 12.25]) * 1e9 for _ in range(n)]
+        maxp = max(k * sum(tile_bytes) for k in n_chunks)
+        Q = rng.choice([0, maxp, 2 * maxp + 7])
+        E = rng.choice([0, 1, 3, 8])
+        hold = rng.random() < 0.5
+        free_layers = [rng.randint(0, L) for _ in range(n)] if rng.random() < 0.5 else None
+        free_units = [f * k * tiles for f, k in zip(free_layers, n_chunks)] if free_layers else None
+        req, first, cnt, rel = oc.wdrr_plan([k * L * tiles for k in n_chunks], tile_bytes, weights,
+                                            quantum_bytes=Q, entry_units=E, hold_rates=hold,
+                                            free_units=free_units, layer_packets=L)
+        got = list(zip(req.tolist(), first.tolist(), cnt.tolist()))
+        want, wrel = dp.layer_payload_plan(n_chunks, L, tiles, tile_bytes, weights, Q=Q, E=E or 8,
+                                           rates=weights if hold else None, free_layers=free_layers)
+        assert got == want, case
+        assert rel.tolist() == (wrel if hold else [0] * len(want)), case
+
+
+def test_layer_packet_errors():
+    with pytest.raises(oc.ObjcacheError) as e:     # 7 units are not 2 whole layers
+        oc.wdrr_plan([7], [32768], [1.0], layer_packets=2)
+    assert e.value.code == oc.OC_EINVAL
+    with pytest.raises(oc.ObjcacheError) as e:     # Q below a 4-unit layer payload
+        oc.wdrr_plan([8], [32768], [1.0], quantum_bytes=65536, layer_packets=2)
+    assert e.value.code == oc.OC_EINVAL
+    with pytest.raises(oc.ObjcacheError) as e:     # free units must be whole layers
+        oc.wdrr_plan([8], [32768], [1.0], free_units=[3], layer_packets=2)
+    assert e.value.code == oc.OC_EINVAL

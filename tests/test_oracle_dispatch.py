@@ -201,3 +201,109 @@ def test_plan_layer_major_units():
     assert rel == sorted(rel)
     with pytest.raises(ValueError):
         dp.plan([1], L=1, tiles=1, tile_bytes=[1 << 20], weights=[1.0], Q=4096)
+
+
+# ---- Alg. A2 line 7 literally: packets are whole layer payloads ----------------------------
+def _ints(s, conv=int):
+    return [conv(x) for x in s.split()] if s.strip() else []
+
+
+@pytest.mark.parametrize("row", read_golden("wdrr_layer_examples.csv"), ids=lambda r: r["example"])
+def test_layer_payload_plan_hand_worked(row):
+    n_chunks, tile_bytes = _ints(row["n_chunks"]), _ints(row["tile_bytes"])
+    rates = _ints(row["rates"], float) or None
+    free = _ints(row["free_layers"]) or None
+    ents, rel = dp.layer_payload_plan(n_chunks, int(row["L"]), len(tile_bytes), tile_bytes,
+                                      _ints(row["weights"], float), Q=int(row["Q"]), E=int(row["E"]),
+                                      rates=rates, free_layers=free)
+    want = [tuple(int(v) for v in e.split(":")) for e in row["entries"].split()]
+    assert ents == want
+    if rates:
+        assert rel == _ints(row["release_us"])
+
+
+def _random_batch(rng):
+    n = rng.randint(1, 5)
+    L = rng.randint(1, 6)
+    tiles = rng.randint(1, 3)
+    tile_bytes = [rng.choice([8, 12, 16, 32]) for _ in range(tiles)]
+    n_chunks = [rng.randint(0, 7) for _ in range(n)]
+    w = [rng.choice([1.0, 1.5, 2.0, 3.0, 7.25]) for _ in range(n)]
+    return n_chunks, L, tiles, tile_bytes, w
+
+
+def test_layer_payload_plan_covers_each_request_in_layer_order():
+    """Conservation and order: every unit of every request exactly once, each request's units in
+    layer-major order, and every dispatched layer whole (no entry run splits a layer between two
+    visits) -- what makes the packet a 'layer payload'."""
+    rng = random.Random(21)
+    for _ in range(300):
+        n_chunks, L, tiles, tile_bytes, w = _random_batch(rng)
+        ents, _ = dp.layer_payload_plan(n_chunks, L, tiles, tile_bytes, w, E=rng.randint(1, 9))
+        got = [[] for _ in n_chunks]
+        for f, first, cnt in ents:
+            got[f].extend(range(first, first + cnt))
+        for f, n in enumerate(n_chunks):
+            assert got[f] == list(range(n * tiles * L))
+        # runs (before the cut into entries) start and end on layer boundaries
+        upl = [n * tiles for n in n_chunks]
+        for f, first, cnt in dp.runs([(f, u) for f, a, c in ents for u in range(a, a + c)]):
+            assert first % upl[f] == 0 and cnt % upl[f] == 0
+
+
+def test_unit_plan_tracks_layer_payload_plan():
+    """Pin of reading c21 (the library's unit-granular DRR stands for Alg. A2's layer-payload DRR).
+    Both are DRR with quanta proportional to the same weights, so while every request is backlogged
+    each keeps request i's bytes within 2*q_i + Max of the fluid share B*q_i/sum(q) after B bytes
+    (Shreedhar-Varghese: k*q_i - Max < sent_i <= k*q_i after k rounds, and sum q >= n*Max).  Hence
+    on every prefix of the unit plan, request i's cumulative bytes differ from the layer-payload
+    plan's (at the same total, up to the entry in progress) by at most (2*q_i + Max) of one plan
+    plus that of the other.  Checked on random batches of 64-layer requests (many rounds before
+    anyone finishes); a unit plan that ignores or inverts the weights fails it."""
+    rng = random.Random(5)
+    for _ in range(60):
+        n = rng.randint(2, 4)
+        L, tiles = 64, rng.randint(1, 2)
+        tile_bytes = [rng.choice([8, 16]) for _ in range(tiles)]
+        n_chunks = [rng.randint(4, 8) for _ in range(n)]
+        w = [float(rng.randint(1, 4)) for _ in range(n)]
+        usz = [dp.unit_sizes(k, L, tiles, tile_bytes) for k in n_chunks]
+        maxU, maxP = max(tile_bytes), max(k * sum(tile_bytes) for k in n_chunks)
+        # small quanta make the rounds fine enough for the bound to bite (default Q = 256 KiB
+        # exceeds these toy requests): Q = the largest packet of each plan
+        eu, _ = dp.plan(n_chunks, L, tiles, tile_bytes, w, Q=maxU, E=1)
+        ep, _ = dp.layer_payload_plan(n_chunks, L, tiles, tile_bytes, w, Q=maxP, E=1)
+        qU, qP = dp.quanta(w, maxU), dp.quanta(w, maxP)
+        pu, pp = dp.bytes_by_flow_prefix(eu, usz), dp.bytes_by_flow_prefix(ep, usz)
+        total = [sum(x) for x in usz]
+        assert pu[-1][1] == pp[-1][1] == tuple(total)
+        k = 0
+        for B, per_u in pu:
+            while pp[k + 1][0] < B:
+                k += 1
+            lo, hi = pp[k][1], pp[k + 1][1] if pp[k][0] < B else pp[k][1]
+            if any(per_u[i] >= total[i] or hi[i] >= total[i] for i in range(n)):
+                break   # only while every request is backlogged in both plans
+            for i in range(n):
+                bound = (2 * qU[i] + maxU) + (2 * qP[i] + maxP)
+                assert lo[i] - bound <= per_u[i] <= hi[i] + bound
+
+
+def test_layer_payload_plan_fairness_bound():
+    """The layer-payload plan is a DRR like any other: Shreedhar-Varghese's normalised fairness
+    bound holds between backlogged requests on every prefix, with Max = the largest layer payload."""
+    rng = random.Random(9)
+    for _ in range(200):
+        n_chunks, L, tiles, tile_bytes, w = _random_batch(rng)
+        sizes = [dp.layer_payload_sizes(n, L, tile_bytes) for n in n_chunks]
+        mx = max([s for f in sizes for s in f], default=1)
+        q = dp.quanta(w, dp.default_quantum(mx))
+        sent = [0] * len(sizes)
+        left = [len(f) if f and f[0] > 0 else 0 for f in sizes]
+        for f, p in dp.drr_order(sizes, q):
+            sent[f] += sizes[f][p]
+            left[f] -= 1
+            live = [i for i in range(len(sizes)) if left[i] > 0]
+            for a in live:
+                for b in live:
+                    assert abs(sent[a] / q[a] - sent[b] / q[b]) < 2 + mx / min(q[a], q[b])
