@@ -80,6 +80,19 @@ def chunk_payload(seed: int, payload_id, nbytes: int) -> np.ndarray:
     return words.view(np.uint8)[:nbytes]
 
 
+def chunk_payload_range(seed: int, payload_id, offset: int, nbytes: int) -> np.ndarray:
+    """Bytes [offset, offset + nbytes) of chunk_payload(seed, payload_id, ...), regenerated on their
+    own (offset a multiple of 8): the PCG64 stream advanced by offset/8 words.  Lets at-size checks
+    draw one layer slice of one chunk without the whole corpus in memory."""
+    if offset % 8:
+        raise ValueError("offset must be a multiple of 8")
+    owner, block = payload_id
+    bg = np.random.PCG64([seed, 0xC4C4, int(owner), int(block)])
+    bg.advance(offset // 8)
+    words = bg.random_raw(-(-nbytes // 8)).astype(np.uint64, copy=False)
+    return words.view(np.uint8)[:nbytes]
+
+
 def payloads(seed: int, payload_ids, nbytes: int) -> np.ndarray:
     """Stack of chunk payloads, shape [len(payload_ids), nbytes]."""
     out = np.empty((len(payload_ids), nbytes), dtype=np.uint8)

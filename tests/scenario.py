@@ -115,3 +115,44 @@ def lib_target(oc, dest: Dest, base: int):
         return oc.FlatTarget(base + dest.flat_off, dest.flat_cap)
     return oc.PagedTarget([base + x for x in dest.k_off], [base + x for x in dest.v_off], dest.block_stride,
                           dest.token_stride, dest.head_stride, dest.block_size, dest.block_table, dest.first_token)
+
+
+class SynthStore:
+    """Oracle-side chunk store whose objects are regenerated from ``synth`` on demand: RangeGet(H, o,
+    S) (Alg. A1 line 5) returns bytes [o, o+S) of the chunk's seeded payload.  For at-size checks
+    (8-9 GiB corpora) that a dict of payloads would not hold; what it returns equals what
+    ``oracle.store.ChunkStore`` would return after put()s of the same payloads."""
+
+    def __init__(self, seed, keys, payload_ids):
+        self.seed = seed
+        self.ids = {bytes(k): pid for k, pid in zip(keys, payload_ids)}
+
+    def __contains__(self, key):
+        return bytes(key) in self.ids
+
+    def range_get(self, key, offset, length):
+        return synth.chunk_payload_range(self.seed, self.ids[bytes(key)], offset, length).tobytes()
+
+
+def put_in_batches(store, lay: OLayout, seed, keys, payload_ids, batch=256):
+    """Library-side puts of a large corpus, `batch` chunks of synth payload at a time."""
+    n_new = 0
+    for i in range(0, len(payload_ids), batch):
+        n_new += store.put_chunks(keys[i:i + batch], payload_stack(lay, seed, payload_ids[i:i + batch]))
+    return n_new
+
+
+def oracle_layer(lay: OLayout, ostore, okeys_list, dest: Dest, layer: int):
+    """Expected bytes of layer `layer`'s region of a paged NHD destination (its K and V caches,
+    [2][pool][Bs][row], sentinel 0xA5 where no token lands) and the region's offset: Alg. A1's
+    gather (oracle.assemble.gather_layer) of the layer, then the paged scatter into a buffer holding
+    just that region (the target's bases rebased to it)."""
+    assert dest.kind == "nhd"
+    lo = dest.k_off[layer]
+    hi = dest.v_off[layer] + (dest.v_off[layer] - dest.k_off[layer])
+    rebased = OPaged([x - lo for x in dest.k_off], [x - lo for x in dest.v_off], dest.block_stride,
+                     dest.token_stride, dest.head_stride, dest.block_size, dest.block_table, dest.first_token)
+    desc = obuild(ostore, okeys_list, lay, rebased)
+    region = synth.sentinel(hi - lo)
+    scatter_paged_advanced_index(gather_layer(ostore, desc, layer), layer, desc, region)
+    return lo, region

@@ -31,3 +31,9 @@ def test_block_table_distinct_and_seeded():
     bt = synth.block_table(3, 100, 150)
     assert len(set(bt.tolist())) == 100 and bt.min() >= 0 and bt.max() < 150
     assert np.array_equal(bt, synth.block_table(3, 100, 150))
+
+
+def test_chunk_payload_range_is_a_slice_of_the_chunk():
+    full = synth.chunk_payload(5, (1, 7), 4096)
+    for off, n in ((0, 64), (8, 100), (2048, 2048), (4000, 96)):
+        assert np.array_equal(synth.chunk_payload_range(5, (1, 7), off, n), full[off:off + n])
