@@ -380,6 +380,16 @@ OC_API int oc_layer_times(oc_desc* desc, uint64_t* out);
  * OC_ERANGE. */
 OC_API int oc_emulate_compute(uint64_t ns, uint64_t* stamps, void* stream);
 
+/* Measurement support (not a step of the method): with the environment variable
+ * OC_TRACE=1, every single-descriptor BULK launch records, per copy CTA b
+ * (1 <= b < 2048), 8 GPU-global-timer stamps of its ramp: [0] CTA start,
+ * [1] barriers initialised, [2] first claim returned, [3] first load issued,
+ * [4] first unit in shared memory, [5] first unit's stores issued, [6] first
+ * retire handed to the signaler, [7] signaler's first release published.
+ * Copies the last traced launch's min(n, 2048*8) stamps (slot b*8+i; 0 =
+ * not reached) into `out` (host).  Blocks until the device is idle. */
+OC_API int oc_trace_read(uint64_t* out, uint64_t n);
+
 /* ---- bandwidth scheduling (Sec. 3.6) --------------------------- */
 typedef enum {
     OC_POL_EQUAL = 0,         /* B / n                                    */

@@ -111,6 +111,7 @@ _SIGS = {
     "oc_sync_layer": [_vp, ctypes.c_uint32],
     "oc_layer_times": [_vp, c_u64p],
     "oc_emulate_compute": [ctypes.c_uint64, _vp, _vp],
+    "oc_trace_read": [c_u64p, ctypes.c_uint64],
     "oc_schedule_bandwidth": [ctypes.c_int, ctypes.POINTER(CProfile), ctypes.c_uint64, ctypes.c_double,
                               ctypes.c_double, ctypes.POINTER(ctypes.c_double)],
     "oc_pool_create": [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, ctypes.POINTER(_vp)],
@@ -635,6 +636,13 @@ def emulate_compute(ns: int, stream=None, stamps=None):
     layer's compute window C_l; `stamps` (device tensor/address, 2 x u64) receives start and end."""
     addr = None if stamps is None else (int(stamps.data_ptr()) if hasattr(stamps, "data_ptr") else int(stamps))
     _check(_lib.oc_emulate_compute(int(ns), addr, _stream(stream)))
+
+
+def trace_read() -> np.ndarray:
+    """Measurement support: the last OC_TRACE=1 launch's ramp stamps, [2048 CTAs, 8] (ns, 0 = none)."""
+    out = np.zeros(2048 * 8, dtype=np.uint64)
+    _check(_lib.oc_trace_read(out.ctypes.data_as(c_u64p), out.size))
+    return out.reshape(2048, 8)
 
 
 def abi_version() -> int:

@@ -124,12 +124,41 @@ cudaError_t set_bulk_smem(uint32_t smem) {
     return raise_smem_attr((const void*)fetch_bulk_kernel<MODE>, attr_set, smem);
 }
 
+// Measurement support (OC_TRACE=1, oc_trace_read): one ramp-trace buffer per device.
+std::mutex g_trace_mu;
+uint64_t* g_trace_buf[kMaxDevices] = {};
+uint64_t* g_trace_last = nullptr;
+
+uint64_t* trace_buffer(int device, cudaStream_t s) {
+    static const bool on = [] {
+        const char* e = std::getenv("OC_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (!on || device < 0 || device >= kMaxDevices) return nullptr;
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    uint64_t*& b = g_trace_buf[device];
+    const size_t bytes = (size_t)kTraceCtas * kTraceSlots * sizeof(uint64_t);
+    if (!b && cudaMalloc((void**)&b, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        b = nullptr;
+        return nullptr;
+    }
+    if (cudaMemsetAsync(b, 0, bytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    g_trace_last = b;
+    return b;
+}
+
 // One launch copies units [g0, g1); it claims them from the descriptor's counter starting at
 // d->grab_ctr and advances that counter by (units + copy CTAs) -- see claim_unit.
 int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
     if (p.stages < 2) return fail(OC_ENOTSUP, "bulk engine: two units do not fit in shared memory (use LDST)");
     OC_CUDA(set_bulk_smem<kSingle>(p.smem));
-    fetch_bulk_kernel<kSingle><<<p.copy_ctas + 1, 64, p.smem, s>>>(d->dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
+    DevDesc dd = d->dd;
+    dd.trace = trace_buffer(d->device, s);
+    fetch_bulk_kernel<kSingle><<<p.copy_ctas + 1, 64, p.smem, s>>>(dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
                                                                  p.stage_bytes);
     OC_CUDA(cudaGetLastError());
     d->grab_ctr += (g1 - g0) + p.copy_ctas;
@@ -851,6 +880,16 @@ OC_API int oc_layer_times(oc_desc* h, uint64_t* out) {
     oc::DeviceGuard dg(d->device);
     OC_CUDA(cudaEventSynchronize(d->done_ev));
     OC_CUDA(cudaMemcpy(out, d->dd.ts, (d->geo.L + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return OC_OK;
+}
+
+OC_API int oc_trace_read(uint64_t* out, uint64_t n) {
+    if (!out) return oc::fail(OC_EINVAL, "trace_read: null out");
+    std::lock_guard<std::mutex> lk(oc::g_trace_mu);
+    if (!oc::g_trace_last) return oc::fail(OC_EINVAL, "trace_read: no traced launch (set OC_TRACE=1)");
+    OC_CUDA(cudaDeviceSynchronize());
+    const uint64_t m = std::min<uint64_t>(n, (uint64_t)oc::kTraceCtas * oc::kTraceSlots);
+    OC_CUDA(cudaMemcpy(out, oc::g_trace_last, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return OC_OK;
 }
 

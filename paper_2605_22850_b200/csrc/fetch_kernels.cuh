@@ -59,6 +59,11 @@ __device__ __forceinline__ void red_add_relaxed(uint32_t* p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Measurement support (OC_TRACE=1): stamp slot i of this CTA's ramp trace.
+__device__ __forceinline__ void trace_stamp(const DevDesc& d, uint32_t i) {
+    if (d.trace && blockIdx.x < kTraceCtas) d.trace[blockIdx.x * kTraceSlots + i] = globaltimer();
+}
+
 // ---- unit geometry -------------------------------------------------------------------------------
 // Layer l of chunk j is 2G rows at [lS, (l+1)S) of the slot: K rows 0..G-1, then V rows G..2G-1
 // (KV_L2TD, reading c2).  A unit is R consecutive rows q0 .. q0+R-1 of that slice -- contiguous
@@ -496,6 +501,8 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     uint64_t* bars = (uint64_t*)smem;
     uint8_t* buf = smem + 128;
     const uint32_t lane = threadIdx.x & 31;
+    const bool tr = !BATCH && d0.trace != nullptr;  // ramp trace (measurement support)
+    if (tr && threadIdx.x == 0) d0.trace[blockIdx.x * kTraceSlots + 0] = t0;
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < stages; s++) mbar_init(&bars[s], 1);
         for (uint32_t f = 0; f < kFifo; f++) {
@@ -505,6 +512,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) trace_stamp(d0, 1);
     if (threadIdx.x >= 32) {  // ---- signaler warp
         if (threadIdx.x != 32) return;
         // Each round takes every record already in the FIFO (waiting only for the first), merges
@@ -541,6 +549,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
             if (m) {
                 fence_acq_rel_gpu();
                 for (int e = 0; e < m; e++) red_add_relaxed(&(BATCH ? ba.descs[rq[e]] : d0).unit_cnt[ly[e]], nn[e]);
+                if (tr && d0.trace[blockIdx.x * kTraceSlots + 7] == 0) trace_stamp(d0, 7);
             }
         }
         return;
@@ -564,6 +573,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     // overlaps a unit's copy instead of stalling the issue loop -- with a small copy-CTA budget
     // that latency would otherwise cap each CTA at one unit per round trip.
     uint32_t next_raw = lane == 0 ? atomicAdd(claim_ctr, 1u) : 0u;
+    if (tr && lane == 0) trace_stamp(d0, 2);
     // kWdrr: the entry being consumed (lane 0) and the launch's common start time
     uint32_t cur_req = 0, cur_next = 0, cur_left = 0, cur_rel = 0;
     SegCache seg_cache;  // kByPos (lane 0)
@@ -680,6 +690,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
             if (paced)
                 while (globaltimer() < release_time(k)) __nanosleep(2000);
             issue_load(k);
+            if (tr && k == 0) trace_stamp(d0, 3);
         }
     __syncwarp();
 
@@ -692,6 +703,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         const uint32_t s = k % stages;
         const UnitGeo u = unit_geo(d, g);
         mbar_wait(&bars[s], (k / stages) & 1u);
+        if (tr && k == 0 && lane == 0) trace_stamp(d0, 4);
         const uint8_t* sbuf = buf + (size_t)s * stage_bytes;
         if (d.nhd) {
             // Lane r owns row r if row r starts a run: the unit's first row, a block's first slot,
@@ -718,6 +730,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
             }
         }
         bulk_commit();
+        if (tr && k == 0 && lane == 0) trace_stamp(d0, 5);
         bulk_wait_read<1>();  // unit k-1's stage is free once its stores have read shared memory
         __syncwarp();
         const uint32_t kl = k + stages - 1;  // next unit to load, into unit k-1's stage
@@ -761,6 +774,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
             if (lane == 0) {
                 for (uint32_t r = next_retire; r <= k; r++) retire(r);
                 flush();
+                if (tr && next_retire == 0) trace_stamp(d0, 6);
             }
             next_retire = k + 1;
         } else if (k + 1 - next_retire >= 8) {

@@ -160,7 +160,10 @@ struct DevDesc {
     FastDiv div_vpr;
     FastDiv div_Bs;
     FastDiv div_hdv;          // (d*p)/16
+    uint64_t* trace;          // measurement support (OC_TRACE=1): per-CTA ramp stamps, else null
 };
+constexpr uint32_t kTraceSlots = 8;     // stamps per CTA (fetch_kernels.cuh, bulk engine)
+constexpr uint32_t kTraceCtas = 2048;   // CTAs traced per launch
 
 struct Desc {
     Store* store;
