@@ -272,8 +272,18 @@ typedef struct {
                                 fetch (layer-major) is released no earlier than
                                 t0 + b/pace_Bps, so the request never exceeds its
                                 rate (the held rate of Alg. A2 line 6)          */
-    uint32_t reserved;       /* 0 */
+    uint32_t flags;          /* OC_FETCH_OVERLAP: the launch may start while the
+                                stream's previous fetch launch is still draining
+                                (programmatic dependent launch, no wait on its
+                                memory): the caller guarantees the work before it
+                                on the stream neither writes this fetch's
+                                destination nor produces anything it reads (e.g.
+                                back-to-back fetches of different requests).  The
+                                previous fetch's tail and this one's ramp overlap.
+                                Single-descriptor TMA (BULK) launches only; other
+                                engines ignore it.  0 = stream order.            */
 } oc_fetch_opts;
+#define OC_FETCH_OVERLAP 1u
 
 /* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and
  * return at once.  One fetch may be in flight per descriptor at a time; a

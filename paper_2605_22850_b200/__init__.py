@@ -36,6 +36,7 @@ TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
 BATCH_BY_REQUEST, BATCH_BY_POSITION = 0, 1
 COPY_LDST, COPY_BULK, COPY_CE, COPY_AUTO = 0, 1, 2, 3
+FETCH_OVERLAP = 1
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -60,7 +61,7 @@ class CTarget(ctypes.Structure):
 class CFetchOpts(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_uint32), ("engine", ctypes.c_uint32), ("max_ctas", ctypes.c_uint32),
                 ("unit_bytes", ctypes.c_uint32), ("pace_Bps", ctypes.c_double), ("pace_strict", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32)]
 
 
 class CWdrrOpts(ctypes.Structure):
@@ -415,9 +416,11 @@ class Descriptor:
         return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
 
     def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_AUTO, max_ctas=0, unit_bytes=0,
-                        pace_Bps=0.0, pace_strict=False):
+                        pace_Bps=0.0, pace_strict=False, overlap=False):
+        """`overlap`: OC_FETCH_OVERLAP -- the launch may overlap the stream's previous fetch's tail
+        (the caller guarantees that work does not touch this fetch's destination or sources)."""
         o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
-                       1 if pace_strict else 0, 0)
+                       1 if pace_strict else 0, FETCH_OVERLAP if overlap else 0)
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))
 
     def scatter_flat(self, flat_base: int, flat_capacity: int, stream=None, max_ctas=0, unit_bytes=0):

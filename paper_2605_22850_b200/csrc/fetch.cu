@@ -74,7 +74,8 @@ BulkPlan plan_bulk(const DevDesc& dd, int sms, uint32_t max_ctas, uint64_t units
     while (true) {
         uint32_t per_cta = std::min<uint32_t>(sm_bytes / per_sm - 1024 - kBulkStaticSmem, 227 * 1024);
         uint32_t st = per_cta > 128 ? (per_cta - 128) / p.stage_bytes : 0;
-        st = std::min<uint32_t>(st, (uint32_t)std::max(2, env_int("OC_BULK_STAGES", 16)));
+        // at most 16: the ring's mbarriers live in the first 128 bytes of the dynamic shared memory
+        st = std::min<uint32_t>(st, (uint32_t)std::min(16, std::max(2, env_int("OC_BULK_STAGES", 16))));
         if (st >= 2 || per_sm == 1) {
             p.stages = st >= 2 ? st : 0;  // 0: a unit does not fit twice in shared memory
             break;
@@ -153,15 +154,34 @@ uint64_t* trace_buffer(int device, cudaStream_t s) {
 
 // One launch copies units [g0, g1); it claims them from the descriptor's counter starting at
 // d->grab_ctr and advances that counter by (units + copy CTAs) -- see claim_unit.
-int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s) {
+// Copy CTA b takes unit g0 + b - 1 first (no claim), so the grid never exceeds the units; the
+// counter then advances by exactly g1 - g0 (see the kernel's claim).  With `overlap`
+// (OC_FETCH_OVERLAP) the launch is a programmatic dependent of the stream's previous kernel: it
+// may start once that kernel's CTAs have made their last claims (griddepcontrol.launch_dependents)
+// and it does not wait for that kernel's memory -- the caller guarantees independence.
+int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream_t s, bool overlap = false) {
     if (p.stages < 2) return fail(OC_ENOTSUP, "bulk engine: two units do not fit in shared memory (use LDST)");
+    if (p.copy_ctas == 0 || p.copy_ctas > g1 - g0) return fail(OC_EINVAL, "bulk engine: more copy CTAs than units");
     OC_CUDA(set_bulk_smem<kSingle>(p.smem));
     DevDesc dd = d->dd;
     dd.trace = trace_buffer(d->device, s);
-    fetch_bulk_kernel<kSingle><<<p.copy_ctas + 1, 64, p.smem, s>>>(dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
-                                                                 p.stage_bytes);
-    OC_CUDA(cudaGetLastError());
-    d->grab_ctr += (g1 - g0) + p.copy_ctas;
+    static const uint32_t ramp = (env_int("OC_RAMP_STATIC2", 1) ? kRampStatic2 : 0u) |
+                                 (env_int("OC_RAMP_FIRST_LAYER", 1) ? kRampFirstLayer : 0u);
+    dd.ramp = ramp;
+    const uint32_t extra = (ramp & kRampStatic2) ? ramp_extra(g0, g1, dd.units_per_layer, p.copy_ctas) : 0u;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.copy_ctas + 1);
+    cfg.blockDim = dim3(64);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = overlap ? attr : nullptr;
+    cfg.numAttrs = overlap ? 1 : 0;
+    OC_CUDA(cudaLaunchKernelEx(&cfg, fetch_bulk_kernel<kSingle>, dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
+                               p.stage_bytes));
+    d->grab_ctr += g1 - g0 - extra;  // counter claims: units past the static ones + one overshoot per CTA
     return OC_OK;
 }
 
@@ -475,7 +495,8 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     } else if (o.mode == OC_FETCH_PERSISTENT) {
         BulkPlan p = plan_bulk(dd, sms, max_ctas, total_units);
         if (paced) shallow_ring(&p);
-        int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, 0, (uint32_t)total_units, s)
+        const bool overlap = (o.flags & OC_FETCH_OVERLAP) != 0;
+        int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, 0, (uint32_t)total_units, s, overlap)
                                           : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
         if (rc) return rc;
     } else {

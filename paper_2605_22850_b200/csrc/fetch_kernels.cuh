@@ -50,6 +50,14 @@ __device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_max_release(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Programmatic dependent launch: this CTA will issue no more claims, so a dependent launch (the
+// stream's next fetch, OC_FETCH_OVERLAP) may start claiming from the counter.  No-op otherwise.
+__device__ __forceinline__ void allow_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // Release pattern in two parts: one fence for a group of relaxed reductions.
@@ -124,7 +132,9 @@ __device__ void observe_layers(const DevDesc& d, uint32_t l0, uint32_t l1) {
             ns = min(ns * 2, 256u);
         }
         d.ts[1 + l] = globaltimer();
-        st_release(d.ready, base + l + 1u);
+        // max, not a plain store: with OC_FETCH_OVERLAP the next fetch of this descriptor may
+        // already announce its early layers while this one announces its last ones
+        red_max_release(d.ready, base + l + 1u);
     }
 }
 
@@ -492,9 +502,12 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     if (blockIdx.x == 0) {
         if (BATCH) {
             if (threadIdx.x < 32) observe_batch(ba, t0);
-        } else if (threadIdx.x == 0) {
-            if (g0 == 0 && d0.staged != 1) d0.ts[0] = t0;  // CE engine: stamped when the copies start
-            observe_layers(d0, g0 / d0.units_per_layer, g1 / d0.units_per_layer);
+        } else {
+            allow_dependents();  // the observer never claims
+            if (threadIdx.x == 0) {
+                if (g0 == 0 && d0.staged != 1) d0.ts[0] = t0;  // CE engine: stamped when the copies start
+                observe_layers(d0, g0 / d0.units_per_layer, g1 / d0.units_per_layer);
+            }
         }
         return;
     }
@@ -503,17 +516,21 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     const uint32_t lane = threadIdx.x & 31;
     const bool tr = !BATCH && d0.trace != nullptr;  // ramp trace (measurement support)
     if (tr && threadIdx.x == 0) d0.trace[blockIdx.x * kTraceSlots + 0] = t0;
-    if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < stages; s++) mbar_init(&bars[s], 1);
-        for (uint32_t f = 0; f < kFifo; f++) {
-            mbar_init(&fifo_full[f], 1);
-            mbar_init(&fifo_empty[f], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // kSingle: the first unit is static (below); start the load of its source address now, so its
+    // latency overlaps the barrier set-up
+    const uint8_t* src0 = (MODE == kSingle && threadIdx.x == 0) ? unit_src(d0, unit_geo(d0, g0 + blockIdx.x - 1))
+                                                                 : nullptr;
+    // barriers: one per thread (stages <= 16 ring slots, 2 * kFifo FIFO slots)
+    if (threadIdx.x < stages) mbar_init(&bars[threadIdx.x], 1);
+    if (threadIdx.x < kFifo) {
+        mbar_init(&fifo_full[threadIdx.x], 1);
+        mbar_init(&fifo_empty[threadIdx.x], 1);
     }
+    // the inits (generic proxy) before the TMA's complete_tx (async proxy); no cluster peers
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (tr && threadIdx.x == 0) trace_stamp(d0, 1);
     if (threadIdx.x >= 32) {  // ---- signaler warp
+        if (!BATCH) allow_dependents();  // it never claims
         if (threadIdx.x != 32) return;
         // Each round takes every record already in the FIFO (waiting only for the first), merges
         // records of the same (request, layer), then publishes them with ONE GPU-scope release
@@ -572,7 +589,17 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     // The claim for the next unit is issued one claim ahead, so the atomic's round trip (~1 us)
     // overlaps a unit's copy instead of stalling the issue loop -- with a small copy-CTA budget
     // that latency would otherwise cap each CTA at one unit per round trip.
-    uint32_t next_raw = lane == 0 ? atomicAdd(claim_ctr, 1u) : 0u;
+    // kSingle: copy CTA b's first unit is g0 + b - 1 (the host sizes the grid to at most the
+    // launch's units), so the first load goes out without a claim round trip; later claims come
+    // from the counter, which maps value c to unit g0 + copy CTAs + (c - grab_base).
+    // kRampStatic2: the first layer's remainder goes to CTAs 1..extra as static second units, and
+    // the counter then starts after them.
+    const uint32_t copy_ctas = gridDim.x - 1;
+    const uint32_t cta_i = blockIdx.x - 1u;
+    const uint32_t extra = (MODE == kSingle && (d0.ramp & kRampStatic2))
+                               ? ramp_extra(g0, g1, d0.units_per_layer, copy_ctas) : 0u;
+    const bool static2 = extra != 0 && cta_i < extra;
+    uint32_t next_raw = (lane == 0 && MODE != kSingle) ? atomicAdd(claim_ctr, 1u) : 0u;
     if (tr && lane == 0) trace_stamp(d0, 2);
     // kWdrr: the entry being consumed (lane 0) and the launch's common start time
     uint32_t cur_req = 0, cur_next = 0, cur_left = 0, cur_rel = 0;
@@ -624,13 +651,27 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
                 req = rs.req;
             }
         } else if (!exhausted) {
-            // Each copy CTA stops after its first claim past g1: a launch advances the counter by
-            // exactly (units + copy CTAs), so the host knows the next launch's grab_base.
-            const uint32_t gg = g0 + (next_raw - grab_base);
+            // Each copy CTA stops after its first counter claim past g1.  kSingle: the static first
+            // units plus one overshoot per CTA -- the counter advances by exactly the launch's
+            // units; batches: by (units + copy CTAs).  The host knows the next launch's grab_base.
+            uint32_t gg;
+            bool take_next = true;  // issue the next counter claim (one ahead)
+            if (MODE == kSingle) {
+                if (k == 0) {
+                    gg = g0 + cta_i;
+                } else if (k == 1 && static2) {
+                    gg = g0 + copy_ctas + cta_i;
+                    take_next = false;  // the claim issued at k = 0 is still ahead
+                } else {
+                    gg = g0 + copy_ctas + extra + (next_raw - grab_base);
+                }
+            } else {
+                gg = g0 + (next_raw - grab_base);
+            }
             if (gg >= g1) {
                 exhausted = true;
             } else {
-                next_raw = atomicAdd(claim_ctr, 1u);
+                if (take_next) next_raw = atomicAdd(claim_ctr, 1u);
                 const Resolved rs = resolve<MODE>(d0, ba, gg, seg_cache);
                 g = rs.g;
                 req = rs.req;
@@ -647,7 +688,7 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         const uint32_t bytes = (uint32_t)(u.nrows * d.row);
         const uint32_t s = k % stages;
         mbar_expect_tx(&bars[s], bytes);
-        bulk_load(buf + (size_t)s * stage_bytes, unit_src(d, u), bytes, &bars[s]);
+        bulk_load(buf + (size_t)s * stage_bytes, (MODE == kSingle && k == 0) ? src0 : unit_src(d, u), bytes, &bars[s]);
     };
     // kSingle: minimal pacer, layer l released at t0 + l * pace.  kWdrr: the entry's
     // release time after the launch's start (Alg. A2 line 6, reading c22).
@@ -684,16 +725,25 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         pend_cnt++;
     };
 
+    // Prologue: units 0 .. stages-2 (plus a static second unit with a 2-stage ring).
+    const uint32_t prologue = max(stages - 1u, static2 ? 2u : 1u);
+    uint32_t issued = 0;  // units claimed and loaded so far (warp-uniform after the shuffle)
     if (lane == 0)
-        for (uint32_t k = 0; k + 1 < stages; k++) {
+        for (uint32_t k = 0; k < prologue; k++) {
             if (!claim(k)) break;
             if (paced)
                 while (globaltimer() < release_time(k)) __nanosleep(2000);
             issue_load(k);
+            issued++;
             if (tr && k == 0) trace_stamp(d0, 3);
         }
+    issued = __shfl_sync(0xffffffffu, issued, 0);
     __syncwarp();
+    // kRampFirstLayer: the launch's first layer (kSingle)
+    const uint32_t first_layer = MODE == kSingle ? fdiv(g0, d0.div_upl) : 0u;
+    const bool first_layer_hold = MODE == kSingle && !paced && (d0.ramp & kRampFirstLayer);
 
+    bool triggered = false;    // allow_dependents() issued (warp-uniform)
     uint32_t next_retire = 0;  // first unit not yet retired (same value in every lane)
     uint32_t k = 0;
     for (;; k++) {
@@ -702,12 +752,30 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         const DevDesc& d = desc_of(k);
         const uint32_t s = k % stages;
         const UnitGeo u = unit_geo(d, g);
+        // Row-contiguous targets with units of <= 32 rows (32 KiB at Llama layouts): lane r's
+        // destination run is computed while the unit's load is still in flight, so the block-table
+        // and base loads do not delay the stores.  Lane r owns row r if row r starts a run: the
+        // unit's first row, a block's first slot, or the first V row; a run ends at the next one.
+        const bool lane_rows = d.nhd && u.nrows <= 32;
+        uint64_t run_dst = 0;
+        uint32_t run_bytes = 0;
+        if (lane_rows && lane < u.nrows) {
+            const uint32_t q = u.q0 + lane;
+            uint32_t slot;
+            const uint64_t dst = row_addr(d, u.layer, u.j, q, &slot);
+            if (lane == 0 || slot == 0 || q == d.G) {
+                uint32_t len = min(u.nrows - lane, d.Bs - slot);
+                if (q < d.G) len = min(len, d.G - q);
+                run_dst = dst;
+                run_bytes = (uint32_t)(len * d.row);
+            }
+        }
         mbar_wait(&bars[s], (k / stages) & 1u);
         if (tr && k == 0 && lane == 0) trace_stamp(d0, 4);
         const uint8_t* sbuf = buf + (size_t)s * stage_bytes;
-        if (d.nhd) {
-            // Lane r owns row r if row r starts a run: the unit's first row, a block's first slot,
-            // or the first V row.  A run ends at the next such row.
+        if (lane_rows) {
+            if (run_bytes) bulk_store(run_dst, sbuf + (size_t)lane * d.row, run_bytes);
+        } else if (d.nhd) {
             for (uint32_t r = lane; r < u.nrows; r += 32) {
                 const uint32_t q = u.q0 + r;
                 uint32_t slot;
@@ -734,10 +802,39 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         bulk_wait_read<1>();  // unit k-1's stage is free once its stores have read shared memory
         __syncwarp();
         const uint32_t kl = k + stages - 1;  // next unit to load, into unit k-1's stage
+        const bool need = kl >= issued;      // not already loaded by the prologue
         uint32_t got = 0;
-        if (lane == 0) got = claim(kl) ? 1u : 0u;
+        if (need && lane == 0) got = claim(kl) ? 1u : 0u;
         got = __shfl_sync(0xffffffffu, got, 0);
-        if (got) {
+        if (need && !got && !triggered) {  // this CTA's claims are over: a dependent launch may start
+            allow_dependents();
+            triggered = true;
+        }
+        if (need && got) {
+            issued++;
+            if (first_layer_hold && u.layer == first_layer) {
+                // the first layer is complete in this CTA before any later layer's load goes out
+                const uint32_t ln = lane == 0 ? fdiv(s_unit[kl % 32], d.div_upl) : 0u;
+                if (__shfl_sync(0xffffffffu, ln, 0) != first_layer) {
+                    bulk_wait<0>();
+                    fence_proxy_async_global();
+                    __syncwarp();
+                    if (lane == 0) {
+                        for (uint32_t r = next_retire; r <= k; r++) retire(r);
+                        // Publish the first layer's units from this warp, not through the signaler:
+                        // no loads or stores of this CTA are in flight now (and the other CTAs of
+                        // the SM are at the same point), so the GPU-scope release is cheap; the
+                        // signaler's fence would queue behind the next layer's traffic.
+                        if (tr) trace_stamp(d0, 1);
+                        if (pend_cnt) {
+                            red_add_release(&d0.unit_cnt[pend_layer], pend_cnt);
+                            pend_cnt = 0;
+                        }
+                        if (tr) trace_stamp(d0, 6);
+                    }
+                    next_retire = k + 1;
+                }
+            }
             if (paced) {
                 uint32_t hold = lane == 0 ? (globaltimer() < release_time(kl) ? 1u : 0u) : 0u;
                 hold = __shfl_sync(0xffffffffu, hold, 0);

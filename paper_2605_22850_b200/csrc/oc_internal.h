@@ -161,7 +161,23 @@ struct DevDesc {
     FastDiv div_Bs;
     FastDiv div_hdv;          // (d*p)/16
     uint64_t* trace;          // measurement support (OC_TRACE=1): per-CTA ramp stamps, else null
+    uint32_t ramp;            // kRampStatic2 | kRampFirstLayer (single-descriptor BULK launches)
 };
+// First-layer ramp of a single-descriptor BULK launch (fetch_kernels.cuh):
+//   kRampStatic2     the first layer's units beyond one per copy CTA are also assigned statically
+//                    (CTA b's second unit), so the whole first layer is loaded at once
+//   kRampFirstLayer  a CTA retires its first-layer units before it loads a later layer's unit, so
+//                    the first layer's completion is not queued behind the next layer's traffic
+constexpr uint32_t kRampStatic2 = 1, kRampFirstLayer = 2;
+// Units a launch of units [g0, g1) assigns statically as second units (kRampStatic2): the first
+// layer's remainder beyond the copy CTAs' first units, at most one per CTA.
+inline __host__ __device__ uint32_t ramp_extra(uint32_t g0, uint32_t g1, uint32_t upl, uint32_t copy_ctas) {
+    const uint64_t layer_end = ((uint64_t)(g0 / upl) + 1) * upl;
+    const uint32_t first_end = layer_end < g1 ? (uint32_t)layer_end : g1;
+    const uint32_t base2 = g0 + copy_ctas;
+    if (first_end <= base2) return 0u;
+    return first_end - base2 < copy_ctas ? first_end - base2 : copy_ctas;
+}
 constexpr uint32_t kTraceSlots = 8;     // stamps per CTA (fetch_kernels.cuh, bulk engine)
 constexpr uint32_t kTraceCtas = 2048;   // CTAs traced per launch
 

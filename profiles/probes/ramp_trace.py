@@ -11,8 +11,8 @@ import paper_2605_22850_b200 as oc, synth
 lay = synth.LLAMA3_8B.as_tuple()
 L, G, Bs = lay[0], lay[4], 16
 row, S, chunk = oc.geometry(lay)
-names = ["cta_start", "bar_init", "claim1", "load1_issued", "unit1_in_smem", "stores1_issued",
-         "retire1_pushed", "signal1_published"]
+names = ["cta_start", "first_layer_retired", "claim1", "load1_issued", "unit1_in_smem", "stores1_issued",
+         "first_layer_released", "signal1_published"]
 out = {}
 for N in (256, 224):
     store = oc.Store(lay, capacity=4 * N)
@@ -41,7 +41,7 @@ for N in (256, 224):
         d.fetch_layerwise(s)
         s.synchronize()
         t = d.layer_times().astype(np.int64)
-        tr = oc.trace_read().astype(np.int64)
+        tr = oc.trace_read().astype(np.int64) if os.environ.get("OC_TRACE") == "1" else np.zeros((2048, 8), np.int64)
         live = tr[1:][tr[1:, 0] > 0]
         rel = np.where(live > 0, live - t[0], -1)
         rows.append(rel)
@@ -63,6 +63,14 @@ for N in (256, 224):
     s.synchronize()
     res["b2b_us_per_fetch"] = round(a.elapsed_time(b) * 1e3 / 20, 2)
     res["b2b_TBps"] = round(2 * N * S * L * 20 / (a.elapsed_time(b) / 1e3) / 1e12, 3)
+    for _ in range(2):   # OC_FETCH_OVERLAP: each launch overlaps the previous one's tail
+        a.record(s)
+        for i in range(40):
+            descs[i % 4].fetch_layerwise(s, overlap=True)
+        b.record(s)
+        s.synchronize()
+    res["b2b_overlap_us_per_fetch"] = round(a.elapsed_time(b) * 1e3 / 40, 2)
+    res["b2b_overlap_TBps"] = round(2 * N * S * L * 40 / (a.elapsed_time(b) / 1e3) / 1e12, 3)
     out[f"N{N}"] = res
     for d in descs:
         d.close()
