@@ -1,41 +1,32 @@
 """Benchmark of the ObjectCache hot path on B200 (contract: one JSON line on rank 0).
 
 Workload (BASELINE.json configs[1]): Llama-3-8B KV layout (32 layers, 8 KV heads, d = 128, bf16),
-one request with a 4K-token prefix hit (N = 256 chunks of G = 16 tokens), delivered into a
-fragmented vLLM-style paged cache (Bs = 16, NHD).  A step is one whole fetch_layerwise of the
-request: the layer-major gather + paged scatter of all 32 layers (Alg. A1), the layers
-announced in order, and the consumer stream waiting on the last announcement.  Four independent
-request sets (own chunks, own cache) rotate so that consecutive steps touch 4 GiB > L2.
+one request per step with a 4K-token prefix hit (N = 256 chunks of G = 16 tokens), delivered into
+a fragmented vLLM-style paged cache (Bs = 16, NHD): the layer-major gather + paged scatter of all
+32 layers (Alg. A1), announced layer by layer; details in benchlib/headline.py.
 
-  value      (read + write) HBM bytes of the fetch / device time, all ranks (weak scaling)
-  e2e        same metric through the public API with the chunk store in pinned HOST memory:
-             per step match_prefix + build_descriptor + fetch (GPU reads the host slab over
-             PCIe) + waits + D2H of the layer-ready stamps, wall clock
-  roofline   dominant kernel (fetch_bulk_kernel): algorithmic bytes per launch / mean
-             launch time from CUDA events on the copy stream, vs MEASURED_PEAKS.json hbm_gbs
-  stall      added TTFT (ms) over the compute windows of Table A5 (4K and 64K, 87.5% hit)
+  value         read + write HBM bytes (2*N*S*L per step) / device time of the timed region, whole
+                job (every rank fetches its own requests: weak scaling), max over ranks
+  roofline      the fetch kernel (fetch_bulk_kernel<0>): the same bytes / the copy stream's span
+                over the K launches, vs MEASURED_PEAKS.json hbm_gbs
+  e2e           the same metric through the public C-ABI calls, HBM tier (match -> build (H2D of the
+                descriptor) -> fetch -> wait -> D2H of the layer stamps), pipelined; `pcie_tier`
+                inside it: the pinned-host store, in PCIe GB/s
   cpu_baseline  the oracle (tests-only CPU code) on a bounded sample, 1 core
+  legs          stall (added TTFT at 4K/64K), config3 (64K hit, verified), config5 (mixed requests
+                over the job's GPUs, strong scaling, NVLink peer reads, verified); optional legs by flag
 
 --impl reference runs the oracle itself as the reference arm (rank 0 only).
 """
 import argparse
 import json
 import os
-import statistics
-import subprocess
 import sys
-import threading
-import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-
-METRIC = "layerwise KV gather+scatter GB/s vs HBM peak; added per-layer stall ms at 4K/64K"
-UNIT = "GB/s"
-N_CHUNKS_4K = 256
-ROTATE = 4
+from benchlib.common import METRIC, UNIT, bench_config, dist_env  # noqa: E402
 
 
 def parse():
@@ -46,228 +37,39 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--mode", default="persistent", choices=["persistent", "per_layer"])
     p.add_argument("--engine", default="bulk", choices=["bulk", "ldst"])
+    p.add_argument("--no-overlap", action="store_true", help="headline launches in plain stream order "
+                   "(no OC_FETCH_OVERLAP)")
     p.add_argument("--no-stall", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-config3", action="store_true", help="skip BASELINE config 3 (64K-token hit, 8 GiB)")
+    p.add_argument("--no-config5", action="store_true", help="skip config 5 (mixed requests over the job's GPUs)")
     p.add_argument("--stall64k", type=int, default=1)
-    p.add_argument("--profile", action="store_true", help="no soak / clock sampling (for ncu runs)")
-    p.add_argument("--corun", action="store_true", help="fetches co-running with a bf16 GEMM stream: both "
-                   "throughputs vs the copy-CTA budget (adds a 'corun' object)")
-    p.add_argument("--no-granularity", action="store_true", help="skip the G = 16/64/256 sweep and the "
-                   "unfused gather->flat->scatter comparison")
-    p.add_argument("--serve", type=int, default=0, help="config 5 on one GPU: this many mixed 4K/64K requests "
-                   "streaming through a bounded paged pool with FIFO block admission")
-    p.add_argument("--no-offload", action="store_true", help="skip the offload (put_from_paged) leg")
-    p.add_argument("--no-config3", action="store_true", help="skip BASELINE config 3 (64K-token hit, 8 GiB: "
-                   "HBM store vs pinned-host store with SM zero-copy and copy-engine paths)")
-    p.add_argument("--p2p", action="store_true", help="N>1: cross-GPU leg (every rank fetches a 4K request "
-                   "whose chunks live on the next rank's GPU: CUDA IPC import, NVLink P2P reads by the same "
-                   "kernel); opt-in because it has only been run with peers sharing one GPU")
-    p.add_argument("--sensitivity", action="store_true", help="Fig. 14 analog: TTFT increase at a 10 Gbps vs "
-                   "100 Gbps cap, layerwise vs chunkwise, Table A5 cells")
-    p.add_argument("--crossover", action="store_true", help="Eq. 2 / Fig. 13 analog: layerwise vs chunkwise "
-                   "added TTFT over 1K-64K contexts, HBM and pinned-host tiers")
-    p.add_argument("--sweep", action="store_true", help="rate sweep (Fig. 15 analog): added TTFT of one "
-                   "paced request vs rate / r*, against Eq. 3 (adds a 'sweep' object)")
-    p.add_argument("--pool", type=int, default=0, help="streaming multi-tenant runtime: this many requests "
-                   "arrive over time (Poisson) into oc.TenantPool epochs (100 ms) under a shared cap, per policy "
-                   "and dispatch (adds a 'pool' object)")
-    p.add_argument("--stall-gemm", action="store_true", help="added TTFT with real per-layer prefill compute: "
-                   "each layer's miss tokens through the four projection GEMMs of a Llama-3-8B layer (random "
-                   "bf16 weights) on the consumer stream, instead of timer spins (adds a 'stall_gemm' object)")
-    p.add_argument("--hash", type=int, default=0, help="chain keys of this many 4K-token requests: one GPU launch "
-                   "(oc_chunk_keys_batch) vs the host's SHA-extension loop (adds a 'hash' object)")
-    p.add_argument("--batch", default="", help="NxM: N 4K-token + M 64K-token concurrent requests (config 5, "
-                   "one GPU): one batched launch vs per-request launches (adds a 'batch' object)")
-    p.add_argument("--sched", default="", help="comma list of paper scheduler workloads to run (A,B,C): "
-                   "concurrent paced fetches under a shared cap, per policy (adds a 'sched' object)")
+    p.add_argument("--profile", action="store_true", help="headline only, no soak / clock sampling (ncu runs)")
+    p.add_argument("--stall-gemm", action="store_true", help="added TTFT with real prefill (GEMMs + attention)")
+    p.add_argument("--stall-gemm-hbm-only", action="store_true")
+    p.add_argument("--sched", default="", help="comma list of scheduler workloads (A,B,C,70B; 70B = config 4)")
+    p.add_argument("--corun", action="store_true")
+    p.add_argument("--granularity", action="store_true", help="G = 16/64/256 and the unfused flow")
+    p.add_argument("--serve", type=int, default=0, help="old weak-scaling serving leg with this many requests")
+    p.add_argument("--offload", action="store_true")
+    p.add_argument("--p2p", action="store_true")
+    p.add_argument("--sensitivity", action="store_true")
+    p.add_argument("--crossover", action="store_true")
+    p.add_argument("--sweep", action="store_true")
+    p.add_argument("--pool", type=int, default=0)
+    p.add_argument("--hash", type=int, default=0)
+    p.add_argument("--batch", default="")
     return p.parse_args()
 
 
-# ---- shared helpers ---------------------------------------------------------------------------------
-def peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    try:
-        with open(path) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
-    except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
-
-
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except Exception:
-        return None
-
-
-class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 50 ms while running."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index):
-        self.index = index
-        self.rows = []
-        self.proc = None
-
-    def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
-    def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4)
-                          if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
-
-
-def in_harness_copy(torch, dev, stream, nbytes):
-    """Read+write GB/s of a plain device-to-device copy_ of nbytes (the MEASURED_PEAKS method, run
-    in this process under this run's clocks)."""
-    src = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    dst = torch.empty_like(src)
-    ts = []
-    with torch.cuda.stream(stream):
-        src.fill_(1)
-        for i in range(23):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            dst.copy_(src)
-            b.record(stream)
-            if i >= 3:
-                ts.append((a, b))
-    stream.synchronize()
-    ms = statistics.median(a.elapsed_time(b) for a, b in ts)
-    del src, dst
-    torch.cuda.empty_cache()
-    return 2 * nbytes / (ms / 1e3) / 1e9
-
-
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
-# ---- the reference arm: the oracle, timed on host cores ---------------------------------------------
-class OracleWorkload:
-    """The oracle's Alg. A1 gather + paged scatter on one seeded request (setup untimed)."""
-
-    def __init__(self, seed, n_chunks, lay):
-        import synth
-        from oracle import keys as okeys
-        from oracle.descriptor import PagedTarget, build_descriptor
-        from oracle.geometry import chunk_bytes, chunk_layer_bytes, row_bytes, head_bytes
-        from oracle.store import ChunkStore
-        G = lay.chunk_tokens
-        (t,), (ids,) = synth.family_streams(seed, G, 0, [n_chunks])
-        keys = okeys.chunk_keys(t, G)
-        self.st = ChunkStore(lay)
-        self.st.put(keys, synth.payloads(seed, ids, chunk_bytes(lay)))
-        row, self.S, Bs = row_bytes(lay), chunk_layer_bytes(lay), 16
-        need = -(-n_chunks * G // Bs)
-        pool = need + need // 4
-        bt = synth.block_table(seed, need, pool).tolist()
-        per_kv = pool * Bs * row
-        k = [l * 2 * per_kv for l in range(lay.num_layers)]
-        tgt = PagedTarget(k, [x + per_kv for x in k], Bs * row, row, head_bytes(lay), Bs, bt, 0)
-        self.dst = synth.sentinel(lay.num_layers * 2 * per_kv)
-        self.desc = build_descriptor(self.st, keys, lay, tgt)
-        self.n = n_chunks
-
-    def run(self, layers):
-        """Returns (algorithmic read+write bytes, seconds)."""
-        from oracle.assemble import gather_layer, scatter_paged
-        t0 = time.perf_counter()
-        for l in layers:
-            scatter_paged(gather_layer(self.st, self.desc, l), l, self.desc, self.dst)
-        return 2 * self.n * self.S * len(layers), time.perf_counter() - t0
-
-
-def cores_used():
-    try:
-        return len(os.sched_getaffinity(0)), os.cpu_count()
-    except Exception:
-        return 1, os.cpu_count()
-
-
-def bench_config(args, lay_t, ws):
-    """The N=1 workload (BASELINE configs[1]) -- shared by both arms so their lines compare."""
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    return {"workload": "llama3-8b KV layout, single request, 4K-token prefix hit (N=256 x G=16), "
-                        "paged NHD cache Bs=16 fragmented",
-            "layout": {"L": L, "n_kv": lay_t[1], "d": lay_t[2], "p": lay_t[3], "G": G, "Bs": Bs},
-            "fetch_mode": args.mode, "engine": args.engine, "tier": "hbm",
-            "l2": f"inputs larger than L2: {ROTATE} rotating request sets, "
-                  f"{ROTATE * 2 * N_CHUNKS_4K * 2 * G * lay_t[1] * lay_t[2] * lay_t[3] * L / 2**30:.1f} GiB "
-                  "touched per rotation",
-            "parallelism": f"replicas x{ws} (independent requests per GPU, no collective)"}
-
-
-def run_reference(args):
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return
-    import synth
-    from oracle.geometry import Layout
-    lay = Layout(*synth.LLAMA3_8B.as_tuple())
-    # one step = one layer of the full 4K request (N = 256 chunks: 16 MiB read + 16 MiB written)
-    wl = OracleWorkload(1, N_CHUNKS_4K, lay)
-    for i in range(args.warmup):
-        wl.run([i % lay.num_layers])
-    tot_b, tot_s = 0, 0.0
-    for i in range(args.steps):
-        b, s = wl.run([i % lay.num_layers])
-        tot_b += b
-        tot_s += s
-    v = tot_b / tot_s / 1e9
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": bench_config(args, synth.LLAMA3_8B.as_tuple(), ws),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} steps, each one layer of the 4K request (256 chunks, G=16, "
-                                   "Bs=16): Alg. A1 gather + paged scatter, single-threaded numpy"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
-
-
-# ---- our arm ------------------------------------------------------------------------------------------
 def main_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2605_22850_b200 as oc
     import synth
+    from benchlib import configs, e2e, extra, headline, reference, stall
 
     ws, rank, local = dist_env()
     # OC_BENCH_DIST_BACKEND=gloo lets several ranks share one GPU to exercise the N>1 code path
@@ -281,167 +83,71 @@ def main_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    mode = oc.FETCH_PERSISTENT if args.mode == "persistent" else oc.FETCH_PER_LAYER
-    engine = oc.COPY_BULK if args.engine == "bulk" else oc.COPY_LDST
-    fopts = {"mode": mode, "engine": engine}
     lay_t = synth.LLAMA3_8B.as_tuple()
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    N = N_CHUNKS_4K
-
-    def make_sets(tier, store_cap):
-        store = oc.Store(lay_t, capacity=store_cap, tier=tier, device=local)
-        sets = []
-        for r in range(ROTATE):
-            (tok,), (ids,) = synth.family_streams(1000 * rank + r, G, 0, [N])
-            keys = oc.chunk_keys(tok, G)
-            pl = torch.from_numpy(synth.payloads(1000 * rank + r, ids, chunk))
-            store.put_chunks(keys, pl if tier == oc.TIER_PINNED_HOST else pl.to(dev))
-            need = N * G // Bs
-            pool = need + need // 4
-            bt = synth.block_table(77 + r, need, pool)
-            cache = torch.empty((L, 2, pool, Bs, row), dtype=torch.uint8, device=dev)
-            per_kv = pool * Bs * row
-            base = cache.data_ptr()
-            kb = [base + l * 2 * per_kv for l in range(L)]
-            tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs, bt, 0)
-            sets.append((tok, keys, tgt, cache))
-        return store, sets
-
-    store, sets = make_sets(oc.TIER_HBM, ROTATE * N)
-    descs = [oc.build_descriptor(store, k, lay_t, t) for (_, k, t, _) in sets]
-    copy_s = torch.cuda.Stream(device=dev)
-    cons_s = torch.cuda.Stream(device=dev)
-    bytes_per_step = 2 * N * S * L                    # read + write
-
-    def step(i, ev_pair=None):
-        d = descs[i % ROTATE]
-        if ev_pair:
-            ev_pair[0].record(copy_s)
-        d.fetch_layerwise(copy_s, **fopts)
-        if ev_pair:
-            ev_pair[1].record(copy_s)
-        # The consumer waits on the last layer: layers are announced strictly in order, so this
-        # completes after every layer's ready signal.  (Per-layer waits interleaved with compute
-        # are exercised by the stall leg; one wait op per layer costs ~6 us of host time here.)
-        d.wait_layer(L - 1, cons_s)
-
-    clocks = ClockSampler(local)
-    if not args.profile:
-        clocks.start()
-        time.sleep(0.3)
-    for i in range(args.warmup):
-        step(i)
-    t_soak = time.perf_counter()
-    i = 0
-    while not args.profile and time.perf_counter() - t_soak < 1.0:   # keep the GPU loaded while sampling
-        step(i)
-        i += 1
-        if i % 64 == 0:
-            torch.cuda.synchronize()
-    torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_start.record(copy_s)
-    for i in range(args.steps):
-        step(i, evs[i])
-    t_end.record(cons_s)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    launch_ms = [a.elapsed_time(b) for a, b in evs]
-    if ws > 1:
-        t = torch.tensor([elapsed_ms], device=dev if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)                # max over ranks
-        elapsed_ms = float(t.item())
-    ms_per_step = elapsed_ms / args.steps
-    value = ws * bytes_per_step * args.steps / (elapsed_ms / 1e3) / 1e9
-    peak, peak_src = peaks()
-    mean_launch_ms = statistics.mean(launch_ms)
-    achieved = bytes_per_step / (mean_launch_ms / 1e3) / 1e9
-    harness_copy = in_harness_copy(torch, dev, copy_s, bytes_per_step // 2) if not args.profile else None
-
+    head = headline.run(args, oc, torch, dev, lay_t, ws, rank, dist, backend)
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8", "data": "synthetic (seeded PCG64 chunk bytes, Llama-3 vocab tokens)",
-        "config": bench_config(args, lay_t, ws),
-        "kv_delivered_GBps": value / 2,
-        "frac_of_spec_8TBps": value / 8000.0,
-        # SURVEY 8(d) second denominator: a device-to-device torch copy_ of the step's size, timed here
-        "in_harness_copy": None if harness_copy is None else {
-            "GBps": round(harness_copy, 1), "kernel_frac": round(achieved / harness_copy, 4),
-            "value_frac": round(value / ws / harness_copy, 4),
-            "method": "torch copy_ of %d MiB device to device on the copy stream, read + write counted, "
-                      "median of 20 after 3 warm-ups" % (bytes_per_step // 2 >> 20)},
-        "launch_us": {q: float(np.percentile(launch_ms, p)) * 1e3 for q, p in (("p10", 10), ("p50", 50), ("p90", 90))},
-        "gpu_launches": args.steps * (1 if mode == oc.FETCH_PERSISTENT else L),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(), "peak_source": peak_src,
-                     "kernel": ("fetch_bulk_kernel" if engine == oc.COPY_BULK else
-                                "fetch_persistent_kernel" if mode == oc.FETCH_PERSISTENT else "fetch_layer_kernel"),
-                     "bytes_per_launch": bytes_per_step if mode == oc.FETCH_PERSISTENT else bytes_per_step // L,
-                     "mean_launch_us": mean_launch_ms * 1e3 if mode == oc.FETCH_PERSISTENT
-                     else mean_launch_ms * 1e3 / L},
-        "clocks": clk,
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded PCG64 chunk bytes, Llama-3 vocab tokens)",
+        "config": dict(bench_config(args, lay_t, ws), launch=head["launch"]),
+        "gpu_launches": head["gpu_launches"], "roofline": head["roofline"], "clocks": head["clocks"],
+        "kernel": {k: head[k] for k in ("isolated_launch_us", "X0_us_isolated", "in_harness_copy", "verified")},
     }
-    for d in descs:
-        d.close()
-    del sets
-    store.close()
-    torch.cuda.empty_cache()
-
-    if not args.no_e2e:                            # every rank: the whole job's end-to-end rate
-        # the pinned-host tier's best engine: copy-engine transfers into an HBM stage + scatter
-        e2e = e2e_leg(args, oc, torch, dev, lay_t, {"engine": oc.COPY_CE}, ws, backend)
-        e2e_sm = e2e_leg(args, oc, torch, dev, lay_t, fopts, ws, backend)
+    legs = {}
+    if not args.no_e2e and not args.profile:
+        e = e2e.hbm_tier(args, oc, torch, dev, lay_t, ws, rank, dist, backend)
+        e["pcie_tier"] = e2e.pcie_tier(args, oc, torch, dev, lay_t, {"engine": oc.COPY_CE}, ws, backend)
         if rank == 0:
-            e2e["sm_zero_copy"] = {"value": e2e_sm["value"], "ms_per_step": e2e_sm["ms_per_step"],
-                                   "tier": e2e_sm["tier"]}
-            out["e2e"] = e2e
-    if rank == 0 and args.sched:
-        out["sched"] = sched_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and args.batch:
-        out["batch"] = batch_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and args.stall_gemm:
-        out["stall_gemm"] = stall_gemm_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and args.hash:
-        out["hash"] = hash_leg(args, oc, torch, dev)
-    if rank == 0 and args.pool:
-        out["pool"] = pool_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and not args.no_granularity and not args.profile:
-        out["granularity"] = granularity_leg(args, oc, torch, dev, lay_t, fopts)
-    if ws > 1 and args.p2p:                        # every rank: chunks homed on the next GPU (a11)
-        res = p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
-        if rank == 0:
-            out["p2p"] = res
-    if args.serve:                                 # every rank serves its share (config 5)
-        res = serve_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
-        if rank == 0:
-            out["serve"] = res
-    if rank == 0 and not args.no_offload and not args.profile:
-        out["offload"] = offload_leg(args, oc, torch, dev, lay_t)
+            e["frac_of_value"] = round(e["value"] / head["value"], 4)
+            out["e2e"] = e
+    if rank == 0 and not args.no_stall and not args.profile:
+        legs["stall"] = stall.stall_leg(args, oc, torch, dev, lay_t, {"engine": oc.COPY_BULK},
+                                        tiers=(("hbm", oc.TIER_HBM), ("pinned_host", oc.TIER_PINNED_HOST),
+                                               ("pinned_host_ce", oc.TIER_PINNED_HOST)), timelines=False)
     if rank == 0 and not args.no_config3 and not args.profile:
-        out["config3"] = config3_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and args.sensitivity:
-        out["sensitivity"] = sensitivity_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and args.crossover:
-        out["crossover"] = crossover_leg(args, oc, torch, dev, lay_t, fopts)
-    if rank == 0 and args.sweep:
-        out["sweep"] = sweep_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and args.corun:
-        out["corun"] = corun_leg(args, oc, torch, dev, lay_t)
-    if rank == 0 and not args.no_stall:
-        out["stall"] = stall_leg(args, oc, torch, dev, lay_t, fopts)
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline_leg()
-        if "config3" in out:   # the oracle's GB/s next to the GPU's for config 3 too
-            out["config3"]["oracle_cpu"] = cpu_config3_leg()
+        legs["config3"] = configs.config3_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and args.stall_gemm:
+        legs["stall_gemm"] = stall.stall_gemm_leg(args, oc, torch, dev, lay_t)
+    if rank == 0 and args.sched:
+        legs["sched"] = configs.sched_leg(args, oc, torch, dev, lay_t)
+    fopts = {"engine": oc.COPY_BULK}
+    for flag, name, fn in (("corun", "corun", lambda: extra.corun_leg(args, oc, torch, dev, lay_t)),
+                           ("granularity", "granularity", lambda: extra.granularity_leg(args, oc, torch, dev, lay_t, fopts)),
+                           ("offload", "offload", lambda: extra.offload_leg(args, oc, torch, dev, lay_t)),
+                           ("sensitivity", "sensitivity", lambda: extra.sensitivity_leg(args, oc, torch, dev, lay_t)),
+                           ("crossover", "crossover", lambda: extra.crossover_leg(args, oc, torch, dev, lay_t, fopts)),
+                           ("sweep", "sweep", lambda: extra.sweep_leg(args, oc, torch, dev, lay_t)),
+                           ("pool", "pool", lambda: extra.pool_leg(args, oc, torch, dev, lay_t)),
+                           ("hash", "hash", lambda: extra.hash_leg(args, oc, torch, dev)),
+                           ("batch", "batch", lambda: extra.batch_leg(args, oc, torch, dev, lay_t))):
+        if rank == 0 and getattr(args, flag):
+            legs[name] = fn()
+    if ws > 1 and args.p2p:
+        res = extra.p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
+        if rank == 0:
+            legs["p2p"] = res
+    if args.serve:
+        res = extra.serve_leg(args, oc, torch, dev, lay_t, ws, rank, backend)
+        if rank == 0:
+            legs["serve"] = res
+    if not args.no_config5 and not args.profile:
+        # a child process group per job (own port): a fault there cannot take this line with it
+        from benchlib import config5
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        if ws > 1:
+            dist.barrier()
+        res = config5.spawn(ws, rank, local)
+        if ws > 1:
+            dist.barrier()
+        if rank == 0:
+            legs["config5"] = res
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
+        out["cpu_baseline"] = reference.cpu_baseline_leg()
+        if "config3" in legs:   # the oracle's GB/s next to the GPU's for config 3 too
+            legs["config3"]["oracle_cpu"] = reference.cpu_config3_leg()
+    if legs:
+        out["legs"] = legs
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -449,1484 +155,10 @@ def main_ours(args):
         print(json.dumps(out), flush=True)
 
 
-def config3_leg(args, oc, torch, dev, lay_t):
-    """BASELINE config 3: Llama-3-8B layout, one request with a 64K-token prefix hit (N = 4096
-    chunks, 8 GiB of KV), from an HBM store and from a pinned-host store (SM zero-copy reads and the
-    copy-engine path), into a fragmented paged cache.  GB/s counts r+w (2*N*S*L) per fetch; the
-    pinned rows also give the PCIe read rate against an in-harness pinned->device copy of 1 GiB."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    N = 65536 // G
-    need = N * G // Bs
-    cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-    per_kv = need * Bs * row
-    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-    tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
-                         synth.block_table(64, need, need), 0)
-    (tok,), _ = synth.family_streams(6464, G, 0, [N])
-    keys = oc.chunk_keys(tok, G)
-    h = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()      # in-harness PCIe reference
-    dd = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
-    best_h2d = 0.0
-    for _ in range(3):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        dd.copy_(h, non_blocking=True)
-        b.record()
-        torch.cuda.synchronize()
-        best_h2d = max(best_h2d, (1 << 30) / a.elapsed_time(b) / 1e6)
-    del h, dd
-    peak, _ = peaks()
-    rw = 2 * N * S * L
-    out = {"workload": f"llama3-8b KV layout, one request, 64K-token prefix hit (N={N}, {N * chunk / 2**30:.0f} GiB)",
-           "h2d_copy_GBps": round(best_h2d, 1)}
-    gen = torch.Generator(device=dev).manual_seed(64)
-    for tier_name, tier, engines in (("hbm", oc.TIER_HBM, (("bulk", oc.COPY_BULK),)),
-                                     ("pinned_host", oc.TIER_PINNED_HOST, (("bulk_zero_copy", oc.COPY_BULK),
-                                                                           ("copy_engine", oc.COPY_CE)))):
-        store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
-        for b0 in range(0, N, 512):
-            pl = torch.randint(0, 256, (512, chunk), dtype=torch.uint8, device=dev, generator=gen)
-            store.put_chunks(keys[b0:b0 + 512], pl)
-            del pl
-        d = oc.build_descriptor(store, keys, lay_t, tgt)
-        s = torch.cuda.Stream(device=dev)
-        for eng_name, eng in engines:
-            d.fetch_layerwise(s, engine=eng)
-            s.synchronize()
-            ms = []
-            for _ in range(3):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(s)
-                d.fetch_layerwise(s, engine=eng)
-                b.record(s)
-                s.synchronize()
-                ms.append(a.elapsed_time(b))
-            t = min(ms)
-            t_ = d.layer_times().astype(np.int64)
-            row_out = {"ms": round(t, 3), "GBps_rw": round(rw / t / 1e6, 1), "X0_ms": round((t_[1] - t_[0]) / 1e6, 4)}
-            if tier == oc.TIER_HBM:
-                row_out["frac_of_hbm_peak"] = round(rw / t / 1e6 / peak, 3)
-            else:
-                row_out["pcie_read_GBps"] = round(rw / 2 / t / 1e6, 1)
-                row_out["frac_of_h2d_copy"] = round(rw / 2 / t / 1e6 / best_h2d, 3)
-            out[f"{tier_name}_{eng_name}"] = row_out
-        d.close()
-        store.close()
-        torch.cuda.empty_cache()
-    del cache
-    torch.cuda.empty_cache()
-    return out
-
-
-def p2p_leg(args, oc, torch, dev, lay_t, ws, rank, backend="nccl"):
-    """SURVEY 8(a) a11 / config 5's cross-GPU reads: rank r's store holds a 4K-token request's
-    chunks in its HBM; the stores are exchanged once (CUDA IPC export blobs over all_gather_object)
-    and rank r fetches the request homed on rank (r+1) mod N into its own paged cache -- the same
-    fused kernel, its TMA loads crossing NVLink.  All ranks fetch concurrently; time = max over
-    ranks of the device time of K fetches.  GB/s counts r+w (2*N*S*L) per fetch; the NVLink
-    ingress per GPU is half of it.  Rank 0 checks two sampled layers byte for byte against the
-    payload regenerated from the peer's seed."""
-    import synth
-    from paper_2605_22850_b200 import dist as odist
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    N = N_CHUNKS_4K
-    seed_of = lambda r: 31000 + r
-    store = oc.Store(lay_t, capacity=N, tier=oc.TIER_HBM, device=dev.index)
-    (tok,), (ids,) = synth.family_streams(seed_of(rank), G, 0, [N])
-    store.put_chunks(oc.chunk_keys(tok, G), torch.from_numpy(synth.payloads(seed_of(rank), ids, chunk)).to(dev))
-    torch.cuda.synchronize()
-    blobs = odist.exchange_blobs(store.export())
-    src_rank = (rank + 1) % ws
-    peer = oc.Store.import_(blobs[src_rank], device=dev.index)
-    local = oc.Store(lay_t, capacity=1, tier=oc.TIER_HBM, device=dev.index)   # resolves through its peer
-    local.attach_peer(peer)
-    (ptok,), (pids,) = synth.family_streams(seed_of(src_rank), G, 0, [N])
-    keys = local.match_prefix(ptok)
-    need = N * G // Bs
-    bt = synth.block_table(55 + rank, need, need + need // 4)
-    cache = torch.empty((L, 2, need + need // 4, Bs, row), dtype=torch.uint8, device=dev)
-    per_kv = cache.shape[2] * Bs * row
-    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-    tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs, bt, 0)
-    d = oc.build_descriptor(local, keys, lay_t, tgt)
-    s = torch.cuda.Stream(device=dev)
-    steps = max(5, min(args.steps, 50))
-    for _ in range(3):
-        d.fetch_layerwise(s)
-    s.synchronize()
-    ok = None
-    if rank == 0:                                   # sampled check of what crossed NVLink
-        pl = synth.payloads(seed_of(src_rank), pids, chunk)
-        slots = bt[np.arange(N * G) // Bs].astype(np.int64) * Bs + np.arange(N * G) % Bs
-        ok = True
-        for l in (0, L - 1):
-            want = pl[:, l * S:(l + 1) * S].reshape(N, 2, G, row)
-            for kv in (0, 1):
-                got = cache[l, kv].reshape(-1, row)[torch.from_numpy(slots).to(dev)].cpu().numpy()
-                ok &= bool(np.array_equal(got, want[:, kv].reshape(N * G, row)))
-    if ws > 1:
-        torch.distributed.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(s)
-    for _ in range(steps):
-        d.fetch_layerwise(s)
-    b.record(s)
-    s.synchronize()
-    ms = odist.max_over_ranks(a.elapsed_time(b), device=dev if backend == "nccl" else None)
-    # in-harness P2P reference: a copy-engine copy of the peer's slab into local HBM (SURVEY 8(d))
-    from cuda.bindings import runtime as cudart
-    pbase, pbytes = peer.slab
-    nb = int(min(pbytes, 1 << 30))
-    scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
-    best = 0.0
-    for _ in range(3):
-        a.record(s)
-        err, = cudart.cudaMemcpyAsync(scratch.data_ptr(), pbase, nb, cudart.cudaMemcpyKind.cudaMemcpyDefault,
-                                      s.cuda_stream)
-        b.record(s)
-        s.synchronize()
-        if err == cudart.cudaError_t.cudaSuccess:
-            best = max(best, nb / a.elapsed_time(b) / 1e6)
-    del scratch
-    d.close()
-    if ws > 1:
-        torch.distributed.barrier()                 # peers done reading before any store goes away
-    local.close()
-    peer.close()
-    store.close()
-    del cache
-    torch.cuda.empty_cache()
-    rw = 2 * N * S * L
-    return {"workload": f"each rank fetches a 4K-token hit (N={N}) homed on the next rank's GPU",
-            "ranks": ws, "steps": steps, "GBps_rw_aggregate": round(ws * rw * steps / ms / 1e6, 1),
-            "nvlink_ingress_GBps_per_gpu": round(rw / 2 * steps / ms / 1e6, 1),
-            "ms_per_fetch_max_over_ranks": round(ms / steps, 4), "rank0_sampled_layers_bit_exact": ok,
-            "p2p_copy_engine_GBps_rank0": round(best, 1),
-            "ingress_frac_of_p2p_copy": round(rw / 2 * steps / ms / 1e6 / best, 3) if best else None,
-            "peers_share_one_gpu": torch.cuda.device_count() < ws}
-
-
-def e2e_leg(args, oc, torch, dev, lay_t, fopts, ws=1, backend="nccl"):
-    """Public API end to end with the chunk store in pinned host memory (wall clock)."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    N = N_CHUNKS_4K
-    store = oc.Store(lay_t, capacity=ROTATE * N, tier=oc.TIER_PINNED_HOST, device=dev.index)
-    reqs = []
-    for r in range(ROTATE):
-        (tok,), (ids,) = synth.family_streams(500 + r, G, 0, [N])
-        store.put_chunks(oc.chunk_keys(tok, G), synth.payloads(500 + r, ids, chunk))
-        need = N * G // Bs
-        pool = need + need // 4
-        bt = synth.block_table(91 + r, need, pool)
-        cache = torch.empty((L, 2, pool, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = pool * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs, bt, 0)
-        reqs.append((tok, tgt, cache))
-    copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    stamps = torch.empty(L + 1, dtype=torch.int64).pin_memory()
-
-    def one(i):
-        tok, tgt, _ = reqs[i % ROTATE]
-        keys = store.match_prefix(tok)                       # host: SHA-256 chain + probe
-        d = oc.build_descriptor(store, keys, lay_t, tgt)     # host: resolve + one H2D upload
-        d.fetch_layerwise(copy_s, **fopts)                 # GPU reads host slab over PCIe
-        for l in range(L):
-            d.wait_layer(l, cons_s)
-        stamps.numpy()[:] = d.layer_times().astype(np.int64)  # D2H of the result (layer-ready stamps)
-        d.close()
-
-    steps = max(4, min(args.steps, 40))
-    for i in range(min(3, args.warmup) + 1):
-        one(i)
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for i in range(steps):
-        one(i)
-    torch.cuda.synchronize()
-    secs = time.perf_counter() - t0
-    if ws > 1:                                      # whole job: all ranks' bytes / the slowest rank
-        from paper_2605_22850_b200 import dist as odist
-        secs = odist.max_over_ranks(secs, device=dev if backend == "nccl" else None)
-    store.close()
-    del reqs
-    torch.cuda.empty_cache()
-    bytes_per_step = 2 * N * S * L
-    desc_bytes = N * 8 + 2 * L * 8 + (N * G // Bs + N * G // Bs // 4) * 4
-    return {"value": ws * bytes_per_step * steps / secs / 1e9, "unit": UNIT,
-            "h2d_bytes_per_step": ws * (N * S * L + desc_bytes), "d2h_bytes_per_step": ws * (L + 1) * 8,
-            "steps": steps, "ms_per_step": secs / steps * 1e3,
-            "tier": ("pinned_host (copy engine: one strided transfer per layer into an HBM stage, then "
-                     "the scatter kernel)" if fopts.get("engine") == oc.COPY_CE else
-                     "pinned_host (PCIe zero-copy reads by the fetch kernel)"),
-            "timing": "host wall clock around match_prefix + build_descriptor + fetch + waits + D2H (max over ranks)"}
-
-
-def stall_leg(args, oc, torch, dev, lay_t, fopts, cells=None, tiers=None, windows_sel=("a100", "b200"),
-              timelines=True, optlocal=True):
-    """Added TTFT of a prefix hit over per-layer compute windows (Eq. 3).
-
-    The consumer stream waits on layer l (wait_layer), then runs the compute window C_l as a
-    %globaltimer spin (oc.emulate_compute) that stamps its start/end on the clock of the fetch's
-    layer-ready stamps.  TTFT runs from the fetch launch to the end of the last layer's compute
-    (free-running copy stream, reading c14).  Baselines: (i) the same consumer chain, waits
-    included, with the KV already delivered (resident KV); (ii) the paper's opt-local-LW analog
-    (P:1000-1003): a pre-aggregated layer-major buffer copied contiguously layer by layer (one
-    cudaMemcpyAsync + event per layer).  added = TTFT - TTFT(resident).  Per-layer device stalls:
-    stall_0 = start_0 - launch, stall_l = start_l - end_(l-1), minus the resident chain's gaps.
-    a8 check: the free-running recurrence start_l = max(ready_l, end_(l-1) + gap) with the
-    measured ready_l, C_l and resident gaps predicts the measured last end."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    stamps = torch.zeros((L, 2), dtype=torch.int64, device=dev)
-    cur = {"fo": fopts}                            # fetch options of the tier being measured
-
-    def chain(copy_s, cons_s, d, C_ns, fetch=True, events=None):
-        """Returns (TTFT ms from the launch event, stamps [L,2] ns)."""
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record(copy_s)
-        cons_s.wait_event(a)
-        if d is not None and fetch:
-            d.fetch_layerwise(copy_s, **cur["fo"])
-        elif events is not None:
-            events(copy_s)
-        for l in range(L):
-            if d is not None:
-                d.wait_layer(l, cons_s)
-            elif events is not None:
-                cons_s.wait_event(events.ev[l])
-            oc.emulate_compute(C_ns, cons_s, stamps[l])
-        b.record(cons_s)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b), stamps.cpu().numpy().copy()
-
-    res = {"timelines": {}}
-    if cells is None:
-        cells = [("4k", 4096, 3584, 63.47)] + ([("64k", 65536, 57344, 2423.90)] if args.stall64k else [])
-    if tiers is None:
-        tiers = (("hbm", oc.TIER_HBM), ("pinned_host", oc.TIER_PINNED_HOST), ("pinned_host_ce", oc.TIER_PINNED_HOST),
-                 ("pinned_host_hot1", oc.TIER_PINNED_HOST))
-    for name, ctx, cached, t_total_ms in cells:
-        N = cached // G
-        windows = {"a100": t_total_ms / L if t_total_ms else None,             # Table A5 (A100)
-                   "b200": prefill_window_s("llama3-8b", ctx, cached / ctx) * 1e3}  # FLOP model
-        windows = {k: v for k, v in windows.items() if k in windows_sel and v is not None}
-        need = N * G // Bs
-        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = need * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        bt = synth.block_table(5, need, need)
-        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs, bt, 0)
-        copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-        for tier_name, tier in tiers:
-            cur["fo"] = {"engine": oc.COPY_CE} if tier_name.endswith("_ce") else fopts
-            store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
-            if tier_name.endswith("_hot1"):            # layer 0 of every chunk mirrored in HBM
-                store.set_hot_layers(1)
-            (tok,), _ = synth.family_streams(9000 + N, G, 0, [N])
-            keys = oc.chunk_keys(tok, G)
-            gen = torch.Generator(device=dev).manual_seed(N)
-            for b0 in range(0, N, 512):
-                pl = torch.randint(0, 256, (min(N, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev,
-                                   generator=gen)
-                store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
-                del pl
-            d = oc.build_descriptor(store, keys, lay_t, tgt)
-            d_cw = oc.build_descriptor(store, keys, lay_t, tgt, oc.DELIVER_CHUNK_MAJOR)
-            ol = None
-            if optlocal:
-                # opt-local-LW analog: layer-major pre-aggregated source [L][N*S] on the same tier
-                src = torch.empty((L, N * S), dtype=torch.uint8, device=dev) if tier == oc.TIER_HBM else \
-                    torch.empty((L, N * S), dtype=torch.uint8, pin_memory=True)
-                dst = torch.empty((L, N * S), dtype=torch.uint8, device=dev)
-
-                class _OL:
-                    ev = [torch.cuda.Event() for _ in range(L)]
-
-                    def __call__(self, s):
-                        with torch.cuda.stream(s):
-                            for l in range(L):
-                                dst[l].copy_(src[l], non_blocking=True)
-                                self.ev[l].record(s)
-                ol = _OL()
-            for wname, C_ms in windows.items():
-                C_ns = int(round(C_ms * 1e6))
-                d.fetch_layerwise(copy_s, **cur["fo"])
-                torch.cuda.synchronize()
-                base_runs = [chain(copy_s, cons_s, d, C_ns, fetch=False) for _ in range(3)]
-                base, bst = min(base_runs, key=lambda r: r[0])
-                gaps = (bst[1:, 0] - bst[:-1, 1]).astype(np.float64)       # resident-chain gap between windows
-                gap_ns = float(np.median(gaps))
-                runs = []
-                for it in range(3):
-                    ttft, st = chain(copy_s, cons_s, d, C_ns)
-                    t = d.layer_times().astype(np.int64)
-                    runs.append((ttft - base, ttft, t, st))
-                best = min(runs, key=lambda r: r[0])
-                _, ttft, t, st = best
-                ready = t[1:] - t[0]
-                start, end = st[:, 0] - t[0], st[:, 1] - t[0]
-                stall = np.empty(L)
-                stall[0] = start[0]
-                stall[1:] = start[1:] - end[:-1] - gap_ns
-                # a8 free-running recurrence with the measured ready_l, C_l and resident gaps
-                e_prev = None
-                for l in range(L):
-                    s_l = ready[l] if e_prev is None else max(ready[l], e_prev + gap_ns)
-                    e_prev = s_l + (end[l] - start[l])
-                cw = min(chain(copy_s, cons_s, d_cw, C_ns)[0] for _ in range(2)) - base
-                key = f"{name}_{tier_name}" + ("" if wname == "a100" else "_b200win")
-                cell = {"N": N, "window": wname, "C_ms_per_layer": round(C_ms, 4), "added_ms": round(best[0], 4),
-                        "added_per_layer_ms": round(best[0] / L, 5),
-                        "X0_ms": round(ready[0] / 1e6, 4), "transfer_ms": round(ready[-1] / 1e6, 4),
-                        "ttft_ms": round(ttft, 3), "baseline_ttft_ms": round(base, 3),
-                        "resident_gap_us": round(gap_ns / 1e3, 2),
-                        "device_stall_ms": {"layer0": round(stall[0] / 1e6, 4),
-                                            "layers_1_to_L-1": round(float(stall[1:].sum()) / 1e6, 4),
-                                            "max_layer": round(float(stall[1:].max()) / 1e6, 4) if L > 1 else 0.0},
-                        "a8_model_end_ms": round(e_prev / 1e6, 4), "measured_end_ms": round(end[-1] / 1e6, 4),
-                        "added_ms_chunkwise": round(cw, 4), "payload_MiB": N * S * L / 2**20}
-                if ol is not None:
-                    ol(copy_s)
-                    torch.cuda.synchronize()
-                    cell["added_ms_opt_local_lw"] = round(min(chain(copy_s, cons_s, None, C_ns, events=ol)[0]
-                                                              for _ in range(2)) - base, 4)
-                res[key] = cell
-                if timelines and name == "4k":  # per-layer device timeline (the overlap evidence)
-                    res["timelines"][key] = {"layer_ready_ms": [round(x / 1e6, 4) for x in ready],
-                                             "compute_start_ms": [round(x / 1e6, 4) for x in start],
-                                             "compute_end_ms": [round(x / 1e6, 4) for x in end]}
-            d_cw.close()
-            d.close()
-            store.close()
-            del ol
-            torch.cuda.empty_cache()
-        del cache
-        torch.cuda.empty_cache()
-    res["windows"] = ("a100: Table A5 per-layer compute (P:2706-2713); b200: FLOP model at half the measured "
-                      "sustained bf16 rate; %globaltimer spin (oc.emulate_compute); baseline = the same chain "
-                      "(waits included) with the KV already delivered; opt_local_lw = pre-aggregated layer-major "
-                      "buffer on the same tier, one contiguous copy + event per layer; times relative to the "
-                      "fetch kernel's start")
-    return res
-
-
-def serve_leg(args, oc, torch, dev, lay_t, ws=1, rank=0, backend="nccl"):
-    """Config 5: a stream of concurrent mixed requests through the public API
-    into a bounded paged KV pool.  Corpus: 32 x 4K-token + 4 x 64K-token prefix families (48 GiB
-    in all); requests pick 4K/64K 50/50, a family by Zipf(1.1), hit 50% or 87.5%.  The pool
-    (48 GiB of [L][2][blocks][Bs][row] per GPU) hands out blocks from a free list in FIFO
-    admission order (a fragmented, seeded initial order); a request is admitted when its blocks
-    are free, gets a descriptor over its blocks, is fetched on one of 8 streams, and its blocks
-    return to the free list when its fetch's completion event fires.
-    With N ranks (weak scaling, R requests per rank): family g is homed on rank g mod N, each
-    rank's store holds its home families, the stores are exchanged once at setup (CUDA IPC blobs,
-    all_gather_object) and attached as peers, and a rank's requests pick a local family with
-    probability p_aff = 0.875 -- the rest read their chunks from a peer GPU inside the same fetch
-    kernel (NVLink P2P loads).  No collective on the data path.  GB/s = 2*N*S*L summed over all
-    requests / the max over ranks of the device time from the first launch to the last
-    completion."""
-    import collections
-    import synth
-    from paper_2605_22850_b200 import dist as odist
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    R = args.serve
-    fam_short, fam_long = (int(x) for x in os.environ.get("OC_SERVE_FAMILIES", "32,4").split(","))
-    n_short, n_long = 4096 // G, 65536 // G
-    home_of = lambda long, f: (f + fam_short * int(long)) % ws
-    mine = [(lg, f, n) for lg, nf, n in ((False, fam_short, n_short), (True, fam_long, n_long))
-            for f in range(nf) if home_of(lg, f) == rank]
-    store = oc.Store(lay_t, capacity=max(1, sum(n for _, _, n in mine)), tier=oc.TIER_HBM, device=dev.index)
-    gen = torch.Generator(device=dev).manual_seed(5 + rank)
-    fam_keys = {}
-    for long, nf, n in ((False, fam_short, n_short), (True, fam_long, n_long)):
-        for f in range(nf):
-            (tok,), _ = synth.family_streams(8000 + 100 * long + f, G, 0, [n])
-            keys = oc.chunk_keys(tok, G)
-            fam_keys[(long, f)] = keys
-            if home_of(long, f) != rank:
-                continue
-            for b0 in range(0, n, 512):
-                pl = torch.randint(0, 256, (min(n, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
-                store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
-                del pl
-    peers = []
-    if ws > 1:                                     # setup only: exchange store handles, attach peers
-        torch.cuda.synchronize()
-        blobs = odist.exchange_blobs(store.export())
-        for r, blob in enumerate(blobs):
-            if r != rank:
-                p = oc.Store.import_(blob, device=dev.index)
-                store.attach_peer(p)
-                peers.append(p)
-    pool_blocks = (int(os.environ.get("OC_SERVE_POOL_GIB", "48")) << 30) // (L * 2 * Bs * row)
-    cache = torch.empty((L, 2, pool_blocks, Bs, row), dtype=torch.uint8, device=dev)
-    per_kv = pool_blocks * Bs * row
-    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-    vb = [x + per_kv for x in kb]
-    reqs = synth.serving_requests(11 + rank, R, fam_short, fam_long, home_of=home_of if ws > 1 else None, rank=rank)
-    remote_bytes = sum(2 * (int((65536 if lg else 4096) * h) // G) * S * L for lg, f, h in reqs if home_of(lg, f) != rank)
-    streams = [torch.cuda.Stream(device=dev) for _ in range(8)]
-    start = torch.cuda.Event(enable_timing=True)
-
-    def run():
-        free = collections.deque(int(b) for b in synth.block_table(3, pool_blocks, pool_blocks))
-        pending = collections.deque(enumerate(reqs))
-        inflight = []
-        total_bytes, fetch_us, wait_blocks, n_done = 0, [], 0, 0
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-        start.record(streams[0])
-        for s in streams[1:]:
-            s.wait_event(start)
-        ends = []
-        t_host = time.perf_counter()
-        while pending or inflight:
-            still = []
-            for ev, d, blocks, nb in inflight:
-                if ev.query():
-                    t = d.layer_times().astype(np.int64)
-                    fetch_us.append((t[L] - t[0]) / 1e3)
-                    d.close()
-                    free.extend(blocks)
-                    n_done += 1
-                else:
-                    still.append((ev, d, blocks, nb))
-            inflight = still
-            admitted = False
-            while pending:
-                i, (long, fam, hit) = pending[0]
-                n = int((65536 if long else 4096) * hit) // G
-                need = n * G // Bs
-                if len(free) < need:
-                    wait_blocks += 1
-                    break
-                pending.popleft()
-                blocks = [free.popleft() for _ in range(need)]
-                tgt = oc.PagedTarget(kb, vb, Bs * row, row, lay_t[2] * lay_t[3], Bs, np.asarray(blocks, np.int32), 0)
-                try:
-                    d = oc.build_descriptor(store, fam_keys[(long, fam)][:n], lay_t, tgt)
-                    s = streams[i % len(streams)]
-                    d.fetch_layerwise(s)
-                except oc.ObjcacheError:
-                    print(f"serve: request {i} (long={long}, family={fam}, hit={hit}, N={n}, "
-                          f"blocks {min(blocks)}..{max(blocks)}, {len(inflight)} in flight) failed",
-                          file=sys.stderr)
-                    raise
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record(s)
-                ends.append(ev)
-                inflight.append((ev, d, blocks, n))
-                total_bytes += 2 * n * S * L
-                admitted = True
-            if not admitted and inflight:
-                inflight[0][0].synchronize()
-        torch.cuda.synchronize()
-        host_s = time.perf_counter() - t_host
-        dev_ms = max(start.elapsed_time(e) for e in ends)
-        return total_bytes, dev_ms, host_s, fetch_us, wait_blocks
-
-    def run_batched(max_batch=64):
-        """The same admission, but every admission step launches the requests it admitted as ONE
-        position-major batch (oc.BATCH_BY_POSITION): requests of one prefix family read their
-        shared chunks together.  Blocks return when the batch's completion event fires."""
-        free = collections.deque(int(b) for b in synth.block_table(3, pool_blocks, pool_blocks))
-        pending = collections.deque(enumerate(reqs))
-        inflight = []
-        total_bytes, n_batches, sizes = 0, 0, []
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-        start.record(streams[0])
-        for s in streams[1:]:
-            s.wait_event(start)
-        ends = []
-        t_host = time.perf_counter()
-        while pending or inflight:
-            still = []
-            for ev, b, ds, blocks in inflight:
-                if ev.query():
-                    b.close()
-                    for d in ds:
-                        d.close()
-                    free.extend(blocks)
-                else:
-                    still.append((ev, b, ds, blocks))
-            inflight = still
-            ds, blocks_all = [], []
-            while pending and len(ds) < max_batch:
-                i, (long, fam, hit) = pending[0]
-                n = int((65536 if long else 4096) * hit) // G
-                need = n * G // Bs
-                if len(free) < need:
-                    break
-                pending.popleft()
-                blocks = [free.popleft() for _ in range(need)]
-                tgt = oc.PagedTarget(kb, vb, Bs * row, row, lay_t[2] * lay_t[3], Bs, np.asarray(blocks, np.int32), 0)
-                ds.append(oc.build_descriptor(store, fam_keys[(long, fam)][:n], lay_t, tgt))
-                blocks_all += blocks
-                total_bytes += 2 * n * S * L
-            if ds:
-                b = oc.Batch(ds, order=oc.BATCH_BY_POSITION)
-                s = streams[n_batches % len(streams)]
-                b.fetch(s)
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record(s)
-                ends.append(ev)
-                inflight.append((ev, b, ds, blocks_all))
-                n_batches += 1
-                sizes.append(len(ds))
-            elif inflight:
-                inflight[0][0].synchronize()
-        torch.cuda.synchronize()
-        host_s = time.perf_counter() - t_host
-        dev_ms = max(start.elapsed_time(e) for e in ends)
-        return total_bytes, dev_ms, host_s, n_batches, sizes
-
-    run()                                               # warm-up pass (descriptor pool, modules)
-    total_bytes, dev_ms, host_s, fetch_us, waits = run()
-    mb = int(os.environ.get("OC_SERVE_MAX_BATCH", "16"))    # profiles/r01_serve.json: 4..64 swept
-    run_batched(mb)
-    tb_b, dev_ms_b, host_s_b, n_batches, sizes = run_batched(mb)
-    red_dev = dev if backend == "nccl" else None
-    max_ms = odist.max_over_ranks(dev_ms, device=red_dev)
-    all_bytes = odist.sum_over_ranks(total_bytes, device=red_dev)
-    all_remote = odist.sum_over_ranks(remote_bytes, device=red_dev)
-    res = {"requests_per_rank": R, "ranks": ws,
-           "mix": f"4K/64K 50/50, Zipf(1.1) over {fam_short} + {fam_long} families, hit 50%/87.5%"
-                  + (f", family g homed on rank g mod {ws}, p_aff 0.875" if ws > 1 else ""),
-           "pool_GiB_per_rank": pool_blocks * L * 2 * Bs * row / 2**30, "bytes_rw": all_bytes,
-           "remote_byte_fraction": round(all_remote / all_bytes, 4),
-           "GBps_device": round(all_bytes / max_ms / 1e6, 1),
-           "GBps_rank0_host_wall": round(total_bytes / host_s / 1e9, 1),
-           "device_ms_max_over_ranks": round(max_ms, 2),
-           "fetch_us_p50_rank0": round(float(np.percentile(fetch_us, 50)), 1),
-           "fetch_us_p99_rank0": round(float(np.percentile(fetch_us, 99)), 1),
-           "admission_stalls_rank0": waits}
-    max_ms_b = odist.max_over_ranks(dev_ms_b, device=red_dev)
-    res["batched_by_position"] = {
-        "how": f"each admission step launches its admitted requests (<= {mb}) as one position-major batch",
-        "GBps_device": round(odist.sum_over_ranks(tb_b, device=red_dev) / max_ms_b / 1e6, 1),
-        "GBps_rank0_host_wall": round(tb_b / host_s_b / 1e9, 1),
-        "device_ms_max_over_ranks": round(max_ms_b, 2), "batches_rank0": n_batches,
-        "batch_size_median_rank0": float(np.median(sizes)) if sizes else 0}
-    del cache
-    if ws > 1:
-        torch.distributed.barrier()                # peers' fetches done before any store goes away
-    store.close()
-    for p in peers:
-        p.close()
-    torch.cuda.empty_cache()
-    return res
-
-
-def offload_leg(args, oc, torch, dev, lay_t):
-    """Offload path: put_from_paged of 4K-token requests (N = 256 chunks)
-    from a fragmented paged cache into fresh slots of an HBM store -- the inverse gather.  Each
-    iteration offloads a new key set (no dedup); 10 offloads are issued back to back on one stream
-    and timed with CUDA events around them.  GB/s = 2*N*S*L per offload / device time per
-    offload; host_us = one call's host time (key reservation + descriptor upload + launch)."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    N = N_CHUNKS_4K
-    iters = 12
-    store = oc.Store(lay_t, capacity=iters * N, tier=oc.TIER_HBM, device=dev.index)
-    need = N * G // Bs
-    pool = need + need // 4
-    cache = torch.randint(0, 256, (L, 2, pool, Bs, row), dtype=torch.uint8, device=dev)
-    per_kv = pool * Bs * row
-    kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-    tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
-                         synth.block_table(21, need, pool), 0)
-    key_sets = []
-    for i in range(iters):
-        (tok,), _ = synth.family_streams(6000 + i, G, 0, [N])
-        key_sets.append(oc.chunk_keys(tok, G))
-    s = torch.cuda.Stream(device=dev)
-    torch.cuda.synchronize()
-    for i in range(2):                              # warm-up (pools, module load)
-        assert oc.put_from_paged(store, key_sets[i], lay_t, tgt, s) == N
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    host_us = []
-    a.record(s)
-    for i in range(2, iters):                       # back to back: the host enqueues ahead of the GPU
-        t0 = time.perf_counter()
-        n_new = oc.put_from_paged(store, key_sets[i], lay_t, tgt, s)
-        host_us.append((time.perf_counter() - t0) * 1e6)
-        assert n_new == N
-    b.record(s)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / (iters - 2)
-    res = {"N": N, "bytes_rw_per_offload": 2 * N * S * L, "GBps": round(2 * N * S * L / ms / 1e6, 1),
-           "ms_per_offload": round(ms, 4), "offloads_timed": iters - 2,
-           "host_us_median": round(float(np.median(host_us)), 1),
-           "engine": os.environ.get("OC_OFFLOAD_ENGINE", "bulk")}
-    store.close()
-    del cache
-    torch.cuda.empty_cache()
-    return res
-
-
-def sensitivity_leg(args, oc, torch, dev, lay_t):
-    """Fig. 14 analog: TTFT increase when the transfer path is capped at 10 Gbps
-    instead of 100 Gbps, layerwise vs chunkwise, for the Table A5 cells (4K/64K x 50%/87.5%, A100
-    windows).  Chunks in the pinned host tier; the cap is the fetch's pacer (layer l released at
-    t0 + l*s/r; chunkwise = the same paced transfer with every wait on the whole prefix).  Model:
-    Eq. 3 with uniform X = s/r (layerwise), L*X + L*C (chunkwise)."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    out = {}
-    for ctx, hit in ((4096, 0.5), (4096, 0.875), (65536, 0.5), (65536, 0.875)):
-        N = int(ctx * hit) // G
-        c = TABLE_A5_T_TOTAL_MS[(ctx, hit)] / L / 1e3                 # A100 windows (P:2706-2713)
-        s = N * S
-        store = oc.Store(lay_t, capacity=N, tier=oc.TIER_PINNED_HOST, device=dev.index)
-        (tok,), _ = synth.family_streams(77 + N, G, 0, [N])
-        keys = oc.chunk_keys(tok, G)
-        gen = torch.Generator(device=dev).manual_seed(N)
-        for b0 in range(0, N, 512):
-            pl = torch.randint(0, 256, (min(N, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
-            store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
-            del pl
-        need = N * G // Bs
-        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = need * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
-                             synth.block_table(9, need, need), 0)
-        descs = {"layerwise": oc.build_descriptor(store, keys, lay_t, tgt),
-                 "chunkwise": oc.build_descriptor(store, keys, lay_t, tgt, oc.DELIVER_CHUNK_MAJOR)}
-        copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-
-        def chain(d, rate):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            a.record(copy_s)
-            cons_s.wait_event(a)
-            d.fetch_layerwise(copy_s, pace_Bps=rate)
-            for l in range(L):
-                d.wait_layer(l, cons_s)
-                oc.emulate_compute(int(c * 1e9), cons_s)
-            b.record(cons_s)
-            torch.cuda.synchronize()
-            return a.elapsed_time(b)
-
-        for d in descs.values():           # warm-up (module load, wait entry point), untimed
-            d.fetch_layerwise(copy_s)
-            for l in range(L):
-                d.wait_layer(l, cons_s)
-                oc.emulate_compute(0, cons_s)
-            torch.cuda.synchronize()
-        cell = {"N": N, "s_MiB": s / 2**20, "C_ms": round(c * 1e3, 3), "r_star_GBps": round(s / c / 1e9, 3)}
-        for mode, d in descs.items():
-            t = {g: chain(d, g * 1e9 / 8) for g in (100, 10)}
-            model = {}
-            for g in (100, 10):
-                X = s / (g * 1e9 / 8)
-                model[g] = (X + (L - 1) * max(X, c) + c) if mode == "layerwise" else L * X + L * c
-            cell[mode] = {"ttft_100G_ms": round(t[100], 2), "ttft_10G_ms": round(t[10], 2),
-                          "increase_pct": round(100 * (t[10] / t[100] - 1), 2),
-                          "model_increase_pct": round(100 * (model[10] / model[100] - 1), 2)}
-        out[f"{ctx // 1024}K,{hit:g}"] = cell
-        for d in descs.values():
-            d.close()
-        store.close()
-        del cache
-        torch.cuda.empty_cache()
-    return out
-
-
-def granularity_leg(args, oc, torch, dev, lay_t, fopts):
-    """Config 2's chunk-size sweep: the 4K-token hit at G = 16, 64, 256
-    (N = 256, 64, 16) through the fused kernel, plus the unfused comparison at G = 16: the same
-    kernel into the paper's flat client buffer [L][N*S] (Alg. A1's B_l), then the client-side
-    scatter into the paged cache (oc scatter_flat; a torch index_copy_ per layer beside it) --
-    4*N*S bytes per layer instead of 2*N*S.  GB/s are
-    algorithmic (2*N*S*L) over device time, best of 20 after warm-up, rotating 2 request sets."""
-    import synth
-    L, Bs = lay_t[0], 16
-    out = {}
-    for G in (16, 64, 256):
-        lay = synth.with_chunk_tokens(synth.LLAMA3_8B, G).as_tuple()
-        row, S, chunk = oc.geometry(lay)
-        N = 4096 // G
-        store = oc.Store(lay, capacity=2 * N, tier=oc.TIER_HBM, device=dev.index)
-        sets = []
-        for r in range(2):
-            (tok,), _ = synth.family_streams(300 + r, G, 0, [N])
-            keys = oc.chunk_keys(tok, G)
-            store.put_chunks(keys, torch.randint(0, 256, (N, chunk), dtype=torch.uint8, device=dev))
-            need = N * G // Bs
-            cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-            per_kv = need * Bs * row
-            kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-            bt = synth.block_table(40 + r, need, need)
-            tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay[2] * lay[3], Bs, bt, 0)
-            d = oc.build_descriptor(store, keys, lay, tgt)
-            flat = None
-            if G == 16:
-                flat = torch.empty((L, N * S), dtype=torch.uint8, device=dev)
-                df = oc.build_descriptor(store, keys, lay, oc.FlatTarget(flat.data_ptr(), flat.numel()))
-                slots = torch.from_numpy((np.asarray(bt, dtype=np.int64)[np.arange(N * G) // Bs] * Bs
-                                          + np.arange(N * G) % Bs)).to(dev)
-                flat = (flat, df, slots)
-            sets.append((d, cache, flat))
-        s = torch.cuda.Stream(device=dev)
-
-        def timed(fn):
-            for i in range(4):
-                fn(i)
-            best = None
-            for i in range(20):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(s)
-                fn(i)
-                b.record(s)
-                torch.cuda.synchronize()
-                ms = a.elapsed_time(b)
-                best = ms if best is None else min(best, ms)
-            return best
-
-        ms = timed(lambda i: sets[i % 2][0].fetch_layerwise(s, **fopts))
-        x0 = [float(t[1] - t[0]) / 1e3 for t in [sets[1][0].layer_times().astype(np.int64)]][0]
-        cell = {"N": N, "S_KiB": S // 1024, "GBps": round(2 * N * S * L / ms / 1e6, 1), "ms": round(ms, 4),
-                "X0_us": round(x0, 2)}
-        if G == 16:
-            def unfused(i):
-                d, cache, (flatb, df, slots) = sets[i % 2]
-                df.fetch_layerwise(s, **fopts)
-                with torch.cuda.stream(s):
-                    for l in range(L):
-                        src = flatb[l].view(N, 2, G, row).permute(1, 0, 2, 3).reshape(2, N * G, row)
-                        cache[l].view(2, -1, row).index_copy_(1, slots, src)
-            def unfused_ours(i):                  # the same two steps, both in our kernels
-                d, cache, (flatb, df, slots) = sets[i % 2]
-                df.fetch_layerwise(s, **fopts)
-                d.scatter_flat(flatb.data_ptr(), flatb.numel(), s)
-            ms_u = timed(unfused)
-            ms_o = timed(unfused_ours)
-            cell["unfused_flat_then_scatter"] = {"GBps_algorithmic": round(2 * N * S * L / ms_o / 1e6, 1),
-                                                 "ms": round(ms_o, 4), "traffic_bytes": 4 * N * S * L,
-                                                 "scatter": "oc scatter_flat (bulk kernel, flat source)",
-                                                 "torch_scatter_GBps_algorithmic": round(2 * N * S * L / ms_u / 1e6, 1),
-                                                 "torch_scatter": "torch permute+index_copy_ per layer"}
-            # correctness of the comparison paths: same bytes as the fused kernel
-            d, cache, _ = sets[0]
-            same = True
-            for fn in (unfused, unfused_ours):
-                with torch.cuda.stream(s):
-                    cache.zero_()
-                fn(0)
-                torch.cuda.synchronize()
-                ref = cache.clone()
-                d.fetch_layerwise(s, **fopts)
-                torch.cuda.synchronize()
-                same &= bool(torch.equal(ref, cache))
-            cell["unfused_equals_fused"] = same
-        out[f"G{G}"] = cell
-        for d, cache, flat in sets:
-            d.close()
-            if flat is not None:
-                flat[1].close()
-        del sets
-        store.close()
-        torch.cuda.empty_cache()
-    return out
-
-
-def crossover_leg(args, oc, torch, dev, lay_t, fopts):
-    """Eq. 2 / Fig. 13 analog: added TTFT of layerwise vs chunkwise
-    delivery across context lengths (87.5% hit, B200 compute windows), per tier.  Theta_B200 is the
-    smallest payload W at which layerwise is not worse than chunkwise."""
-    ctxs = [128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536]
-    cells = [(f"{c}t", c, c * 7 // 8, None) for c in ctxs]
-    res = stall_leg(args, oc, torch, dev, lay_t, fopts, cells=cells, windows_sel=("b200",), timelines=False,
-                    optlocal=False)
-    out = {"windows": "b200 FLOP model, 87.5% hit", "cells": {}}
-    row, S, chunk = oc.geometry(lay_t)
-    for tier in ("hbm", "pinned_host"):
-        theta = None
-        for c in reversed(ctxs):            # smallest W from which layerwise is never worse
-            r = res[f"{c}t_{tier}_b200win"]
-            W = r["N"] * chunk
-            out["cells"][f"{c}t_{tier}"] = {"W_MiB": W / 2**20, "layerwise_ms": r["added_ms"],
-                                            "chunkwise_ms": r["added_ms_chunkwise"],
-                                            "C_ms": r["C_ms_per_layer"], "X0_ms": r["X0_ms"]}
-            if r["added_ms"] > r["added_ms_chunkwise"]:
-                break
-            theta = W
-        out[f"theta_{tier}_MiB"] = None if theta is None else theta / 2**20
-    return out
-
-
-def corun_leg(args, oc, torch, dev, lay_t):
-    """Prefill compute and KV delivery share the GPU (hard part 2): a stream of bf16
-    8192^3 GEMMs (torch.matmul, the compute stand-in) runs concurrently with back-to-back 4K fetches
-    on another stream.  Reported per copy-CTA budget: fetch GB/s and GEMM TFLOP/s alone and together."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    N = N_CHUNKS_4K
-    store = oc.Store(lay_t, capacity=2 * N, tier=oc.TIER_HBM, device=dev.index)
-    descs = []
-    for r in range(2):
-        (tok,), _ = synth.family_streams(600 + r, G, 0, [N])
-        keys = oc.chunk_keys(tok, G)
-        store.put_chunks(keys, torch.randint(0, 256, (N, chunk), dtype=torch.uint8, device=dev))
-        need = N * G // Bs
-        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = need * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
-                             synth.block_table(r, need, need), 0)
-        descs.append((oc.build_descriptor(store, keys, lay_t, tgt), cache))
-    a = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev)
-    b = torch.randn(8192, 8192, dtype=torch.bfloat16, device=dev)
-    cbuf = torch.empty(8192, 8192, dtype=torch.bfloat16, device=dev)
-    gs, fs = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    n_gemm, n_fetch = 40, 200
-    flops = 2 * 8192 ** 3
-
-    def run(do_gemm, do_fetch, fopts):
-        torch.cuda.synchronize()
-        e = {k: torch.cuda.Event(enable_timing=True) for k in ("g0", "g1", "f0", "f1")}
-        if do_gemm:
-            e["g0"].record(gs)
-            with torch.cuda.stream(gs):
-                for _ in range(n_gemm):
-                    torch.matmul(a, b, out=cbuf)
-            e["g1"].record(gs)
-        if do_fetch:
-            e["f0"].record(fs)
-            for i in range(n_fetch):
-                descs[i % 2][0].fetch_layerwise(fs, **fopts)
-            e["f1"].record(fs)
-        torch.cuda.synchronize()
-        res = {}
-        if do_gemm:
-            res["gemm_tflops"] = round(n_gemm * flops / e["g0"].elapsed_time(e["g1"]) / 1e9, 1)
-        if do_fetch:
-            res["fetch_GBps"] = round(n_fetch * 2 * N * S * L / e["f0"].elapsed_time(e["f1"]) / 1e6, 1)
-        return res
-
-    run(True, True, {})                                     # warm up cuBLAS and the fetch path
-    out = {"gemm_alone": run(True, False, {})}
-    for engine, name in ((oc.COPY_BULK, "bulk"), (oc.COPY_LDST, "ldst")):
-        for mc in (0, 148, 64, 32, 16):
-            fo = {"engine": engine, "max_ctas": mc, "unit_bytes": int(os.environ.get("OC_CORUN_UNIT", "0"))}
-            alone = run(False, True, fo)
-            both = run(True, True, fo)
-            out[f"{name}_ctas{mc or 'auto'}"] = {"fetch_alone_GBps": alone["fetch_GBps"],
-                                                 "fetch_corun_GBps": both["fetch_GBps"],
-                                                 "gemm_corun_tflops": both["gemm_tflops"]}
-    for d, _ in descs:
-        d.close()
-    store.close()
-    del a, b, cbuf, descs
-    torch.cuda.empty_cache()
-    return out
-
-
-def sweep_leg(args, oc, torch, dev, lay_t):
-    """Fig. 15 analog: one request from the pinned host tier, paced at f * r*, with
-    the Table A5 A100 compute windows; added TTFT against the resident-KV chain and against Eq. 3
-    with uniform X = s/r, C = c (added = X + (L-1) max(0, X - C)).  The knee sits at f = 1."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda._sleep(1000)
-    e0.record()
-    torch.cuda._sleep(20_000_000)
-    e1.record()
-    torch.cuda.synchronize()
-    cyc_per_ms = 20_000_000 / e0.elapsed_time(e1)
-    out = {}
-    for ctx, hit in ((16384, 0.875), (65536, 0.875)):
-        N = int(ctx * hit) // G
-        c = TABLE_A5_T_TOTAL_MS[(ctx, hit)] / L / 1e3
-        s = N * S
-        rstar = s / c
-        store = oc.Store(lay_t, capacity=N, tier=oc.TIER_PINNED_HOST, device=dev.index)
-        (tok,), _ = synth.family_streams(31 + N, G, 0, [N])
-        keys = oc.chunk_keys(tok, G)
-        gen = torch.Generator(device=dev).manual_seed(N)
-        for b0 in range(0, N, 512):
-            pl = torch.randint(0, 256, (min(N, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
-            store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
-            del pl
-        need = N * G // Bs
-        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = need * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
-                             synth.block_table(3, need, need), 0)
-        d = oc.build_descriptor(store, keys, lay_t, tgt)
-        copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-
-        def chain(pace):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            a.record(copy_s)
-            cons_s.wait_event(a)
-            if pace is not None:
-                d.fetch_layerwise(copy_s, pace_Bps=pace)
-            for l in range(L):
-                if pace is not None:
-                    d.wait_layer(l, cons_s)
-                with torch.cuda.stream(cons_s):
-                    torch.cuda._sleep(int(c * 1e3 * cyc_per_ms))
-            b.record(cons_s)
-            torch.cuda.synchronize()
-            return a.elapsed_time(b)
-
-        base = min(chain(None) for _ in range(2))
-        pts = []
-        for f in (0.25, 0.5, 0.75, 0.9, 1.0, 1.1, 1.25, 1.5, 2.0, 4.0):
-            r = f * rstar
-            added = chain(r) - base
-            X = s / r
-            pts.append({"f": f, "rate_GBps": round(r / 1e9, 3), "added_ms": round(added, 3),
-                        "eq3_added_ms": round((X + (L - 1) * max(0.0, X - c)) * 1e3, 3)})
-        out[f"{ctx // 1024}K,{hit:g}"] = {"r_star_GBps": round(rstar / 1e9, 3), "C_ms": round(c * 1e3, 3),
-                                          "payload_per_layer_MiB": s / 2**20, "points": pts}
-        d.close()
-        store.close()
-        del cache
-        torch.cuda.empty_cache()
-    return out
-
-
-def batch_leg(args, oc, torch, dev, lay_t):
-    """Config 5 on one GPU: concurrent mixed 4K/64K requests (Llama-3-8B layout) whose prefixes
-    come from a few shared families (Zipf-like reuse), each delivered into its own paged cache.
-    Compares one batched launch (layer-major across requests) with one launch per request on one
-    stream and with one launch per request on its own stream.  GB/s = r+w bytes of all requests /
-    device time; per-request X0 (layer-0 ready after the launch) summarises latency."""
-    import synth
-    n4, n64 = (int(x) for x in args.batch.lower().split("x"))
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    fam4, fam64 = 4, 2
-    N4, N64 = 4096 // G, 65536 // G
-    store = oc.Store(lay_t, capacity=fam4 * N4 + fam64 * N64, tier=oc.TIER_HBM, device=dev.index)
-    fam_keys = []
-    gen = torch.Generator(device=dev).manual_seed(55)
-    for f, n in [(f, N4) for f in range(fam4)] + [(fam4 + f, N64) for f in range(fam64)]:
-        (tok,), _ = synth.family_streams(7000 + f, G, 0, [n])
-        keys = oc.chunk_keys(tok, G)
-        for b0 in range(0, n, 512):
-            pl = torch.randint(0, 256, (min(n, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
-            store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
-            del pl
-        fam_keys.append(keys)
-    reqs = []
-    for i in range(n4 + n64):
-        big = i >= n4
-        keys = fam_keys[fam4 + (i % fam64)] if big else fam_keys[i % fam4]
-        n = keys.shape[0]
-        need = n * G // Bs
-        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = need * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
-                             synth.block_table(100 + i, need, need), 0)
-        reqs.append((oc.build_descriptor(store, keys, lay_t, tgt), cache, n))
-    descs = [r[0] for r in reqs]
-    total_bytes = sum(2 * n * S * L for _, _, n in reqs)
-    batch = oc.Batch(descs)
-    batch_pos = oc.Batch(descs, order=oc.BATCH_BY_POSITION)
-    s0 = torch.cuda.Stream(device=dev)
-    streams = [torch.cuda.Stream(device=dev) for _ in descs]
-
-    def timed(fn, reps=3):
-        best = None
-        for _ in range(reps + 1):
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s0)
-            fn(a)
-            for st in streams:
-                s0.wait_stream(st)
-            b.record(s0)
-            torch.cuda.synchronize()
-            ms = a.elapsed_time(b)
-            x0 = [float(t[1] - t[0]) / 1e6 for t in (d.layer_times().astype(np.int64) for d in descs)]
-            if best is None or ms < best[0]:
-                best = (ms, x0)
-        return {"GBps": round(total_bytes / best[0] / 1e6, 1), "ms": round(best[0], 3),
-                "x0_ms_4k_median": round(float(np.median(best[1][:n4])), 4) if n4 else None,
-                "x0_ms_64k_median": round(float(np.median(best[1][n4:])), 4) if n64 else None}
-
-    res = {"requests": f"{n4} x 4K + {n64} x 64K (families: {fam4} x 4K, {fam64} x 64K)",
-           "bytes_rw": total_bytes,
-           "batched_one_launch": timed(lambda a: batch.fetch(s0)),
-           # position-major inside each layer: members sharing a family prefix read each shared
-           # slice together (HBM once, L2 for the rest)
-           "batched_by_position": timed(lambda a: batch_pos.fetch(s0)),
-           # WDRR claim order (Alg. A2 line 7), weights = each request's bytes (equal finish times)
-           "batched_wdrr_by_size": timed(lambda a: batch.fetch(s0, wdrr_weights=[float(n) for _, _, n in reqs])),
-           "per_request_one_stream": timed(lambda a: [d.fetch_layerwise(s0) for d in descs]),
-           "per_request_own_streams": timed(lambda a: [(st.wait_event(a), d.fetch_layerwise(st))
-                                                       for d, st in zip(descs, streams)])}
-    batch.close()
-    batch_pos.close()
-    for d, _, _ in reqs:
-        d.close()
-    del reqs
-    store.close()
-    torch.cuda.empty_cache()
-    return res
-
-
-# The paper's scheduler workloads (Sec. 5.7, P:1172-1198; Table A6, P:2734-2768): requests named
-# by (context, hit rate); per-layer bytes s_i = cached tokens * 4096 B and per-layer compute
-# c_i = T_total / 32 from Table A5 (P:2706-2713, A100); caps 80 / 50 / 50 Gbps; delta = 5 Gbps.
-TABLE_A5_T_TOTAL_MS = {(4096, 0.5): 185.31, (4096, 0.875): 63.47, (16384, 0.5): 955.89, (16384, 0.875): 281.76, (32768, 0.5): 2589.25,
-                       (32768, 0.875): 763.19, (65536, 0.5): 8672.79, (65536, 0.875): 2423.90}
-def prefill_window_s(lay_name, ctx, hit, flops_per_s=0.5 * 1399.5e12):
-    """Per-layer prefill compute exposed by the miss tokens (SURVEY 8(d) sanity model): with m
-    miss tokens after h hit tokens a layer costs 2*m*P_layer + 4*n_heads*d*m*(h + m/2) FLOPs;
-    executed at half of the measured sustained bf16 rate (MEASURED_PEAKS.json)."""
-    h_d, n_heads, d, n_kv, inter = {"llama3-70b": (8192, 64, 128, 8, 28672),
-                                   "llama3-8b": (4096, 32, 128, 8, 14336)}[lay_name]
-    p_layer = 2 * h_d * h_d + 2 * h_d * n_kv * d + 3 * h_d * inter
-    h = ctx * hit
-    m = ctx - h
-    return (2 * m * p_layer + 4 * n_heads * d * m * (h + m / 2)) / flops_per_s
-
-
-def sched_workloads():
-    """name -> (layout, cap Gbps, [(label, context, hit, c seconds per layer)], window source)."""
-    import synth
-    a5 = lambda ctx, hit: TABLE_A5_T_TOTAL_MS[(ctx, hit)] / 32 / 1e3
-    cells = lambda lst: [(f"{c // 1024}K,{h:g}", c, h, a5(c, h)) for c, h in lst]
-    ab = [(16384, 0.5), (16384, 0.875), (65536, 0.5), (65536, 0.875)]
-    w = {"A": (synth.LLAMA3_8B, 80.0, cells(ab), "Table A5 (A100)"),
-         "B": (synth.LLAMA3_8B, 50.0, cells(ab), "Table A5 (A100)"),
-         "C": (synth.LLAMA3_8B, 50.0, cells(ab[:2] + [(32768, 0.5), (32768, 0.875)] + ab[2:]), "Table A5 (A100)")}
-    # BASELINE.json configs[3]: Llama-3-70B layout, 16 concurrent 32K requests (hit 50% / 87.5%
-    # alternating), cap at half the aggregate zero-stall rate (Workload B/C regime).
-    c70 = [(f"32K,{h:g}#{i}", 32768, h, prefill_window_s("llama3-70b", 32768, h))
-           for i, h in enumerate([0.5, 0.875] * 8)]
-    sum_rstar = sum(int(ctx * h) * 4096 / c for _, ctx, h, c in c70)
-    w["70B"] = (synth.LLAMA3_70B, round(sum_rstar / 2 * 8 / 1e9, 3), c70,
-                "FLOP model at 50% of the measured sustained bf16 rate (B200)")
-    return w
-
-
-def stall_gemm_leg(args, oc, torch, dev, lay_t):
-    """Added TTFT with real prefill compute sharing the GPU ("a shape-true Llama
-    layer (random bf16 weights; only shapes matter) over the miss tokens"): per layer the consumer
-    stream waits for the layer's KV (wait_layer) and then runs the layer's four projection GEMMs
-    (QKV 4096x6144, O 4096x4096, gate+up 4096x28672, down 14336x4096) on the m miss tokens; the
-    attention itself is left out.  TTFT = fetch launch -> end of the last layer's GEMMs (CUDA
-    events); added = TTFT - the same GEMM chain with the KV already resident.  Unlike the timer
-    spins of the stall leg, these GEMMs contend with the fetch for SMs and HBM."""
-    import synth
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    w = [torch.randn(k, n, dtype=torch.bfloat16, device=dev) * 0.01
-         for k, n in ((4096, 6144), (4096, 4096), (4096, 28672), (14336, 4096))]
-    out = {}
-    for name, ctx in (("4k", 4096), ("64k", 65536)):
-        cached = ctx * 7 // 8
-        m = ctx - cached
-        N = cached // G
-        x = torch.randn(m, 4096, dtype=torch.bfloat16, device=dev)
-        need = N * G // Bs
-        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = need * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        tgt = oc.PagedTarget(kb, [x_ + per_kv for x_ in kb], Bs * row, row, lay_t[2] * lay_t[3], Bs,
-                             synth.block_table(7, need, need), 0)
-        copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-
-        def layer_gemms():
-            torch.matmul(x, w[0])
-            torch.matmul(x, w[1])
-            gu = torch.matmul(x, w[2])
-            torch.matmul(gu[:, :14336], w[3])
-
-        def chain(d, fopts):
-            torch.cuda.synchronize()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(copy_s)
-            cons_s.wait_event(a0)
-            if d is not None:
-                d.fetch_layerwise(copy_s, **fopts)
-            with torch.cuda.stream(cons_s):
-                for l in range(L):
-                    if d is not None:
-                        d.wait_layer(l, cons_s)
-                    layer_gemms()
-            a1.record(cons_s)
-            torch.cuda.synchronize()
-            return a0.elapsed_time(a1)
-
-        chain(None, {})
-        base = min(chain(None, {}) for _ in range(3))
-        res = {"miss_tokens": m, "hit_chunks": N, "compute_ms_resident": round(base, 3),
-               "compute_ms_per_layer": round(base / L, 4)}
-        for tier_name, tier, variants in (
-                ("hbm", oc.TIER_HBM, (("", {"engine": oc.COPY_BULK}),
-                                      # a copy-CTA budget: the transfer stays ahead of compute on
-                                      # fewer SMs and steals less from the GEMMs
-                                      ("_ctas64", {"engine": oc.COPY_BULK, "max_ctas": 64}),
-                                      ("_ctas16", {"engine": oc.COPY_BULK, "max_ctas": 16}))),
-                ("pinned_host", oc.TIER_PINNED_HOST, (("", {"engine": oc.COPY_BULK}),
-                                                      ("_ce", {"engine": oc.COPY_CE}))),
-                # layer-0 mirror, and the mirror depth that Eq. 3 says removes the stall:
-                # K >= L - (L-1) * C / X with X = one layer over PCIe, C = one layer of compute
-                ("pinned_host_hot1", oc.TIER_PINNED_HOST, (("", {"engine": oc.COPY_BULK}),)),
-                ("pinned_host_hotK", oc.TIER_PINNED_HOST, (("", {"engine": oc.COPY_BULK}),))):
-            store = oc.Store(lay_t, capacity=N, tier=tier, device=dev.index)
-            if tier_name.endswith("_hot1"):
-                store.set_hot_layers(1)
-            elif tier_name.endswith("_hotK"):
-                X = N * S / 51.4e9 * 1e3                      # ms per layer over PCIe (SM path)
-                C = base / L
-                K = oc.hot_layers_for(X, C, L)
-                store.set_hot_layers(K)
-                res["hotK_layers"] = K
-            (tok,), _ = synth.family_streams(9100 + N, G, 0, [N])
-            keys = oc.chunk_keys(tok, G)
-            for b0 in range(0, N, 512):
-                pl = torch.randint(0, 256, (min(N, b0 + 512) - b0, chunk), dtype=torch.uint8, device=dev)
-                store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
-                del pl
-            d = oc.build_descriptor(store, keys, lay_t, tgt)
-            for suffix, fopts in variants:
-                chain(d, fopts)
-                t = min(chain(d, fopts) for _ in range(3))
-                res[tier_name + suffix] = {"ttft_ms": round(t, 3), "added_ms": round(t - base, 3)}
-            d.close()
-            store.close()
-        out[name] = res
-        del cache
-        torch.cuda.empty_cache()
-    return out
-
-
-def hash_leg(args, oc, torch, dev, G=16, ctx=4096):
-    """Chain keys (reading c1) of R requests of 4K tokens (256 keys each): one GPU launch
-    (oc_chunk_keys_batch, one thread per chain; device time from CUDA events around the launch
-    alone) vs the host library's loop over oc_chunk_keys (SHA extensions, one core)."""
-    import synth
-    R = args.hash
-    streams = [synth.tokens(77000 + i, ctx) for i in range(R)]
-    t = time.perf_counter()
-    for st in streams:
-        oc.chunk_keys(st, G)
-    host_s = time.perf_counter() - t
-    flat = torch.from_numpy(np.concatenate(streams).view(np.int32)).to(dev)
-    off = torch.from_numpy((np.arange(R, dtype=np.int64) * ctx)).to(dev)
-    lens = torch.full((R,), ctx, dtype=torch.int64, device=dev)
-    koff = torch.from_numpy(np.arange(R, dtype=np.int64) * (ctx // G)).to(dev)
-    out = torch.empty((R * (ctx // G), 32), dtype=torch.uint8, device=dev)
-    s = torch.cuda.Stream(device=dev)
-    run = lambda: oc._check(oc._lib.oc_chunk_keys_batch(flat.data_ptr(), off.data_ptr(), lens.data_ptr(), R, G, None,
-                                                       out.data_ptr(), koff.data_ptr(), s.cuda_stream))
-    run()
-    s.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(s)
-    run()
-    b.record(s)
-    s.synchronize()
-    gpu_ms = a.elapsed_time(b)
-    same = bool(np.array_equal(out[:ctx // G].cpu().numpy(), oc.chunk_keys(streams[0], G)))
-    keys = R * (ctx // G)
-    return {"requests": R, "keys": keys, "host_ms": round(host_s * 1e3, 2), "gpu_ms": round(gpu_ms, 3),
-            "host_keys_per_s": round(keys / host_s), "gpu_keys_per_s": round(keys / (gpu_ms / 1e3)),
-            "first_request_equal": same}
-
-
-def pool_leg(args, oc, torch, dev, lay_t, epoch_s=0.1, cap_gbps=50.0, delta_gbps=5.0):
-    """Alg. A2 as a running system (Sec. 3.6): requests arrive over time (Poisson) and
-    are submitted to an oc.TenantPool; every 100 ms (reading c16) the host calls pool.epoch(), which
-    retires finished requests, admits the waiting ones under the cap the running ones leave (rates
-    from the policy), and launches them -- as independently paced fetches, or as one WDRR batch per
-    epoch with held rates.  Chunks live in the pinned-host tier (PCIe as the shared link); each
-    request's consumer runs wait_layer(l) + a compute window c_i per layer (Table A5 windows).
-    TTFT_i = end of its last window - its arrival, both stamped on the GPU clock; the no-limit TTFT
-    is L * c_i.  Reported per (policy, dispatch): mean / p50 / p90 TTFT and the sum of added TTFT."""
-    import synth
-    GB = 1e9 / 8
-    L, G, Bs = lay_t[0], lay_t[4], 16
-    row, S, chunk = oc.geometry(lay_t)
-    cells = [(16384, 0.5), (16384, 0.875), (32768, 0.5), (32768, 0.875), (65536, 0.5), (65536, 0.875)]
-    R = args.pool
-    rng = np.random.default_rng(2605)
-    kinds = [cells[i % len(cells)] for i in rng.permutation(R)]
-    bytes_total = sum(int(c * h) // G * S * L for c, h in kinds)
-    mean_gap = bytes_total / (cap_gbps * GB) / R / 0.9      # offered load ~0.9 of the cap
-    arrivals = np.cumsum(rng.exponential(mean_gap, R))
-    arrivals -= arrivals[0]
-    n_max = max(int(c * h) // G for c, h in kinds)
-    store = oc.Store(lay_t, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
-    (tok,), _ = synth.family_streams(4343, G, 0, [n_max])
-    keys = oc.chunk_keys(tok, G)
-    gen = torch.Generator(device=dev).manual_seed(4343)
-    for b0 in range(0, n_max, 128):
-        b1 = min(n_max, b0 + 128)
-        pl = torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
-        store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
-        del pl
-    caches = {}
-    for c, h in set(kinds):                                  # one destination per kind, reused
-        N = int(c * h) // G
-        need = N * G // Bs
-        cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-        per_kv = need * Bs * row
-        kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-        caches[(c, h)] = (cache, oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay_t[2] * lay_t[3],
-                                                Bs, synth.block_table(N, need, need), 0))
-    copy_streams = [torch.cuda.Stream(device=dev) for _ in range(R)]
-    cons_streams = [torch.cuda.Stream(device=dev) for _ in range(R)]
-    stamps = torch.zeros((R, L + 1, 2), dtype=torch.int64, device=dev)
-
-    def run(policy, dispatch):
-        pool = oc.TenantPool(policy, cap_gbps * GB, delta_gbps * GB, 0, dispatch=dispatch)
-        torch.cuda.synchronize()
-        descs, tickets, chained = [None] * R, [None] * R, [False] * R
-        c_of = [TABLE_A5_T_TOTAL_MS[k] / L / 1e3 for k in kinds]
-        t0 = time.perf_counter()
-        nxt, next_epoch = 0, 0.0
-        while True:
-            now = time.perf_counter() - t0
-            while nxt < R and arrivals[nxt] <= now:
-                i = nxt
-                c, h = kinds[i]
-                N = int(c * h) // G
-                descs[i] = oc.build_descriptor(store, keys[:N], lay_t, caches[(c, h)][1])
-                oc.emulate_compute(0, cons_streams[i], stamps[i, 0])          # arrival stamp
-                tickets[i] = pool.submit(descs[i], c_of[i], copy_streams[i])
-                nxt += 1
-            if now >= next_epoch:
-                pool.epoch()
-                next_epoch += epoch_s
-                for i in range(nxt):
-                    if not chained[i] and pool.status(tickets[i])[0] != oc.TENANT_WAITING:
-                        for l in range(L):                    # prefill of layer l after its KV
-                            descs[i].wait_layer(l, cons_streams[i])
-                            oc.emulate_compute(int(c_of[i] * 1e9), cons_streams[i], stamps[i, 1 + l])
-                        chained[i] = True
-            if nxt == R and all(chained):
-                break
-            time.sleep(0.002)
-        torch.cuda.synchronize()
-        st = stamps.cpu().numpy().astype(np.int64)
-        ttft = (st[:, L, 1] - st[:, 0, 0]) / 1e6
-        base = np.array([L * c * 1e3 for c in c_of])
-        pool.close()
-        for d in descs:
-            d.close()
-        return {"ttft_ms_mean": round(float(ttft.mean()), 1), "ttft_ms_p50": round(float(np.median(ttft)), 1),
-                "ttft_ms_p90": round(float(np.percentile(ttft, 90)), 1),
-                "added_ms_sum": round(float((ttft - base).sum()), 1)}
-
-    out = {"requests": R, "cap_gbps": cap_gbps, "delta_gbps": delta_gbps, "epoch_ms": epoch_s * 1e3,
-           "offered_load_of_cap": 0.9, "mix": "Workload C cells (16K/32K/64K x 50%/87.5%), Table A5 windows",
-           "runs": {}}
-    for policy in ("equal", "stall_opt", "cal_stall_opt"):
-        for dname, disp in (("independent", oc.DISPATCH_INDEPENDENT), ("wdrr", oc.DISPATCH_WDRR)):
-            out["runs"][f"{policy}/{dname}"] = run(policy, disp)
-    store.close()
-    del caches
-    torch.cuda.empty_cache()
-    return out
-
-
-def sched_leg(args, oc, torch, dev, lay_t):
-    """Concurrent layerwise fetches under a shared cap: Equal / KV-prop / BW-prop / Stall-opt /
-    Calibrated Stall-opt rates from oc.schedule_bandwidth, enforced by the fetch's pacer (layer l
-    released at t0 + l*s/r), chunks in the pinned host tier (the shared PCIe link plays the
-    paper's shared NIC).  Each request's consumer waits on every layer and then spins for c_i.
-    dTTFT_i = TTFT_i - TTFT_i(no limit); the paper's Table A8 reports the sum per policy."""
-    import synth
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda._sleep(1000)
-    e0.record()
-    torch.cuda._sleep(20_000_000)
-    e1.record()
-    torch.cuda.synchronize()
-    cyc_per_ms = 20_000_000 / e0.elapsed_time(e1)
-    GB = 1e9 / 8                                            # bytes/s per Gbps (decimal)
-    out = {}
-    table = sched_workloads()
-    for wl in [w.strip().upper() for w in args.sched.split(",") if w.strip()]:
-        named, cap_gbps, cells, window_src = table[wl]
-        lay = named.as_tuple()
-        L, G, Bs = lay[0], lay[4], 16
-        row, S, chunk = oc.geometry(lay)
-        n_max = max(int(ctx * hit) // G for _, ctx, hit, _ in cells)
-        store = oc.Store(lay, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
-        store_hot = oc.Store(lay, capacity=n_max, tier=oc.TIER_PINNED_HOST, device=dev.index)
-        store_hot.set_hot_layers(1)                        # the same corpus with layer 0 mirrored in HBM
-        (tok,), _ = synth.family_streams(4242, G, 0, [n_max])
-        keys = oc.chunk_keys(tok, G)                       # one shared-prefix corpus
-        gen = torch.Generator(device=dev).manual_seed(4242)
-        for b0 in range(0, n_max, 128):
-            b1 = min(n_max, b0 + 128)
-            pl = torch.randint(0, 256, (b1 - b0, chunk), dtype=torch.uint8, device=dev, generator=gen)
-            store.put_chunks(keys[b0:b1], pl)
-            store_hot.put_chunks(keys[b0:b1], pl)
-            del pl
-        reqs = []
-        for label, ctx, hit, c in cells:
-            N = int(ctx * hit) // G
-            need = N * G // Bs
-            cache = torch.empty((L, 2, need, Bs, row), dtype=torch.uint8, device=dev)
-            per_kv = need * Bs * row
-            kb = [cache.data_ptr() + l * 2 * per_kv for l in range(L)]
-            tgt = oc.PagedTarget(kb, [x + per_kv for x in kb], Bs * row, row, lay[2] * lay[3], Bs,
-                                 synth.block_table(N, need, need), 0)
-            d = oc.build_descriptor(store, keys[:N], lay, tgt)
-            reqs.append({"cell": label, "N": N, "s": N * S, "c": c, "d": d, "cache": cache,
-                         "d_hot": oc.build_descriptor(store_hot, keys[:N], lay, tgt),
-                         "copy": torch.cuda.Stream(device=dev), "cons": torch.cuda.Stream(device=dev)})
-
-        batch = oc.Batch([r["d"] for r in reqs])
-        batch_hot = oc.Batch([r["d_hot"] for r in reqs])
-
-        def run(rates, dispatch="independent"):
-            """All requests concurrently; rates None = unpaced.  dispatch "independent": one fetch per
-            request paced by its own kernel (a10); "wdrr": one batched launch in WDRR order with
-            every request held at its rate (Alg. A2 lines 6-7).  Returns TTFT per request (ms)."""
-            torch.cuda.synchronize()
-            start = torch.cuda.Event(enable_timing=True)
-            start.record(torch.cuda.current_stream())
-            ends = []
-            for r in reqs:
-                r["copy"].wait_event(start)
-                r["cons"].wait_event(start)
-            if dispatch in ("wdrr", "hot_wdrr"):
-                (batch_hot if dispatch == "hot_wdrr" else batch).fetch(
-                    reqs[0]["copy"], wdrr_weights=[float(x) for x in rates], hold_rates=True)
-            else:
-                dk = "d_hot" if dispatch == "hot_strict" else "d"
-                for i, r in enumerate(reqs):
-                    r[dk].fetch_layerwise(r["copy"], pace_Bps=0.0 if rates is None else float(rates[i]),
-                                          pace_strict=dispatch in ("strict", "hot_strict"))
-            dk = "d_hot" if dispatch.startswith("hot_") else "d"
-            for l in range(L):                              # enqueue layer by layer across requests
-                for r in reqs:
-                    r[dk].wait_layer(l, r["cons"])
-                    with torch.cuda.stream(r["cons"]):
-                        torch.cuda._sleep(int(r["c"] * 1e3 * cyc_per_ms))
-            for r in reqs:
-                e = torch.cuda.Event(enable_timing=True)
-                e.record(r["cons"])
-                ends.append(e)
-            torch.cuda.synchronize()
-            return [start.elapsed_time(e) for e in ends]
-
-        s_i = [r["s"] for r in reqs]
-        c_i = [r["c"] for r in reqs]
-        base = run(None)                                    # "no-limit base" (Table A8)
-        res = {"layout": named.name, "cap_gbps": cap_gbps, "windows": window_src,
-               "requests": [r["cell"] for r in reqs], "c_ms": [round(c * 1e3, 3) for c in c_i],
-               "zero_stall_gbps": [round(s / c / GB, 3) for s, c in zip(s_i, c_i)],
-               "no_limit_ttft_ms": [round(x, 1) for x in base], "policies": {}}
-        for pol in ("equal", "kv_prop", "bw_prop", "stall_opt", "cal_stall_opt"):
-            rates = oc.schedule_bandwidth(pol, s_i, c_i, cap_gbps * GB, 5 * GB)
-            ttft = run(rates)
-            # Eq. 3 with uniform X = s/r and C = c: added = X + (L-1) max(0, X - C)
-            model = [s / r + (L - 1) * max(0.0, s / r - c) for s, c, r in zip(s_i, c_i, rates)]
-            ttft_w = run(rates, "wdrr")
-            ttft_s = run(rates, "strict")
-            ttft_h = run(rates, "hot_strict")
-            ttft_hw = run(rates, "hot_wdrr")
-            res["policies"][pol] = {"rates_gbps": [round(r / GB, 2) for r in rates],
-                                    "ttft_ms": [round(x, 1) for x in ttft],
-                                    "dttft_ms": round(sum(t - b for t, b in zip(ttft, base)), 1),
-                                    "wdrr_ttft_ms": [round(x, 1) for x in ttft_w],
-                                    "wdrr_dttft_ms": round(sum(t - b for t, b in zip(ttft_w, base)), 1),
-                                    "strict_dttft_ms": round(sum(t - b for t, b in zip(ttft_s, base)), 1),
-                                    "hot_strict_dttft_ms": round(sum(t - b for t, b in zip(ttft_h, base)), 1),
-                                    "hot_wdrr_dttft_ms": round(sum(t - b for t, b in zip(ttft_hw, base)), 1),
-                                    # Eq. 3 with layer 0 local: ready_l = l*X, added = (L-1) max(0, X - C)
-                                    "model_hot_dttft_ms": round(sum((L - 1) * max(0.0, s_ / r_ - c_)
-                                                                    for s_, c_, r_ in zip(s_i, c_i, rates)) * 1e3, 1),
-                                    "model_dttft_ms": round(sum(model) * 1e3, 1)}
-        res["equal_over_cal"] = round(res["policies"]["equal"]["dttft_ms"] /
-                                      max(1e-9, res["policies"]["cal_stall_opt"]["dttft_ms"]), 3)
-        res["equal_over_stall_opt"] = round(res["policies"]["equal"]["dttft_ms"] /
-                                            max(1e-9, res["policies"]["stall_opt"]["dttft_ms"]), 3)
-        res["wdrr_equal_over_cal"] = round(res["policies"]["equal"]["wdrr_dttft_ms"] /
-                                           max(1e-9, res["policies"]["cal_stall_opt"]["wdrr_dttft_ms"]), 3)
-        res["dispatch"] = ("dttft_ms: one fetch per request, each paced by its own kernel's minimal pacer "
-                           "(layer release times); strict_dttft_ms: the same fetches paced byte by byte; "
-                           "wdrr_dttft_ms: one batched launch in WDRR claim order, requests held at their "
-                           "rates (Alg. A2 lines 6-7); hot_strict_dttft_ms: strict pacing from a store that "
-                           "mirrors layer 0 in HBM (the link carries layers 1..L-1 only); hot_wdrr_dttft_ms: "
-                           "the WDRR launch from that store (mirrored units first, unpaced; reading c25)")
-        out[wl] = res
-        batch.close()
-        batch_hot.close()
-        for r in reqs:
-            r["d"].close()
-            r["d_hot"].close()
-        del reqs
-        store.close()
-        store_hot.close()
-        torch.cuda.empty_cache()
-    return out
-
-
-def cpu_baseline_leg():
-    import synth
-    from oracle.geometry import Layout
-    lay = Layout(*synth.LLAMA3_8B.as_tuple())
-    wl = OracleWorkload(1, N_CHUNKS_4K, lay)
-    layers = []
-    tot_b, tot_s = 0, 0.0
-    l = 0
-    while tot_s < 10.0 and l < lay.num_layers:
-        b, s = wl.run([l])
-        tot_b += b
-        tot_s += s
-        layers.append(l)
-        l += 1
-    c, ncpu = cores_used()
-    return {"value": tot_b / tot_s / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{len(layers)} of 32 layers of the 4K request (N=256, G=16, Bs=16), "
-                      f"{tot_s:.1f} s, single-threaded Python+numpy (host has {ncpu} cpus, affinity {c})"}
-
-
-def cpu_config3_leg():
-    """The oracle on one layer of the config-3 request (N = 4096 chunks, 256 MiB per layer): the
-    per-layer work depends on N and S only, so the layout is truncated to one layer to keep the
-    host copy of the store at 256 MiB instead of 8 GiB."""
-    import synth
-    from oracle.geometry import Layout
-    L8 = synth.LLAMA3_8B.as_tuple()
-    wl = OracleWorkload(3, 4096, Layout(1, *L8[1:]))
-    b, t = wl.run([0])
-    c, ncpu = cores_used()
-    return {"value": round(b / t / 1e9, 3), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"1 layer of the 64K request (N=4096, 512 MiB read+write), {t:.1f} s, single-threaded "
-                      f"Python+numpy (host has {ncpu} cpus, affinity {c})"}
-
-
 def main():
     args = parse()
     if args.impl == "reference":
+        from benchlib.reference import run_reference
         run_reference(args)
     else:
         main_ours(args)

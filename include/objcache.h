@@ -284,6 +284,12 @@ typedef struct {
                                 engines ignore it.  0 = stream order.            */
 } oc_fetch_opts;
 #define OC_FETCH_OVERLAP 1u
+/* OC_FETCH_FIRST_LAYER_FULL: with max_ctas set, layer 0 (the exposed X_0 of Eq. 3,
+ * P:457-460) is copied by the whole GPU and only layers 1..L-1 by max_ctas CTAs --
+ * for a fetch co-running with prefill compute, which needs layer 0 at once and
+ * the rest at the compute's pace (two launches; each announces its layers).
+ * PERSISTENT mode, kernel engines. */
+#define OC_FETCH_FIRST_LAYER_FULL 2u
 
 /* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and
  * return at once.  One fetch may be in flight per descriptor at a time; a
@@ -380,6 +386,13 @@ OC_API int oc_sync_layer(oc_desc* desc, uint32_t layer);
  * timer: out[0] = kernel start, out[1 + l] = layer l ready.  Blocks until the
  * fetch is complete.  `out` holds L + 1 values. */
 OC_API int oc_layer_times(oc_desc* desc, uint64_t* out);
+
+/* Asynchronous variant for pipelined callers: enqueues on `stream` a wait for
+ * the most recent fetch's completion and a copy of its L + 1 stamps into `out`
+ * (page-locked host or device memory, caller-owned; valid until `stream` has
+ * passed the copy).  Returns at once; the caller synchronises on `stream` (or an
+ * event recorded after this call) before reading `out`. */
+OC_API int oc_layer_times_async(oc_desc* desc, uint64_t* out, void* stream);
 
 /* Measurement support (not a step of the method): the compute window C_l of
  * the stall accounting (Eq. 3; a8).  Enqueues on `stream` (the

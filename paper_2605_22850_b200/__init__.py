@@ -36,7 +36,7 @@ TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
 BATCH_BY_REQUEST, BATCH_BY_POSITION = 0, 1
 COPY_LDST, COPY_BULK, COPY_CE, COPY_AUTO = 0, 1, 2, 3
-FETCH_OVERLAP = 1
+FETCH_OVERLAP, FETCH_FIRST_LAYER_FULL = 1, 2
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -111,6 +111,7 @@ _SIGS = {
     "oc_wait_layer": [_vp, ctypes.c_uint32, _vp],
     "oc_sync_layer": [_vp, ctypes.c_uint32],
     "oc_layer_times": [_vp, c_u64p],
+    "oc_layer_times_async": [_vp, _vp, _vp],
     "oc_emulate_compute": [ctypes.c_uint64, _vp, _vp],
     "oc_trace_read": [c_u64p, ctypes.c_uint64],
     "oc_schedule_bandwidth": [ctypes.c_int, ctypes.POINTER(CProfile), ctypes.c_uint64, ctypes.c_double,
@@ -416,11 +417,13 @@ class Descriptor:
         return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
 
     def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_AUTO, max_ctas=0, unit_bytes=0,
-                        pace_Bps=0.0, pace_strict=False, overlap=False):
+                        pace_Bps=0.0, pace_strict=False, overlap=False, first_layer_full=False):
         """`overlap`: OC_FETCH_OVERLAP -- the launch may overlap the stream's previous fetch's tail
-        (the caller guarantees that work does not touch this fetch's destination or sources)."""
+        (the caller guarantees that work does not touch this fetch's destination or sources).
+        `first_layer_full`: OC_FETCH_FIRST_LAYER_FULL -- with max_ctas, layer 0 uses the whole GPU."""
+        flags = (FETCH_OVERLAP if overlap else 0) | (FETCH_FIRST_LAYER_FULL if first_layer_full else 0)
         o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
-                       1 if pace_strict else 0, FETCH_OVERLAP if overlap else 0)
+                       1 if pace_strict else 0, flags)
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))
 
     def scatter_flat(self, flat_base: int, flat_capacity: int, stream=None, max_ctas=0, unit_bytes=0):
@@ -439,6 +442,12 @@ class Descriptor:
         out = np.zeros(self.num_layers + 1, dtype=np.uint64)
         _check(_lib.oc_layer_times(self._h, out.ctypes.data_as(c_u64p)))
         return out
+
+    def layer_times_async(self, out, stream=None):
+        """Enqueue on `stream` the copy of the stamps into `out` (pinned host or device tensor /
+        address of L + 1 u64), after the fetch completes; read it after synchronising `stream`."""
+        addr = int(out.data_ptr()) if hasattr(out, "data_ptr") else int(out)
+        _check(_lib.oc_layer_times_async(self._h, addr, _stream(stream)))
 
 
 def _ctarget(target, lay):
@@ -470,10 +479,22 @@ def _ctarget(target, lay):
     return t, keep
 
 
+class PreparedTarget:
+    """A target converted to its C form once (for callers that build many descriptors over the
+    same cache blocks: argument marshalling is then per call only for the keys)."""
+
+    def __init__(self, target, layout):
+        self.layout = _layout(layout)
+        self.ctarget, self._keep = _ctarget(target, self.layout)
+
+
 def build_descriptor(store: Store, keys, layout, target, delivery: int = DELIVER_LAYER_MAJOR) -> Descriptor:
     k = _keys_array(keys)
-    lay = _layout(layout)
-    t, keep = _ctarget(target, lay)
+    if isinstance(target, PreparedTarget):
+        lay, t, keep = target.layout, target.ctarget, [target]
+    else:
+        lay = _layout(layout)
+        t, keep = _ctarget(target, lay)
     keep.append(k)
     h, bad = _vp(), ctypes.c_uint64()
     rc = _lib.oc_build_descriptor(store._h, k.ctypes.data, k.shape[0], ctypes.byref(lay), int(delivery),

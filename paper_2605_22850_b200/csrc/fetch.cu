@@ -492,6 +492,18 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
                                               : launch_ldst(d, sms, caps[part], g0, g1, s);
             if (rc) return rc;
         }
+    } else if (o.mode == OC_FETCH_PERSISTENT && (o.flags & OC_FETCH_FIRST_LAYER_FULL) && max_ctas && !paced &&
+               dd.L > 1) {
+        // Layer 0 with the whole GPU (its transfer is exposed before any compute can start), the
+        // rest with the caller's copy-CTA budget (they only have to keep ahead of the compute).
+        const uint32_t ranges[2][2] = {{0, upl}, {upl, (uint32_t)total_units}};
+        const uint32_t caps[2] = {0, max_ctas};
+        for (int part = 0; part < 2; part++) {
+            const uint32_t g0 = ranges[part][0], g1 = ranges[part][1];
+            int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, plan_bulk(dd, sms, caps[part], g1 - g0), g0, g1, s)
+                                              : launch_ldst(d, sms, caps[part], g0, g1, s);
+            if (rc) return rc;
+        }
     } else if (o.mode == OC_FETCH_PERSISTENT) {
         BulkPlan p = plan_bulk(dd, sms, max_ctas, total_units);
         if (paced) shallow_ring(&p);
@@ -901,6 +913,17 @@ OC_API int oc_layer_times(oc_desc* h, uint64_t* out) {
     oc::DeviceGuard dg(d->device);
     OC_CUDA(cudaEventSynchronize(d->done_ev));
     OC_CUDA(cudaMemcpy(out, d->dd.ts, (d->geo.L + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return OC_OK;
+}
+
+OC_API int oc_layer_times_async(oc_desc* h, uint64_t* out, void* stream) {
+    if (!h || !out) return oc::fail(OC_EINVAL, "layer_times_async: null pointer");
+    Desc* d = (Desc*)h;
+    if (!d->fetched) return oc::fail(OC_EINVAL, "layer_times_async: no fetch has been issued");
+    oc::DeviceGuard dg(d->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    OC_CUDA(cudaStreamWaitEvent(s, d->done_ev, 0));
+    OC_CUDA(cudaMemcpyAsync(out, d->dd.ts, (d->geo.L + 1) * sizeof(uint64_t), cudaMemcpyDefault, s));
     return OC_OK;
 }
 
