@@ -40,14 +40,25 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def kernel_src_sha16():
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("fetch_kernels.cuh", "fetch.cu", "oc_internal.h"):
+        with open(os.path.join(ROOT, "paper_2605_22850_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    """(dram bytes per launch of the dominant kernel from the committed ncu --set full summary, whether
+    that capture is of the current kernel sources); (None, False) without a capture."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            s = json.load(f)
+        return s.get("dram_bytes_per_launch"), s.get("kernel_src_sha16") == kernel_src_sha16()
     except Exception:
-        return None
+        return None, False
 
 
 class ClockSampler:

@@ -114,6 +114,7 @@ def run(args, oc, torch, dev, lay_t, ws, rank, dist=None, backend="nccl"):
     value = ws * bytes_per_step * args.steps / (elapsed_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     achieved = bytes_per_step * args.steps / (copy_ms / 1e3) / 1e9
+    traffic, traffic_fresh = ncu_traffic()
 
     # diagnostics outside the timed region: isolated launches (stream order, no overlap)
     iso = []
@@ -152,7 +153,11 @@ def run(args, oc, torch, dev, lay_t, ws, rank, dist=None, backend="nccl"):
         "value": value, "ms_per_step": ms_per_step, "clocks": clk,
         "gpu_launches": args.steps * (L if args.mode == "per_layer" else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(), "peak_source": peak_src, "kernel": "fetch_bulk_kernel<0>",
+                     "traffic": traffic if traffic_fresh else None,
+                     "traffic_source": ("profiles/ncu_full_summary.json (ncu --set full of the current kernel "
+                                        "sources)" if traffic_fresh else
+                                        "none: the committed capture is of older kernel sources"),
+                     "peak_source": peak_src, "kernel": "fetch_bulk_kernel<0>",
                      "bytes_per_launch": bytes_per_step,
                      "mean_launch_us": copy_ms * 1e3 / args.steps,
                      "timing": "CUDA events on the copy stream around the K back-to-back launches"},

@@ -172,7 +172,8 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
     (flash-attn, GQA 32/8 heads; the two partial outputs are summed, not LSE-merged: timing shape
     only), the O projection (4096x4096), gate+up (4096x28672) and down (14336x4096) GEMMs.
     TTFT = fetch launch -> end of the last layer (CUDA events); added = TTFT - the same chain with
-    the KV already resident.  Three runs per variant (mean, min, max).
+    the KV already resident, run right before it on the same streams (5 pairs per variant, the
+    highest and lowest dropped; mean, min, max of the other 3).
 
     Variants of the HBM-tier fetch: the whole GPU (default launch, the fetch runs far ahead of the
     compute and holds SMs the GEMMs want); copy-CTA budgets; first_layer_full (layer 0 -- the
@@ -232,16 +233,31 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
             return a0.elapsed_time(a1)
 
         chain(None, {})
-        base = min(chain(None, {}) for _ in range(3))
+        base = statistics.median(chain(None, {}) for _ in range(3))
         res = {"miss_tokens": m, "hit_chunks": N, "compute_ms_resident": round(base, 3),
                "compute_ms_per_layer": round(base / L, 4),
                "r_star_GBps": round(N * S / (base / L / 1e3) / 1e9, 1)}
         hbm_variants = (("full_gpu", {"engine": oc.COPY_BULK}, None),
+                        # one or two 64 KiB-ring CTAs per SM: the fetch leaves room on every SM for a
+                        # GEMM or attention CTA instead of holding all of them
+                        ("ctas148_u32k", {"engine": oc.COPY_BULK, "max_ctas": 148, "unit_bytes": 32768}, None),
+                        ("ctas296_u32k", {"engine": oc.COPY_BULK, "max_ctas": 296, "unit_bytes": 32768}, None),
                         ("ctas16", {"engine": oc.COPY_BULK, "max_ctas": 16}, None),
                         ("first_full_ctas8", {"engine": oc.COPY_BULK, "max_ctas": 8, "first_layer_full": True}, None),
                         ("first_full_ctas4", {"engine": oc.COPY_BULK, "max_ctas": 4, "first_layer_full": True}, None),
                         ("first_full_ctas8_prio", {"engine": oc.COPY_BULK, "max_ctas": 8, "first_layer_full": True},
-                         (lo_s, hi_s)))
+                         (lo_s, hi_s)),
+                        # LD/ST engine (16 KiB of static shared memory, no ring): copy CTAs small
+                        # enough to share an SM with a GEMM or attention CTA instead of excluding it
+                        ("ldst_first_full_ctas148", {"engine": oc.COPY_LDST, "max_ctas": 148, "first_layer_full": True},
+                         None),
+                        ("ldst_first_full_ctas32", {"engine": oc.COPY_LDST, "max_ctas": 32, "first_layer_full": True},
+                         None),
+                        ("ldst_full_gpu", {"engine": oc.COPY_LDST}, None),
+                        # layer 0 with the whole GPU, then one unit per CTA: the prefill's kernels on a
+                        # higher-priority stream take the SMs as the copy CTAs retire
+                        ("yield_prio", {"engine": oc.COPY_BULK, "yield_sms": True}, (lo_s, hi_s)),
+                        ("yield", {"engine": oc.COPY_BULK, "yield_sms": True}, None))
         tiers = [("hbm", oc.TIER_HBM, hbm_variants)]
         if not getattr(args, "stall_gemm_hbm_only", False):
             tiers += [("pinned_host", oc.TIER_PINNED_HOST, (("sm", {"engine": oc.COPY_BULK}, None),
@@ -258,7 +274,14 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
             for vname, fopts, streams in variants:
                 cs, ks = streams if streams else (None, None)
                 chain(d, fopts, cs, ks)
-                runs = [chain(d, fopts, cs, ks) - base for _ in range(3)]
+                # paired runs: each fetch chain next to a resident chain on the same streams, so a
+                # drift of the compute's own duration cancels
+                runs = []
+                for _ in range(5):
+                    b_ = chain(None, {}, cs, ks)
+                    runs.append(chain(d, fopts, cs, ks) - b_)
+                runs.sort()
+                runs = runs[1:-1]                     # drop the extreme pair of each side
                 t_ = d.layer_times().astype(np.int64)
                 res[f"{tier_name}_{vname}"] = {"added_ms_mean": round(st_.mean(runs), 3),
                                                "added_ms_min": round(min(runs), 3), "added_ms_max": round(max(runs), 3),

@@ -290,6 +290,12 @@ typedef struct {
  * the rest at the compute's pace (two launches; each announces its layers).
  * PERSISTENT mode, kernel engines. */
 #define OC_FETCH_FIRST_LAYER_FULL 2u
+/* OC_FETCH_YIELD: layer 0 with the whole GPU as a persistent launch, then layers
+ * 1..L-1 with one work unit per CTA (a grid of all their units): CTAs retire as they
+ * finish, so the kernels of a higher-priority stream (the co-running prefill) take
+ * their SMs as soon as they are launched and the fetch fills the rest.  Use with a
+ * low-priority copy stream.  PERSISTENT mode, BULK engine, HBM-resident chunks. */
+#define OC_FETCH_YIELD 4u
 
 /* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and
  * return at once.  One fetch may be in flight per descriptor at a time; a

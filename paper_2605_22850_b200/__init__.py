@@ -36,7 +36,7 @@ TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
 BATCH_BY_REQUEST, BATCH_BY_POSITION = 0, 1
 COPY_LDST, COPY_BULK, COPY_CE, COPY_AUTO = 0, 1, 2, 3
-FETCH_OVERLAP, FETCH_FIRST_LAYER_FULL = 1, 2
+FETCH_OVERLAP, FETCH_FIRST_LAYER_FULL, FETCH_YIELD = 1, 2, 4
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -417,11 +417,13 @@ class Descriptor:
         return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
 
     def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_AUTO, max_ctas=0, unit_bytes=0,
-                        pace_Bps=0.0, pace_strict=False, overlap=False, first_layer_full=False):
+                        pace_Bps=0.0, pace_strict=False, overlap=False, first_layer_full=False, yield_sms=False):
         """`overlap`: OC_FETCH_OVERLAP -- the launch may overlap the stream's previous fetch's tail
         (the caller guarantees that work does not touch this fetch's destination or sources).
-        `first_layer_full`: OC_FETCH_FIRST_LAYER_FULL -- with max_ctas, layer 0 uses the whole GPU."""
-        flags = (FETCH_OVERLAP if overlap else 0) | (FETCH_FIRST_LAYER_FULL if first_layer_full else 0)
+        `first_layer_full`: OC_FETCH_FIRST_LAYER_FULL -- with max_ctas, layer 0 uses the whole GPU.
+        `yield_sms`: OC_FETCH_YIELD -- layers after the first one unit per CTA (co-running prefill)."""
+        flags = ((FETCH_OVERLAP if overlap else 0) | (FETCH_FIRST_LAYER_FULL if first_layer_full else 0) |
+                 (FETCH_YIELD if yield_sms else 0))
         o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
                        1 if pace_strict else 0, flags)
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))

@@ -97,8 +97,9 @@ BlockLayout block_layout(uint64_t n, uint32_t L, size_t nb, bool with_pos, bool 
     b.o_ts = align16(b.o_vb + L * 8);
     b.o_cnt = align16(b.o_ts + (L + 1) * 8);
     b.o_ready = align16(b.o_cnt + L * 4);
-    b.o_next = b.o_ready + 4;
-    b.o_bt = align16(b.o_ready + 16);
+    // the claim slots on their own 128-byte line (apart from the polled ready word)
+    b.o_next = (b.o_ready + 4 + 127) & ~size_t(127);
+    b.o_bt = b.o_next + kClaimSlots * kClaimSlotStride * 4;
     b.o_pos = align16(b.o_bt + nb * 4);
     b.o_hot = align16(b.o_pos + (with_pos ? n * 4 : 0));
     b.total = align16(b.o_hot + (with_hot ? n * 8 : 0));

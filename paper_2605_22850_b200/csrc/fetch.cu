@@ -22,6 +22,7 @@
 // PER_LAYER mode each layer is its own launch followed by a CUDA event.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -165,6 +166,9 @@ int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream
     OC_CUDA(set_bulk_smem<kSingle>(p.smem));
     DevDesc dd = d->dd;
     dd.trace = trace_buffer(d->device, s);
+    const uint32_t slot = d->launch_seq++ % kClaimSlots;
+    dd.next_unit = d->dd.next_unit + slot * kClaimSlotStride;
+    const uint32_t grab = d->grab_ctr[slot];
     static const uint32_t ramp = (env_int("OC_RAMP_STATIC2", 1) ? kRampStatic2 : 0u) |
                                  (env_int("OC_RAMP_FIRST_LAYER", 1) ? kRampFirstLayer : 0u);
     dd.ramp = ramp;
@@ -179,9 +183,9 @@ int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = overlap ? attr : nullptr;
     cfg.numAttrs = overlap ? 1 : 0;
-    OC_CUDA(cudaLaunchKernelEx(&cfg, fetch_bulk_kernel<kSingle>, dd, BatchArgs{}, g0, g1, d->grab_ctr, p.stages,
+    OC_CUDA(cudaLaunchKernelEx(&cfg, fetch_bulk_kernel<kSingle>, dd, BatchArgs{}, g0, g1, grab, p.stages,
                                p.stage_bytes));
-    d->grab_ctr += g1 - g0 - extra;  // counter claims: units past the static ones + one overshoot per CTA
+    d->grab_ctr[slot] += g1 - g0 - extra;  // counter claims: units past the static ones + one overshoot per CTA
     return OC_OK;
 }
 
@@ -191,9 +195,12 @@ int launch_ldst(Desc* d, int sms, uint32_t max_ctas, uint32_t g0, uint32_t g1, c
     uint64_t grid = (uint64_t)occ * sms - 1;
     if (max_ctas) grid = std::min<uint64_t>(grid, max_ctas);
     grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, g1 - g0));
-    fetch_ldst_kernel<<<(unsigned)grid + 1, kThreads, 0, s>>>(d->dd, g0, g1, d->grab_ctr);
+    DevDesc dd = d->dd;  // stream-ordered (no dependent launch): its slot's earlier user is done
+    const uint32_t slot = d->launch_seq++ % kClaimSlots;
+    dd.next_unit = d->dd.next_unit + slot * kClaimSlotStride;
+    fetch_ldst_kernel<<<(unsigned)grid + 1, kThreads, 0, s>>>(dd, g0, g1, d->grab_ctr[slot]);
     OC_CUDA(cudaGetLastError());
-    d->grab_ctr += (g1 - g0) + (uint32_t)grid;
+    d->grab_ctr[slot] += (g1 - g0) + (uint32_t)grid;
     return OC_OK;
 }
 
@@ -492,6 +499,19 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
                                               : launch_ldst(d, sms, caps[part], g0, g1, s);
             if (rc) return rc;
         }
+    } else if (o.mode == OC_FETCH_PERSISTENT && (o.flags & OC_FETCH_YIELD) && o.engine == OC_COPY_BULK && !paced &&
+               !host_src) {
+        // Co-running with prefill: layer 0 with the whole GPU (persistent grid), then layers
+        // 1..L-1 with one unit per CTA -- CTAs retire as they finish, so kernels of a higher-priority
+        // stream take their SMs as soon as they are launched and the fetch fills what is left.
+        int rc = launch_bulk(d, plan_bulk(dd, sms, 0, upl), 0, upl, s);
+        if (rc) return rc;
+        if (dd.L > 1) {
+            BulkPlan p = plan_bulk(dd, sms, 0, (uint64_t)total_units - upl);
+            p.copy_ctas = (uint32_t)(total_units - upl);
+            rc = launch_bulk(d, p, upl, (uint32_t)total_units, s);
+            if (rc) return rc;
+        }
     } else if (o.mode == OC_FETCH_PERSISTENT && (o.flags & OC_FETCH_FIRST_LAYER_FULL) && max_ctas && !paced &&
                dd.L > 1) {
         // Layer 0 with the whole GPU (its transfer is exposed before any compute can start), the
@@ -512,9 +532,20 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
                                           : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
         if (rc) return rc;
     } else {
-        const BulkPlan p = plan_bulk(dd, sms, max_ctas, upl);
+        // PER_LAYER: one launch + one CUDA event per layer.  The layers' launches are independent
+        // (disjoint units, sources and destinations), so layer l+1's launch is a programmatic
+        // dependent of layer l's and fills the SMs as layer l's CTAs drain; event l still records
+        // the completion of layer l's launch.  Layer 0 follows the stream's earlier work unless the
+        // caller set OC_FETCH_OVERLAP.
+        // Default grid: 3/4 of the SMs' worth of copy CTAs per layer, so the CTAs of two to three
+        // consecutive layers' launches are resident together -- the next layer's loads are in flight
+        // while this layer's stores drain (profiles/r02_per_layer_sweep.json: 6.69 TB/s at 111 CTAs
+        // vs 5.0 with a full grid per layer, 6.77 for the single persistent launch).
+        const uint32_t pl_ctas = max_ctas ? max_ctas : std::max<uint32_t>(1, (uint32_t)sms * 3 / 4);
+        const BulkPlan p = plan_bulk(dd, sms, pl_ctas, upl);
         for (uint32_t l = 0; l < dd.L; l++) {
-            int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, l * upl, (l + 1) * upl, s)
+            const bool ov = l > 0 || (o.flags & OC_FETCH_OVERLAP);
+            int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, l * upl, (l + 1) * upl, s, ov)
                                               : launch_ldst(d, sms, max_ctas, l * upl, (l + 1) * upl, s);
             if (rc) return rc;
             OC_CUDA(cudaEventRecord(d->events[l], s));

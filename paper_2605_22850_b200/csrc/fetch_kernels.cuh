@@ -499,11 +499,13 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     constexpr bool BATCH = MODE != kSingle;
     __shared__ __align__(8) uint64_t fifo_full[kFifo], fifo_empty[kFifo];
     const uint64_t t0 = globaltimer();
+    // kSingle: a dependent launch (OC_FETCH_OVERLAP, or the next layer's launch in PER_LAYER mode)
+    // may start at once: it claims from another counter slot and waits for its slot's earlier user
+    if (!BATCH) allow_dependents();
     if (blockIdx.x == 0) {
         if (BATCH) {
             if (threadIdx.x < 32) observe_batch(ba, t0);
         } else {
-            allow_dependents();  // the observer never claims
             if (threadIdx.x == 0) {
                 if (g0 == 0 && d0.staged != 1) d0.ts[0] = t0;  // CE engine: stamped when the copies start
                 observe_layers(d0, g0 / d0.units_per_layer, g1 / d0.units_per_layer);
@@ -530,7 +532,6 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (threadIdx.x >= 32) {  // ---- signaler warp
-        if (!BATCH) allow_dependents();  // it never claims
         if (threadIdx.x != 32) return;
         // Each round takes every record already in the FIFO (waiting only for the first), merges
         // records of the same (request, layer), then publishes them with ONE GPU-scope release
@@ -665,6 +666,12 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
                 } else {
                     gg = g0 + copy_ctas + extra + (next_raw - grab_base);
                 }
+                if (k == 0) {
+                    // the slot's previous user (a launch kSlots launches ago, possibly still running
+                    // under a dependent launch) has made all its claims once the counter reaches
+                    // this launch's base; in stream order it has long finished
+                    while ((int32_t)(*(volatile uint32_t*)claim_ctr - grab_base) < 0) __nanosleep(64);
+                }
             } else {
                 gg = g0 + (next_raw - grab_base);
             }
@@ -743,7 +750,6 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
     const uint32_t first_layer = MODE == kSingle ? fdiv(g0, d0.div_upl) : 0u;
     const bool first_layer_hold = MODE == kSingle && !paced && (d0.ramp & kRampFirstLayer);
 
-    bool triggered = false;    // allow_dependents() issued (warp-uniform)
     uint32_t next_retire = 0;  // first unit not yet retired (same value in every lane)
     uint32_t k = 0;
     for (;; k++) {
@@ -806,10 +812,6 @@ __global__ void __launch_bounds__(64) fetch_bulk_kernel(const __grid_constant__ 
         uint32_t got = 0;
         if (need && lane == 0) got = claim(kl) ? 1u : 0u;
         got = __shfl_sync(0xffffffffu, got, 0);
-        if (need && !got && !triggered) {  // this CTA's claims are over: a dependent launch may start
-            allow_dependents();
-            triggered = true;
-        }
         if (need && got) {
             issued++;
             if (first_layer_hold && u.layer == first_layer) {

@@ -133,7 +133,7 @@ struct DevDesc {
     const uint64_t* k_base;   // [L]
     const uint64_t* v_base;   // [L]
     uint32_t* unit_cnt;       // [L] units completed (monotone across fetches)
-    uint32_t* next_unit;      // unit claim counter (monotone across launches)
+    uint32_t* next_unit;      // unit claim counter of this launch's slot (monotone across launches)
     uint32_t* ready;          // (epoch-1)*L + number of layers announced in this fetch (monotone)
     uint64_t* ts;             // [L+1] globaltimer: [0] kernel start, [1+l] layer ready
     uint64_t S;               // bytes of one layer of one chunk
@@ -179,6 +179,12 @@ inline __host__ __device__ uint32_t ramp_extra(uint32_t g0, uint32_t g1, uint32_
     return first_end - base2 < copy_ctas ? first_end - base2 : copy_ctas;
 }
 constexpr uint32_t kTraceSlots = 8;     // stamps per CTA (fetch_kernels.cuh, bulk engine)
+// Claim counters per descriptor: consecutive launches claim from different slots (32 bytes apart),
+// so a launch that starts during the previous one's tail (programmatic dependent launch) cannot mix
+// its claims with that launch's; a launch waits (once, before its first counter claim) until its
+// slot's previous user has made all of its claims.
+constexpr uint32_t kClaimSlots = 4;
+constexpr uint32_t kClaimSlotStride = 8;  // uint32 words
 constexpr uint32_t kTraceCtas = 2048;   // CTAs traced per launch
 
 struct Desc {
@@ -196,7 +202,8 @@ struct Desc {
     DevDesc dd;                // geometry part filled at build; epoch/units/pace at fetch
     uint32_t epoch = 0;
     uint32_t cnt_base = 0;     // unit_cnt[l] before the next fetch (same for every layer)
-    uint32_t grab_ctr = 0;     // *next_unit before the next launch
+    uint32_t grab_ctr[kClaimSlots] = {};  // each claim slot's counter value before its next launch
+    uint32_t launch_seq = 0;   // launches so far: launch n claims from slot n % kClaimSlots
     uint32_t last_mode = OC_FETCH_PERSISTENT;
     bool fetched = false;
     bool poisoned = false;     // a launch failed after the counters moved to a new epoch

@@ -33,6 +33,19 @@ def raw(report):
     return rows[0], rows[1], rows[2:]
 
 
+def kernel_src_sha16():
+    """Hash of the fetch kernel's sources: bench.py reports the committed traffic as stale when the
+    kernel changed after the capture."""
+    import hashlib
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    h = hashlib.sha256()
+    for f in ("fetch_kernels.cuh", "fetch.cu", "oc_internal.h"):
+        with open(os.path.join(root, "paper_2605_22850_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def full(report, dst, algo_bytes=None):
     hdr, units, launches = raw(report)
     res = []
@@ -64,7 +77,8 @@ def full(report, dst, algo_bytes=None):
             rec["achieved_GBps_under_ncu"] = algo_bytes / rec["gpu__time_duration.sum"] / 1e9
         res.append(rec)
     summary = {"report": report, "launches": res,
-               "dram_bytes_per_launch": res[0]["dram_bytes_per_launch"] if res else None}
+               "dram_bytes_per_launch": res[0]["dram_bytes_per_launch"] if res else None,
+               "kernel_src_sha16": kernel_src_sha16()}
     with open(dst, "w") as f:
         json.dump(summary, f, indent=1)
     return summary

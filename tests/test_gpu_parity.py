@@ -477,3 +477,33 @@ def test_overlap_back_to_back(lay, n_chunks):
     for desc in descs:
         desc.close()
     store.close()
+
+
+@pytest.mark.parametrize("lay,n_chunks", [(OLayout(3, 2, 64, 2, 16), 40), (OLayout(32, 8, 128, 2, 16), 64)])
+def test_first_layer_full_and_yield(lay, n_chunks):
+    """The co-running launch shapes: OC_FETCH_FIRST_LAYER_FULL (layer 0 with the whole GPU, the rest
+    under a copy-CTA budget, both engines) and OC_FETCH_YIELD (layer 0 persistent, the rest one unit
+    per CTA on a low-priority stream): same bytes as the oracle, layers announced in order."""
+    req = requests_family(lay, 81, 0, [n_chunks])[0]
+    dest = make_dest(lay, n_chunks, "nhd", Bs=16, first_token=5, seed=82)
+    want = oracle_result(lay, 81, req, dest)
+    store = oc.Store(lay, capacity=n_chunks)
+    store.put_chunks(oc.chunk_keys(req.tokens, lay.chunk_tokens), payload_stack(lay, 81, req.payload_ids))
+    buf = sentinel_buffer(dest.size)
+    d = oc.build_descriptor(store, store.match_prefix(req.tokens), lay, lib_target(oc, dest, buf.data_ptr()))
+    s, cons = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
+    for opts in (dict(engine=oc.COPY_BULK, max_ctas=4, first_layer_full=True),
+                 dict(engine=oc.COPY_LDST, max_ctas=7, first_layer_full=True),
+                 dict(engine=oc.COPY_BULK, yield_sms=True), dict(engine=oc.COPY_BULK)):
+        with torch.cuda.stream(s):
+            buf.fill_(0xA5)
+        d.fetch_layerwise(s, **opts)
+        for l in range(lay.num_layers):
+            d.wait_layer(l, cons)
+        cons.synchronize()
+        s.synchronize()
+        assert_same(buf.cpu().numpy(), want)
+        t = d.layer_times().astype(np.int64)
+        assert np.all(np.diff(t) >= 0), opts
+    d.close()
+    store.close()

@@ -37,3 +37,22 @@ def test_chunk_payload_range_is_a_slice_of_the_chunk():
     full = synth.chunk_payload(5, (1, 7), 4096)
     for off, n in ((0, 64), (8, 100), (2048, 2048), (4000, 96)):
         assert np.array_equal(synth.chunk_payload_range(5, (1, 7), off, n), full[off:off + n])
+
+
+def test_config5_routing_strong_scaling():
+    """Config 5's placement (benchlib/config5.py): the same 128 requests at every N; each served by its
+    family's home rank with probability ~p_aff, otherwise by a seeded uniform draw; N = 1 all local."""
+    from benchlib import config5
+    reqs = synth.serving_requests(5, 2000, config5.N_SHORT, config5.N_LONG)
+    assert reqs == synth.serving_requests(5, 2000, config5.N_SHORT, config5.N_LONG)
+    for ws in (1, 2, 4, 8):
+        home_of = lambda long, f: (f + config5.N_SHORT * int(long)) % ws
+        served = config5.route(reqs, ws, home_of)
+        assert served == config5.route(reqs, ws, home_of)
+        local = np.mean([s == home_of(lg, f) for s, (lg, f, _) in zip(served, reqs)])
+        if ws == 1:
+            assert local == 1.0
+        else:   # off-home draws land on the home rank 1/ws of the time
+            want = config5.P_AFF + (1 - config5.P_AFF) / ws
+            assert abs(local - want) < 0.03
+        assert set(served) <= set(range(ws))
