@@ -171,15 +171,26 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
     query, so their block order does not matter) -- plus causal attention over the m new tokens
     (flash-attn, GQA 32/8 heads; the two partial outputs are summed, not LSE-merged: timing shape
     only), the O projection (4096x4096), gate+up (4096x28672) and down (14336x4096) GEMMs.
-    TTFT = fetch launch -> end of the last layer (CUDA events); added = TTFT - the same chain with
-    the KV already resident, run right before it on the same streams (5 pairs per variant, the
-    highest and lowest dropped; mean, min, max of the other 3).
 
-    Variants of the HBM-tier fetch: the whole GPU (default launch, the fetch runs far ahead of the
-    compute and holds SMs the GEMMs want); copy-CTA budgets; first_layer_full (layer 0 -- the
-    exposed X0 -- with the whole GPU, layers 1..L-1 with a few 1-CTA-per-SM copy CTAs that keep ahead
-    of the compute); and the latter with the copy stream at low and the consumer at high priority."""
-    import statistics as st_
+    Timing: CUDA events after every layer on the consumer stream, from an event on the copy stream
+    just before the fetch launch.  Each measurement is a PAIR run back to back on the same streams:
+    the chain with the fetch, and the same chain on resident KV without waits; added = the
+    difference.  `pairs` pairs per variant; median, min, max reported.
+      added_ms       at the last layer (TTFT)
+      added_settled  at the end of the first layer whose compute ends after the fetch's last layer
+                     was announced, plus one: from there on the two chains run the same kernels on
+                     the same resident KV, so later layers add only the compute's own run-to-run
+                     noise (at 64K, +-1 ms over 688 ms) -- the low-noise estimate of the same
+                     quantity
+    Decomposition (medians): X0 (the fetch's first-layer announcement after its start, device
+    stamps), waits (the same consumer chain on a descriptor whose layers are all announced: the
+    wait_layer calls alone), contention = added_settled - X0 - waits (the copy's SM and HBM use
+    slowing the co-running prefill).
+
+    Variants of the HBM-tier fetch: full_gpu (default launch: the fetch holds every SM until it is
+    done), per_layer (one launch + event per layer), yield (OC_FETCH_YIELD: layer 0 with the whole
+    GPU, then one unit per CTA so the prefill's kernels take SMs back as copy CTAs retire) with the
+    copy stream at low and the consumer at high priority (yield_prio) or both at default priority."""
     import synth
     from flash_attn import flash_attn_func
     L, G, Bs = lay_t[0], lay_t[4], 16
@@ -188,8 +199,11 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
     w = [torch.randn(k, n, dtype=torch.bfloat16, device=dev) * 0.01
          for k, n in ((4096, 6144), (4096, 4096), (4096, 28672), (14336, 4096))]
     out = {"model": "llama3-8b layer: QKV, flash attention over the fetched hit KV + causal over the miss "
-                    "tokens, O, gate+up, down (random bf16 weights)", "runs": 3}
-    for name, ctx in (("4k", 4096), ("64k", 65536)):
+                    "tokens, O, gate+up, down (random bf16 weights)",
+           "method": "paired chains (fetch, resident-no-wait) back to back; CUDA events per layer on the consumer "
+                     "stream; median over pairs"}
+    cells = [("4k", 4096, 11)] + ([("64k", 65536, 5)] if getattr(args, "stall64k", 1) else [])
+    for name, ctx, pairs in cells:
         cached = ctx * 7 // 8
         m = ctx - cached
         N = cached // G
@@ -215,50 +229,38 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
             gu = torch.matmul(x, w[2])
             torch.matmul(gu[:, :14336], w[3])
 
-        def chain(d, fopts, cs=None, ks=None):
-            cs, ks = cs or copy_s, ks or cons_s
+        def chain(d, fopts, cs, ks, waits=True):
+            """Per-layer end times (ms after the launch event) of one consumer chain."""
             torch.cuda.synchronize()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0 = torch.cuda.Event(enable_timing=True)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(L)]
             a0.record(cs)
             ks.wait_event(a0)
-            if d is not None:
+            if fopts is not None:
                 d.fetch_layerwise(cs, **fopts)
             with torch.cuda.stream(ks):
                 for l in range(L):
-                    if d is not None:
+                    if d is not None and waits:
                         d.wait_layer(l, ks)
                     layer_compute(l)
-            a1.record(ks)
+                    ev[l].record(ks)
             torch.cuda.synchronize()
-            return a0.elapsed_time(a1)
+            return np.array([a0.elapsed_time(e) for e in ev])
 
-        chain(None, {})
-        base = statistics.median(chain(None, {}) for _ in range(3))
-        res = {"miss_tokens": m, "hit_chunks": N, "compute_ms_resident": round(base, 3),
-               "compute_ms_per_layer": round(base / L, 4),
-               "r_star_GBps": round(N * S / (base / L / 1e3) / 1e9, 1)}
-        hbm_variants = (("full_gpu", {"engine": oc.COPY_BULK}, None),
-                        # one or two 64 KiB-ring CTAs per SM: the fetch leaves room on every SM for a
-                        # GEMM or attention CTA instead of holding all of them
-                        ("ctas148_u32k", {"engine": oc.COPY_BULK, "max_ctas": 148, "unit_bytes": 32768}, None),
-                        ("ctas296_u32k", {"engine": oc.COPY_BULK, "max_ctas": 296, "unit_bytes": 32768}, None),
-                        ("ctas16", {"engine": oc.COPY_BULK, "max_ctas": 16}, None),
-                        ("first_full_ctas8", {"engine": oc.COPY_BULK, "max_ctas": 8, "first_layer_full": True}, None),
-                        ("first_full_ctas4", {"engine": oc.COPY_BULK, "max_ctas": 4, "first_layer_full": True}, None),
-                        ("first_full_ctas8_prio", {"engine": oc.COPY_BULK, "max_ctas": 8, "first_layer_full": True},
-                         (lo_s, hi_s)),
-                        # LD/ST engine (16 KiB of static shared memory, no ring): copy CTAs small
-                        # enough to share an SM with a GEMM or attention CTA instead of excluding it
-                        ("ldst_first_full_ctas148", {"engine": oc.COPY_LDST, "max_ctas": 148, "first_layer_full": True},
-                         None),
-                        ("ldst_first_full_ctas32", {"engine": oc.COPY_LDST, "max_ctas": 32, "first_layer_full": True},
-                         None),
-                        ("ldst_full_gpu", {"engine": oc.COPY_LDST}, None),
-                        # layer 0 with the whole GPU, then one unit per CTA: the prefill's kernels on a
-                        # higher-priority stream take the SMs as the copy CTAs retire
-                        ("yield_prio", {"engine": oc.COPY_BULK, "yield_sms": True}, (lo_s, hi_s)),
-                        ("yield", {"engine": oc.COPY_BULK, "yield_sms": True}, None))
-        tiers = [("hbm", oc.TIER_HBM, hbm_variants)]
+        def med(v):
+            v = sorted(v)
+            return {"median": round(statistics.median(v), 4), "min": round(v[0], 4), "max": round(v[-1], 4)}
+
+        chain(None, None, copy_s, cons_s)
+        base0 = chain(None, None, copy_s, cons_s)
+        res = {"miss_tokens": m, "hit_chunks": N, "pairs": pairs, "compute_ms_resident": round(float(base0[-1]), 3),
+               "compute_ms_per_layer": round(float(base0[-1]) / L, 4),
+               "r_star_GBps": round(N * S / (float(base0[-1]) / L / 1e3) / 1e9, 1)}
+        tiers = [("hbm", oc.TIER_HBM, (("full_gpu", {"engine": oc.COPY_BULK}, None),
+                                       ("per_layer", {"mode": oc.FETCH_PER_LAYER}, None),
+                                       ("yield", {"engine": oc.COPY_BULK, "yield_sms": True}, None),
+                                       ("yield_prio", {"engine": oc.COPY_BULK, "yield_sms": True}, (lo_s, hi_s)),
+))]
         if not getattr(args, "stall_gemm_hbm_only", False):
             tiers += [("pinned_host", oc.TIER_PINNED_HOST, (("sm", {"engine": oc.COPY_BULK}, None),
                                                             ("ce", {"engine": oc.COPY_CE}, None)))]
@@ -271,22 +273,37 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                 store.put_chunks(keys[b0:b0 + pl.shape[0]], pl)
                 del pl
             d = oc.build_descriptor(store, keys, lay_t, tgt)
+            if tier == oc.TIER_HBM:
+                # the waits alone: every layer already announced when the chain is enqueued
+                d.fetch_layerwise(copy_s)
+                torch.cuda.synchronize()
+                wv = []
+                for _ in range(pairs):
+                    b_ = chain(None, None, copy_s, cons_s)
+                    wv.append(float(chain(d, None, copy_s, cons_s)[-1] - b_[-1]))
+                res["waits_only_ms"] = med(wv)
             for vname, fopts, streams in variants:
-                cs, ks = streams if streams else (None, None)
+                cs, ks = streams if streams else (copy_s, cons_s)
                 chain(d, fopts, cs, ks)
-                # paired runs: each fetch chain next to a resident chain on the same streams, so a
-                # drift of the compute's own duration cancels
-                runs = []
-                for _ in range(5):
-                    b_ = chain(None, {}, cs, ks)
-                    runs.append(chain(d, fopts, cs, ks) - b_)
-                runs.sort()
-                runs = runs[1:-1]                     # drop the extreme pair of each side
-                t_ = d.layer_times().astype(np.int64)
-                res[f"{tier_name}_{vname}"] = {"added_ms_mean": round(st_.mean(runs), 3),
-                                               "added_ms_min": round(min(runs), 3), "added_ms_max": round(max(runs), 3),
-                                               "X0_ms": round((t_[1] - t_[0]) / 1e6, 4),
-                                               "fetch_span_ms": round((t_[L] - t_[0]) / 1e6, 3)}
+                added, settled, x0, span = [], [], [], []
+                for _ in range(pairs):
+                    b_ = chain(None, None, cs, ks)
+                    f_ = chain(d, fopts, cs, ks)
+                    t_ = d.layer_times().astype(np.int64)
+                    span_ms = (t_[L] - t_[0]) / 1e6
+                    k = int(np.searchsorted(b_, span_ms, side="right"))   # first layer ending after it
+                    k = min(k + 1, L - 1)
+                    added.append(float(f_[-1] - b_[-1]))
+                    settled.append(float(f_[k] - b_[k]))
+                    x0.append((t_[1] - t_[0]) / 1e6)
+                    span.append(span_ms)
+                cell = {"added_ms": med(added), "added_settled_ms": med(settled),
+                        "X0_ms": round(statistics.median(x0), 4), "fetch_span_ms": round(statistics.median(span), 3)}
+                if tier == oc.TIER_HBM:
+                    cell["decomposition_ms"] = {
+                        "X0": cell["X0_ms"], "waits": res["waits_only_ms"]["median"],
+                        "contention": round(statistics.median(settled) - cell["X0_ms"] - res["waits_only_ms"]["median"], 4)}
+                res[f"{tier_name}_{vname}"] = cell
             d.close()
             store.close()
         out[name] = res

@@ -382,11 +382,22 @@ OC_API int oc_wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* til
 /* wait_layer (NotifyLayerReady, Alg. A1 line 7): make `consumer_stream` wait,
  * without blocking the host, until layer `layer` of the most recent fetch is
  * in place.  Layers become ready in increasing order.  For CHUNK_MAJOR
- * delivery every layer waits for the whole prefix (Eq. 2 chunkwise). */
+ * delivery every layer waits for the whole prefix (Eq. 2 chunkwise).
+ * PERSISTENT mode: if the layer is already announced when the call is made (the
+ * announcing kernel also writes a pinned host copy of the ready word, after the
+ * device word), nothing is enqueued -- the bytes are already in place. */
 OC_API int oc_wait_layer(oc_desc* desc, uint32_t layer, void* consumer_stream);
 
 /* Host-blocking variant of wait_layer. */
 OC_API int oc_sync_layer(oc_desc* desc, uint32_t layer);
+
+/* layers_ready: *n = how many layers of the most recent fetch are announced, as
+ * the host sees it now (non-blocking poll of the pinned copy of the ready word;
+ * a layer counted here is in place in device memory).  PERSISTENT-mode fetches
+ * (kernel and CE engines); for a PER_LAYER fetch, the layers whose CUDA event
+ * has completed.  CHUNK_MAJOR delivery reports 0 or L.  EINVAL if no fetch was
+ * issued; ENOTSUP if the descriptor has no host mirror (pinned allocation failed). */
+OC_API int oc_layers_ready(oc_desc* desc, uint32_t* n);
 
 /* Per-layer ready times of the most recent fetch, in ns of the GPU global
  * timer: out[0] = kernel start, out[1 + l] = layer l ready.  Blocks until the

@@ -110,6 +110,7 @@ _SIGS = {
                      c_u32p, c_u32p, ctypes.c_uint64, c_u64p],
     "oc_wait_layer": [_vp, ctypes.c_uint32, _vp],
     "oc_sync_layer": [_vp, ctypes.c_uint32],
+    "oc_layers_ready": [_vp, ctypes.POINTER(ctypes.c_uint32)],
     "oc_layer_times": [_vp, c_u64p],
     "oc_layer_times_async": [_vp, _vp, _vp],
     "oc_emulate_compute": [ctypes.c_uint64, _vp, _vp],
@@ -439,6 +440,11 @@ class Descriptor:
 
     def sync_layer(self, layer: int):
         _check(_lib.oc_sync_layer(self._h, int(layer)))
+
+    def layers_ready(self) -> int:
+        n = ctypes.c_uint32(0)
+        _check(_lib.oc_layers_ready(self._h, ctypes.byref(n)))
+        return n.value
 
     def layer_times(self) -> np.ndarray:
         out = np.zeros(self.num_layers + 1, dtype=np.uint64)

@@ -357,6 +357,9 @@ OC_API int oc_build_descriptor(oc_store* sh, const oc_key* keys, uint64_t n, con
     rc = oc::upload_block(d->device, g, src, v, nullptr, "build_descriptor", &d->dev_mem, &d->dev_mem_class, &d->dd,
                           nullptr, &d->up, false, nullptr, hot_layers ? &hot : nullptr, hot_layers);
     if (rc) return rc;
+    // Without a mirror (pinned allocation failed) wait_layer always enqueues its stream wait.
+    d->ready_host = oc::ready_mirror_alloc();
+    d->dd.ready_host = d->ready_host;
     d->dd.chunk_major = delivery == OC_DELIVER_CHUNK_MAJOR;
     oc::plan_units(d.get(), 0);
     *out = (oc_desc*)d.release();
@@ -497,6 +500,7 @@ OC_API int oc_desc_free(oc_desc* h) {
         if (d->sync_stream) cudaStreamDestroy(d->sync_stream);
         oc::ce_release(d);
         oc::dev_pool_free(d->device, d->dev_mem, d->dev_mem_class);
+        oc::ready_mirror_free(d->ready_host);
         cudaGetLastError();
     }
     delete d;

@@ -324,7 +324,8 @@ int launch_fetch_ce(Desc* d, const oc_fetch_opts& o, cudaStream_t s) {
                                           (const void*)((hot ? d->run_hot[r] : d->run_src[r]) + (uint64_t)l * d->geo.S),
                                           hot ? d->run_hot_pitch[r] : d->geo.chunk, d->geo.S,
                                           d->run_len[r], cudaMemcpyDefault, kit.stream));
-            announce_kernel<<<1, 1, 0, kit.stream>>>(d->dd.ts + 1 + l, d->dd.ready, (epoch - 1u) * L + l + 1u);
+            announce_kernel<<<1, 1, 0, kit.stream>>>(d->dd.ts + 1 + l, d->dd.ready, d->dd.ready_host,
+                                                     (epoch - 1u) * L + l + 1u);
             OC_CUDA(cudaGetLastError());
         }
         OC_CUDA(cudaEventRecord(kit.ce_done[L - 1], kit.stream));
@@ -509,6 +510,7 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
         if (dd.L > 1) {
             BulkPlan p = plan_bulk(dd, sms, 0, (uint64_t)total_units - upl);
             p.copy_ctas = (uint32_t)(total_units - upl);
+            shallow_ring(&p);  // one unit per CTA: the smallest ring (2 stages) is the smallest footprint
             rc = launch_bulk(d, p, upl, (uint32_t)total_units, s);
             if (rc) return rc;
         }
@@ -905,6 +907,10 @@ OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {
         return OC_OK;
     }
     const uint32_t target = (d->epoch - 1u) * L + want_layer + 1u;
+    // Already announced (the host mirror is written after the device word, with system-scope
+    // release): the layer's bytes are in device memory, so nothing needs to be enqueued -- a stream
+    // wait costs the consumer ~1-4 us of launch pipelining even when its condition already holds.
+    if (d->ready_host && (int32_t)(__atomic_load_n(d->ready_host, __ATOMIC_ACQUIRE) - target) >= 0) return OC_OK;
     int urc = oc::upload_order(&d->up, s);  // the ready word lives in the uploaded block
     if (urc) return urc;
     if (!oc::force_wait_kernel()) {
@@ -927,13 +933,36 @@ OC_API int oc_sync_layer(oc_desc* h, uint32_t layer) {
         OC_CUDA(cudaEventSynchronize(d->events[want_layer]));
         return OC_OK;
     }
-    // Persistent mode: a private stream waits on the ready word; the host blocks on an event after it.
+    // Persistent mode: already announced per the host mirror, else a private stream waits on the
+    // ready word and the host blocks on an event after it.
+    const uint32_t target = (d->epoch - 1u) * d->geo.L + want_layer + 1u;
+    if (d->ready_host && (int32_t)(__atomic_load_n(d->ready_host, __ATOMIC_ACQUIRE) - target) >= 0) return OC_OK;
     if (!d->sync_stream) OC_CUDA(cudaStreamCreateWithFlags(&d->sync_stream, cudaStreamNonBlocking));
     if (!d->sync_ev) OC_CUDA(cudaEventCreateWithFlags(&d->sync_ev, cudaEventDisableTiming | cudaEventBlockingSync));
     int rc = oc_wait_layer(h, layer, d->sync_stream);
     if (rc) return rc;
     OC_CUDA(cudaEventRecord(d->sync_ev, d->sync_stream));
     OC_CUDA(cudaEventSynchronize(d->sync_ev));
+    return OC_OK;
+}
+
+OC_API int oc_layers_ready(oc_desc* h, uint32_t* n) {
+    if (!h || !n) return oc::fail(OC_EINVAL, "layers_ready: null pointer");
+    Desc* d = (Desc*)h;
+    if (!d->fetched) return oc::fail(OC_EINVAL, "layers_ready: no fetch has been issued");
+    const uint32_t L = d->geo.L;
+    uint32_t k = 0;
+    if (d->last_mode == OC_FETCH_PER_LAYER) {
+        oc::DeviceGuard dg(d->device);
+        while (k < L && cudaEventQuery(d->events[k]) == cudaSuccess) k++;
+        cudaGetLastError();
+    } else {
+        if (!d->ready_host) return oc::fail(OC_ENOTSUP, "layers_ready: descriptor has no host mirror");
+        const int32_t a = (int32_t)(__atomic_load_n(d->ready_host, __ATOMIC_ACQUIRE) - (d->epoch - 1u) * L);
+        k = a <= 0 ? 0u : std::min<uint32_t>((uint32_t)a, L);
+    }
+    if (d->delivery == OC_DELIVER_CHUNK_MAJOR && k < L) k = 0;
+    *n = k;
     return OC_OK;
 }
 

@@ -54,6 +54,14 @@ __device__ __forceinline__ void red_max_release(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// The host's copy of a ready word (pinned, mapped): a system-scope release store after the device
+// word, so a host thread that reads `v` there may skip its stream wait for any layer <= v.  Not
+// monotone under overlapped fetches of one descriptor (a lower value may land last); the host then
+// merely enqueues a wait it could have skipped.
+__device__ __forceinline__ void mirror_ready(uint32_t* host_word, uint32_t v) {
+    if (host_word) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(host_word), "r"(v) : "memory");
+}
+
 // Programmatic dependent launch: this CTA will issue no more claims, so a dependent launch (the
 // stream's next fetch, OC_FETCH_OVERLAP) may start claiming from the counter.  No-op otherwise.
 __device__ __forceinline__ void allow_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -135,6 +143,7 @@ __device__ void observe_layers(const DevDesc& d, uint32_t l0, uint32_t l1) {
         // max, not a plain store: with OC_FETCH_OVERLAP the next fetch of this descriptor may
         // already announce its early layers while this one announces its last ones
         red_max_release(d.ready, base + l + 1u);
+        mirror_ready(d.ready_host, base + l + 1u);
     }
 }
 
@@ -469,6 +478,7 @@ __device__ void observe_batch(const BatchArgs& ba, uint64_t t0) {
             while (l < d.L && (int32_t)(ld_acquire(&d.unit_cnt[l]) - d.cnt_target) >= 0) {
                 d.ts[1 + l] = globaltimer();
                 st_release(d.ready, base + l + 1u);
+                mirror_ready(d.ready_host, base + l + 1u);
                 l++;
                 moved = true;
             }
@@ -1099,9 +1109,10 @@ __global__ void stamp_kernel(uint64_t* ts) { ts[0] = globaltimer(); }
 
 // CE engine into a flat client buffer: layer l has landed (the copies before this kernel on the
 // copy stream are complete) -- stamp it and announce it, as the fetch kernel's observer does.
-__global__ void announce_kernel(uint64_t* ts, uint32_t* ready, uint32_t value) {
+__global__ void announce_kernel(uint64_t* ts, uint32_t* ready, uint32_t* ready_host, uint32_t value) {
     ts[0] = globaltimer();
     st_release(ready, value);
+    mirror_ready(ready_host, value);
 }
 
 __global__ void wait_geq_kernel(const uint32_t* addr, uint32_t value) {

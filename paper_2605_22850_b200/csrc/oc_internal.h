@@ -135,6 +135,7 @@ struct DevDesc {
     uint32_t* unit_cnt;       // [L] units completed (monotone across fetches)
     uint32_t* next_unit;      // unit claim counter of this launch's slot (monotone across launches)
     uint32_t* ready;          // (epoch-1)*L + number of layers announced in this fetch (monotone)
+    uint32_t* ready_host;     // pinned host copy of `ready`, written after it (wait_layer's fast path)
     uint64_t* ts;             // [L+1] globaltimer: [0] kernel start, [1+l] layer ready
     uint64_t S;               // bytes of one layer of one chunk
     uint64_t row;             // bytes of one token row (n_kv*d*p)
@@ -221,6 +222,7 @@ struct Desc {
     void* stage_mem = nullptr;
     uint64_t stage_class = 0;
     struct CeKit* ce_kit = nullptr;  // copy stream + per-layer events, pooled per (device, L)
+    uint32_t* ready_host = nullptr;  // pinned mirror of dd.ready (ready_mirror_alloc)
 };
 
 // CE engine resources returned to their pool when a descriptor is freed (fetch.cu).
@@ -230,6 +232,10 @@ void ce_release(Desc* d);
 // memory (device = -1), recycled instead of returned to the driver.
 void* dev_pool_alloc(int device, size_t n, uint64_t* cls_out);
 void dev_pool_free(int device, void* p, uint64_t cls);
+// A pinned, device-mapped word (its own 64-byte line) that mirrors a descriptor's ready word, so
+// the host can see which layers are announced without a device round trip; zeroed on allocation.
+uint32_t* ready_mirror_alloc();
+void ready_mirror_free(uint32_t* w);
 
 
 // Plan work units of about `unit_bytes` bytes and fill the unit fields of d->dd.

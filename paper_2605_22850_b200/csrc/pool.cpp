@@ -52,4 +52,33 @@ void dev_pool_free(int device, void* p, uint64_t cls) {
     g_pool.free_by_class[key_of(device, cls)].push_back(p);
 }
 
+namespace {
+std::mutex g_mirror_mu;
+std::vector<uint32_t*> g_mirror_free;
+constexpr size_t kMirrorLine = 64, kMirrorSlab = 64 * 1024;
+}  // namespace
+
+uint32_t* ready_mirror_alloc() {
+    std::lock_guard<std::mutex> lk(g_mirror_mu);
+    if (g_mirror_free.empty()) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, kMirrorSlab, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        for (size_t o = kMirrorSlab; o >= kMirrorLine; o -= kMirrorLine)
+            g_mirror_free.push_back((uint32_t*)((uint8_t*)p + o - kMirrorLine));
+    }
+    uint32_t* w = g_mirror_free.back();
+    g_mirror_free.pop_back();
+    __atomic_store_n(w, 0u, __ATOMIC_RELEASE);
+    return w;
+}
+
+void ready_mirror_free(uint32_t* w) {
+    if (!w) return;
+    std::lock_guard<std::mutex> lk(g_mirror_mu);
+    g_mirror_free.push_back(w);
+}
+
 }  // namespace oc
