@@ -190,7 +190,9 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
     Variants of the HBM-tier fetch: full_gpu (default launch: the fetch holds every SM until it is
     done), per_layer (one launch + event per layer), yield (OC_FETCH_YIELD: layer 0 with the whole
     GPU, then one unit per CTA so the prefill's kernels take SMs back as copy CTAs retire) with the
-    copy stream at low and the consumer at high priority (yield_prio) or both at default priority."""
+    copy stream at low and the consumer at high priority (yield_prio) or both at default priority,
+    and gated_u32k (oc_fetch_layers: layers 0-1 at once, layer l+2 requested on a highest-priority
+    stream after the consumer's attention of layer l, so it runs beside the MLP GEMMs)."""
     import synth
     from flash_attn import flash_attn_func
     L, G, Bs = lay_t[0], lay_t[4], 16
@@ -218,13 +220,17 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
         copy_s, cons_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         lo_s, hi_s = torch.cuda.Stream(device=dev, priority=0), torch.cuda.Stream(device=dev, priority=-1)
 
-        def layer_compute(l):
+        gate_s = torch.cuda.Stream(device=dev, priority=-2)   # clamped to the device's highest priority
+
+        def layer_compute(l, after_attn=None):
             qkv = torch.matmul(x, w[0])
             q = qkv[:, :4096].view(1, m, 32, d_h)
             kn = qkv[:, 4096:5120].view(1, m, n_kv, d_h)
             vn = qkv[:, 5120:].view(1, m, n_kv, d_h)
             a_hit = flash_attn_func(q, kvb[l, 0].unsqueeze(0), kvb[l, 1].unsqueeze(0), causal=False)
             a_new = flash_attn_func(q, kn, vn, causal=True)
+            if after_attn is not None:
+                after_attn(l)
             torch.matmul((a_hit + a_new).view(m, 4096), w[1])
             gu = torch.matmul(x, w[2])
             torch.matmul(gu[:, :14336], w[3])
@@ -236,13 +242,28 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(L)]
             a0.record(cs)
             ks.wait_event(a0)
-            if fopts is not None:
+            hook = None
+            if fopts is not None and "gated" in fopts:
+                # co-run schedule through oc_fetch_layers: the first k0 layers at once with the whole
+                # GPU; layer l + k0 on a highest-priority stream gated on the consumer's attention of
+                # layer l, so it runs beside layer l's MLP GEMMs (lean CTAs fit beside a GEMM CTA)
+                g = dict(fopts["gated"])
+                k0 = g.pop("k0")
+                d.fetch_layers(0, k0, cs, unit_bytes=g.get("unit_bytes", 0))
+
+                def hook(l):
+                    if l + k0 < L:
+                        e = torch.cuda.Event()
+                        e.record(ks)
+                        gate_s.wait_event(e)
+                        d.fetch_layers(l + k0, l + k0 + 1, gate_s, **g)
+            elif fopts is not None:
                 d.fetch_layerwise(cs, **fopts)
             with torch.cuda.stream(ks):
                 for l in range(L):
                     if d is not None and waits:
                         d.wait_layer(l, ks)
-                    layer_compute(l)
+                    layer_compute(l, hook)
                     ev[l].record(ks)
             torch.cuda.synchronize()
             return np.array([a0.elapsed_time(e) for e in ev])
@@ -260,7 +281,10 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                                        ("per_layer", {"mode": oc.FETCH_PER_LAYER}, None),
                                        ("yield", {"engine": oc.COPY_BULK, "yield_sms": True}, None),
                                        ("yield_prio", {"engine": oc.COPY_BULK, "yield_sms": True}, (lo_s, hi_s)),
-))]
+                                       # the co-run schedule through oc_fetch_layers (measured worse:
+                                       # profiles/r02_stall_gemm_gated.json)
+                                       ("gated_u32k", {"gated": {"k0": 2, "engine": oc.COPY_BULK, "max_ctas": 148,
+                                                                 "unit_bytes": 32768}}, None)))]
         if not getattr(args, "stall_gemm_hbm_only", False):
             tiers += [("pinned_host", oc.TIER_PINNED_HOST, (("sm", {"engine": oc.COPY_BULK}, None),
                                                             ("ce", {"engine": oc.COPY_CE}, None)))]

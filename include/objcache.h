@@ -297,11 +297,35 @@ typedef struct {
  * low-priority copy stream.  PERSISTENT mode, BULK engine, HBM-resident chunks. */
 #define OC_FETCH_YIELD 4u
 
+/* OC_FETCH_LEAN: the TMA engine's copy CTAs keep the smallest shared-memory ring
+ * (two units), so with small units (unit_bytes = 8192: ~18 KiB per CTA) a copy CTA
+ * fits on an SM beside a co-running GEMM's CTA (cuBLAS sm_100 tiles leave ~19 KiB)
+ * instead of excluding it.  PERSISTENT mode, BULK engine. */
+#define OC_FETCH_LEAN 16u
+
 /* fetch_layerwise: enqueue the transfer of all L layers on `copy_stream` and
  * return at once.  One fetch may be in flight per descriptor at a time; a
  * second fetch must be ordered after the first (same stream or an event).
  * opts = NULL selects the defaults (persistent, AUTO engine, auto grid, unpaced). */
 OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* copy_stream);
+
+/* fetch_layers: the transfer of layers [l0, l1) only, so the consumer decides
+ * when each part of the fetch runs (e.g. layer l+2 enqueued on a copy stream
+ * that waits for the consumer's attention of layer l, so the copy co-runs with
+ * that layer's MLP GEMMs instead of the attention).  l0 = 0 opens a new fetch
+ * exactly like fetch_layerwise (same contract; it fixes the unit size) and
+ * launches its first l1 layers; every later call continues it and must start
+ * where the previous call stopped (l0 = previous l1), in any stream order the
+ * caller guarantees (no two ranges of one fetch may overlap in time with a new
+ * fetch).  Layers are announced (wait_layer, layers_ready, layer_times) as each
+ * range completes.  A new fetch of the descriptor (any entry point) is refused
+ * with EINVAL until all L layers of the open one have been requested.
+ * opts: PERSISTENT mode, BULK or LDST engine (AUTO picks between them), unpaced;
+ * max_ctas and OC_FETCH_LEAN apply per call; unit_bytes only with l0 = 0 (a later
+ * call may repeat the same value or pass 0).  Errors: ERANGE (l0 >= l1 or l1 > L),
+ * EINVAL (out of order), ENOTSUP (other modes, engines, pacing). */
+OC_API int oc_fetch_layers(oc_desc* desc, uint32_t l0, uint32_t l1, const oc_fetch_opts* opts,
+                           void* copy_stream);
 
 /* scatter_flat -- the client half of the paper's unfused flow (Alg. A1 line 6 RDMA-writes B_l into
  * the client buffer; the client then copies it into its paged KV cache): a

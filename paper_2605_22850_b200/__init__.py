@@ -36,7 +36,7 @@ TENANT_WAITING, TENANT_RUNNING, TENANT_DONE, TENANT_CHUNKWISE = 0, 1, 2, 3
 DISPATCH_INDEPENDENT, DISPATCH_WDRR = 0, 1
 BATCH_BY_REQUEST, BATCH_BY_POSITION = 0, 1
 COPY_LDST, COPY_BULK, COPY_CE, COPY_AUTO = 0, 1, 2, 3
-FETCH_OVERLAP, FETCH_FIRST_LAYER_FULL, FETCH_YIELD = 1, 2, 4
+FETCH_OVERLAP, FETCH_FIRST_LAYER_FULL, FETCH_YIELD, FETCH_LEAN = 1, 2, 4, 16
 POLICIES = {"equal": 0, "kv_prop": 1, "bw_prop": 2, "stall_opt": 3, "cal_stall_opt": 4}
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -100,6 +100,7 @@ _SIGS = {
     "oc_desc_free": [_vp],
     "oc_desc_info": [_vp, c_u64p, c_u64p, c_u64p],
     "oc_fetch_layerwise": [_vp, ctypes.POINTER(CFetchOpts), _vp],
+    "oc_fetch_layers": [_vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(CFetchOpts), _vp],
     "oc_batch_create": [ctypes.POINTER(_vp), ctypes.c_uint32, ctypes.POINTER(_vp)],
     "oc_fetch_batch": [_vp, ctypes.POINTER(CFetchOpts), _vp],
     "oc_batch_free": [_vp],
@@ -396,6 +397,14 @@ class FlatTarget:
     capacity: int
 
 
+def _fetch_opts(mode, engine, max_ctas, unit_bytes, pace_Bps, pace_strict, overlap, first_layer_full, yield_sms,
+                lean):
+    flags = ((FETCH_OVERLAP if overlap else 0) | (FETCH_FIRST_LAYER_FULL if first_layer_full else 0) |
+             (FETCH_YIELD if yield_sms else 0) | (FETCH_LEAN if lean else 0))
+    return CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
+                      1 if pace_strict else 0, flags)
+
+
 class Descriptor:
     def __init__(self, handle, store, layout, keepalive):
         self._h = handle
@@ -418,16 +427,21 @@ class Descriptor:
         return {"n_chunks": n.value, "payload_W": W.value, "units_per_layer": u.value}
 
     def fetch_layerwise(self, stream=None, mode=FETCH_PERSISTENT, engine=COPY_AUTO, max_ctas=0, unit_bytes=0,
-                        pace_Bps=0.0, pace_strict=False, overlap=False, first_layer_full=False, yield_sms=False):
+                        pace_Bps=0.0, pace_strict=False, overlap=False, first_layer_full=False, yield_sms=False,
+                        lean=False):
         """`overlap`: OC_FETCH_OVERLAP -- the launch may overlap the stream's previous fetch's tail
         (the caller guarantees that work does not touch this fetch's destination or sources).
         `first_layer_full`: OC_FETCH_FIRST_LAYER_FULL -- with max_ctas, layer 0 uses the whole GPU.
-        `yield_sms`: OC_FETCH_YIELD -- layers after the first one unit per CTA (co-running prefill)."""
-        flags = ((FETCH_OVERLAP if overlap else 0) | (FETCH_FIRST_LAYER_FULL if first_layer_full else 0) |
-                 (FETCH_YIELD if yield_sms else 0))
-        o = CFetchOpts(int(mode), int(engine), int(max_ctas), int(unit_bytes), float(pace_Bps),
-                       1 if pace_strict else 0, flags)
+        `yield_sms`: OC_FETCH_YIELD -- layers after the first one unit per CTA (co-running prefill).
+        `lean`: OC_FETCH_LEAN -- the smallest shared-memory ring per copy CTA."""
+        o = _fetch_opts(mode, engine, max_ctas, unit_bytes, pace_Bps, pace_strict, overlap, first_layer_full,
+                        yield_sms, lean)
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))
+
+    def fetch_layers(self, l0: int, l1: int, stream=None, engine=COPY_AUTO, max_ctas=0, unit_bytes=0, lean=False):
+        """oc_fetch_layers: layers [l0, l1) of the current fetch (l0 = 0 opens a new one)."""
+        o = _fetch_opts(FETCH_PERSISTENT, engine, max_ctas, unit_bytes, 0.0, False, False, False, False, lean)
+        _check(_lib.oc_fetch_layers(self._h, int(l0), int(l1), ctypes.byref(o), _stream(stream)))
 
     def scatter_flat(self, flat_base: int, flat_capacity: int, stream=None, max_ctas=0, unit_bytes=0):
         """Scatter a layer-major payload [L][N][S] at device address flat_base into this
@@ -657,6 +671,10 @@ def match_prefix(store: Store, tokens, parent: Optional[bytes] = None) -> np.nda
 
 def fetch_layerwise(desc: Descriptor, stream=None, **opts):
     desc.fetch_layerwise(stream, **opts)
+
+
+def fetch_layers(desc: Descriptor, l0: int, l1: int, stream=None, **opts):
+    desc.fetch_layers(l0, l1, stream, **opts)
 
 
 def wait_layer(desc: Descriptor, layer: int, stream=None):

@@ -396,6 +396,7 @@ int launch_scatter_flat(Desc* d, uint64_t flat, uint64_t cap, const oc_fetch_opt
     if (cap < d->N * d->geo.L * d->geo.S) return fail(OC_ERANGE, "scatter_flat: flat payload smaller than N*L*S");
     if (flat % 16) return fail(OC_EALIGN, "scatter_flat: flat base not 16-byte aligned");
     if (d->poisoned) return fail(OC_ECUDA, "scatter_flat: descriptor unusable after a failed launch");
+    if (d->range_open) return fail(OC_EINVAL, "scatter_flat: the previous fetch_layers fetch is incomplete");
     DeviceGuard dg(d->device);
     int urc = upload_order(&d->up, s);
     if (urc) return urc;
@@ -426,10 +427,52 @@ int launch_scatter_flat(Desc* d, uint64_t flat, uint64_t cap, const oc_fetch_opt
     return OC_OK;
 }
 
-int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
+// Layers [l0, l1) of the descriptor's current fetch (oc_fetch_layers): l0 == 0 opens a new fetch
+// like fetch_layerwise and launches only its first layers; l0 > 0 continues it where the previous
+// call stopped.  One launch per call over the range's units, announced by its observer CTA.
+int launch_fetch_range(Desc* d, const oc_fetch_opts& oin, uint32_t l0, uint32_t l1, cudaStream_t s) {
+    const uint32_t L = d->geo.L;
+    if (l0 >= l1 || l1 > L) return fail(OC_ERANGE, "fetch_layers: need l0 < l1 <= L");
+    if (l0 == 0) return launch_fetch(d, oin, s, l1);
+    if (!d->fetched || d->range_open != l0)
+        return fail(OC_EINVAL, "fetch_layers: layers must follow the previous call's range (l0 = its l1)");
     oc_fetch_opts o = oin;
+    if (o.engine == OC_COPY_AUTO) o.engine = d->dd.nhd ? OC_COPY_BULK : OC_COPY_LDST;
+    if (o.mode != OC_FETCH_PERSISTENT || o.pace_Bps != 0 || (o.engine != OC_COPY_BULK && o.engine != OC_COPY_LDST))
+        return fail(OC_ENOTSUP, "fetch_layers: PERSISTENT mode, BULK or LDST engine, unpaced");
+    if (o.unit_bytes && o.unit_bytes != d->range_unit_bytes)
+        return fail(OC_EINVAL, "fetch_layers: the unit size is fixed by the call with l0 = 0");
+    if (d->poisoned) return fail(OC_ECUDA, "fetch_layers: descriptor unusable after a failed launch");
+    DeviceGuard dg(d->device);
+    const int sms = device_sm_count(d->device);
+    const uint32_t upl = d->dd.units_per_layer;
+    d->poisoned = true;
+    int rc;
+    if (o.engine == OC_COPY_BULK) {
+        BulkPlan p = plan_bulk(d->dd, sms, o.max_ctas, (uint64_t)(l1 - l0) * upl);
+        if (o.flags & OC_FETCH_LEAN) shallow_ring(&p);
+        rc = launch_bulk(d, p, l0 * upl, l1 * upl, s);
+    } else {
+        rc = launch_ldst(d, sms, o.max_ctas, l0 * upl, l1 * upl, s);
+    }
+    if (rc) return rc;
+    OC_CUDA(cudaEventRecord(d->done_ev, s));
+    d->poisoned = false;
+    d->range_open = l1 < L ? l1 : 0;
+    d->last_stream = s;
+    return OC_OK;
+}
+
+int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s, uint32_t l_end) {
+    oc_fetch_opts o = oin;
+    if (d->range_open)
+        return fail(OC_EINVAL, "fetch: the previous fetch_layers fetch is incomplete (fetch its remaining layers)");
+    const bool ranged = l_end < d->geo.L;
     if (o.mode != OC_FETCH_PERSISTENT && o.mode != OC_FETCH_PER_LAYER)
         return fail(OC_EINVAL, "fetch_layerwise: unknown mode");
+    if (ranged && (o.mode != OC_FETCH_PERSISTENT || o.pace_Bps != 0 || o.engine == OC_COPY_CE ||
+                   (o.flags & (OC_FETCH_YIELD | OC_FETCH_FIRST_LAYER_FULL))))
+        return fail(OC_ENOTSUP, "fetch_layers: PERSISTENT mode, BULK or LDST engine, unpaced");
     // AUTO: the TMA engine where destination rows are contiguous (NHD, flat); with a head-split
     // target (HND) every row becomes n_kv stores of d*p bytes, which holds the TMA engine to
     // 4.2 TB/s at 4K while 16-byte LD/ST streams at 6.3 (profiles/r01_hnd_probe.txt).  Strict
@@ -439,7 +482,7 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
         // B_l directly (no stage, no SMs): 53.3 GB/s of PCIe reads at 1 run, 51.5 at 4, against
         // 51.4 for SM zero-copy reads (profiles/r01_flat_auto.txt); with many runs per layer its
         // per-transfer cost wins (45.6 GB/s at 16 runs; profiles/r01_ce2d.txt).
-        const bool ce = d->flat_base && d->host_chunks == d->N && !d->run_first.empty() &&
+        const bool ce = !ranged && d->flat_base && d->host_chunks == d->N && !d->run_first.empty() &&
                         d->run_first.size() <= 4 && o.pace_Bps == 0 && o.mode == OC_FETCH_PERSISTENT;
         o.engine = ce ? OC_COPY_CE
                       : (d->dd.nhd || (o.pace_Bps > 0 && o.pace_strict)) ? OC_COPY_BULK : OC_COPY_LDST;
@@ -470,7 +513,8 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     uint32_t max_ctas = o.max_ctas;
     if (!max_ctas && host_src) max_ctas = (uint32_t)std::max(1, env_int("OC_HOST_COPY_CTAS", 8));
     // PCIe-bound fetches keep 32 KiB units: finer units finish layer 0 sooner on a slow link.
-    plan_units(d, o.unit_bytes ? o.unit_bytes : default_unit_bytes(host_src ? 0 : max_ctas, device_sm_count(d->device)));
+    d->range_unit_bytes = o.unit_bytes ? o.unit_bytes : default_unit_bytes(host_src ? 0 : max_ctas, device_sm_count(d->device));
+    plan_units(d, d->range_unit_bytes);
     DevDesc& dd = d->dd;
     const uint64_t total_units = (uint64_t)dd.units_per_layer * dd.L;
     if (total_units >= (1ull << 32)) return fail(OC_ERANGE, "fetch_layerwise: too many units");
@@ -487,7 +531,13 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     d->poisoned = true;
     const uint32_t upl = dd.units_per_layer;
     const bool paced = dd.pace_ns || dd.pace_ns_per_byte > 0.0;
-    if (o.mode == OC_FETCH_PERSISTENT && dd.hot_layers && host_src && !paced) {
+    if (ranged) {
+        BulkPlan p = plan_bulk(dd, sms, max_ctas, (uint64_t)l_end * upl);
+        if (o.flags & OC_FETCH_LEAN) shallow_ring(&p);
+        int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, 0, l_end * upl, s)
+                                          : launch_ldst(d, sms, max_ctas, 0, l_end * upl, s);
+        if (rc) return rc;
+    } else if (o.mode == OC_FETCH_PERSISTENT && dd.hot_layers && host_src && !paced) {
         // Hot layers mirrored in HBM: they go first with an HBM-sized grid (X0 at HBM speed), the
         // rest follows from host memory with the PCIe-sized grid; each launch announces its layers.
         const uint32_t k_units = std::min(dd.hot_layers, dd.L) * upl;
@@ -528,7 +578,7 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
         }
     } else if (o.mode == OC_FETCH_PERSISTENT) {
         BulkPlan p = plan_bulk(dd, sms, max_ctas, total_units);
-        if (paced) shallow_ring(&p);
+        if (paced || (o.flags & OC_FETCH_LEAN)) shallow_ring(&p);
         const bool overlap = (o.flags & OC_FETCH_OVERLAP) != 0;
         int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, 0, (uint32_t)total_units, s, overlap)
                                           : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
@@ -558,6 +608,7 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s) {
     d->last_mode = o.mode;
     d->last_stream = s;
     d->fetched = true;
+    d->range_open = ranged ? l_end : 0;
     return OC_OK;
 }
 
@@ -610,8 +661,10 @@ int fetch_batch(Batch* b, const oc_fetch_opts& o, const oc_wdrr_opts* wdrr, cuda
         return fail(OC_ENOTSUP, "fetch_batch: batches use the BULK or LDST engine");
     if (o.pace_Bps != 0)
         return fail(OC_ENOTSUP, "fetch_batch: pace_Bps is per request (fetch_layerwise); WDRR batches use hold_rates");
-    for (Desc* d : b->descs)
+    for (Desc* d : b->descs) {
         if (d->poisoned) return fail(OC_ECUDA, "fetch_batch: a descriptor is unusable after a failed launch");
+        if (d->range_open) return fail(OC_EINVAL, "fetch_batch: a member's fetch_layers fetch is incomplete");
+    }
     DeviceGuard dg(b->device);
     OC_CUDA(cudaEventSynchronize(b->staged));  // previous upload done with the staging buffers
     DevDesc* st = (DevDesc*)b->stage;
@@ -797,6 +850,15 @@ OC_API int oc_fetch_layerwise(oc_desc* h, const oc_fetch_opts* opts, void* strea
     o.engine = OC_COPY_AUTO;
     if (opts) o = *opts;
     return oc::launch_fetch((Desc*)h, o, (cudaStream_t)stream);
+}
+
+OC_API int oc_fetch_layers(oc_desc* h, uint32_t l0, uint32_t l1, const oc_fetch_opts* opts, void* stream) {
+    if (!h) return oc::fail(OC_EINVAL, "fetch_layers: null descriptor");
+    oc_fetch_opts o{};
+    o.mode = OC_FETCH_PERSISTENT;
+    o.engine = OC_COPY_AUTO;
+    if (opts) o = *opts;
+    return oc::launch_fetch_range((Desc*)h, o, l0, l1, (cudaStream_t)stream);
 }
 
 OC_API int oc_batch_create(oc_desc* const* descs, uint32_t n, oc_batch** out) {

@@ -223,6 +223,8 @@ struct Desc {
     uint64_t stage_class = 0;
     struct CeKit* ce_kit = nullptr;  // copy stream + per-layer events, pooled per (device, L)
     uint32_t* ready_host = nullptr;  // pinned mirror of dd.ready (ready_mirror_alloc)
+    uint32_t range_open = 0;         // oc_fetch_layers: next layer of an incomplete fetch (0: none)
+    uint32_t range_unit_bytes = 0;   // unit size of the current fetch (fixed for its continuations)
 };
 
 // CE engine resources returned to their pool when a descriptor is freed (fetch.cu).
@@ -249,7 +251,8 @@ int wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* tile_bytes, u
               std::vector<WdrrEntry>* out);
 
 // kernel launchers (fetch.cu)
-int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s);
+int launch_fetch(Desc* d, const oc_fetch_opts& o, cudaStream_t s, uint32_t l_end = UINT32_MAX);
+int launch_fetch_range(Desc* d, const oc_fetch_opts& o, uint32_t l0, uint32_t l1, cudaStream_t s);
 // Offload gather: new chunk j (slot dd.src[j]) <- the paged rows of request chunk pos[j].
 // The caller orders `s` after the block's upload first.
 int launch_offload(const DevDesc& dd, const uint32_t* pos, int device, cudaStream_t s, bool host_dst);
