@@ -53,6 +53,9 @@ def route(reqs, ws, home_of, seed=5):
 
 
 def main():
+    if os.environ.get("OC_HANG_DUMP_S"):               # debugging support: stacks of a stuck rank
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["OC_HANG_DUMP_S"]), exit=True)
     import torch
     import torch.distributed as dist
 
@@ -65,13 +68,24 @@ def main():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # OC_BENCH_DIST_BACKEND=gloo: several ranks share one GPU (the N>1 code path on a one-GPU box;
+    # NCCL refuses duplicate GPUs); peer stores are then IPC-imported from the same device
+    backend = os.environ.get("OC_BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = {"world_size": ws, "backend": None}
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        comm = {"world_size": dist.get_world_size(), "backend": dist.get_backend(),
-                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+        comm = {"world_size": dist.get_world_size(), "backend": dist.get_backend()}
+        if backend == "nccl":
+            comm["nccl_version"] = ".".join(str(x) for x in torch.cuda.nccl.version())
+        else:
+            comm["peers_share_one_gpu"] = True
     lay_t = synth.LLAMA3_8B.as_tuple()
     L, G, Bs = lay_t[0], lay_t[4], 16
     row, S, chunk = oc.geometry(lay_t)
@@ -200,7 +214,7 @@ def main():
 
     run()                                           # warm-up pass
     total, dev_ms, host_s = run()                   # timed pass
-    red = dev
+    red = dev if backend == "nccl" else "cpu"
     max_ms = odist.max_over_ranks(dev_ms, device=red)
     all_bytes = odist.sum_over_ranks(total, device=red)
     all_remote = odist.sum_over_ranks(remote_bytes, device=red)
@@ -252,11 +266,15 @@ def main():
         print(json.dumps(res), flush=True)
 
 
-def spawn(ws, rank, local, timeout=600):
+def spawn(ws, rank, local, timeout=420):
     """Run this leg as a child process of a bench rank (its own process group on MASTER_PORT + 17).
     Returns the parsed JSON (rank 0) or {"error": ...}."""
     import subprocess
-    env = dict(os.environ, WORLD_SIZE=str(ws), RANK=str(rank), LOCAL_RANK=str(local),
+    # Not inherited: torchrun's TORCHELASTIC_* variables -- TORCHELASTIC_USE_AGENT_STORE makes the
+    # child's env:// rendezvous connect to an agent store on the new port that nobody serves (a hang
+    # until the timeout, seen with two ranks).
+    base = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC_")}
+    env = dict(base, WORLD_SIZE=str(ws), RANK=str(rank), LOCAL_RANK=str(local),
                MASTER_ADDR=os.environ.get("MASTER_ADDR", "127.0.0.1"),
                MASTER_PORT=str(int(os.environ.get("MASTER_PORT", "29500")) + 17))
     try:

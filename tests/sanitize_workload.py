@@ -10,7 +10,7 @@ from scenario import lib_target, make_dest, oracle_result, payload_stack, reques
 
 lay = Layout(2, 2, 64, 2, 16)
 ok = 0
-SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3,4,5").split(",")
+SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3,4,5,6").split(",")
 for kind in (("nhd", "hnd") if "1" in SECTIONS else ()):
     for engine in (oc.COPY_BULK, oc.COPY_LDST):
         for mode in (oc.FETCH_PERSISTENT, oc.FETCH_PER_LAYER):
@@ -180,5 +180,26 @@ if "5" in SECTIONS:
         want = b"".join(okeys.chunk_keys(t, 16))
         assert g.tobytes() == want
         ok += 1
+if "6" in SECTIONS:
+    # round 2: a fetch in layer ranges (oc_fetch_layers, lean ring) and the host mirror's fast path
+    lay4 = Layout(4, 2, 64, 2, 16)
+    req = requests_family(lay4, 6, 0, [7])[0]
+    with oc.Store(lay4, capacity=8) as st:
+        keys = oc.chunk_keys(req.tokens, 16)
+        st.put_chunks(keys, payload_stack(lay4, 6, req.payload_ids))
+        for engine, lean in ((oc.COPY_BULK, True), (oc.COPY_BULK, False), (oc.COPY_LDST, False)):
+            dest = make_dest(lay4, 7, "nhd", Bs=8, first_token=3, seed=2)
+            buf = sentinel_buffer(dest.size)
+            d = oc.build_descriptor(st, keys, lay4, lib_target(oc, dest, buf.data_ptr()))
+            s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+            for l0, l1 in ((0, 1), (1, 3), (3, 4)):
+                d.fetch_layers(l0, l1, s, engine=engine, unit_bytes=1024, lean=lean)
+            for l in range(4):
+                d.wait_layer(l, cons)
+            cons.synchronize()
+            assert d.layers_ready() == 4
+            assert np.array_equal(buf.cpu().numpy(), oracle_result(lay4, 6, req, dest))
+            d.close()
+            ok += 1
 torch.cuda.synchronize()
 print("sanitize workload ok", ok)
