@@ -66,7 +66,7 @@ def run(args, oc, torch, dev, lay_t, ws, rank, dist=None, backend="nccl"):
     if args.engine == "ldst":
         fopts = {"engine": oc.COPY_LDST}
     if args.mode == "per_layer":
-        fopts = {"mode": oc.FETCH_PER_LAYER}
+        fopts = {"mode": oc.FETCH_PER_LAYER, "overlap": overlap}
 
     def step(i):
         d = descs[i % ROTATE]
@@ -170,5 +170,6 @@ def run(args, oc, torch, dev, lay_t, ws, rank, dist=None, backend="nccl"):
                       "warm-ups" % (bytes_per_step // 2 >> 20)},
         "verified": ver,
         "launch": ("back-to-back fetches of rotating requests with OC_FETCH_OVERLAP (programmatic dependent "
-                   "launch)" if overlap and "mode" not in fopts and "engine" not in fopts else "stream order"),
+                   "launch)" if fopts.get("overlap") else "stream order") +
+                  (", one launch + CUDA event per layer" if args.mode == "per_layer" else ""),
     }

@@ -315,10 +315,11 @@ OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* co
  * that layer's MLP GEMMs instead of the attention).  l0 = 0 opens a new fetch
  * exactly like fetch_layerwise (same contract; it fixes the unit size) and
  * launches its first l1 layers; every later call continues it and must start
- * where the previous call stopped (l0 = previous l1), in any stream order the
- * caller guarantees (no two ranges of one fetch may overlap in time with a new
- * fetch).  Layers are announced (wait_layer, layers_ready, layer_times) as each
- * range completes.  A new fetch of the descriptor (any entry point) is refused
+ * where the previous call stopped (l0 = previous l1).  Ranges may be enqueued on
+ * different streams and may run concurrently; layers are still announced
+ * (wait_layer, layers_ready, layer_times) strictly in order -- a range's layers
+ * only after every earlier layer.  A new fetch of the descriptor must be
+ * ordered after all ranges of the open one (as for fetch_layerwise).  A new fetch of the descriptor (any entry point) is refused
  * with EINVAL until all L layers of the open one have been requested.
  * opts: PERSISTENT mode, BULK or LDST engine (AUTO picks between them), unpaced;
  * max_ctas and OC_FETCH_LEAN apply per call; unit_bytes only with l0 = 0 (a later

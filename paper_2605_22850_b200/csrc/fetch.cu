@@ -444,10 +444,13 @@ int launch_fetch_range(Desc* d, const oc_fetch_opts& oin, uint32_t l0, uint32_t 
         return fail(OC_EINVAL, "fetch_layers: the unit size is fixed by the call with l0 = 0");
     if (d->poisoned) return fail(OC_ECUDA, "fetch_layers: descriptor unusable after a failed launch");
     DeviceGuard dg(d->device);
+    int urc = upload_order(&d->up, s);  // the kernel reads the descriptor block
+    if (urc) return urc;
     const int sms = device_sm_count(d->device);
     const uint32_t upl = d->dd.units_per_layer;
     d->poisoned = true;
     int rc;
+    d->dd.wait_prev_layers = 1;  // this launch's copy of the descriptor (launches take it by value)
     if (o.engine == OC_COPY_BULK) {
         BulkPlan p = plan_bulk(d->dd, sms, o.max_ctas, (uint64_t)(l1 - l0) * upl);
         if (o.flags & OC_FETCH_LEAN) shallow_ring(&p);
@@ -455,6 +458,7 @@ int launch_fetch_range(Desc* d, const oc_fetch_opts& oin, uint32_t l0, uint32_t 
     } else {
         rc = launch_ldst(d, sms, o.max_ctas, l0 * upl, l1 * upl, s);
     }
+    d->dd.wait_prev_layers = 0;
     if (rc) return rc;
     OC_CUDA(cudaEventRecord(d->done_ev, s));
     d->poisoned = false;

@@ -137,6 +137,17 @@ __device__ __forceinline__ void complete_units(const DevDesc& d, uint32_t layer,
 // the last reduction synchronises with every release reduction before it).
 __device__ void observe_layers(const DevDesc& d, uint32_t l0, uint32_t l1) {
     const uint32_t base = (d.epoch - 1u) * d.L;
+    // oc_fetch_layers: a range may run beside the range covering the earlier layers (another
+    // stream): announce nothing before those are announced, so `ready` (and its host copy) only ever
+    // move through the layers in order.  (PER_LAYER launches are waited on through their CUDA
+    // events, and the other split launches are stream-ordered.)
+    if (d.wait_prev_layers && l0 > 0) {
+        uint32_t ns = 64;
+        while ((int32_t)(ld_acquire(d.ready) - (base + l0)) < 0) {
+            __nanosleep(ns);
+            ns = min(ns * 2, 1024u);
+        }
+    }
     for (uint32_t l = l0; l < l1; l++) {
         uint32_t ns = 32;
         while ((int32_t)(ld_acquire(&d.unit_cnt[l]) - d.cnt_target) < 0) {

@@ -163,6 +163,8 @@ struct DevDesc {
     FastDiv div_hdv;          // (d*p)/16
     uint64_t* trace;          // measurement support (OC_TRACE=1): per-CTA ramp stamps, else null
     uint32_t ramp;            // kRampStatic2 | kRampFirstLayer (single-descriptor BULK launches)
+    uint32_t wait_prev_layers;  // oc_fetch_layers continuation: the observer first waits for the
+                                // earlier layers' announcement (layers announced in order)
 };
 // First-layer ramp of a single-descriptor BULK launch (fetch_kernels.cuh):
 //   kRampStatic2     the first layer's units beyond one per copy CTA are also assigned statically

@@ -119,3 +119,26 @@ def test_range_errors():
     s.synchronize()
     d.close()
     st.close()
+
+
+def test_later_range_running_first_is_announced_in_order():
+    """Range [0, 2) waits 30 ms behind a spin on its stream while range [2, 8) runs at once on
+    another: layers 2.. complete first but are announced only after layers 0-1 (the observer of a
+    later range waits for the earlier layers' announcement)."""
+    import time
+    lay = OLayout(8, 8, 128, 2, 16)
+    st, req, dest, buf, d = _setup(lay, 29, 84)
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    oc.emulate_compute(30_000_000, a)
+    d.fetch_layers(0, 2, a)
+    d.fetch_layers(2, 8, b)
+    time.sleep(0.01)
+    assert d.layers_ready() == 0           # range [2, 8) is done or running, layers 0-1 are not
+    b.synchronize()                        # the later range's kernel ends only after announcing
+    assert d.layers_ready() == lay.num_layers
+    a.synchronize()
+    t = d.layer_times().astype(np.int64)
+    assert np.all(np.diff(t[1:]) >= 0)
+    assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 84, req, dest))
+    d.close()
+    st.close()
