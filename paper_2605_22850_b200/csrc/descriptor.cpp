@@ -493,6 +493,10 @@ OC_API int oc_desc_free(oc_desc* h) {
         oc::DeviceGuard dg(d->device);
         // Defer until the last fetch has finished with the descriptor's device memory.
         if (d->fetched && d->done_ev) cudaEventSynchronize(d->done_ev);
+        for (auto ev : d->range_evs) {  // an incomplete ranged fetch: every range's launch
+            cudaEventSynchronize(ev);
+            cudaEventDestroy(ev);
+        }
         oc::upload_release(&d->up);
         for (auto ev : d->events) cudaEventDestroy(ev);
         if (d->done_ev) cudaEventDestroy(d->done_ev);

@@ -427,6 +427,24 @@ int launch_scatter_flat(Desc* d, uint64_t flat, uint64_t cap, const oc_fetch_opt
     return OC_OK;
 }
 
+// oc_fetch_layers: the ranges of one fetch may be on different streams, so each records its own
+// completion event, and the final range's stream waits for all of them before done_ev -- done_ev
+// (which desc_free, layer_times and the next fetch rely on) then covers the whole fetch.
+int record_range(Desc* d, cudaStream_t s, bool last) {
+    if (d->n_ranges >= d->range_evs.size()) {
+        cudaEvent_t ev = nullptr;
+        OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        d->range_evs.push_back(ev);
+    }
+    OC_CUDA(cudaEventRecord(d->range_evs[d->n_ranges++], s));
+    if (last) {
+        for (uint32_t k = 0; k + 1 < d->n_ranges; k++) OC_CUDA(cudaStreamWaitEvent(s, d->range_evs[k], 0));
+        d->n_ranges = 0;
+    }
+    OC_CUDA(cudaEventRecord(d->done_ev, s));
+    return OC_OK;
+}
+
 // Layers [l0, l1) of the descriptor's current fetch (oc_fetch_layers): l0 == 0 opens a new fetch
 // like fetch_layerwise and launches only its first layers; l0 > 0 continues it where the previous
 // call stopped.  One launch per call over the range's units, announced by its observer CTA.
@@ -460,7 +478,8 @@ int launch_fetch_range(Desc* d, const oc_fetch_opts& oin, uint32_t l0, uint32_t 
     }
     d->dd.wait_prev_layers = 0;
     if (rc) return rc;
-    OC_CUDA(cudaEventRecord(d->done_ev, s));
+    rc = record_range(d, s, l1 == L);
+    if (rc) return rc;
     d->poisoned = false;
     d->range_open = l1 < L ? l1 : 0;
     d->last_stream = s;
@@ -607,7 +626,13 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s, uint32_t l_e
             OC_CUDA(cudaEventRecord(d->events[l], s));
         }
     }
-    OC_CUDA(cudaEventRecord(d->done_ev, s));
+    if (ranged) {
+        d->n_ranges = 0;
+        int rrc = record_range(d, s, false);
+        if (rrc) return rrc;
+    } else {
+        OC_CUDA(cudaEventRecord(d->done_ev, s));
+    }
     d->poisoned = false;
     d->last_mode = o.mode;
     d->last_stream = s;

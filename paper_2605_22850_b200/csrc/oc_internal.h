@@ -226,6 +226,8 @@ struct Desc {
     struct CeKit* ce_kit = nullptr;  // copy stream + per-layer events, pooled per (device, L)
     uint32_t* ready_host = nullptr;  // pinned mirror of dd.ready (ready_mirror_alloc)
     uint32_t range_open = 0;         // oc_fetch_layers: next layer of an incomplete fetch (0: none)
+    std::vector<cudaEvent_t> range_evs;  // oc_fetch_layers: completion of each range of the open fetch
+    uint32_t n_ranges = 0;               // ranges recorded in range_evs for the open fetch
     uint32_t range_unit_bytes = 0;   // unit size of the current fetch (fixed for its continuations)
 };
 
