@@ -309,7 +309,9 @@ typedef struct {
  * opts = NULL selects the defaults (persistent, AUTO engine, auto grid, unpaced). */
 OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* copy_stream);
 
-/* fetch_layers: the transfer of layers [l0, l1) only, so the consumer decides
+/* fetch_layers (Alg. A1's per-layer loop, split at the caller's layer
+ * boundaries; the serving node's call order match -> descriptor -> layer waits,
+ * P:720-729): the transfer of layers [l0, l1) only, so the consumer decides
  * when each part of the fetch runs (e.g. layer l+2 enqueued on a copy stream
  * that waits for the consumer's attention of layer l, so the copy co-runs with
  * that layer's MLP GEMMs instead of the attention).  l0 = 0 opens a new fetch
@@ -416,7 +418,8 @@ OC_API int oc_wait_layer(oc_desc* desc, uint32_t layer, void* consumer_stream);
 /* Host-blocking variant of wait_layer. */
 OC_API int oc_sync_layer(oc_desc* desc, uint32_t layer);
 
-/* layers_ready: *n = how many layers of the most recent fetch are announced, as
+/* layers_ready (NotifyLayerReady, Alg. A1 line 7, seen from the host):
+ * *n = how many layers of the most recent fetch are announced, as
  * the host sees it now (non-blocking poll of the pinned copy of the ready word;
  * a layer counted here is in place in device memory).  PERSISTENT-mode fetches
  * (kernel and CE engines); for a PER_LAYER fetch, the layers whose CUDA event
