@@ -280,8 +280,9 @@ typedef struct {
                                 destination nor produces anything it reads (e.g.
                                 back-to-back fetches of different requests).  The
                                 previous fetch's tail and this one's ramp overlap.
-                                Single-descriptor TMA (BULK) launches only; other
-                                engines ignore it.  0 = stream order.            */
+                                Single-descriptor kernel launches (BULK, LDST);
+                                the CE engine and batches ignore it.  0 = stream
+                                order.                                           */
 } oc_fetch_opts;
 #define OC_FETCH_OVERLAP 1u
 /* OC_FETCH_FIRST_LAYER_FULL: with max_ctas set, layer 0 (the exposed X_0 of Eq. 3,

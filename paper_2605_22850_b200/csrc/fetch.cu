@@ -189,17 +189,26 @@ int launch_bulk(Desc* d, const BulkPlan& p, uint32_t g0, uint32_t g1, cudaStream
     return OC_OK;
 }
 
-int launch_ldst(Desc* d, int sms, uint32_t max_ctas, uint32_t g0, uint32_t g1, cudaStream_t s) {
+int launch_ldst(Desc* d, int sms, uint32_t max_ctas, uint32_t g0, uint32_t g1, cudaStream_t s,
+                bool overlap = false) {
     // one CTA slot of the first wave is the observer's
     static int occ = occupancy((const void*)fetch_ldst_kernel, kThreads, 0);
     uint64_t grid = (uint64_t)occ * sms - 1;
     if (max_ctas) grid = std::min<uint64_t>(grid, max_ctas);
     grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, g1 - g0));
-    DevDesc dd = d->dd;  // stream-ordered (no dependent launch): its slot's earlier user is done
+    DevDesc dd = d->dd;
     const uint32_t slot = d->launch_seq++ % kClaimSlots;
     dd.next_unit = d->dd.next_unit + slot * kClaimSlotStride;
-    fetch_ldst_kernel<<<(unsigned)grid + 1, kThreads, 0, s>>>(dd, g0, g1, d->grab_ctr[slot]);
-    OC_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid + 1);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = overlap ? attr : nullptr;
+    cfg.numAttrs = overlap ? 1 : 0;
+    OC_CUDA(cudaLaunchKernelEx(&cfg, fetch_ldst_kernel, dd, g0, g1, d->grab_ctr[slot]));
     d->grab_ctr[slot] += (g1 - g0) + (uint32_t)grid;
     return OC_OK;
 }
@@ -604,7 +613,7 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s, uint32_t l_e
         if (paced || (o.flags & OC_FETCH_LEAN)) shallow_ring(&p);
         const bool overlap = (o.flags & OC_FETCH_OVERLAP) != 0;
         int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, 0, (uint32_t)total_units, s, overlap)
-                                          : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s);
+                                          : launch_ldst(d, sms, max_ctas, 0, (uint32_t)total_units, s, overlap);
         if (rc) return rc;
     } else {
         // PER_LAYER: one launch + one CUDA event per layer.  The layers' launches are independent

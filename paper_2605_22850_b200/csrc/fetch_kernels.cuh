@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(kThreads, 4) fetch_ldst_kernel(const DevDesc d
     __shared__ uint64_t s_dst[2][kMaxRows];
     __shared__ uint32_t s_g[2];
     const uint64_t t0 = globaltimer();
+    // a dependent launch (OC_FETCH_OVERLAP: the stream's next fetch) may be scheduled at once; it
+    // claims from another counter slot and first waits for that slot's previous user (below)
+    allow_dependents();
     if (blockIdx.x == 0) {
         if (threadIdx.x == 0) {
             if (g0 == 0) d.ts[0] = t0;
@@ -222,6 +225,9 @@ __global__ void __launch_bounds__(kThreads, 4) fetch_ldst_kernel(const DevDesc d
     bool pending = false;
     uint32_t next_g = 0;
     if (threadIdx.x == 0) {  // claims stop after the first one past g1: exactly one per CTA overshoots
+        // the slot's previous user (a launch kClaimSlots launches ago, possibly still running under a
+        // dependent launch) has made all its claims once the counter reaches this launch's base
+        while ((int32_t)(*(volatile uint32_t*)d.next_unit - grab_base) < 0) __nanosleep(64);
         s_g[0] = claim_unit(d, g0, grab_base);
         next_g = s_g[0] < g1 ? claim_unit(d, g0, grab_base) : s_g[0];  // one ahead hides the latency
     }

@@ -445,24 +445,27 @@ def test_gather_to_flat_then_scatter_flat(kind, Bs, first, unit_bytes):
 
 
 # ---- OC_FETCH_OVERLAP: back-to-back launches overlapping each other's tails ----------------------
+@pytest.mark.parametrize("kind,engine", [("nhd", "bulk"), ("nhd", "ldst"), ("hnd", "ldst")])
 @pytest.mark.parametrize("lay,n_chunks", [(OLayout(2, 2, 16, 2, 16), 10), (OLayout(3, 2, 64, 2, 16), 40),
                                           (OLayout(32, 8, 128, 2, 16), 64)])
-def test_overlap_back_to_back(lay, n_chunks):
+def test_overlap_back_to_back(lay, n_chunks, kind, engine):
     """Several requests fetched back to back with OC_FETCH_OVERLAP (each launch may start during the
-    previous one's tail), the same descriptor twice in a row included: every destination equals the
-    oracle, consumer waits on each request's last layer complete, layer times are monotone."""
+    previous one's tail), the same descriptor twice in a row included, with the TMA engine and the
+    LD/ST engine (NHD and head-split HND targets): every destination equals the oracle, consumer
+    waits on each request's last layer complete, layer times are monotone."""
+    eng = oc.COPY_BULK if engine == "bulk" else oc.COPY_LDST
     reqs = [requests_family(lay, 60 + i, 0, [n_chunks])[0] for i in range(3)]
     store = oc.Store(lay, capacity=3 * n_chunks)
     for i, r in enumerate(reqs):
         store.put_chunks(oc.chunk_keys(r.tokens, lay.chunk_tokens), payload_stack(lay, 60 + i, r.payload_ids))
-    dests = [make_dest(lay, n_chunks, "nhd", Bs=16, first_token=3 * i, seed=70 + i) for i in range(3)]
+    dests = [make_dest(lay, n_chunks, kind, Bs=16, first_token=3 * i, seed=70 + i) for i in range(3)]
     bufs = [sentinel_buffer(d.size) for d in dests]
     descs = [oc.build_descriptor(store, store.match_prefix(r.tokens), lay, lib_target(oc, d, b.data_ptr()))
              for r, d, b in zip(reqs, dests, bufs)]
     s, cons = torch.cuda.Stream(), torch.cuda.Stream()
     order = [0, 1, 2, 2, 0, 1, 1, 2, 0] * 3
     for i in order:
-        descs[i].fetch_layerwise(s, overlap=True)
+        descs[i].fetch_layerwise(s, overlap=True, engine=eng)
         descs[i].wait_layer(lay.num_layers - 1, cons)
     cons.synchronize()
     s.synchronize()
