@@ -153,6 +153,7 @@ def run(args, oc, torch, dev, lay_t, ws, rank, dist=None, backend="nccl"):
         "value": value, "ms_per_step": ms_per_step, "clocks": clk,
         "gpu_launches": args.steps * (L if args.mode == "per_layer" else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "frac_of_spec": round(achieved / 8000.0, 4),   # both denominators (8 TB/s spec)
                      "traffic": traffic if traffic_fresh else None,
                      "traffic_source": ("profiles/ncu_full_summary.json (ncu --set full of the current kernel "
                                         "sources)" if traffic_fresh else
