@@ -20,6 +20,9 @@ Remote   remote_byte_fraction = bytes of requests served off their family's home
 Verified a second, identical pass checks every request on completion: all per-layer digests
          against the oracle (benchlib.verify); rank 0 also checks one 4K request in full and one
          64K request's first and last layers byte for byte.
+Batched  `batched_by_position`: the same passes with each admission step's requests (at most 16)
+         fetched as one position-major batch (oc.BATCH_BY_POSITION: prefix-family members read
+         their shared chunks together), timed and digest-verified the same way.
 
 Run as `python -m benchlib.config5` under the bench's rank environment (bench.py spawns one child
 per rank on its own port, so a fault here cannot take the contract line with it); rank 0 prints
@@ -41,6 +44,7 @@ N_SHORT, N_LONG = 16, 2
 R_REQUESTS = 128
 P_AFF = 0.875
 POOL_GIB = 40
+BATCH_MAX = 16
 
 
 def route(reqs, ws, home_of, seed=5):
@@ -151,11 +155,28 @@ def main():
     checks = {"digest_requests": 0, "digest_ok": 0, "full": {}}
     expect = {}
 
-    def run(check=False):
+    def check_member(d, blocks, q, lg, f, n):
+        idx = verify.slot_index(torch, dev, blocks, n * G, Bs)
+        got = verify.gpu_digests(torch, cache, idx, n, G, T_dev)
+        checks["digest_requests"] += 1
+        checks["digest_ok"] += int(np.array_equal(got, expect[(lg, f)].request(n)))
+        if rank == 0 and ("short" if not lg else "long") not in checks["full"]:
+            fam = fams[(lg, f)]
+            layers = range(L) if not lg else (0, L - 1)
+            ok, nbytes, t_or, _ = verify.full_check(torch, Layout(*lay_t), fam["seed"], fam["keys"][:n],
+                                                    fam["ids"][:n], cache, idx, layers)
+            checks["full"]["short" if not lg else "long"] = {
+                "request": q, "layers": len(layers), "bit_exact": ok, "bytes": nbytes, "oracle_s": round(t_or, 2)}
+
+    def run(check=False, batch=0):
+        """One pass over this rank's requests.  batch = 0: one fetch_layerwise per request (8 copy
+        streams); batch = B > 0: the requests admitted in one admission step (at most B) are fetched
+        as ONE position-major batch (oc.BATCH_BY_POSITION), so members of one prefix family read
+        their shared chunks together; blocks return when the whole batch completes."""
         free = collections.deque(int(b) for b in synth.block_table(3, pool_blocks, pool_blocks))
         pending = collections.deque(reqs)
-        inflight = []
-        total = 0
+        inflight = []                               # (event, Batch or None, members)
+        total, n_launch = 0, 0
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -166,28 +187,21 @@ def main():
         t_host = time.perf_counter()
         while pending or inflight:
             still = []
-            for ev, d, blocks, q, lg, f, n in inflight:
+            for ev, bt_, members in inflight:
                 if ev.query():
-                    if check:
-                        idx = verify.slot_index(torch, dev, blocks, n * G, Bs)
-                        got = verify.gpu_digests(torch, cache, idx, n, G, T_dev)
-                        checks["digest_requests"] += 1
-                        checks["digest_ok"] += int(np.array_equal(got, expect[(lg, f)].request(n)))
-                        if rank == 0 and ("short" if not lg else "long") not in checks["full"]:
-                            fam = fams[(lg, f)]
-                            layers = range(L) if not lg else (0, L - 1)
-                            ok, nbytes, t_or, _ = verify.full_check(torch, Layout(*lay_t), fam["seed"], fam["keys"][:n],
-                                                                    fam["ids"][:n], cache, idx, layers)
-                            checks["full"]["short" if not lg else "long"] = {
-                                "request": q, "layers": len(layers), "bit_exact": ok, "bytes": nbytes,
-                                "oracle_s": round(t_or, 2)}
-                    d.close()
-                    free.extend(blocks)
+                    for m in members:
+                        if check:
+                            check_member(*m)
+                        free.extend(m[1])
+                    if bt_ is not None:
+                        bt_.close()
+                    for m in members:
+                        m[0].close()
                 else:
-                    still.append((ev, d, blocks, q, lg, f, n))
+                    still.append((ev, bt_, members))
             inflight = still
-            admitted = False
-            while pending:
+            step, admitted = [], False
+            while pending and (batch == 0 or len(step) < batch):
                 q, lg, f, h = pending[0]
                 n = n_of(lg, h)
                 need = n * G // Bs
@@ -197,16 +211,31 @@ def main():
                 blocks = [free.popleft() for _ in range(need)]
                 tgt = oc.PagedTarget(kb, vb, Bs * row, row, lay_t[2] * lay_t[3], Bs, np.asarray(blocks, np.int32), 0)
                 d = oc.build_descriptor(store, fams[(lg, f)]["keys"][:n], lay_t, tgt)
-                s = streams[q % len(streams)]
-                d.fetch_layerwise(s)
+                total += 2 * n * S * L
+                admitted = True
+                if batch == 0:
+                    s = streams[q % len(streams)]
+                    d.fetch_layerwise(s)
+                    ev = torch.cuda.Event(enable_timing=True)
+                    ev.record(s)
+                    ends.append(ev)
+                    inflight.append((ev, None, [(d, blocks, q, lg, f, n)]))
+                else:
+                    step.append((d, blocks, q, lg, f, n))
+            if step:
+                bt_ = oc.Batch([m[0] for m in step], order=oc.BATCH_BY_POSITION)
+                s = streams[n_launch % len(streams)]
+                n_launch += 1
+                bt_.fetch(s)
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record(s)
                 ends.append(ev)
-                inflight.append((ev, d, blocks, q, lg, f, n))
-                total += 2 * n * S * L
-                admitted = True
-            if not admitted and inflight:
-                inflight[0][0].synchronize()
+                inflight.append((ev, bt_, step))
+            if not admitted:
+                if inflight:
+                    inflight[0][0].synchronize()
+                elif pending:
+                    raise RuntimeError("config5: a request needs more blocks than the pool holds")
         torch.cuda.synchronize()
         host_s = time.perf_counter() - t_host
         dev_ms = max((start.elapsed_time(e) for e in ends), default=0.0)
@@ -231,6 +260,15 @@ def main():
     run(check=True)
     ok_all = odist.sum_over_ranks(checks["digest_ok"], device=red)
     n_all = odist.sum_over_ranks(checks["digest_requests"], device=red)
+    # the same requests with each admission step fetched as one position-major batch (at most
+    # BATCH_MAX members; profiles/r01_serve.json swept 4..64 and found 16 best), timed, then verified
+    run(batch=BATCH_MAX)                            # warm-up pass
+    _, dev_ms_b, _ = run(batch=BATCH_MAX)
+    max_ms_b = odist.max_over_ranks(dev_ms_b, device=red)
+    c_ok, c_n = checks["digest_ok"], checks["digest_requests"]
+    run(check=True, batch=BATCH_MAX)
+    ok_b = odist.sum_over_ranks(checks["digest_ok"] - c_ok, device=red)
+    n_b = odist.sum_over_ranks(checks["digest_requests"] - c_n, device=red)
     t_oracle_max = odist.max_over_ranks(t_oracle, device=red)
     oracle_bytes_all = odist.sum_over_ranks(oracle_bytes, device=red)
     if ws > 1:
@@ -253,6 +291,13 @@ def main():
                         "oracle_digest_s_max_over_ranks": round(t_oracle_max, 1),
                         "oracle_s_per_verified_GB": round(t_oracle_max * ws / (oracle_bytes_all / 1e9), 3)
                         if oracle_bytes_all else None}}
+    res["batched_by_position"] = {
+        "max_members": BATCH_MAX, "GBps_aggregate": round(all_bytes / max_ms_b / 1e6, 1),
+        "GBps_per_gpu": round(all_bytes / max_ms_b / 1e6 / ws, 1), "device_ms_max_over_ranks": round(max_ms_b, 2),
+        "note": "algorithmic bytes (2*N*S*L per request) as above; members of one prefix family read shared chunks "
+                "once, so this is delivered bandwidth, not DRAM traffic",
+        "verified": {"requests_digest_equal": int(ok_b), "requests": int(n_b),
+                     "all_layers_all_requests": int(ok_b) == int(n_b) and n_b > 0}}
     if ws > 1 and p2p_GBps:
         res["nvlink_ingress_frac_of_p2p_copy"] = round(res["nvlink_ingress_GBps_per_gpu"] / p2p_GBps, 3)
     del cache
