@@ -246,6 +246,7 @@ def main():
     red = dev if backend == "nccl" else "cpu"
     max_ms = odist.max_over_ranks(dev_ms, device=red)
     all_bytes = odist.sum_over_ranks(total, device=red)
+    per_rank = [odist.sum_over_ranks(total if r == rank else 0, device=red) for r in range(ws)]  # load balance
     all_remote = odist.sum_over_ranks(remote_bytes, device=red)
     # verification pass: the oracle's digests of every family prefix this rank's requests use
     t0 = time.perf_counter()
@@ -278,6 +279,8 @@ def main():
                         f"50%/87.5%, p_aff {P_AFF}; the same corpus and requests at every N (strong scaling)"),
            "n_gpus": ws, "comm": comm,
            "requests_per_rank_rank0": len(reqs), "bytes_rw": all_bytes,
+           "bytes_rw_per_rank": per_rank,
+           "busiest_rank_share": round(max(per_rank) / all_bytes, 4) if all_bytes else None,
            "GBps_aggregate": round(all_bytes / max_ms / 1e6, 1),
            "GBps_per_gpu": round(all_bytes / max_ms / 1e6 / ws, 1),
            "device_ms_max_over_ranks": round(max_ms, 2),
