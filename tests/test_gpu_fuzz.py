@@ -1,0 +1,83 @@
+"""Randomised parity: 200 seeded configurations drawn over the whole option space -- layout (L,
+n_kv, d, p, G), chunk count, target (paged NHD / head-split HND / flat), block size and first-token
+offset, store tier (HBM, pinned host), engine (AUTO, TMA, LD/ST, copy engine), mode (persistent,
+per-layer events), unit size, copy-CTA cap,
+and delivery as one fetch or as layer ranges (oc_fetch_layers) -- each delivery compared byte for
+byte, sentinels included, with the oracle's Alg. A1 gather + paged scatter.  The
+draws are deterministic (seeded), so a failure names a reproducible case."""
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2605_22850_b200 as oc  # noqa: E402
+from oracle.geometry import Layout as OLayout  # noqa: E402
+from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(i):
+    r = random.Random(9000 + i)
+    lay = OLayout(r.choice([1, 2, 3, 5, 8]), r.choice([1, 2, 4, 8]), r.choice([8, 16, 64, 128]),
+                  r.choice([1, 2, 4]), r.choice([4, 8, 16, 32]))
+    if (lay.head_dim * lay.elem_bytes) % 16:        # d*p must be a 16-byte multiple (OC_EALIGN otherwise)
+        lay = OLayout(lay.num_layers, lay.kv_heads, lay.head_dim, 16 // lay.head_dim * 2, lay.chunk_tokens)
+    row = lay.kv_heads * lay.head_dim * lay.elem_bytes
+    kind = r.choice(["nhd", "nhd", "hnd", "flat"])
+    opts = {}
+    engine = r.choice(["auto", "bulk", "ldst"])
+    if engine != "auto":
+        opts["engine"] = oc.COPY_BULK if engine == "bulk" else oc.COPY_LDST
+    if r.random() < 0.3:
+        opts["max_ctas"] = r.choice([1, 3, 17, 150])
+    if r.random() < 0.4:
+        opts["unit_bytes"] = r.choice([row, 2 * row, 4096, 16384, 65536])
+    ranged = r.random() < 0.25 and lay.num_layers > 1
+    if not ranged and r.random() < 0.25:
+        opts["mode"] = oc.FETCH_PER_LAYER
+    host = r.random() < 0.2                         # pinned-host chunk store (PCIe reads)
+    if host and not ranged and "mode" not in opts and r.random() < 0.5:
+        opts["engine"] = oc.COPY_CE                 # copy engine into an HBM stage + the scatter kernel
+        opts.pop("max_ctas", None)
+    return dict(lay=lay, n=r.randint(1, 40), kind=kind, Bs=r.choice([1, 4, 8, 16, 32]),
+                first=r.randint(0, 20) if kind != "flat" else 0, opts=opts, ranged=ranged, seed=9100 + i,
+                split=r.randint(1, lay.num_layers - 1) if ranged else 0,
+                tier=oc.TIER_PINNED_HOST if host else oc.TIER_HBM)
+
+
+@pytest.mark.parametrize("i", range(200))
+def test_random_configuration(i):
+    c = _case(i)
+    lay, n = c["lay"], c["n"]
+    req = requests_family(lay, c["seed"], 0, [n])[0]
+    st = oc.Store(lay, capacity=n, tier=c["tier"], device=0)
+    keys = oc.chunk_keys(req.tokens, lay.chunk_tokens)
+    st.put_chunks(keys, payload_stack(lay, c["seed"], req.payload_ids))
+    dest = make_dest(lay, n, c["kind"], Bs=c["Bs"], first_token=c["first"], seed=c["seed"])
+    buf = sentinel_buffer(dest.size)
+    d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+    s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+    if c["ranged"]:
+        ro = {k: v for k, v in c["opts"].items() if k in ("engine", "max_ctas", "unit_bytes")}
+        if ro.get("engine") is None and c["kind"] == "flat":
+            ro["engine"] = oc.COPY_BULK
+        d.fetch_layers(0, c["split"], s, **ro)
+        d.fetch_layers(c["split"], lay.num_layers, s, **{k: v for k, v in ro.items() if k != "unit_bytes"})
+    else:
+        d.fetch_layerwise(s, **c["opts"])
+    for l in range(lay.num_layers):
+        d.wait_layer(l, cons)
+    cons.synchronize()
+    s.synchronize()
+    assert d.layers_ready() == lay.num_layers
+    got = buf.cpu().numpy()
+    want = oracle_result(lay, c["seed"], req, dest)
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, f"case {i} {c}: {bad.size} bytes differ, first at {bad[:4]}"
+    t = d.layer_times().astype(np.int64)
+    assert np.all(np.diff(t[1:]) >= 0), f"case {i}: layers announced out of order"
+    d.close()
+    st.close()
