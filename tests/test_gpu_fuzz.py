@@ -81,3 +81,59 @@ def test_random_configuration(i):
     assert np.all(np.diff(t[1:]) >= 0), f"case {i}: layers announced out of order"
     d.close()
     st.close()
+
+
+def _batch_case(i):
+    r = random.Random(7000 + i)
+    lay = OLayout(r.choice([1, 2, 4, 6]), r.choice([1, 2, 8]), r.choice([16, 64, 128]), 2, r.choice([8, 16, 32]))
+    n_members = r.randint(1, 6)
+    shared = r.randint(0, 6)                        # members of one prefix family share `shared` chunks
+    own = [r.randint(0 if shared else 1, 12) for _ in range(n_members)]
+    kinds = [r.choice(["nhd", "nhd", "hnd"]) for _ in range(n_members)]
+    order = r.choice(["request", "position", "wdrr", "wdrr_held", "wdrr_layer"])
+    engine = r.choice(["auto", "bulk", "ldst"]) if order in ("request", "position") else "bulk"
+    return dict(lay=lay, shared=shared, own=own, kinds=kinds, order=order, engine=engine,
+                Bs=r.choice([4, 8, 16]), seed=7100 + i, unit=r.choice([0, 0, 4096, 16384]),
+                max_ctas=r.choice([0, 0, 2, 9]))
+
+
+@pytest.mark.parametrize("i", range(60))
+def test_random_batch(i):
+    """One launch for several requests of one prefix family (shared chunks read through one store
+    slot), in a random claim order -- by request, position-major, or weighted deficit round robin
+    (unit or layer-payload packets, rates held or not; Alg. A2 line 7) -- every member's delivery
+    byte-exact against the oracle."""
+    c = _batch_case(i)
+    lay = c["lay"]
+    reqs = requests_family(lay, c["seed"], c["shared"], c["own"])
+    st = oc.Store(lay, capacity=c["shared"] + sum(c["own"]), device=0)
+    for rq in reqs:
+        st.put_chunks(oc.chunk_keys(rq.tokens, lay.chunk_tokens), payload_stack(lay, c["seed"], rq.payload_ids))
+    dests = [make_dest(lay, rq.n_chunks, k, Bs=c["Bs"], first_token=j % 5, seed=c["seed"] + j)
+             for j, (rq, k) in enumerate(zip(reqs, c["kinds"]))]
+    bufs = [sentinel_buffer(dd.size) for dd in dests]
+    descs = [oc.build_descriptor(st, st.match_prefix(rq.tokens), lay, lib_target(oc, dd, b.data_ptr()))
+             for rq, dd, b in zip(reqs, dests, bufs)]
+    order = oc.BATCH_BY_POSITION if c["order"] == "position" else oc.BATCH_BY_REQUEST
+    b = oc.Batch(descs, order=order)
+    s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+    eng = {"auto": oc.COPY_AUTO, "bulk": oc.COPY_BULK, "ldst": oc.COPY_LDST}[c["engine"]]
+    kw = dict(engine=eng, unit_bytes=c["unit"], max_ctas=c["max_ctas"])
+    if c["order"].startswith("wdrr"):
+        rates = [float(random.Random(c["seed"] + j).choice([2e9, 5e9, 2e10])) for j in range(len(descs))]
+        kw.update(wdrr_weights=rates, hold_rates=c["order"] == "wdrr_held",
+                  layer_packets=lay.num_layers if c["order"] == "wdrr_layer" else 0)
+    b.fetch(s, **kw)
+    for dsc in descs:
+        dsc.wait_layer(lay.num_layers - 1, cons)
+    cons.synchronize()
+    s.synchronize()
+    for j, (rq, dd, buf) in enumerate(zip(reqs, dests, bufs)):
+        got = buf.cpu().numpy()
+        want = oracle_result(lay, c["seed"], rq, dd)
+        bad = np.flatnonzero(got != want)
+        assert bad.size == 0, f"batch case {i} member {j} {c}: {bad.size} bytes differ"
+    b.close()
+    for dsc in descs:
+        dsc.close()
+    st.close()
