@@ -137,3 +137,47 @@ def test_random_batch(i):
     for dsc in descs:
         dsc.close()
     st.close()
+
+
+@pytest.mark.parametrize("i", range(40))
+def test_random_offload(i, monkeypatch):
+    """The offload path (paged KV -> new chunk objects, oc_put_from_paged) on random layouts,
+    targets, block sizes and offsets, both kernels, HBM or pinned-host store: the stored chunks,
+    read back through a flat fetch (the Alg. A1 client buffer), equal the oracle's offload of the
+    same cache bytes followed by its gather."""
+    from oracle import keys as okeys
+    from oracle.assemble import fetch_layerwise as ofetch, offload_paged
+    from oracle.descriptor import FlatTarget as OFlat, build_descriptor as obuild
+    from oracle.geometry import chunk_layer_bytes
+    from oracle.store import ChunkStore
+    from scenario import oracle_target
+    r = random.Random(6000 + i)
+    lay = OLayout(r.choice([1, 2, 3, 5]), r.choice([1, 2, 8]), r.choice([16, 32, 128]), 2, r.choice([8, 16, 32]))
+    n = r.randint(1, 24)
+    kind = r.choice(["nhd", "nhd", "hnd"])
+    monkeypatch.setenv("OC_OFFLOAD_ENGINE", r.choice(["bulk", "ldst"]))
+    tier = oc.TIER_PINNED_HOST if r.random() < 0.25 else oc.TIER_HBM
+    req = requests_family(lay, 6100 + i, 0, [n])[0]
+    src = make_dest(lay, n, kind, Bs=r.choice([4, 8, 16, 32]), first_token=r.randint(0, 19), seed=6100 + i)
+    gen = torch.Generator(device="cuda").manual_seed(6100 + i)
+    cache = torch.randint(0, 256, (src.size,), dtype=torch.uint8, device="cuda", generator=gen)
+    keys = oc.chunk_keys(req.tokens, lay.chunk_tokens)
+    W = n * lay.num_layers * chunk_layer_bytes(lay)
+    with oc.Store(lay, capacity=n, tier=tier) as st:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        assert oc.put_from_paged(st, keys, lay, lib_target(oc, src, cache.data_ptr()), s) == n
+        s.synchronize()
+        flat = sentinel_buffer(W)
+        d = oc.build_descriptor(st, keys, lay, oc.FlatTarget(flat.data_ptr(), W))
+        d.fetch_layerwise(s)
+        d.sync_layer(lay.num_layers - 1)
+        got = flat.cpu().numpy()
+        d.close()
+    ost = ChunkStore(lay)
+    ok_ = okeys.chunk_keys(req.tokens, lay.chunk_tokens)
+    assert offload_paged(ost, ok_, lay, oracle_target(src), cache.cpu().numpy()) == n
+    want = np.full(W, 0xA5, np.uint8)
+    ofetch(ost, obuild(ost, ok_, lay, OFlat(0, W)), want)
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, f"offload case {i}: {bad.size} bytes differ"
