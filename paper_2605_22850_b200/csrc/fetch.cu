@@ -53,6 +53,8 @@ int env_int(const char* name, int dflt) {
     return e && *e ? std::atoi(e) : dflt;
 }
 
+bool env_flag(const char* name, bool dflt) { return env_int(name, dflt ? 1 : 0) != 0; }
+
 // Default unit size (profiles/r01_engine_sweep.txt, r01_corun.json): with the whole GPU, 32 KiB
 // units at 3 CTAs per SM reach the copy roofline; with a copy-CTA budget of at most one CTA per
 // SM (co-running with prefill) 64 KiB units -- a whole chunk-layer slice at Llama layouts --
@@ -627,13 +629,20 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s, uint32_t l_e
         // vs 5.0 with a full grid per layer, 6.77 for the single persistent launch).
         const uint32_t pl_ctas = max_ctas ? max_ctas : std::max<uint32_t>(1, (uint32_t)sms * 3 / 4);
         const BulkPlan p = plan_bulk(dd, sms, pl_ctas, upl);
+        // the layers' launches overlap, so each observer first waits for the earlier layers'
+        // announcement: `ready` and the layer stamps stay in layer order
+        dd.wait_prev_layers = 1;
         for (uint32_t l = 0; l < dd.L; l++) {
             const bool ov = l > 0 || (o.flags & OC_FETCH_OVERLAP);
             int rc = o.engine == OC_COPY_BULK ? launch_bulk(d, p, l * upl, (l + 1) * upl, s, ov)
-                                              : launch_ldst(d, sms, max_ctas, l * upl, (l + 1) * upl, s);
-            if (rc) return rc;
+                                              : launch_ldst(d, sms, max_ctas, l * upl, (l + 1) * upl, s, ov);
+            if (rc) {
+                dd.wait_prev_layers = 0;
+                return rc;
+            }
             OC_CUDA(cudaEventRecord(d->events[l], s));
         }
+        dd.wait_prev_layers = 0;
     }
     if (ranged) {
         d->n_ranges = 0;
@@ -1007,10 +1016,34 @@ OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {
         return OC_OK;
     }
     const uint32_t target = (d->epoch - 1u) * L + want_layer + 1u;
-    // Already announced (the host mirror is written after the device word, with system-scope
-    // release): the layer's bytes are in device memory, so nothing needs to be enqueued -- a stream
-    // wait costs the consumer ~1-4 us of launch pipelining even when its condition already holds.
+    // Already announced (the host mirror is written after the device word, once the layer's bytes
+    // are in device memory): nothing needs to be enqueued -- a stream wait costs the consumer
+    // 1-4 us of launch pipelining even when its condition already holds.
     if (d->ready_host && (int32_t)(__atomic_load_n(d->ready_host, __ATOMIC_ACQUIRE) - target) >= 0) return OC_OK;
+    static const bool relay_on = oc::env_flag("OC_WAIT_RELAY", true);
+    if (relay_on && !oc::force_wait_kernel()) {
+        // The value wait goes on a private relay stream, which records a per-layer CUDA event; the
+        // consumer waits on that event: 0.7 us of consumer-stream time per wait against 2.3 us for
+        // a value wait on the consumer stream itself (profiles/r02_wait_kinds.txt).
+        std::lock_guard<std::mutex> lk(d->relay_mu);
+        if (!d->relay) {
+            int lo = 0, hi = 0;
+            OC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            OC_CUDA(cudaStreamCreateWithPriority(&d->relay, cudaStreamNonBlocking, hi));
+        }
+        if (d->relay_ev.empty()) {
+            d->relay_ev.resize(L, nullptr);
+            for (auto& ev : d->relay_ev) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        }
+        int urc = oc::upload_order(&d->up, d->relay);  // the ready word lives in the uploaded block
+        if (urc) return urc;
+        int rc = oc::stream_wait_geq(d->relay, d->dd.ready, target);
+        if (rc == OC_OK) {
+            OC_CUDA(cudaEventRecord(d->relay_ev[want_layer], d->relay));
+            OC_CUDA(cudaStreamWaitEvent(s, d->relay_ev[want_layer], 0));
+            return OC_OK;
+        }
+    }
     int urc = oc::upload_order(&d->up, s);  // the ready word lives in the uploaded block
     if (urc) return urc;
     if (!oc::force_wait_kernel()) {

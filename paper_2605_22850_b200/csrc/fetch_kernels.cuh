@@ -137,10 +137,10 @@ __device__ __forceinline__ void complete_units(const DevDesc& d, uint32_t layer,
 // the last reduction synchronises with every release reduction before it).
 __device__ void observe_layers(const DevDesc& d, uint32_t l0, uint32_t l1) {
     const uint32_t base = (d.epoch - 1u) * d.L;
-    // oc_fetch_layers: a range may run beside the range covering the earlier layers (another
-    // stream): announce nothing before those are announced, so `ready` (and its host copy) only ever
-    // move through the layers in order.  (PER_LAYER launches are waited on through their CUDA
-    // events, and the other split launches are stream-ordered.)
+    // oc_fetch_layers ranges and PER_LAYER launches may run beside the launch covering the earlier
+    // layers (another stream; programmatic dependent launches): announce nothing before those are
+    // announced, so `ready`, its host copy and the layer stamps only ever move through the layers
+    // in order.  (The other split launches are stream-ordered.)
     if (d.wait_prev_layers && l0 > 0) {
         uint32_t ns = 64;
         while ((int32_t)(ld_acquire(d.ready) - (base + l0)) < 0) {

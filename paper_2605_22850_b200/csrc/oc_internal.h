@@ -228,6 +228,11 @@ struct Desc {
     uint32_t range_open = 0;         // oc_fetch_layers: next layer of an incomplete fetch (0: none)
     std::vector<cudaEvent_t> range_evs;  // oc_fetch_layers: completion of each range of the open fetch
     uint32_t n_ranges = 0;               // ranges recorded in range_evs for the open fetch
+    // wait_layer relay (PERSISTENT mode): a private stream turns the ready word into per-layer CUDA
+    // events, so the consumer stream waits on an event (cheaper in the front end than a value wait)
+    std::mutex relay_mu;
+    cudaStream_t relay = nullptr;
+    std::vector<cudaEvent_t> relay_ev;
     uint32_t range_unit_bytes = 0;   // unit size of the current fetch (fixed for its continuations)
 };
 
