@@ -502,10 +502,7 @@ OC_API int oc_desc_free(oc_desc* h) {
         if (d->done_ev) cudaEventDestroy(d->done_ev);
         if (d->sync_ev) cudaEventDestroy(d->sync_ev);
         if (d->sync_stream) cudaStreamDestroy(d->sync_stream);
-        // the relay's work is finished once the fetch is (its waits target announced layers);
-        // destruction is deferred by the runtime if not
-        for (auto ev : d->relay_ev) cudaEventDestroy(ev);
-        if (d->relay) cudaStreamDestroy(d->relay);
+        oc::relay_release(d);
         oc::ce_release(d);
         oc::dev_pool_free(d->device, d->dev_mem, d->dev_mem_class);
         oc::ready_mirror_free(d->ready_host);

@@ -286,6 +286,57 @@ int ce_kit_get(int device, uint32_t L, CeKit** out) {
 }
 }  // namespace
 
+// wait_layer relay: a high-priority stream and one event per layer.  Creating them costs ~50 us of
+// host time, so they are pooled per (device, L) like the CE kits.
+struct RelayKit {
+    cudaStream_t stream = nullptr;
+    std::vector<cudaEvent_t> ev;
+};
+
+namespace {
+std::mutex g_relay_mu;
+std::unordered_map<uint64_t, std::vector<RelayKit*>> g_relays;
+
+int relay_get(int device, uint32_t L, RelayKit** out) {
+    const uint64_t key = ((uint64_t)(uint32_t)device << 32) | L;
+    {
+        std::lock_guard<std::mutex> lk(g_relay_mu);
+        auto& v = g_relays[key];
+        if (!v.empty()) {
+            *out = v.back();
+            v.pop_back();
+            return OC_OK;
+        }
+    }
+    auto k = std::make_unique<RelayKit>();
+    int lo = 0, hi = 0;
+    OC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    OC_CUDA(cudaStreamCreateWithPriority(&k->stream, cudaStreamNonBlocking, hi));
+    k->ev.resize(L, nullptr);
+    for (auto& e : k->ev) OC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    *out = k.release();
+    return OC_OK;
+}
+}  // namespace
+
+// Called by oc_desc_free after the descriptor's last fetch has completed.  A relay still waiting
+// (a consumer waited on a layer that was never announced) is not reused: it is destroyed, and the
+// runtime releases it when its work ends.
+void relay_release(Desc* d) {
+    RelayKit* k = d->relay;
+    d->relay = nullptr;
+    if (!k) return;
+    if (cudaStreamQuery(k->stream) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_relay_mu);
+        g_relays[((uint64_t)(uint32_t)d->device << 32) | d->geo.L].push_back(k);
+        return;
+    }
+    cudaGetLastError();
+    for (auto e : k->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(k->stream);
+    delete k;
+}
+
 // Called by oc_desc_free after the descriptor's last fetch has completed.
 void ce_release(Desc* d) {
     if (d->ce_kit) {
@@ -1027,20 +1078,16 @@ OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {
         // a value wait on the consumer stream itself (profiles/r02_wait_kinds.txt).
         std::lock_guard<std::mutex> lk(d->relay_mu);
         if (!d->relay) {
-            int lo = 0, hi = 0;
-            OC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            OC_CUDA(cudaStreamCreateWithPriority(&d->relay, cudaStreamNonBlocking, hi));
+            int krc = oc::relay_get(d->device, L, &d->relay);
+            if (krc) return krc;
         }
-        if (d->relay_ev.empty()) {
-            d->relay_ev.resize(L, nullptr);
-            for (auto& ev : d->relay_ev) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        }
-        int urc = oc::upload_order(&d->up, d->relay);  // the ready word lives in the uploaded block
+        cudaStream_t rs = d->relay->stream;
+        int urc = oc::upload_order(&d->up, rs);  // the ready word lives in the uploaded block
         if (urc) return urc;
-        int rc = oc::stream_wait_geq(d->relay, d->dd.ready, target);
+        int rc = oc::stream_wait_geq(rs, d->dd.ready, target);
         if (rc == OC_OK) {
-            OC_CUDA(cudaEventRecord(d->relay_ev[want_layer], d->relay));
-            OC_CUDA(cudaStreamWaitEvent(s, d->relay_ev[want_layer], 0));
+            OC_CUDA(cudaEventRecord(d->relay->ev[want_layer], rs));
+            OC_CUDA(cudaStreamWaitEvent(s, d->relay->ev[want_layer], 0));
             return OC_OK;
         }
     }

@@ -231,13 +231,14 @@ struct Desc {
     // wait_layer relay (PERSISTENT mode): a private stream turns the ready word into per-layer CUDA
     // events, so the consumer stream waits on an event (cheaper in the front end than a value wait)
     std::mutex relay_mu;
-    cudaStream_t relay = nullptr;
-    std::vector<cudaEvent_t> relay_ev;
+    struct RelayKit* relay = nullptr;    // stream + L events, pooled per (device, L) (fetch.cu)
     uint32_t range_unit_bytes = 0;   // unit size of the current fetch (fixed for its continuations)
 };
 
 // CE engine resources returned to their pool when a descriptor is freed (fetch.cu).
 void ce_release(Desc* d);
+// wait_layer relay resources returned to their pool when a descriptor is freed (fetch.cu).
+void relay_release(Desc* d);
 
 // Pooled memory (pool.cpp): power-of-two blocks of device memory on `device`, or of pinned host
 // memory (device = -1), recycled instead of returned to the driver.
