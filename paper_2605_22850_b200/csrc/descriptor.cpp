@@ -498,7 +498,7 @@ OC_API int oc_desc_free(oc_desc* h) {
             cudaEventDestroy(ev);
         }
         oc::upload_release(&d->up);
-        for (auto ev : d->events) cudaEventDestroy(ev);
+        oc::per_layer_events_release(d);
         if (d->done_ev) cudaEventDestroy(d->done_ev);
         if (d->sync_ev) cudaEventDestroy(d->sync_ev);
         if (d->sync_stream) cudaStreamDestroy(d->sync_stream);

@@ -319,6 +319,35 @@ int relay_get(int device, uint32_t L, RelayKit** out) {
 }
 }  // namespace
 
+// PER_LAYER mode's per-layer events, pooled per (device, L) as well (a serving loop builds a
+// descriptor per request; creating L events costs tens of us of host time).
+namespace {
+std::unordered_map<uint64_t, std::vector<std::vector<cudaEvent_t>>> g_layer_evs;  // under g_relay_mu
+}  // namespace
+
+int per_layer_events_get(int device, uint32_t L, std::vector<cudaEvent_t>* out) {
+    {
+        std::lock_guard<std::mutex> lk(g_relay_mu);
+        auto& v = g_layer_evs[((uint64_t)(uint32_t)device << 32) | L];
+        if (!v.empty()) {
+            *out = std::move(v.back());
+            v.pop_back();
+            return OC_OK;
+        }
+    }
+    out->assign(L, nullptr);
+    for (auto& e : *out) OC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return OC_OK;
+}
+
+// Called by oc_desc_free after the descriptor's last fetch has completed (every recorded event is).
+void per_layer_events_release(Desc* d) {
+    if (d->events.empty()) return;
+    std::lock_guard<std::mutex> lk(g_relay_mu);
+    g_layer_evs[((uint64_t)(uint32_t)d->device << 32) | d->geo.L].push_back(std::move(d->events));
+    d->events.clear();
+}
+
 // Called by oc_desc_free after the descriptor's last fetch has completed.  A relay still waiting
 // (a consumer waited on a layer that was never announced) is not reused: it is destroyed, and the
 // runtime releases it when its work ends.
@@ -586,8 +615,8 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s, uint32_t l_e
     if (urc) return urc;
     if (!d->done_ev) OC_CUDA(cudaEventCreateWithFlags(&d->done_ev, cudaEventDisableTiming));
     if (o.mode == OC_FETCH_PER_LAYER && d->events.empty()) {
-        d->events.resize(d->geo.L, nullptr);
-        for (auto& ev : d->events) OC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        int erc = per_layer_events_get(d->device, d->geo.L, &d->events);
+        if (erc) return erc;
     }
     // PCIe-bound sources (pinned host tier) saturate the link from a handful of CTAs.  More CTAs
     // only lengthen the PCIe read queue, and every other GPU read of host memory -- the command

@@ -239,6 +239,9 @@ struct Desc {
 void ce_release(Desc* d);
 // wait_layer relay resources returned to their pool when a descriptor is freed (fetch.cu).
 void relay_release(Desc* d);
+// PER_LAYER mode's events: taken from / returned to a pool per (device, L) (fetch.cu).
+int per_layer_events_get(int device, uint32_t L, std::vector<cudaEvent_t>* out);
+void per_layer_events_release(Desc* d);
 
 // Pooled memory (pool.cpp): power-of-two blocks of device memory on `device`, or of pinned host
 // memory (device = -1), recycled instead of returned to the driver.
