@@ -1,4 +1,4 @@
-"""Randomised parity: 200 seeded configurations drawn over the whole option space -- layout (L,
+"""Randomised parity: 400 seeded configurations drawn over the whole option space -- layout (L,
 n_kv, d, p, G), chunk count, target (paged NHD / head-split HND / flat), block size and first-token
 offset, store tier (HBM, pinned host), engine (AUTO, TMA, LD/ST, copy engine), mode (persistent,
 per-layer events), unit size, copy-CTA cap,
@@ -48,7 +48,7 @@ def _case(i):
                 tier=oc.TIER_PINNED_HOST if host else oc.TIER_HBM)
 
 
-@pytest.mark.parametrize("i", range(200))
+@pytest.mark.parametrize("i", range(400))
 def test_random_configuration(i):
     c = _case(i)
     lay, n = c["lay"], c["n"]
@@ -97,7 +97,7 @@ def _batch_case(i):
                 max_ctas=r.choice([0, 0, 2, 9]))
 
 
-@pytest.mark.parametrize("i", range(60))
+@pytest.mark.parametrize("i", range(120))
 def test_random_batch(i):
     """One launch for several requests of one prefix family (shared chunks read through one store
     slot), in a random claim order -- by request, position-major, or weighted deficit round robin
@@ -139,7 +139,7 @@ def test_random_batch(i):
     st.close()
 
 
-@pytest.mark.parametrize("i", range(40))
+@pytest.mark.parametrize("i", range(80))
 def test_random_offload(i, monkeypatch):
     """The offload path (paged KV -> new chunk objects, oc_put_from_paged) on random layouts,
     targets, block sizes and offsets, both kernels, HBM or pinned-host store: the stored chunks,
