@@ -77,6 +77,18 @@ typedef struct {
 OC_API int oc_geometry(const oc_layout* layout, uint64_t* row_bytes, uint64_t* layer_chunk_bytes,
                        uint64_t* chunk_bytes);
 
+/* Slot pitch: the byte distance between consecutive chunk slots of a store slab
+ * of this layout and tier (slot i at slab base + i*pitch; an object's L*S bytes
+ * at the start of its slot).  The layout of a slot is the paper's chunk object
+ * (P:347-354); how slots are spaced is this library's choice: an HBM slab of
+ * chunks of >= 1 MiB spaces them by the smallest multiple of 32 KiB >= L*S whose
+ * count of 32 KiB granules has no factor 3 or 5 (a layer reads one S-byte slice
+ * per slot, and on B200 such spacings read 6-8% faster than e.g. 2.5 or 5 MiB;
+ * profiles/r02_stride_probe*.txt); pinned-host slabs and smaller chunks are
+ * dense (pitch = L*S).  Pure function (no GPU).  EINVAL on a bad layout, tier or
+ * null out. */
+OC_API int oc_slot_pitch(const oc_layout* layout, int tier, uint64_t* pitch);
+
 /* Eq. 2: returns OC_DELIVER_CHUNK_MAJOR if W < theta, else
  * OC_DELIVER_LAYER_MAJOR (theta = 0 always selects layer-major). */
 OC_API int oc_select_mode(uint64_t payload_W, uint64_t theta);
@@ -127,7 +139,8 @@ OC_API int oc_store_set_hot_layers(oc_store* store, uint32_t hot_layers);
  * EINVAL if X or C is not finite and > 0, or L = 0. */
 OC_API int oc_hot_layers_for(double X_s, double C_s, uint32_t L, uint32_t* K);
 
-/* Slab base device address and size in bytes (for IPC export and tests). */
+/* Slab base device address and size in bytes = capacity * oc_slot_pitch (for
+ * IPC export and tests). */
 OC_API int oc_store_slab(const oc_store* store, uint64_t* base, uint64_t* bytes);
 
 /* put_chunks (P:224 offload; P:36-40 immutable, content-addressed writes):

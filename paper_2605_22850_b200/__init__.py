@@ -85,6 +85,7 @@ _SIGS = {
     "oc_store_destroy": [_vp],
     "oc_store_count": [_vp, c_u64p],
     "oc_store_slab": [_vp, c_u64p, c_u64p],
+    "oc_slot_pitch": [ctypes.POINTER(CLayout), ctypes.c_int, c_u64p],
     "oc_store_set_hot_layers": [_vp, ctypes.c_uint32],
     "oc_hot_layers_for": [ctypes.c_double, ctypes.c_double, ctypes.c_uint32, c_u32p],
     "oc_put_chunks": [_vp, _vp, _vp, ctypes.c_uint64, c_u64p, c_u64p],
@@ -205,6 +206,14 @@ def geometry(layout):
     return row.value, S.value, ch.value
 
 
+def slot_pitch(layout, tier: int = 0) -> int:
+    """oc_slot_pitch: byte distance between consecutive slots of a store slab of this layout/tier."""
+    p = ctypes.c_uint64()
+    lay = _layout(layout)
+    _check(_lib.oc_slot_pitch(ctypes.byref(lay), int(tier), ctypes.byref(p)))
+    return p.value
+
+
 def select_mode(payload_W: int, theta: int) -> int:
     """Eq. 2 delivery mode (DELIVER_CHUNK_MAJOR if W < theta else DELIVER_LAYER_MAJOR)."""
     return _lib.oc_select_mode(int(payload_W), int(theta))
@@ -321,6 +330,10 @@ class Store:
         b, n = ctypes.c_uint64(), ctypes.c_uint64()
         _check(_lib.oc_store_slab(self._h, ctypes.byref(b), ctypes.byref(n)))
         return b.value, n.value
+
+    @property
+    def slot_pitch(self) -> int:
+        return slot_pitch(self.layout, self.tier)
 
     def put_chunks(self, keys, payloads) -> int:
         k = _keys_array(keys)

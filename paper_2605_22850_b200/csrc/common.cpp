@@ -89,6 +89,25 @@ int stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t value) {
 
 }  // namespace oc
 
+namespace oc {
+// Slot pitch of a store slab (profiles/r02_stride_probe*.txt).  A layer of a request reads one
+// S-byte slice from each of its chunks' slots, i.e. N slices spaced by the slot pitch.  On B200 the
+// HBM read rate of that pattern depends on the spacing alone: spacings whose count of 32 KiB
+// granules has a factor 3 or 5 run at 4.9-6.45 TB/s (2.5 and 5 MiB: 6.1; 7.5 MiB: 4.9), spacings
+// free of both (powers of two, 5 MiB + 32 KiB, 2.5 MiB + 64 KiB, ...) at 6.54-6.64, the same as
+// randomly placed slices.  So an HBM slab of chunks of >= 1 MiB spaces its slots by the smallest
+// multiple of 32 KiB >= L*S free of the factors 3 and 5 (at most 2 granules more: <= 1.3% of a
+// 5 MiB slot).  Pinned-host slabs are PCIe-bound and keep dense slots (the copy engine reads runs
+// of consecutive slots as one strided transfer of pitch L*S).
+uint64_t slot_pitch(const Geometry& g, int tier) {
+    constexpr uint64_t q = 32768;
+    if (tier != OC_TIER_HBM || g.chunk < (1ull << 20)) return g.chunk;
+    uint64_t u = (g.chunk + q - 1) / q;
+    while (u % 3 == 0 || u % 5 == 0) u++;
+    return u * q;
+}
+}  // namespace oc
+
 extern "C" {
 
 OC_API const char* oc_last_error(void) { return oc::g_last_error.c_str(); }
@@ -119,6 +138,16 @@ OC_API int oc_geometry(const oc_layout* layout, uint64_t* row_bytes, uint64_t* l
     if (row_bytes) *row_bytes = g.row;
     if (layer_chunk_bytes) *layer_chunk_bytes = g.S;
     if (chunk_bytes) *chunk_bytes = g.chunk;
+    return OC_OK;
+}
+
+OC_API int oc_slot_pitch(const oc_layout* layout, int tier, uint64_t* pitch) {
+    if (!pitch) return oc::fail(OC_EINVAL, "slot_pitch: null out");
+    oc::Geometry g;
+    int rc = oc::make_geometry(layout, &g);
+    if (rc) return rc;
+    if (tier != OC_TIER_HBM && tier != OC_TIER_PINNED_HOST) return oc::fail(OC_EINVAL, "slot_pitch: bad tier");
+    *pitch = oc::slot_pitch(g, tier);
     return OC_OK;
 }
 

@@ -400,7 +400,7 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
             }
             const uint64_t slot = s->count++;
             s->index.emplace(keys[i], slot);
-            dst.push_back((uint64_t)(uintptr_t)s->slab + slot * g.chunk);
+            dst.push_back((uint64_t)(uintptr_t)s->slab + slot * s->pitch);
             pos.push_back((uint32_t)i);
         }
     }
@@ -410,7 +410,7 @@ OC_API int oc_put_from_paged(oc_store* sh, const oc_key* keys, uint64_t n, const
         std::unique_lock<std::shared_mutex> lk(s->mu);
         for (uint32_t p : pos) s->index.erase(keys[p]);
         // give the slots back when nobody reserved after them (they are the slab's last ones)
-        const uint64_t first = (dst.front() - (uint64_t)(uintptr_t)s->slab) / g.chunk;
+        const uint64_t first = (dst.front() - (uint64_t)(uintptr_t)s->slab) / s->pitch;
         if (s->count == first + dst.size()) s->count = first;
         if (n_new) *n_new = 0;
     };

@@ -48,6 +48,8 @@ struct Geometry {
     uint64_t chunk;  // L*S
 };
 int make_geometry(const oc_layout* lay, Geometry* g);
+// Byte distance between consecutive slots of a store slab (common.cpp; >= g.chunk).
+uint64_t slot_pitch(const Geometry& g, int tier);
 bool same_layout(const oc_layout& a, const oc_layout& b);
 
 // ---- keys --------------------------------------------------------------------
@@ -87,6 +89,7 @@ struct Store {
     int tier;
     int device;
     uint64_t capacity;
+    uint64_t pitch = 0;       // slot i at slab + i * pitch (slot_pitch: >= geo.chunk)
     uint8_t* slab = nullptr;  // device address (HBM, mapped host, or IPC-mapped peer)
     bool owns_slab = true;
     bool ipc_mapped = false;

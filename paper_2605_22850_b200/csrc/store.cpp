@@ -21,6 +21,7 @@ struct ExportHeader {
     uint32_t tier;
     uint64_t capacity;
     uint64_t count;
+    uint64_t pitch;
     cudaIpcMemHandle_t handle;
 };
 
@@ -32,7 +33,7 @@ bool store_resolve(Store* s, const oc_key& k, uint64_t* addr, int* tier, uint64_
         std::shared_lock<std::shared_mutex> lk(s->mu);
         auto it = s->index.find(k);
         if (it != s->index.end()) {
-            *addr = (uint64_t)(uintptr_t)s->slab + it->second * s->geo.chunk;
+            *addr = (uint64_t)(uintptr_t)s->slab + it->second * s->pitch;
             if (tier) *tier = s->tier;
             if (hot) *hot = s->hot_layers ? (uint64_t)(uintptr_t)s->hot_slab + it->second * s->hot_layers * s->geo.S : 0;
             if (hot_layers) *hot_layers = s->hot_layers;
@@ -75,7 +76,8 @@ OC_API int oc_store_create(const oc_layout* layout, int tier, int device, uint64
     if (rc) return rc;
     if (tier != OC_TIER_HBM && tier != OC_TIER_PINNED_HOST) return oc::fail(OC_EINVAL, "store_create: bad tier");
     if (capacity == 0) return oc::fail(OC_EINVAL, "store_create: capacity must be >= 1");
-    if (capacity > (1ull << 40) / 1 || (unsigned __int128)capacity * g.chunk >> 62)
+    const uint64_t pitch = oc::slot_pitch(g, tier);
+    if (capacity > (1ull << 40) / 1 || (unsigned __int128)capacity * pitch >> 62)
         return oc::fail(OC_EINVAL, "store_create: capacity too large");
     if (g.row % 16 || g.hd % 16) return oc::fail(OC_EALIGN, "store_create: n_kv*d*p and d*p must be multiples of 16");
     int ndev = 0;
@@ -88,7 +90,8 @@ OC_API int oc_store_create(const oc_layout* layout, int tier, int device, uint64
     s->tier = tier;
     s->device = device;
     s->capacity = capacity;
-    uint64_t bytes = capacity * g.chunk;
+    s->pitch = pitch;
+    uint64_t bytes = capacity * pitch;
     void* p = nullptr;
     cudaError_t e;
     if (tier == OC_TIER_HBM) e = cudaMalloc(&p, bytes);
@@ -172,7 +175,7 @@ OC_API int oc_store_slab(const oc_store* h, uint64_t* base, uint64_t* bytes) {
     if (!h) return oc::fail(OC_EINVAL, "store_slab: null store");
     const Store* s = (const Store*)h;
     if (base) *base = (uint64_t)(uintptr_t)s->slab;
-    if (bytes) *bytes = s->capacity * s->geo.chunk;
+    if (bytes) *bytes = s->capacity * s->pitch;
     return OC_OK;
 }
 
@@ -215,7 +218,7 @@ OC_API int oc_put_chunks(oc_store* h, const oc_key* keys, const void* payloads, 
             OC_CUDA(cudaStreamSynchronize(s->put_stream));
             a.resize(cb);
             b.resize(cb);
-            OC_CUDA(cudaMemcpy(a.data(), s->slab + it->second * cb, cb, cudaMemcpyDefault));
+            OC_CUDA(cudaMemcpy(a.data(), s->slab + it->second * s->pitch, cb, cudaMemcpyDefault));
             OC_CUDA(cudaMemcpy(b.data(), src + i * cb, cb, cudaMemcpyDefault));
             if (std::memcmp(a.data(), b.data(), cb) != 0) {
                 if (bad_index) *bad_index = i;
@@ -232,7 +235,7 @@ OC_API int oc_put_chunks(oc_store* h, const oc_key* keys, const void* payloads, 
             return oc::fail(OC_EFULL, "put_chunks: store capacity exhausted");
         }
         uint64_t slot = s->count;
-        OC_CUDA(cudaMemcpyAsync(s->slab + slot * cb, src + i * cb, cb, cudaMemcpyDefault, s->put_stream));
+        OC_CUDA(cudaMemcpyAsync(s->slab + slot * s->pitch, src + i * cb, cb, cudaMemcpyDefault, s->put_stream));
         if (s->hot_layers) {  // the chunk's first layers are its first hot_layers * S bytes
             const uint64_t hb = (uint64_t)s->hot_layers * s->geo.S;
             OC_CUDA(cudaMemcpyAsync(s->hot_slab + slot * hb, src + i * cb, hb, cudaMemcpyDefault, s->put_stream));
@@ -316,6 +319,7 @@ OC_API int oc_store_export(oc_store* h, void* buf, uint64_t* size) {
     hd.tier = s->tier;
     hd.capacity = s->capacity;
     hd.count = s->count;
+    hd.pitch = s->pitch;
     {
         oc::DeviceGuard dg(s->device);
         OC_CUDA(cudaIpcGetMemHandle(&hd.handle, s->slab));
@@ -345,6 +349,8 @@ OC_API int oc_store_import(const void* buf, uint64_t size, int device, oc_store*
     auto s = std::make_unique<Store>();
     int rc = oc::make_geometry(&hd.layout, &s->geo);
     if (rc) return rc;
+    if (hd.pitch < s->geo.chunk || hd.pitch % 16) return oc::fail(OC_EINVAL, "store_import: corrupt slot pitch");
+    s->pitch = hd.pitch;
     s->layout = hd.layout;
     s->tier = hd.tier;
     s->device = device;

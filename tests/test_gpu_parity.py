@@ -73,10 +73,11 @@ def test_tiny_store_match_and_dedup():
         # lookup returns slot addresses inside the slab, and the slots hold the put bytes
         addrs = st.lookup(oc.chunk_keys(b.tokens, 16))
         base, nbytes = st.slab
-        n = pb.shape[1]
+        n, pitch = pb.shape[1], st.slot_pitch
+        assert pitch >= n and nbytes == 16 * pitch
         assert len(set(addrs.tolist())) == 11
         for ad in addrs:
-            assert (int(ad) - base) % n == 0 and int(ad) - base + n <= nbytes
+            assert (int(ad) - base) % pitch == 0 and int(ad) - base + n <= nbytes
 
 
 @pytest.mark.parametrize("kind", ["nhd", "hnd", "flat"])
