@@ -82,9 +82,9 @@ OC_API int oc_geometry(const oc_layout* layout, uint64_t* row_bytes, uint64_t* l
  * at the start of its slot).  The layout of a slot is the paper's chunk object
  * (P:347-354); how slots are spaced is this library's choice: an HBM slab of
  * chunks of >= 1 MiB spaces them by the smallest multiple of 32 KiB >= L*S whose
- * count of 32 KiB granules has no factor 3 or 5 (a layer reads one S-byte slice
- * per slot, and on B200 such spacings read 6-8% faster than e.g. 2.5 or 5 MiB;
- * profiles/r02_stride_probe*.txt); pinned-host slabs and smaller chunks are
+ * count of 32 KiB granules has no factor 3, 5 or 7 (a layer reads one S-byte slice
+ * per slot, and on B200 such spacings read up to 9% faster than e.g. 2.5 or 5 MiB;
+ * profiles/r02_pitch_sweep.txt); pinned-host slabs and smaller chunks are
  * dense (pitch = L*S).  Pure function (no GPU).  EINVAL on a bad layout, tier or
  * null out. */
 OC_API int oc_slot_pitch(const oc_layout* layout, int tier, uint64_t* pitch);

@@ -1,4 +1,5 @@
 // Errors, geometry (Eq. 1), the Eq. 2 mode rule, fast division and driver entry points.
+#include <cstdlib>
 #include <cuda.h>
 
 #include "oc_internal.h"
@@ -90,20 +91,26 @@ int stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t value) {
 }  // namespace oc
 
 namespace oc {
-// Slot pitch of a store slab (profiles/r02_stride_probe*.txt).  A layer of a request reads one
-// S-byte slice from each of its chunks' slots, i.e. N slices spaced by the slot pitch.  On B200 the
-// HBM read rate of that pattern depends on the spacing alone: spacings whose count of 32 KiB
-// granules has a factor 3 or 5 run at 4.9-6.45 TB/s (2.5 and 5 MiB: 6.1; 7.5 MiB: 4.9), spacings
-// free of both (powers of two, 5 MiB + 32 KiB, 2.5 MiB + 64 KiB, ...) at 6.54-6.64, the same as
-// randomly placed slices.  So an HBM slab of chunks of >= 1 MiB spaces its slots by the smallest
-// multiple of 32 KiB >= L*S free of the factors 3 and 5 (at most 2 granules more: <= 1.3% of a
-// 5 MiB slot).  Pinned-host slabs are PCIe-bound and keep dense slots (the copy engine reads runs
-// of consecutive slots as one strided transfer of pitch L*S).
+// Slot pitch of a store slab (profiles/r02_stride_probe.txt, r02_pitch_sweep.txt).  A layer of a
+// request reads one S-byte slice from each of its chunks' slots, i.e. N slices spaced by the slot
+// pitch.  On B200 the HBM read rate of that pattern depends on the spacing: counted in 32 KiB
+// granules, multiples of 5 read at 4.9-6.6 TB/s (160 = 5 MiB: 6.23; 180: 4.95; 90: 5.84), multiples
+// of 3 at 6.52-6.72, most others at 6.7-6.8 like randomly placed slices; 161 = 7 * 23 read at 6.66
+// (98, 112, 196 at 6.79-6.80: a factor 7 is not always slow).  So an HBM slab of chunks of >= 1 MiB
+// spaces its slots by the smallest multiple of 32 KiB >= L*S whose granule count has no factor 3, 5
+// or 7 (Llama-3-70B: 163 granules, +1.9%; powers of two, e.g. Llama-3-8B's 2 MiB, stay dense).
+// Pinned-host slabs are PCIe-bound and keep dense slots (the copy engine reads runs of consecutive
+// slots as one strided transfer of pitch L*S).
 uint64_t slot_pitch(const Geometry& g, int tier) {
     constexpr uint64_t q = 32768;
     if (tier != OC_TIER_HBM || g.chunk < (1ull << 20)) return g.chunk;
+    // OC_SLOT_PITCH_KIB: sweep override (a multiple of 32 >= L*S/1024; ignored otherwise)
+    if (const char* e = std::getenv("OC_SLOT_PITCH_KIB")) {
+        const uint64_t v = std::strtoull(e, nullptr, 10) << 10;
+        if (v >= g.chunk && v % q == 0) return v;
+    }
     uint64_t u = (g.chunk + q - 1) / q;
-    while (u % 3 == 0 || u % 5 == 0) u++;
+    while (u % 3 == 0 || u % 5 == 0 || u % 7 == 0) u++;
     return u * q;
 }
 }  // namespace oc
