@@ -1065,10 +1065,17 @@ __global__ void __launch_bounds__(32) offload_bulk_kernel(const __grid_constant_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
+    // CTA b's first unit is b (the grid never exceeds the job's units), so its first loads go out
+    // without a claim round trip; later units come from the counter (value c -> unit grid + c),
+    // claimed one ahead so the atomic's latency overlaps a unit's copy, as in fetch_bulk_kernel.
+    uint32_t next_raw = lane == 0 ? atomicAdd(d.next_unit, 1u) : 0u;
     auto claim = [&](uint32_t k) {  // all lanes; returns whether unit k exists
-        uint32_t g = 0;
         if (lane == 0) {
-            g = atomicAdd(d.next_unit, 1u);
+            uint32_t g = blockIdx.x;
+            if (k != 0) {
+                g = gridDim.x + next_raw;
+                if (g < total) next_raw = atomicAdd(d.next_unit, 1u);
+            }
             s_unit[k % 32] = g < total ? g : kEnd;
         }
         __syncwarp();
