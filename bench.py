@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--profile", action="store_true", help="headline only, no soak / clock sampling (ncu runs)")
     p.add_argument("--stall-gemm", action="store_true", help="added TTFT with real prefill (GEMMs + attention)")
     p.add_argument("--stall-gemm-hbm-only", action="store_true")
+    p.add_argument("--stall-gemm-cells", default="4k,64k", help="comma list of stall-gemm cells (4k, 64k)")
+    p.add_argument("--stall-gemm-variants", default="", help="comma list of HBM-tier variants (default: all)")
     p.add_argument("--sched", default="", help="comma list of scheduler workloads (A,B,C,70B; 70B = config 4)")
     p.add_argument("--corun", action="store_true")
     p.add_argument("--granularity", action="store_true", help="G = 16/64/256 and the unfused flow")

@@ -205,6 +205,8 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
            "method": "paired chains (fetch, resident-no-wait) back to back; CUDA events per layer on the consumer "
                      "stream; median over pairs"}
     cells = [("4k", 4096, 11)] + ([("64k", 65536, 5)] if getattr(args, "stall64k", 1) else [])
+    keep = set(getattr(args, "stall_gemm_cells", "4k,64k").split(","))
+    cells = [c for c in cells if c[0] in keep]
     for name, ctx, pairs in cells:
         cached = ctx * 7 // 8
         m = ctx - cached
@@ -285,6 +287,9 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                                        # profiles/r02_stall_gemm_gated.json)
                                        ("gated_u32k", {"gated": {"k0": 2, "engine": oc.COPY_BULK, "max_ctas": 148,
                                                                  "unit_bytes": 32768}}, None)))]
+        sel = [v for v in getattr(args, "stall_gemm_variants", "").split(",") if v]
+        if sel:
+            tiers = [(tn, t, tuple(v for v in vs if v[0] in sel)) for tn, t, vs in tiers]
         if not getattr(args, "stall_gemm_hbm_only", False):
             tiers += [("pinned_host", oc.TIER_PINNED_HOST, (("sm", {"engine": oc.COPY_BULK}, None),
                                                             ("ce", {"engine": oc.COPY_CE}, None)))]

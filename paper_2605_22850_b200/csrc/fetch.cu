@@ -675,6 +675,13 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s, uint32_t l_e
             BulkPlan p = plan_bulk(dd, sms, 0, (uint64_t)total_units - upl);
             p.copy_ctas = (uint32_t)(total_units - upl);
             shallow_ring(&p);  // one unit per CTA: the smallest ring (2 stages) is the smallest footprint
+            // OC_YIELD_CTAS_PER_SM=k (measurement knob): pad the CTA's shared memory so that at most
+            // k copy CTAs share an SM (less HBM pressure in the consumer's kernel tails)
+            if (const int k = env_int("OC_YIELD_CTAS_PER_SM", 0); k > 0) {
+                const uint32_t f = (228u * 1024u) / (uint32_t)k;  // per-CTA footprint: k fit, k + 1 do not
+                const uint32_t dyn = std::min<uint32_t>(f - 1024u - kBulkStaticSmem, 227u * 1024u);
+                p.smem = std::max(p.smem, dyn);
+            }
             rc = launch_bulk(d, p, upl, (uint32_t)total_units, s);
             if (rc) return rc;
         }
