@@ -283,6 +283,11 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                                        ("per_layer", {"mode": oc.FETCH_PER_LAYER}, None),
                                        ("yield", {"engine": oc.COPY_BULK, "yield_sms": True}, None),
                                        ("yield_prio", {"engine": oc.COPY_BULK, "yield_sms": True}, (lo_s, hi_s)),
+                                       # finer units: smaller copy CTAs, more of them per SM in a tail
+                                       ("yield_prio_u16k", {"engine": oc.COPY_BULK, "yield_sms": True,
+                                                            "unit_bytes": 16384}, (lo_s, hi_s)),
+                                       ("yield_prio_u8k", {"engine": oc.COPY_BULK, "yield_sms": True,
+                                                           "unit_bytes": 8192}, (lo_s, hi_s)),
                                        # the co-run schedule through oc_fetch_layers (measured worse:
                                        # profiles/r02_stall_gemm_gated.json)
                                        ("gated_u32k", {"gated": {"k0": 2, "engine": oc.COPY_BULK, "max_ctas": 148,
