@@ -10,12 +10,17 @@ import torch.multiprocessing as mp  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def _owner(q, done):
+# the tiny layout (dense slots) and one whose HBM slots are padded (oc_slot_pitch: 1.25 MiB chunks,
+# 40 granules of 32 KiB -> 41): the importer must use the exporter's pitch
+LAYOUTS = [(2, 2, 64, 2, 16), (20, 8, 128, 2, 16)]
+
+
+def _owner(q, done, lay_t):
     import paper_2605_22850_b200 as oc
     from oracle.geometry import Layout
     from scenario import payload_stack, requests_family
     torch.cuda.set_device(0)
-    lay = Layout(2, 2, 64, 2, 16)
+    lay = Layout(*lay_t)
     req = requests_family(lay, 31, 0, [12])[0]
     keys = oc.chunk_keys(req.tokens, 16)
     st = oc.Store(lay, capacity=16)
@@ -25,17 +30,20 @@ def _owner(q, done):
     st.close()
 
 
-def test_export_import_across_processes():
+@pytest.mark.parametrize("lay_t", LAYOUTS)
+def test_export_import_across_processes(lay_t):
     import paper_2605_22850_b200 as oc
     from oracle.geometry import Layout
     from scenario import lib_target, make_dest, oracle_result, payload_stack, requests_family, sentinel_buffer
     ctx = mp.get_context("spawn")
     q, done = ctx.Queue(), ctx.Event()
-    p = ctx.Process(target=_owner, args=(q, done))
+    p = ctx.Process(target=_owner, args=(q, done, lay_t))
     p.start()
     try:
         blob = q.get(timeout=120)
-        lay = Layout(2, 2, 64, 2, 16)
+        lay = Layout(*lay_t)
+        if lay_t == LAYOUTS[1]:
+            assert oc.slot_pitch(lay_t, oc.TIER_HBM) == 41 * 32768 > oc.geometry(lay_t)[2]
         req = requests_family(lay, 31, 0, [12])[0]
         keys = oc.chunk_keys(req.tokens, 16)
         local = oc.Store(lay, capacity=16)

@@ -126,3 +126,48 @@ def test_offload_into_pinned_host_store(monkeypatch, engine):
     want = np.full(W, 0xA5, np.uint8)
     fetch_layerwise(ost, obuild(ost, ok, lay, OFlat(0, W)), want)
     assert np.array_equal(got, want)
+
+
+def test_offload_into_padded_slots_then_fetch():
+    """A layout whose HBM slots are padded (oc_slot_pitch: 1.25 MiB chunks -> 41 granules of 32 KiB):
+    offload (put_from_paged) and put_chunks write at slot * pitch, lookups return those addresses,
+    and fetches of both read them back -- byte-exact against the oracle's offload + Alg. A1."""
+    from scenario import payload_stack
+    lay = OLayout(20, 8, 128, 2, 16)
+    lay_t = (20, 8, 128, 2, 16)
+    chunk = oc.geometry(lay_t)[2]
+    pitch = oc.slot_pitch(lay_t, oc.TIER_HBM)
+    assert pitch == 41 * 32768 and chunk == 40 * 32768
+    N = 5
+    r1, r2 = requests_family(lay, 42, 0, [N, N])
+    src = make_dest(lay, N, "nhd", Bs=16, first_token=0, seed=42)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    cache = torch.randint(0, 256, (src.size,), dtype=torch.uint8, device="cuda", generator=gen)
+    k1, k2 = oc.chunk_keys(r1.tokens, 16), oc.chunk_keys(r2.tokens, 16)
+    W = N * lay.num_layers * chunk_layer_bytes(lay)
+    with oc.Store(lay, capacity=2 * N) as st:
+        assert st.slot_pitch == pitch and st.slab[1] == 2 * N * pitch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        assert oc.put_from_paged(st, k1, lay, lib_target(oc, src, cache.data_ptr()), s) == N
+        s.synchronize()
+        assert st.put_chunks(k2, payload_stack(lay, 42, r2.payload_ids)) == N
+        base = st.slab[0]
+        addrs = sorted(int(a) - base for a in st.lookup(list(k1) + list(k2)))
+        assert addrs == [i * pitch for i in range(2 * N)]
+        got = []
+        for keys in (k1, k2):
+            flat = sentinel_buffer(W)
+            d = oc.build_descriptor(st, keys, lay, oc.FlatTarget(flat.data_ptr(), W))
+            d.fetch_layerwise(s)
+            d.sync_layer(lay.num_layers - 1)
+            got.append(flat.cpu().numpy())
+            d.close()
+    ost = ChunkStore(lay)
+    ok1, ok2 = okeys.chunk_keys(r1.tokens, 16), okeys.chunk_keys(r2.tokens, 16)
+    assert offload_paged(ost, ok1, lay, oracle_target(src), cache.cpu().numpy()) == N
+    want1 = np.full(W, 0xA5, np.uint8)
+    fetch_layerwise(ost, obuild(ost, ok1, lay, OFlat(0, W)), want1)
+    assert np.array_equal(got[0], want1)
+    from scenario import Dest, oracle_result
+    assert np.array_equal(got[1], oracle_result(lay, 42, r2, Dest(kind="flat", size=W, flat_off=0, flat_cap=W)))
