@@ -148,6 +148,7 @@ def bench_config(args, lay_t, ws):
                         "paged NHD cache Bs=16 fragmented",
             "layout": {"L": L, "n_kv": lay_t[1], "d": lay_t[2], "p": lay_t[3], "G": G, "Bs": Bs},
             "fetch_mode": args.mode, "engine": args.engine, "tier": "hbm",
+            "store_slots": "random slab positions (the rotating requests' chunks put in one seeded interleaving)",
             "l2": f"inputs larger than L2: {ROTATE} rotating request sets, "
                   f"{ROTATE * 2 * N_CHUNKS_4K * 2 * G * lay_t[1] * lay_t[2] * lay_t[3] * L / 2**30:.1f} GiB "
                   "touched per rotation",

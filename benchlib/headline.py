@@ -25,19 +25,22 @@ from . import verify
 
 
 def build_sets(oc, torch, dev, lay_t, n_chunks, rank, seed_base=1000, tier=None, rotate=ROTATE):
-    """ROTATE request sets in one store: synth payloads (regenerable by the oracle), each with its
-    own fragmented paged cache (pool = 1.25 x the blocks needed) and prepared target."""
+    """ROTATE request sets in one store: synth payloads (regenerable by the oracle) put in one seeded
+    random interleaving, so every request's chunks sit at random slab positions (SURVEY 8(d)
+    config 2), each request with its own fragmented paged cache (pool = 1.25 x the blocks needed)
+    and prepared target."""
     import synth
     L, G, Bs = lay_t[0], lay_t[4], 16
     row, S, chunk = oc.geometry(lay_t)
     store = oc.Store(lay_t, capacity=rotate * n_chunks, tier=oc.TIER_HBM if tier is None else tier,
                      device=dev.index)
-    sets = []
+    sets, reqs = [], []
     for r in range(rotate):
         seed = seed_base * rank + 1000 + r
         (tok,), (ids,) = synth.family_streams(seed, G, 0, [n_chunks])
-        keys = oc.chunk_keys(tok, G)
-        verify.fill_store([store], keys, seed, ids, chunk)
+        reqs.append((oc.chunk_keys(tok, G), seed, ids, tok))
+    verify.fill_store_scattered(store, [q[:3] for q in reqs], chunk, order_seed=seed_base * rank + 7)
+    for r, (keys, seed, ids, tok) in enumerate(reqs):
         need = n_chunks * G // Bs
         pool = need + need // 4
         bt = synth.block_table(77 + r, need, pool)

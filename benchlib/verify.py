@@ -70,6 +70,36 @@ def fill_store(stores, keys, seed, payload_ids, chunk_bytes, batch=128, threads=
     return time.perf_counter() - t0
 
 
+def fill_store_scattered(store, requests, chunk_bytes, order_seed, batch=128, threads=None):
+    """Put the chunks of several requests -- `requests` = [(keys, seed, payload_ids), ...] -- in one
+    seeded random interleaving, so each request's chunks land at random slots of the append-only
+    slab ("store slots at random (hash-addressed) slab positions").  Payloads
+    are the same synth bytes fill_store puts.  Returns seconds spent."""
+    t0 = time.perf_counter()
+    threads = threads or host_threads()
+    pairs = [(r, i) for r, (_, _, ids) in enumerate(requests) for i in range(len(ids))]
+    order = np.random.Generator(np.random.PCG64([order_seed, 0x51])).permutation(len(pairs))
+    starts = list(range(0, len(order), batch))
+
+    def gen(b0):
+        sel = [pairs[k] for k in order[b0:b0 + batch]]
+        keys = np.stack([np.asarray(requests[r][0][i]) for r, i in sel])
+        pl = np.empty((len(sel), chunk_bytes), dtype=np.uint8)
+        for row, (r, i) in enumerate(sel):
+            pl[row] = synth.chunk_payload(requests[r][1], requests[r][2][i], chunk_bytes)
+        return keys, pl
+
+    with ThreadPoolExecutor(threads) as ex:   # at most `threads` batches generated ahead
+        futs = [ex.submit(gen, b0) for b0 in starts[:threads]]
+        for i in range(len(starts)):
+            keys, pl = futs[i].result()
+            futs[i] = None
+            if i + threads < len(starts):
+                futs.append(ex.submit(gen, starts[i + threads]))
+            store.put_chunks(keys, pl)
+    return time.perf_counter() - t0
+
+
 # ---- GPU side: read back what a fetch delivered -----------------------------------------------------
 def slot_index(torch, dev, block_table, n_tokens, Bs, first_token=0):
     """Row index (block * Bs + slot) of each of the prefix's n_tokens in a [pool*Bs, row] view."""

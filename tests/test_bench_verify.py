@@ -75,3 +75,33 @@ def test_full_check_against_oracle_gather():
     cache[1, 1, bt[0], 0, 0] ^= 0xFF
     ok, _, _, _ = verify.full_check(torch, lay, 8, keys, ids, cache, idx, [1])
     assert not ok
+
+
+def test_fill_store_scattered_interleaves_and_puts_synth_bytes():
+    """fill_store_scattered: every (key, payload) pair of every request is put exactly once, with
+    the synth payload fill_store would put, in an order that interleaves the requests (so a
+    request's chunks land at scattered slots of an append-only slab)."""
+    lay = Layout(2, 2, 16, 2, 16)
+    cb = chunk_bytes(lay)
+
+    class Rec:
+        def __init__(self):
+            self.keys, self.rows = [], []
+
+        def put_chunks(self, keys, pl):
+            self.keys += [bytes(k) for k in np.asarray(keys)]
+            self.rows += [r.copy() for r in pl]
+
+    reqs = []
+    for r in range(3):
+        (tok,), (ids,) = synth.family_streams(300 + r, 16, 0, [20])
+        reqs.append((np.frombuffer(b"".join(okeys.chunk_keys(tok, 16)), np.uint8).reshape(-1, 32), 300 + r, ids))
+    rec = Rec()
+    verify.fill_store_scattered(rec, reqs, cb, order_seed=5, batch=7, threads=2)
+    want = {bytes(k): synth.chunk_payload(seed, pid, cb) for keys, seed, ids in reqs for k, pid in zip(keys, ids)}
+    assert len(rec.keys) == len(want) == 60 and set(rec.keys) == set(want)
+    for k, row in zip(rec.keys, rec.rows):
+        assert np.array_equal(row, want[k])
+    owner = {bytes(k): r for r, (keys, _, _) in enumerate(reqs) for k in keys}
+    slots_of_0 = [i for i, k in enumerate(rec.keys) if owner[k] == 0]
+    assert slots_of_0 != list(range(slots_of_0[0], slots_of_0[0] + 20))   # not one contiguous run
