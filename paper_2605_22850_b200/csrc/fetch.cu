@@ -1107,11 +1107,16 @@ OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {
     // are in device memory): nothing needs to be enqueued -- a stream wait costs the consumer
     // 1-4 us of launch pipelining even when its condition already holds.
     if (d->ready_host && (int32_t)(__atomic_load_n(d->ready_host, __ATOMIC_ACQUIRE) - target) >= 0) return OC_OK;
-    static const bool relay_on = oc::env_flag("OC_WAIT_RELAY", true);
+    // OC_WAIT_RELAY=1 (opt-in): the value wait goes on a private relay stream, which records a
+    // per-layer CUDA event, and the consumer waits on that event: 0.7 us of consumer-stream time per
+    // wait against 2.3 us for a value wait on the consumer stream itself (profiles/r02_wait_kinds.txt).
+    // Not the default: a blocked value wait stalls the hardware queue its stream is mapped to, and
+    // with many concurrent requests (a relay stream each, beside their copy and consumer streams)
+    // queues are shared -- another request's fetch or consumer behind it waits too.  Workload C's six
+    // unpaced requests took 7.9-8.7 s instead of 0.3-8.7 s with relays, and the paced ones measured
+    // 2.4-4.2x Eq. 3 instead of 1.00 (profiles/r02_sched_relay_hazard.json).
+    const bool relay_on = oc::env_flag("OC_WAIT_RELAY", false);
     if (relay_on && !oc::force_wait_kernel()) {
-        // The value wait goes on a private relay stream, which records a per-layer CUDA event; the
-        // consumer waits on that event: 0.7 us of consumer-stream time per wait against 2.3 us for
-        // a value wait on the consumer stream itself (profiles/r02_wait_kinds.txt).
         std::lock_guard<std::mutex> lk(d->relay_mu);
         if (!d->relay) {
             int krc = oc::relay_get(d->device, L, &d->relay);
