@@ -10,7 +10,7 @@ from scenario import lib_target, make_dest, oracle_result, payload_stack, reques
 
 lay = Layout(2, 2, 64, 2, 16)
 ok = 0
-SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3,4,5,6").split(",")
+SECTIONS = os.environ.get("OC_SAN_SECTIONS", "1,2,3,4,5,6,7").split(",")
 for kind in (("nhd", "hnd") if "1" in SECTIONS else ()):
     for engine in (oc.COPY_BULK, oc.COPY_LDST):
         for mode in (oc.FETCH_PERSISTENT, oc.FETCH_PER_LAYER):
@@ -201,5 +201,38 @@ if "6" in SECTIONS:
             assert np.array_equal(buf.cpu().numpy(), oracle_result(lay4, 6, req, dest))
             d.close()
             ok += 1
+if "7" in SECTIONS:
+    # the yield launch (layer 0 persistent, then one unit per CTA), waits through the opt-in relay
+    # stream, and a store whose HBM slots are padded (oc_slot_pitch) filled by put_chunks + offload
+    lay20 = Layout(20, 8, 128, 2, 16)                     # 1.25 MiB chunks -> 41-granule pitch
+    r1, r2 = requests_family(lay20, 12, 0, [3, 3])
+    with oc.Store(lay20, capacity=6) as st:
+        k1, k2 = oc.chunk_keys(r1.tokens, 16), oc.chunk_keys(r2.tokens, 16)
+        st.put_chunks(k1, payload_stack(lay20, 12, r1.payload_ids))
+        dest = make_dest(lay20, 3, "nhd", Bs=16, seed=3)
+        buf = sentinel_buffer(dest.size)
+        d = oc.build_descriptor(st, k1, lay20, lib_target(oc, dest, buf.data_ptr()))
+        s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+        os.environ["OC_WAIT_RELAY"] = "1"
+        d.fetch_layerwise(s, yield_sms=True)
+        for l in range(20):
+            d.wait_layer(l, cons)
+        cons.synchronize()
+        os.environ.pop("OC_WAIT_RELAY")
+        want = oracle_result(lay20, 12, r1, dest)
+        assert np.array_equal(buf.cpu().numpy(), want)
+        ok += 1
+        # offload request 1's delivered blocks under request 2's keys into the padded slots, then
+        # fetch them back: request 2's keys now hold request 1's bytes
+        s.wait_stream(cons)
+        assert oc.put_from_paged(st, k2, lay20, lib_target(oc, dest, buf.data_ptr()), s) == 3
+        buf2 = sentinel_buffer(dest.size)
+        d2 = oc.build_descriptor(st, k2, lay20, lib_target(oc, dest, buf2.data_ptr()))
+        d2.fetch_layerwise(s)
+        d2.sync_layer(19)
+        assert np.array_equal(buf2.cpu().numpy(), want)
+        ok += 1
+        d.close()
+        d2.close()
 torch.cuda.synchronize()
 print("sanitize workload ok", ok)
