@@ -251,14 +251,15 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                 # layer l, so it runs beside layer l's MLP GEMMs (lean CTAs fit beside a GEMM CTA)
                 g = dict(fopts["gated"])
                 k0 = g.pop("k0")
+                gs = cs if g.pop("low", False) else gate_s
                 d.fetch_layers(0, k0, cs, unit_bytes=g.get("unit_bytes", 0))
 
                 def hook(l):
                     if l + k0 < L:
                         e = torch.cuda.Event()
                         e.record(ks)
-                        gate_s.wait_event(e)
-                        d.fetch_layers(l + k0, l + k0 + 1, gate_s, **g)
+                        gs.wait_event(e)
+                        d.fetch_layers(l + k0, l + k0 + 1, gs, **g)
             elif fopts is not None:
                 d.fetch_layerwise(cs, **fopts)
             with torch.cuda.stream(ks):
@@ -291,7 +292,13 @@ def stall_gemm_leg(args, oc, torch, dev, lay_t):
                                        # the co-run schedule through oc_fetch_layers (measured worse:
                                        # profiles/r02_stall_gemm_gated.json)
                                        ("gated_u32k", {"gated": {"k0": 2, "engine": oc.COPY_BULK, "max_ctas": 148,
-                                                                 "unit_bytes": 32768}}, None)))]
+                                                                 "unit_bytes": 32768}}, None),
+                                       # the same gating on a LOW-priority copy stream with one unit per
+                                       # CTA: layer l+2's copy waits for layer l's attention to end, then
+                                       # fills the SMs the O/MLP GEMMs leave free
+                                       ("gated_low_yield", {"gated": {"k0": 2, "engine": oc.COPY_BULK,
+                                                                      "yield_sms": True, "low": True}},
+                                        (lo_s, hi_s))))]
         sel = [v for v in getattr(args, "stall_gemm_variants", "").split(",") if v]
         if sel:
             tiers = [(tn, t, tuple(v for v in vs if v[0] in sel)) for tn, t, vs in tiers]

@@ -338,8 +338,10 @@ OC_API int oc_fetch_layerwise(oc_desc* desc, const oc_fetch_opts* opts, void* co
  * ordered after all ranges of the open one (as for fetch_layerwise).  A new fetch of the descriptor (any entry point) is refused
  * with EINVAL until all L layers of the open one have been requested.
  * opts: PERSISTENT mode, BULK or LDST engine (AUTO picks between them), unpaced;
- * max_ctas and OC_FETCH_LEAN apply per call; unit_bytes only with l0 = 0 (a later
- * call may repeat the same value or pass 0).  Errors: ERANGE (l0 >= l1 or l1 > L),
+ * max_ctas and OC_FETCH_LEAN apply per call; OC_FETCH_YIELD on a call with l0 > 0
+ * and the BULK engine launches one copy CTA per unit (as the yield launch's later
+ * layers); unit_bytes only with l0 = 0 (a later call may repeat the same value or
+ * pass 0).  Errors: ERANGE (l0 >= l1 or l1 > L),
  * EINVAL (out of order), ENOTSUP (other modes, engines, pacing). */
 OC_API int oc_fetch_layers(oc_desc* desc, uint32_t l0, uint32_t l1, const oc_fetch_opts* opts,
                            void* copy_stream);

@@ -451,9 +451,11 @@ class Descriptor:
                         yield_sms, lean)
         _check(_lib.oc_fetch_layerwise(self._h, ctypes.byref(o), _stream(stream)))
 
-    def fetch_layers(self, l0: int, l1: int, stream=None, engine=COPY_AUTO, max_ctas=0, unit_bytes=0, lean=False):
-        """oc_fetch_layers: layers [l0, l1) of the current fetch (l0 = 0 opens a new one)."""
-        o = _fetch_opts(FETCH_PERSISTENT, engine, max_ctas, unit_bytes, 0.0, False, False, False, False, lean)
+    def fetch_layers(self, l0: int, l1: int, stream=None, engine=COPY_AUTO, max_ctas=0, unit_bytes=0, lean=False,
+                     yield_sms=False):
+        """oc_fetch_layers: layers [l0, l1) of the current fetch (l0 = 0 opens a new one).
+        `yield_sms` (l0 > 0, TMA engine): one unit per CTA, as OC_FETCH_YIELD's later layers."""
+        o = _fetch_opts(FETCH_PERSISTENT, engine, max_ctas, unit_bytes, 0.0, False, False, False, yield_sms, lean)
         _check(_lib.oc_fetch_layers(self._h, int(l0), int(l1), ctypes.byref(o), _stream(stream)))
 
     def scatter_flat(self, flat_base: int, flat_capacity: int, stream=None, max_ctas=0, unit_bytes=0):

@@ -563,6 +563,10 @@ int launch_fetch_range(Desc* d, const oc_fetch_opts& oin, uint32_t l0, uint32_t 
     if (o.engine == OC_COPY_BULK) {
         BulkPlan p = plan_bulk(d->dd, sms, o.max_ctas, (uint64_t)(l1 - l0) * upl);
         if (o.flags & OC_FETCH_LEAN) shallow_ring(&p);
+        if (o.flags & OC_FETCH_YIELD) {  // one unit per CTA, as the yield launch's later layers
+            p.copy_ctas = (l1 - l0) * upl;
+            shallow_ring(&p);
+        }
         rc = launch_bulk(d, p, l0 * upl, l1 * upl, s);
     } else {
         rc = launch_ldst(d, sms, o.max_ctas, l0 * upl, l1 * upl, s);

@@ -31,6 +31,8 @@ def _setup(lay, n, seed, kind="nhd", Bs=16, first_token=0):
     ([(0, 2), (2, 8)], {"engine": oc.COPY_BULK, "max_ctas": 7, "unit_bytes": 8192, "lean": True}),
     ([(0, 1)] + [(l, l + 1) for l in range(1, 8)], {"engine": oc.COPY_LDST, "max_ctas": 5}),
     ([(0, 8)], {"lean": True}),
+    # later ranges with one copy CTA per unit (OC_FETCH_YIELD on a continuation)
+    ([(0, 2)] + [(l, l + 1) for l in range(2, 8)], {"engine": oc.COPY_BULK, "yield_later": True}),
 ])
 def test_ranges_equal_oracle(ranges, opts):
     lay = OLayout(8, 8, 128, 2, 16)
@@ -38,11 +40,13 @@ def test_ranges_equal_oracle(ranges, opts):
     streams = [torch.cuda.Stream(), torch.cuda.Stream(priority=-1)]
     cons = torch.cuda.Stream()
     prev = None
+    opts = dict(opts)
+    yield_later = opts.pop("yield_later", False)
     for i, (l0, l1) in enumerate(ranges):
         s = streams[i % 2]
         if prev is not None:          # ranges of one fetch in sequence (the caller's guarantee)
             s.wait_event(prev)
-        d.fetch_layers(l0, l1, s, **opts)
+        d.fetch_layers(l0, l1, s, **opts, **({"yield_sms": True} if yield_later and l0 > 0 else {}))
         prev = torch.cuda.Event()
         prev.record(s)
         for l in range(l0, l1):
