@@ -119,3 +119,41 @@ def test_config4_70b_32k_request():
     _check_pads(dest, bufs)
     del bufs
     torch.cuda.empty_cache()
+
+
+def test_bench_headline_launch_configuration():
+    """The headline exactly as bench.py times it (benchlib.headline.build_sets: the rotating requests'
+    chunks at random slab positions, fragmented paged caches; fetches back to back with
+    OC_FETCH_OVERLAP on one copy stream, the consumer waiting on each request's last layer): every
+    rotating request's 32 layers read back through its block table equal the oracle's Alg. A1
+    payloads byte for byte, and the rest of each cache keeps its sentinel."""
+    from benchlib import headline, verify
+    from benchlib.common import ROTATE
+    lay_t = synth.LLAMA3_8B.as_tuple()
+    lay = OLayout(*lay_t)
+    L, G = lay_t[0], lay_t[4]
+    dev = torch.device("cuda", 0)
+    store, sets = headline.build_sets(oc, torch, dev, lay_t, 256, rank=0)
+    for st in sets:
+        st["cache"].fill_(0xA5)
+    descs = [oc.build_descriptor(store, st["keys"], lay_t, st["target"]) for st in sets]
+    copy_s, cons_s = torch.cuda.Stream(), torch.cuda.Stream()
+    copy_s.wait_stream(torch.cuda.current_stream())
+    for i in range(3 * ROTATE):                     # back to back, overlapped, rotating
+        descs[i % ROTATE].fetch_layerwise(copy_s, overlap=True)
+        descs[i % ROTATE].wait_layer(L - 1, cons_s)
+    torch.cuda.synchronize()
+    for st in sets:
+        idx = verify.slot_index(torch, dev, st["bt"], 256 * G, 16)
+        ok, nbytes, _, _ = verify.full_check(torch, lay, st["seed"], st["keys"], st["ids"], st["cache"], idx,
+                                             range(L))
+        assert ok and nbytes == 256 * L * oc.geometry(lay_t)[1], st["seed"]
+        rows = st["cache"].view(L, 2, -1, oc.geometry(lay_t)[0])
+        mask = torch.ones(rows.shape[2], dtype=torch.bool, device=dev)
+        mask[idx] = False
+        assert bool((rows[:, :, mask] == 0xA5).all()), st["seed"]
+    for d in descs:
+        d.close()
+    store.close()
+    del sets
+    torch.cuda.empty_cache()
