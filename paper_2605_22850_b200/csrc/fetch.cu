@@ -600,8 +600,14 @@ int launch_fetch(Desc* d, const oc_fetch_opts& oin, cudaStream_t s, uint32_t l_e
         // B_l directly (no stage, no SMs): 53.3 GB/s of PCIe reads at 1 run, 51.5 at 4, against
         // 51.4 for SM zero-copy reads (profiles/r01_flat_auto.txt); with many runs per layer its
         // per-transfer cost wins (45.6 GB/s at 16 runs; profiles/r01_ce2d.txt).
-        const bool ce = !ranged && d->flat_base && d->host_chunks == d->N && !d->run_first.empty() &&
-                        d->run_first.size() <= 4 && o.pace_Bps == 0 && o.mode == OC_FETCH_PERSISTENT;
+        // A PAGED target fed that way with large layers (>= 32 MiB: a 64K hit) too: one strided
+        // transfer per layer into an HBM stage, then the scatter kernel -- 55.5 GB/s of PCIe reads
+        // against 51.2 for zero-copy (config 3, profiles/r02_bench.json legs.config3), X0 4.9 vs
+        // 5.3 ms; at 4K (14-16 MiB layers) the per-layer stage/scatter/announce steps cost more than
+        // they gain (spin-window added TTFT 0.74 vs 0.59 ms), so zero-copy stays.
+        const bool few_runs = !ranged && d->host_chunks == d->N && !d->run_first.empty() &&
+                              d->run_first.size() <= 4 && o.pace_Bps == 0 && o.mode == OC_FETCH_PERSISTENT;
+        const bool ce = few_runs && (d->flat_base || (d->hot_layers == 0 && d->N * d->geo.S >= (32ull << 20)));
         o.engine = ce ? OC_COPY_CE
                       : (d->dd.nhd || (o.pace_Bps > 0 && o.pace_strict)) ? OC_COPY_BULK : OC_COPY_LDST;
     }

@@ -231,3 +231,24 @@ def test_attach_peer_rejects_cycles():
             assert e.value.code == oc.OC_EINVAL
         req = requests_family(lay, 44, 0, [2])[0]
         assert a.match_prefix(req.tokens).shape[0] == 0   # a miss walks a -> b -> c and stops
+
+
+@pytest.mark.parametrize("kind", ["nhd", "hnd"])
+def test_auto_engine_large_layers_from_pinned_host(kind):
+    """AUTO with a pinned-host store and >= 32 MiB layers (here 64 chunks x 512 KiB) into a paged
+    target takes the copy engine + scatter path; with smaller layers zero-copy -- both byte-exact."""
+    lay = OLayout(2, 64, 128, 2, 16)                  # row 16 KiB, S = 512 KiB
+    for n in (64, 8):                                  # 32 MiB layers (CE) and 4 MiB layers (zero-copy)
+        req = requests_family(lay, 13, 0, [n])[0]
+        with oc.Store(lay, capacity=n, tier=oc.TIER_PINNED_HOST) as st:
+            keys = oc.chunk_keys(req.tokens, 16)
+            st.put_chunks(keys, payload_stack(lay, 13, req.payload_ids))
+            dest = make_dest(lay, n, kind, Bs=16, first_token=0, seed=4)
+            buf = sentinel_buffer(dest.size)
+            d = oc.build_descriptor(st, keys, lay, lib_target(oc, dest, buf.data_ptr()))
+            s, cons = torch.cuda.Stream(), torch.cuda.Stream()
+            d.fetch_layerwise(s)                       # engine = COPY_AUTO
+            d.wait_layer(lay.num_layers - 1, cons)
+            cons.synchronize()
+            assert np.array_equal(buf.cpu().numpy(), oracle_result(lay, 13, req, dest)), n
+            d.close()
