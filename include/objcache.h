@@ -176,7 +176,10 @@ OC_API int oc_store_attach_peer(oc_store* store, oc_store* peer);
 /* Multi-process sharing of an HBM store (config 5, NVLink P2P):
  * export writes an opaque blob (CUDA IPC handle + key table) of *size bytes
  * (call with buf = NULL to query the size); import opens it in another process
- * as a read-only peer store bound to GPU `device`, usable with attach_peer. */
+ * as a read-only peer store bound to GPU `device`, usable with attach_peer.  The blob
+ * carries the exporter's slot pitch.  import: EINVAL for a blob that is not an
+ * export of this library version, is truncated, names slots beyond its capacity,
+ * or whose capacity x pitch exceeds the mapped allocation. */
 OC_API int oc_store_export(oc_store* store, void* buf, uint64_t* size);
 OC_API int oc_store_import(const void* buf, uint64_t size, int device, oc_store** out);
 

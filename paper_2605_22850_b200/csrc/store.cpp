@@ -7,6 +7,8 @@
 // valid for the store's lifetime.  The key index is single-writer / multi-reader.
 #include <algorithm>
 
+#include <cuda.h>
+
 #include "oc_internal.h"
 
 namespace oc {
@@ -24,6 +26,27 @@ struct ExportHeader {
     uint64_t pitch;
     cudaIpcMemHandle_t handle;
 };
+
+// Size of the allocation an (IPC-mapped) device pointer lies in, through cuMemGetAddressRange
+// resolved via the runtime (no link-time libcuda).  0 when unavailable.
+uint64_t mapped_bytes(const void* p) {
+    typedef CUresult (*PFN_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static std::once_flag once;
+    static PFN_range fn = nullptr;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_range)f;
+        cudaGetLastError();
+    });
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (!fn || fn(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS) return 0;
+    return (uint64_t)size - ((uint64_t)(uintptr_t)p - (uint64_t)base);
+}
 
 }  // namespace
 
@@ -373,6 +396,13 @@ OC_API int oc_store_import(const void* buf, uint64_t size, int device, oc_store*
         oc::DeviceGuard dg(device);
         void* p = nullptr;
         OC_CUDA(cudaIpcOpenMemHandle(&p, hd.handle, cudaIpcMemLazyEnablePeerAccess));
+        // the blob's capacity x pitch must lie inside the mapped slab (a corrupt or foreign blob
+        // would otherwise send fetches past its end)
+        const uint64_t have = oc::mapped_bytes(p);
+        if (have && (unsigned __int128)hd.capacity * hd.pitch > have) {
+            cudaIpcCloseMemHandle(p);
+            return oc::fail(OC_EINVAL, "store_import: capacity x slot pitch exceeds the mapped slab");
+        }
         s->slab = (uint8_t*)p;
         s->ipc_mapped = true;
     }

@@ -48,6 +48,13 @@ def test_export_import_across_processes(lay_t):
         keys = oc.chunk_keys(req.tokens, 16)
         local = oc.Store(lay, capacity=16)
         local.put_chunks(keys[:6], payload_stack(lay, 31, req.payload_ids[:6]))
+        # a blob whose capacity x pitch exceeds the mapped slab is refused (and its mapping closed)
+        bad = bytearray(blob)
+        cap = int.from_bytes(bad[32:40], "little")
+        assert cap == 16 and int.from_bytes(bad[48:56], "little") == oc.slot_pitch(lay_t, oc.TIER_HBM)
+        bad[32:40] = (cap * 4096).to_bytes(8, "little")
+        with pytest.raises(oc.ObjcacheError):
+            oc.Store.import_(bytes(bad), device=0)
         peer = oc.Store.import_(blob, device=0)
         assert peer.count == 6
         with pytest.raises(oc.ObjcacheError):
