@@ -79,7 +79,9 @@ def config3_leg(args, oc, torch, dev, lay_t):
                 ms.append(a.elapsed_time(b))
             t = min(ms)
             t_ = d.layer_times().astype(np.int64)
-            row_out = {"ms": round(t, 3), "GBps_rw": round(rw / t / 1e6, 1), "X0_ms": round((t_[1] - t_[0]) / 1e6, 4)}
+            xl = np.diff(t_[1:]) / 1e6                      # X_l, l >= 1: gaps between announcements
+            row_out = {"ms": round(t, 3), "GBps_rw": round(rw / t / 1e6, 1), "X0_ms": round((t_[1] - t_[0]) / 1e6, 4),
+                       "X_layer_ms": {"median": round(float(np.median(xl)), 4), "max": round(float(xl.max()), 4)}}
             if tier == oc.TIER_HBM:
                 row_out["frac_of_hbm_peak"] = round(rw / t / 1e6 / peak, 3)
             else:
