@@ -432,10 +432,12 @@ OC_API int oc_wdrr_plan(const uint64_t* n_units, uint32_t n, const uint32_t* til
  * PERSISTENT mode: if the layer is already announced when the call is made (the
  * announcing kernel also writes a pinned host copy of the ready word, after the
  * device word), nothing is enqueued -- the bytes are already in place.
- * Otherwise a stream value wait (cuStreamWaitValue32 on the ready word) goes on
- * `consumer_stream` (a one-thread spin kernel with OC_WAIT_KERNEL=1; a private relay
- * stream + CUDA event with OC_WAIT_RELAY=1 -- cheaper for the consumer stream, but
- * its blocked waits can hold up other streams sharing a hardware queue).
+ * Otherwise a one-thread kernel that spins on the ready word goes on
+ * `consumer_stream` (it holds one CTA slot, never a hardware queue).  Opt-in:
+ * OC_WAIT_VALUE=1, a stream value wait (cuStreamWaitValue32) on `consumer_stream`;
+ * OC_WAIT_RELAY=1, the value wait on a private relay stream + a CUDA event.  A
+ * blocked value wait stalls the hardware queue its stream is mapped to, and streams
+ * share queues (CUDA_DEVICE_MAX_CONNECTIONS): a producer mapped behind it waits too.
  * PER_LAYER mode: cudaStreamWaitEvent on the layer's event. */
 OC_API int oc_wait_layer(oc_desc* desc, uint32_t layer, void* consumer_stream);
 

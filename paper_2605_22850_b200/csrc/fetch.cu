@@ -1117,15 +1117,19 @@ OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {
     // are in device memory): nothing needs to be enqueued -- a stream wait costs the consumer
     // 1-4 us of launch pipelining even when its condition already holds.
     if (d->ready_host && (int32_t)(__atomic_load_n(d->ready_host, __ATOMIC_ACQUIRE) - target) >= 0) return OC_OK;
-    // OC_WAIT_RELAY=1 (opt-in): the value wait goes on a private relay stream, which records a
-    // per-layer CUDA event, and the consumer waits on that event: 0.7 us of consumer-stream time per
-    // wait against 2.3 us for a value wait on the consumer stream itself (profiles/r02_wait_kinds.txt).
-    // Not the default: a blocked value wait stalls the hardware queue its stream is mapped to, and
-    // with many concurrent requests (a relay stream each, beside their copy and consumer streams)
-    // queues are shared -- another request's fetch or consumer behind it waits too.  Workload C's six
-    // unpaced requests took 7.9-8.7 s instead of 0.3-8.7 s with relays, and the paced ones measured
-    // 2.4-4.2x Eq. 3 instead of 1.00 (profiles/r02_sched_relay_hazard.json).
+    // The default wait is a one-thread kernel on the consumer stream that spins on the ready word:
+    // it holds one CTA slot, never the stream's hardware queue.  A stream value wait
+    // (cuStreamWaitValue32) stalls the hardware queue its stream is mapped to, and streams share
+    // queues (CUDA_DEVICE_MAX_CONNECTIONS, 8 by default): a producer stream mapped behind a blocked
+    // consumer waits too.  Measured (profiles/r02_wait_queue_hazard.json): the headline's next fetch
+    // queued behind the consumer's wait for the previous one (overlap lost, 6.31 instead of 6.72 TB/s
+    // with one connection, and once with the default 8); with relay streams (value wait on a
+    // per-descriptor relay stream + event) workload C's requests all ended after the largest one
+    // (2.4-4.2x Eq. 3 instead of 1.00; profiles/r02_sched_relay_hazard.json).
+    // OC_WAIT_VALUE=1: the value wait on the consumer stream (2.3 us of consumer-stream time per
+    // wait); OC_WAIT_RELAY=1: the relay (0.7 us; profiles/r02_wait_kinds.txt).  Both opt-in.
     const bool relay_on = oc::env_flag("OC_WAIT_RELAY", false);
+    const bool value_on = oc::env_flag("OC_WAIT_VALUE", false);
     if (relay_on && !oc::force_wait_kernel()) {
         std::lock_guard<std::mutex> lk(d->relay_mu);
         if (!d->relay) {
@@ -1144,7 +1148,7 @@ OC_API int oc_wait_layer(oc_desc* h, uint32_t layer, void* stream) {
     }
     int urc = oc::upload_order(&d->up, s);  // the ready word lives in the uploaded block
     if (urc) return urc;
-    if (!oc::force_wait_kernel()) {
+    if (value_on && !oc::force_wait_kernel()) {
         int rc = oc::stream_wait_geq(s, d->dd.ready, target);
         if (rc == OC_OK) return OC_OK;
     }

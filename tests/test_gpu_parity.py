@@ -257,10 +257,10 @@ def test_llama70b_layout_sampled_layers():
 @pytest.mark.parametrize("engine", ENGINES)
 def test_wait_layer_orders_consumer(monkeypatch, wait_kind, engine):
     """A consumer stream that waits on layer l and then snapshots layer l must see final bytes even
-    though the (paced) fetch is still running -- for each way a wait is enqueued (a stream value wait
-    on the consumer stream, the spin kernel, the opt-in relay stream + event)."""
-    if wait_kind == "kernel":
-        monkeypatch.setenv("OC_WAIT_KERNEL", "1")
+    though the (paced) fetch is still running -- for each way a wait is enqueued (the default spin
+    kernel, the opt-in stream value wait on the consumer stream, the opt-in relay stream + event)."""
+    if wait_kind == "value":
+        monkeypatch.setenv("OC_WAIT_VALUE", "1")
     if wait_kind == "relay":
         monkeypatch.setenv("OC_WAIT_RELAY", "1")
     lay = OLayout(6, 2, 64, 2, 16)
